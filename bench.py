@@ -1,0 +1,326 @@
+"""Benchmark: training images/s of the Zhang MNIST CNN (fwd + bwd + SGD), BASELINE.json configs[1].
+
+Workload (N=1): the paper protocol -- 10k synthetic 28x28 images (synth::make_set(10000, 1)), batch 100,
+lr 0.05, init_params(42).  One bench *step* = one epoch = 100 SGD groups of 100 images (one launch of the
+persistent cooperative train kernel).  ``--steps 10`` times exactly the 10-epoch protocol (the timed run
+starts from init_params(42), so its epoch losses are checked against the reference's golden values).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--mode fast|exact] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU, NCCL): weak scaling -- every rank owns a 100-image shard of each
+global group of 100*N images (static_chunk, runtime.cpp:138-145) over a 10k*N-image corpus; per group:
+shard forward/backward/reduction kernel -> ncclAllReduce of the 3,898-float gradient sum (+ fp64 loss)
+-> sgd kernel.  ``--impl reference`` times the reference's own CPU net::train (oracle/_ref, the
+unmodified tensorloom library) with all host threads on the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training images/sec (fwd+bwd+SGD), Zhang MNIST CNN, batch 100 and batch sweep, 1/2/4/8 B200"
+FLOP_PER_TRAIN_IMAGE = 1_048_320  # 524,160 MAC algorithmic
+FP32_LANES_PER_SM = 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--mode", choices=["fast", "exact"], default="fast")
+    ap.add_argument("--batch", type=int, default=100, help="per-GPU images per SGD group")
+    ap.add_argument("--n", type=int, default=10000, help="per-GPU corpus size")
+    ap.add_argument("--grid", type=int, default=0, help="CTAs of the persistent kernel (0 = auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---- clocks sampled during the timed region (NVML) -------------------------------------------------
+class ClockSampler:
+    BAD = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+           "hw_power_brake_slowdown": 0x80}
+    NOTE = {"sw_power_cap": 0x4}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv, self.err = None, str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv:
+            self._t.join()
+
+    def summary(self) -> dict:
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        reasons = [k for k, v in {**self.BAD, **self.NOTE}.items() if self.reasons & v]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def golden_losses():
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "protocol.json")) as f:
+            return [float(v) for v in json.load(f)["epoch_mean_loss"]]
+    except Exception:
+        return None
+
+
+# ---- reference CPU path (oracle/_ref = the unmodified tensorloom library) ---------------------------
+def reference_epochs(images, labels, epochs_budget_s: float, max_epochs: int, batch: int):
+    """Times net::train of the reference on whole epochs with all host threads; returns img/s, info."""
+    from oracle import Reference  # reference arm / cpu_baseline only
+    from paper_1912_05234_b200.runtime import init_params
+    R = Reference()
+    cores = os.cpu_count() or 1
+    R.set_workers(cores)
+    p = init_params(42)
+    done, t_total = 0, 0.0
+    while done < max_epochs:
+        t0 = time.perf_counter()
+        p, _ = R.train(images, labels, p, rate=0.05, epochs=1, batch=batch)
+        t_total += time.perf_counter() - t0
+        done += 1
+        if t_total >= epochs_budget_s:
+            break
+    return done * len(labels) / t_total, {"cores": cores, "epochs": done, "seconds": t_total}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1912_05234_b200.runtime import synth_make_set
+    images, labels = synth_make_set(args.n, 1)
+    from oracle import Reference
+    R = Reference()
+    cores = os.cpu_count() or 1
+    R.set_workers(cores)
+    from paper_1912_05234_b200.runtime import init_params
+    p = init_params(42)
+    for _ in range(args.warmup):
+        p, _ = R.train(images, labels, p, rate=0.05, epochs=1, batch=args.batch)
+    p = init_params(42)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        p, _ = R.train(images, labels, p, rate=0.05, epochs=1, batch=args.batch)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = args.steps * args.n / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: synth::make_set(10000, 1), init_params(42)",
+        "config": {"workload": "Zhang CNN paper protocol, 1 epoch of 10k images at batch 100 per step",
+                   "batch": args.batch, "n_images": args.n, "epochs_per_step": 1},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} epochs x {args.n} images, net::train with "
+                                   f"set_global_config({{{cores},4096}})"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm ----------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1912_05234_b200 import Context
+    from paper_1912_05234_b200.runtime import init_params, synth_make_set
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    B, n_per = args.batch, args.n
+    n_total = n_per * world
+    images, labels = synth_make_set(n_total, 1)
+    stream = torch.cuda.current_stream()
+    ctx = Context(local, mode=args.mode)
+    ctx.set_stream(stream.cuda_stream)
+    if args.grid:
+        ctx.set_grid(args.grid)
+
+    d_x = torch.from_numpy(images).to(dev)
+    d_y = torch.from_numpy(labels).to(dev)
+    p0 = init_params(42)
+    d_p = torch.zeros(3904, device=dev)
+    d_loss = torch.zeros(max(args.steps, args.warmup, 1) + 1, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def reset():
+        d_p.zero_()
+        d_p[:3898] = torch.from_numpy(p0).to(dev)
+
+    if world == 1:
+        def epoch(e):
+            ctx.train_device(d_x.data_ptr(), d_y.data_ptr(), n_total, d_p.data_ptr(), 0.05, e, 1, B,
+                             d_loss.data_ptr())
+        launches_per_step = 1
+    else:
+        from paper_1912_05234_b200.parallel import DeviceShardStep
+        dp = DeviceShardStep(ctx, d_x, d_y, n_total, B * world, world, rank)
+
+        def epoch(e):
+            dp.epoch(d_p, 0.05, d_loss, e)
+        launches_per_step = 2 * dp.groups_per_epoch
+
+    # warm-up (not timed), then the timed protocol from init_params(42)
+    reset()
+    for w in range(args.warmup):
+        epoch(w % max(args.steps, 1))
+    torch.cuda.synchronize()
+    reset()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.fill_(float(s))  # L2 flush between timed steps, outside the event pair
+            starts[s].record(stream)
+            epoch(s)
+            ends[s].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t)
+    losses = d_loss[: args.steps].cpu().numpy().tolist()
+    value = args.steps * n_total / (total_ms / 1e3)
+
+    # roofline of the dominant kernel (the persistent train kernel = the whole step)
+    info = ctx.info()
+    peaks = measured_peaks()
+    max_mhz = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = info["sm_count"] * FP32_LANES_PER_SM * 2 * max_mhz * 1e6 / 1e12
+    flop_per_launch = n_per * FLOP_PER_TRAIN_IMAGE
+    achieved = flop_per_launch / (total_ms / args.steps / 1e3) / 1e12
+    clocks = clk.summary()
+
+    result = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": f"synthetic: synth::make_set({n_total}, 1) (reference generator restated in C++), init_params(42)",
+        "config": {"workload": "Zhang CNN paper protocol (BASELINE configs[1]): 1 step = 1 epoch of "
+                               f"{n_per} images/GPU at batch {B}/GPU, lr 0.05",
+                   "batch_per_gpu": B, "global_batch": B * world, "n_images": n_total, "epochs_per_step": 1,
+                   "mode": args.mode, "parallelism": f"dp{world}", "grid": args.grid or "auto",
+                   "l2": "flushed between timed steps (256 MiB write outside the event pair)"},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp32_peak, "traffic": None,
+                     "per_launch": f"{n_per} images x {FLOP_PER_TRAIN_IMAGE} algorithmic FLOP",
+                     "peak_source": f"{info['sm_count']} SMs x 128 FP32 lanes x 2 x sm_max_mhz {max_mhz} "
+                                    "(MEASURED_PEAKS.json clocks); FFMA-bound path (no HBM/tensor bound)"},
+        "clocks": clocks,
+        "epoch_mean_loss": losses,
+    }
+    gl = golden_losses()
+    if gl and world == 1 and args.steps == 10 and n_per == 10000 and B == 100:
+        rel = max(abs(a - b) / abs(b) for a, b in zip(losses, gl))
+        result["parity"] = {"epoch_loss_max_rel_vs_reference": rel, "tolerance": 1e-4,
+                            "bitwise": all("%.17g" % a == "%.17g" % b for a, b in zip(losses, gl))}
+
+    # end-to-end through the public host API (net::train with host buffers; H2D + D2H inside)
+    if not args.no_e2e and world == 1:
+        pin_x = torch.from_numpy(images).pin_memory()
+        pin_y = torch.from_numpy(labels).pin_memory()
+        px, py = pin_x.numpy(), pin_y.numpy()
+        p = p0.copy()
+        ctx.train(p, px, py, rate=0.05, epochs=1, batch=B)  # warm-up (allocations)
+        torch.cuda.synchronize()
+        times = []
+        p = p0.copy()
+        for s in range(args.steps):
+            flush.fill_(float(s))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            p, _ = ctx.train(p, px, py, rate=0.05, epochs=1, batch=B)
+            times.append(time.perf_counter() - t0)
+        result["e2e"] = {"value": args.steps * n_total / sum(times), "unit": "images/s",
+                         "h2d_bytes_per_step": images.nbytes + labels.nbytes + 3898 * 4,
+                         "d2h_bytes_per_step": 3898 * 4 + 8,
+                         "api": "tlb_train (net::train) on pinned host buffers, wall clock per call"}
+        result["gpu_launches"] += args.steps
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, meta = reference_epochs(images[:n_per], labels[:n_per], 10.0, 3, B)
+        result["cpu_baseline"] = {"value": v, "unit": "images/s", "cores": meta["cores"], "kind": "reference",
+                                  "sample": f"{meta['epochs']} epoch(s) x {n_per} images at batch {B}, reference "
+                                            f"net::train (oracle/_ref) with {meta['cores']} workers, "
+                                            f"{meta['seconds']:.1f} s"}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

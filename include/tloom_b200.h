@@ -1,0 +1,155 @@
+/*
+ * tloom_b200.h -- C ABI of the B200-native tensorloom hot path (libtloom_b200.so).
+ *
+ * This is the drop-in boundary for the reference's training path.  The reference
+ * exposes it as the C++ headers proj/include/tloom/{nn,network,mnist}.hpp; our C++ mirror of those
+ * headers (include/tloom/*.hpp, same names and exceptions) and any FFI binding (ctypes, cgo, JNI)
+ * sit on top of these entry points.  Plain pointers and sizes only; no torch or C++ types.
+ *
+ * Conventions
+ *  - Every call returns TLB_OK (0) or an error code; tlb_last_error() returns the message of the
+ *    calling thread's last failure.  Codes map 1:1 onto the reference's exception taxonomy
+ *    (proj/include/tloom/errors.hpp:9-31) so the C++ layer rethrows the same types and messages.
+ *  - "Host" entry points take host buffers, stage them to HBM, run, copy results back and return
+ *    after device completion (the reference's synchronous semantics).  "_device" entry points take
+ *    device pointers and enqueue on the context stream without synchronising.
+ *  - Parameters / gradients are flat fp32 in write_flat order k1,b1,k2,b2,fc,b
+ *    (proj/src/network.cpp:186-193), TLB_NPARAM = 3898 floats.  Device-side parameter buffers are
+ *    padded to TLB_PSTRIDE = 3904 floats.
+ *  - Images are [n][28][28] fp32 in [0,1] (mnist::MnistSet, proj/include/tloom/mnist.hpp:14-19),
+ *    labels int32 0..9.
+ *  - Mode TLB_MODE_EXACT (default) reproduces the reference bit for bit (same per-element summation
+ *    order, no FMA, glibc expf restatement, example-order batch reduction).  TLB_MODE_FAST uses FFMA
+ *    and per-CTA partial sums (deterministic; within 1e-4 relative of the reference).
+ */
+#ifndef TLOOM_B200_H
+#define TLOOM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TLB_OK 0
+#define TLB_ERR_ERROR 1  /* tloom::Error       */
+#define TLB_ERR_SHAPE 2  /* tloom::ShapeError  */
+#define TLB_ERR_BOUNDS 3 /* tloom::BoundsError */
+#define TLB_ERR_FORMAT 4 /* tloom::FormatError */
+#define TLB_ERR_VALUE 5  /* tloom::ValueError  */
+#define TLB_ERR_CUDA 10
+#define TLB_ERR_NCCL 11
+#define TLB_ERR_ARG 12
+
+#define TLB_MODE_EXACT 0
+#define TLB_MODE_FAST 1
+
+#define TLB_NPARAM 3898
+#define TLB_PSTRIDE 3904
+#define TLB_NACT 5290 /* c1[6,24,24] s1[6,12,12] c2[12,1,8,8] s2[12,1,4,4] out[10,1,1,1,1] */
+#define TLB_CELL 3899 /* gradient row + loss, network.cpp:218 */
+
+typedef struct tlb_ctx tlb_ctx;
+/* on_epoch(epoch, mean_loss) of net::train (network.hpp:79-80, network.cpp:246-248). */
+typedef void (*tlb_epoch_cb)(int epoch, double mean_loss, void* user);
+
+const char* tlb_last_error(void);
+const char* tlb_version(void);
+
+/* ---- context: device, stream, mode, workspaces ------------------------------------------------ */
+int tlb_ctx_create(int device, tlb_ctx** out);
+int tlb_ctx_destroy(tlb_ctx* ctx);
+/* Use a caller-owned cudaStream_t (NULL = the context's own stream). */
+int tlb_ctx_set_stream(tlb_ctx* ctx, void* cuda_stream);
+int tlb_ctx_set_mode(tlb_ctx* ctx, int mode);
+int tlb_ctx_get_mode(const tlb_ctx* ctx, int* mode);
+/* CTAs of the persistent train kernel (0 = auto); clamped to the co-resident maximum. */
+int tlb_ctx_set_grid(tlb_ctx* ctx, int ctas);
+int tlb_ctx_info(const tlb_ctx* ctx, int* sm_count, int* train_ctas_per_sm, int* eval_ctas_per_sm,
+                 int64_t* smem_bytes_per_cta);
+int tlb_synchronize(tlb_ctx* ctx);
+
+/* ---- host-side helpers of the reference API --------------------------------------------------- */
+/* net::init_params (network.cpp:56-79). */
+int tlb_init_params(uint64_t seed, float* params_out /* TLB_NPARAM */);
+/* synth::make_digits / make_set (synth.cpp:117-161): n 28x28 glyph images + labels. */
+int tlb_synth_make_digits(int64_t n, uint64_t seed, uint8_t* pixels_out, int32_t* labels_out);
+int tlb_synth_make_set(int64_t n, uint64_t seed, float* images_out, int32_t* labels_out);
+/* mnist::make_set invariants (mnist.cpp:126-154): pixels in [0,1], labels in 0..9 (ValueError). */
+int tlb_validate_set(const float* images, const int32_t* labels, int64_t n);
+
+/* ---- network, host buffers (replaces tloom::net, network.hpp:59-86) --------------------------- */
+/* net::train (network.cpp:209-251): params updated in place; epoch_loss[epochs] = mean losses.
+ * Errors as the reference: n==0, epochs<0, !(rate>0) -> TLB_ERR_ERROR; batch<1 -> TLB_ERR_ERROR. */
+int tlb_train(tlb_ctx* ctx, const float* images, const int32_t* labels, int64_t n, float* params,
+              float rate, int32_t epochs, int64_t batch, double* epoch_loss, tlb_epoch_cb on_epoch,
+              void* user);
+/* net::forward (network.cpp:81-95) for n images: yhat [n][10]; acts [n][TLB_NACT] (nullable). */
+int tlb_forward(tlb_ctx* ctx, const float* images, int64_t n, const float* params, float* yhat,
+                float* acts);
+/* forward + net::backward + net::loss per example: cells [n][TLB_CELL] (3898 grads + loss).
+ * Targets: dense [n][10] (nullable) else one_hot(labels). */
+int tlb_forward_backward(tlb_ctx* ctx, const float* images, const int32_t* labels,
+                         const float* targets, int64_t n, const float* params, float* cells,
+                         float* acts);
+/* net::predict / net::evaluate (network.cpp:253-280): pred [n] (nullable), correct count. */
+int tlb_evaluate(tlb_ctx* ctx, const float* images, const int32_t* labels, int64_t n,
+                 const float* params, int32_t* pred, int64_t* correct);
+/* net::sgd_step (network.cpp:171-180): out = p - rate * (g / (float)batch). */
+int tlb_sgd_step(tlb_ctx* ctx, const float* params, const float* grads, float rate, int64_t batch,
+                 float* out);
+
+/* ---- network, device-resident buffers (async on the context stream) --------------------------- */
+/* Runs epochs [epoch_begin, epoch_begin+epochs) of net::train in one persistent kernel launch.
+ * d_params: [TLB_PSTRIDE]; d_epoch_loss: indexed by absolute epoch. */
+int tlb_train_device(tlb_ctx* ctx, const float* d_images, const int32_t* d_labels, int64_t n,
+                     float* d_params, float rate, int32_t epoch_begin, int32_t epochs, int64_t batch,
+                     double* d_epoch_loss);
+/* One data-parallel shard of one SGD group: group `group` (examples [group*batch, ...) of the
+ * dataset, network.cpp:225-234) restricted to its examples [shard_lo, shard_hi).
+ * d_grad_sum[0..3897] = fixed-order sum of the shard's gradient rows; d_loss_sum[0] = fp64 sum of
+ * its per-example losses.  Feed both to an allreduce, then tlb_apply_sgd_device. */
+int tlb_train_shard_device(tlb_ctx* ctx, const float* d_images, const int32_t* d_labels, int64_t n,
+                           int64_t batch, int64_t group, int64_t shard_lo, int64_t shard_hi,
+                           const float* d_params, float* d_grad_sum, double* d_loss_sum);
+/* sgd_step on device buffers (post-allreduce): d_params -= rate * (d_grad_sum / m). */
+int tlb_apply_sgd_device(tlb_ctx* ctx, float* d_params, const float* d_grad_sum, float rate,
+                         int64_t m);
+int tlb_evaluate_device(tlb_ctx* ctx, const float* d_images, const int32_t* d_labels, int64_t n,
+                        const float* d_params, int32_t* d_pred, unsigned long long* d_correct);
+
+/* ---- generic layer ops, host buffers (replaces tloom::nn, nn.hpp:12-58) ------------------------
+ * Shapes are int64 extent arrays, rank <= 8, row-major.  Shape preconditions are checked with the
+ * reference's ShapeError messages before any data is touched. */
+int tlb_nn_conv(tlb_ctx* ctx, const float* in, const int64_t* in_shape, int in_rank, const float* k,
+                const int64_t* k_shape, int k_rank, float* out);
+int tlb_nn_mconv(tlb_ctx* ctx, const float* in, const int64_t* in_shape, int in_rank, const float* k,
+                 const int64_t* k_shape, int k_rank, const float* b, const int64_t* b_shape,
+                 int b_rank, float* out);
+int tlb_nn_sigmoid(tlb_ctx* ctx, const float* x, int64_t n, float* out);
+int tlb_nn_backsigmoid(tlb_ctx* ctx, const float* d, const float* o, int64_t n, float* out);
+int tlb_nn_avgpool(tlb_ctx* ctx, const float* in, const int64_t* shape, int rank, float* out);
+int tlb_nn_backavgpool(tlb_ctx* ctx, const float* d, const int64_t* shape, int rank, float* out);
+int tlb_nn_backweights(tlb_ctx* ctx, const float* d, const int64_t* d_shape, int d_rank,
+                       const float* in, const int64_t* in_shape, int in_rank, float* out);
+int tlb_nn_backbias(tlb_ctx* ctx, const float* d, int64_t n, float* out);
+int tlb_nn_backin(tlb_ctx* ctx, const float* d, const int64_t* d_shape, int d_rank, const float* k,
+                  const int64_t* k_shape, int k_rank, const int64_t* in_shape, int in_rank,
+                  float* out);
+/* Result-shape functions (nn.hpp:12-32); out_shape must hold 8 extents. */
+int tlb_nn_conv_shape(const int64_t* in_shape, int in_rank, const int64_t* k_shape, int k_rank,
+                      int64_t* out_shape, int* out_rank);
+int tlb_nn_mconv_shape(const int64_t* in_shape, int in_rank, const int64_t* k_shape, int k_rank,
+                       const int64_t* b_shape, int b_rank, int64_t* out_shape, int* out_rank);
+int tlb_nn_avgpool_shape(const int64_t* shape, int rank, int64_t* out_shape, int* out_rank);
+int tlb_nn_backavgpool_shape(const int64_t* shape, int rank, int64_t* out_shape, int* out_rank);
+int tlb_nn_backin_shape(const int64_t* d_shape, int d_rank, const int64_t* k_shape, int k_rank,
+                        const int64_t* in_shape, int in_rank, int64_t* out_shape, int* out_rank);
+
+/* Test hook: device glibc-expf restatement over float bit patterns [start, start+n). */
+int tlb_expf_range(tlb_ctx* ctx, uint32_t start_bits, int64_t n, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TLOOM_B200_H */

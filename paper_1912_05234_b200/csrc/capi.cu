@@ -1,0 +1,697 @@
+// capi.cu -- implementation of the C ABI declared in include/tloom_b200.h.
+//
+// Owns the per-context device workspaces and maps the reference API (tloom::nn / tloom::net,
+// proj/include/tloom/{nn,network}.hpp) onto the sm_100a kernels.  Argument checks reproduce the
+// reference's error conditions and messages (nn.cpp:37-94, network.cpp:209-214, mnist.cpp:169-170).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tlb_capi_internal.h"
+#include "tlb_launch.h"
+#include "tloom_b200.h"
+
+namespace tlb {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+}  // namespace tlb
+
+using tlb::fail;
+
+#define TLB_CUDA(expr)                                                                           \
+  do {                                                                                           \
+    const cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                       \
+      return fail(TLB_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " + \
+                                    #expr);                                                      \
+  } while (0)
+
+#define TLB_TRY(expr)           \
+  do {                          \
+    const int rc_ = (expr);     \
+    if (rc_ != TLB_OK) return rc_; \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct tlb_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  int mode = TLB_MODE_EXACT;
+  int grid_override = 0;
+  int occ_train[2] = {0, 0};
+  int occ_eval[2] = {0, 0};
+  DevBuf work, losses, barrier;    // persistent-train workspaces
+  DevBuf stage[6];                 // host-API staging buffers
+};
+
+namespace {
+
+bool exact(const tlb_ctx* c) { return c->mode == TLB_MODE_EXACT; }
+
+int set_device(tlb_ctx* c) {
+  TLB_CUDA(cudaSetDevice(c->device));
+  return TLB_OK;
+}
+
+std::string shape_str(const int64_t* s, int r) {
+  std::string out = "[";
+  for (int i = 0; i < r; ++i) {
+    if (i) out += ',';
+    out += std::to_string(s[i]);
+  }
+  return out + "]";
+}
+
+int check_rank(int r, const char* who) {
+  if (r < 0 || r > 8)
+    return fail(TLB_ERR_SHAPE, std::string(who) + ": rank " + std::to_string(r) + " exceeds maximum 8");
+  return TLB_OK;
+}
+
+int64_t count_of(const int64_t* s, int r) {
+  int64_t c = 1;
+  for (int a = 0; a < r; ++a) c *= s[a];
+  return c;
+}
+
+// conv_result_shape (nn.cpp:37-49)
+int conv_shape(const int64_t* in, int ir, const int64_t* k, int kr, int64_t* out) {
+  if (ir != kr)
+    return fail(TLB_ERR_SHAPE, "conv: input rank " + std::to_string(ir) + " and kernel rank " +
+                                   std::to_string(kr) + " differ");
+  for (int a = 0; a < ir; ++a) {
+    if (k[a] > in[a])
+      return fail(TLB_ERR_SHAPE, "conv: kernel shape " + shape_str(k, kr) + " exceeds input shape " +
+                                     shape_str(in, ir) + " on axis " + std::to_string(a));
+    out[a] = in[a] - k[a] + 1;
+  }
+  return TLB_OK;
+}
+
+// mconv_result_shape (nn.cpp:51-60)
+int mconv_shape(const int64_t* in, int ir, const int64_t* k, int kr, const int64_t* b, int br, int64_t* out,
+                int* orank) {
+  if (br != 1) return fail(TLB_ERR_SHAPE, "mconv: bias shape " + shape_str(b, br) + " is not rank 1");
+  if (kr != ir + 1)
+    return fail(TLB_ERR_SHAPE, "mconv: kernel stack rank " + std::to_string(kr) + " must be input rank + 1 = " +
+                                   std::to_string(ir + 1));
+  if (kr < 1 || k[0] != b[0])
+    return fail(TLB_ERR_SHAPE, "mconv: " + std::to_string(kr < 1 ? 0 : k[0]) + " kernels but " +
+                                   std::to_string(b[0]) + " biases");
+  if (1 + ir > 8) return fail(TLB_ERR_SHAPE, "Shape::concat: combined rank exceeds maximum");
+  out[0] = b[0];
+  TLB_TRY(conv_shape(in, ir, k + 1, kr - 1, out + 1));
+  *orank = ir + 1;
+  return TLB_OK;
+}
+
+// avgpool_result_shape (nn.cpp:62-77)
+int avgpool_shape(const int64_t* s, int r, int64_t* out) {
+  if (r < 2) return fail(TLB_ERR_SHAPE, "avgpool: rank " + std::to_string(r) + " input, need rank >= 2");
+  for (int a = 0; a < r; ++a) {
+    if (a >= r - 2) {
+      if (s[a] % 2 != 0)
+        return fail(TLB_ERR_SHAPE, "avgpool: axis " + std::to_string(a) + " extent " + std::to_string(s[a]) +
+                                       " is not even");
+      out[a] = s[a] / 2;
+    } else {
+      out[a] = s[a];
+    }
+  }
+  return TLB_OK;
+}
+
+// backavgpool_result_shape (nn.cpp:79-86)
+int backavgpool_shape(const int64_t* s, int r, int64_t* out) {
+  if (r < 2)
+    return fail(TLB_ERR_SHAPE, "backavgpool: rank " + std::to_string(r) + " input, need rank >= 2");
+  for (int a = 0; a < r; ++a) out[a] = a >= r - 2 ? s[a] * 2 : s[a];
+  return TLB_OK;
+}
+
+// backin_result_shape (nn.cpp:88-94)
+int backin_shape(const int64_t* d, int dr, const int64_t* k, int kr, const int64_t* in, int ir, int64_t* out) {
+  int64_t expected[8];
+  TLB_TRY(conv_shape(in, ir, k, kr, expected));
+  bool same = dr == ir;
+  for (int a = 0; same && a < dr; ++a) same = d[a] == expected[a];
+  if (!same)
+    return fail(TLB_ERR_SHAPE, "backin: error shape " + shape_str(d, dr) + " does not match shape(in)" +
+                                   " - shape(k) + 1 = " + shape_str(expected, ir));
+  for (int a = 0; a < ir; ++a) out[a] = in[a];
+  return TLB_OK;
+}
+
+// Staging: copy host arrays into a context staging slot.
+template <class T>
+int stage_in(tlb_ctx* c, int slot, const T* host, size_t count, T** dev) {
+  TLB_CUDA(c->stage[slot].ensure(std::max<size_t>(count, 1) * sizeof(T)));
+  *dev = static_cast<T*>(c->stage[slot].p);
+  if (count) TLB_CUDA(cudaMemcpyAsync(*dev, host, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  return TLB_OK;
+}
+
+template <class T>
+int stage_out(tlb_ctx* c, int slot, size_t count, T** dev) {
+  TLB_CUDA(c->stage[slot].ensure(std::max<size_t>(count, 1) * sizeof(T)));
+  *dev = static_cast<T*>(c->stage[slot].p);
+  return TLB_OK;
+}
+
+template <class T>
+int fetch(tlb_ctx* c, T* host, const T* dev, size_t count) {
+  if (count) TLB_CUDA(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+  TLB_CUDA(cudaStreamSynchronize(c->stream));
+  return TLB_OK;
+}
+
+int train_grid(tlb_ctx* c, int64_t m_max) {
+  const int occ = c->occ_train[exact(c) ? 1 : 0];
+  const int coop = std::max(1, occ * c->sm_count);
+  if (c->grid_override > 0) return std::min(c->grid_override, coop);
+  const int64_t want = std::max<int64_t>(c->sm_count, std::min<int64_t>(m_max, coop));
+  return (int)std::min<int64_t>(want, coop);
+}
+
+int plain_grid(tlb_ctx* c, int64_t n) {
+  const int occ = c->occ_eval[exact(c) ? 1 : 0];
+  const int64_t cap = (int64_t)std::max(1, occ) * c->sm_count;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(n, cap));
+}
+
+int check_train_args(int64_t n, int32_t epochs, float rate, int64_t batch) {
+  // network.cpp:211-214 then mnist::batches (mnist.cpp:170)
+  if (n == 0) return fail(TLB_ERR_ERROR, "train: empty dataset");
+  if (epochs < 0) return fail(TLB_ERR_ERROR, "train: negative epoch count");
+  if (!(rate > 0.0f)) return fail(TLB_ERR_ERROR, "train: rate must be > 0");
+  if (batch < 1) return fail(TLB_ERR_ERROR, "batches: size must be >= 1, got " + std::to_string(batch));
+  if (n < 0) return fail(TLB_ERR_ARG, "train: negative dataset size");
+  return TLB_OK;
+}
+
+// Enqueue epochs [epoch_begin, epoch_begin + epochs) on device buffers.
+int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, int64_t n, float* d_params,
+                  float rate, int32_t epoch_begin, int32_t epochs, int64_t batch, double* d_epoch_loss,
+                  int64_t shard_lo = 0, int64_t shard_hi = 0, int64_t group = -1, float* grad_out = nullptr,
+                  double* loss_out = nullptr) {
+  const int64_t spe = (n + batch - 1) / batch;
+  const int64_t m_max = std::min<int64_t>(batch, n);
+  const int64_t m_local = grad_out ? std::max<int64_t>(0, std::min(shard_hi, m_max) - shard_lo) : m_max;
+  const int grid = train_grid(c, std::max<int64_t>(m_local, 1));
+  const int64_t rows = exact(c) ? std::max<int64_t>(m_local, 1) : grid;
+  TLB_CUDA(c->work.ensure((size_t)rows * TLB_PSTRIDE * sizeof(float)));
+  TLB_CUDA(c->losses.ensure((size_t)std::max<int64_t>(m_local, 1) * sizeof(float)));
+  TLB_CUDA(c->barrier.ensure(sizeof(unsigned int)));
+  tlb::TrainArgs a{};
+  a.images = d_images;
+  a.labels = d_labels;
+  a.n = n;
+  a.batch = batch;
+  a.rate = rate;
+  a.steps_per_epoch = spe;
+  if (group >= 0) {
+    a.step_begin = group;
+    a.step_end = group + 1;
+  } else {
+    a.step_begin = (int64_t)epoch_begin * spe;
+    a.step_end = (int64_t)(epoch_begin + epochs) * spe;
+  }
+  a.params = d_params;
+  a.work = static_cast<float*>(c->work.p);
+  a.losses = static_cast<float*>(c->losses.p);
+  a.epoch_loss = d_epoch_loss;
+  a.barrier = static_cast<unsigned int*>(c->barrier.p);
+  a.shard_lo = shard_lo;
+  a.shard_hi = shard_hi;
+  a.grad_out = grad_out;
+  a.loss_out = loss_out;
+  if (a.step_end <= a.step_begin) return TLB_OK;
+  TLB_CUDA(tlb::launch_train(exact(c), a, grid, c->stream));
+  return TLB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tlb_last_error(void) { return tlb::g_last_error.c_str(); }
+
+const char* tlb_version(void) { return "tloom-b200 0.1 (sm_100a)"; }
+
+int tlb_ctx_create(int device, tlb_ctx** out) {
+  if (!out) return fail(TLB_ERR_ARG, "tlb_ctx_create: null output");
+  *out = nullptr;
+  int count = 0;
+  TLB_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count)
+    return fail(TLB_ERR_ARG, "tlb_ctx_create: device " + std::to_string(device) + " out of range (" +
+                                 std::to_string(count) + " devices)");
+  TLB_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  TLB_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(TLB_ERR_CUDA, std::string("tlb_ctx_create: device is ") + prop.name + " (sm_" +
+                                  std::to_string(prop.major) + std::to_string(prop.minor) +
+                                  "); this build targets sm_100a (B200)");
+  tlb_ctx* c = new tlb_ctx();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = tlb::train_occupancy(false, &c->occ_train[0]);
+  if (e == cudaSuccess) e = tlb::train_occupancy(true, &c->occ_train[1]);
+  if (e == cudaSuccess) e = tlb::eval_occupancy(false, &c->occ_eval[0]);
+  if (e == cudaSuccess) e = tlb::eval_occupancy(true, &c->occ_eval[1]);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(TLB_ERR_CUDA, std::string("tlb_ctx_create: ") + cudaGetErrorString(e));
+  }
+  c->stream = c->own_stream;
+  *out = c;
+  return TLB_OK;
+}
+
+int tlb_ctx_destroy(tlb_ctx* c) {
+  if (!c) return TLB_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->work.release();
+  c->losses.release();
+  c->barrier.release();
+  for (auto& s : c->stage) s.release();
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+  return TLB_OK;
+}
+
+int tlb_ctx_set_stream(tlb_ctx* c, void* stream) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+  return TLB_OK;
+}
+
+int tlb_ctx_set_mode(tlb_ctx* c, int mode) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  if (mode != TLB_MODE_EXACT && mode != TLB_MODE_FAST)
+    return fail(TLB_ERR_ARG, "tlb_ctx_set_mode: unknown mode " + std::to_string(mode));
+  c->mode = mode;
+  return TLB_OK;
+}
+
+int tlb_ctx_get_mode(const tlb_ctx* c, int* mode) {
+  if (!c || !mode) return fail(TLB_ERR_ARG, "null argument");
+  *mode = c->mode;
+  return TLB_OK;
+}
+
+int tlb_ctx_set_grid(tlb_ctx* c, int ctas) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  c->grid_override = std::max(0, ctas);
+  return TLB_OK;
+}
+
+int tlb_ctx_info(const tlb_ctx* c, int* sm, int* occ_train, int* occ_eval, int64_t* smem) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  const int x = c->mode == TLB_MODE_EXACT ? 1 : 0;
+  if (sm) *sm = c->sm_count;
+  if (occ_train) *occ_train = c->occ_train[x];
+  if (occ_eval) *occ_eval = c->occ_eval[x];
+  if (smem) *smem = (int64_t)tlb::smem_bytes();
+  return TLB_OK;
+}
+
+int tlb_synchronize(tlb_ctx* c) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  TLB_CUDA(cudaStreamSynchronize(c->stream));
+  return TLB_OK;
+}
+
+// ---- network, host buffers ------------------------------------------------------------------
+int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n, float* params, float rate,
+              int32_t epochs, int64_t batch, double* epoch_loss, tlb_epoch_cb on_epoch, void* user) {
+  if (!c || !params) return fail(TLB_ERR_ARG, "tlb_train: null argument");
+  TLB_TRY(check_train_args(n, epochs, rate, batch));
+  if (!images || !labels) return fail(TLB_ERR_ARG, "tlb_train: null dataset");
+  for (int64_t i = 0; i < n; ++i)  // mnist::one_hot (mnist.cpp:161-167) of every label
+    if (labels[i] < 0 || labels[i] > 9)
+      return fail(TLB_ERR_VALUE, "one_hot: label " + std::to_string(labels[i]) + " out of range 0..9");
+  TLB_TRY(set_device(c));
+  if (epochs == 0) return TLB_OK;
+  float* d_img;
+  int32_t* d_lab;
+  float* d_p;
+  double* d_loss;
+  TLB_TRY(stage_in(c, 0, images, (size_t)n * 784, &d_img));
+  TLB_TRY(stage_in(c, 1, labels, (size_t)n, &d_lab));
+  TLB_TRY(stage_out(c, 2, TLB_PSTRIDE, &d_p));
+  TLB_CUDA(cudaMemsetAsync(d_p, 0, TLB_PSTRIDE * sizeof(float), c->stream));
+  TLB_CUDA(cudaMemcpyAsync(d_p, params, TLB_NPARAM * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  TLB_TRY(stage_out(c, 3, (size_t)epochs, &d_loss));
+  if (!on_epoch) {
+    TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, 0, epochs, batch, d_loss));
+  } else {
+    for (int32_t e = 0; e < epochs; ++e) {
+      TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, e, 1, batch, d_loss));
+      double mean = 0.0;
+      TLB_TRY(fetch(c, &mean, d_loss + e, 1));
+      on_epoch(e + 1, mean, user);
+    }
+  }
+  TLB_CUDA(cudaMemcpyAsync(params, d_p, TLB_NPARAM * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  if (epoch_loss) TLB_CUDA(cudaMemcpyAsync(epoch_loss, d_loss, epochs * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  TLB_CUDA(cudaStreamSynchronize(c->stream));
+  return TLB_OK;
+}
+
+static int run_cells(tlb_ctx* c, const float* images, const int32_t* labels, const float* targets, int64_t n,
+                     const float* params, float* cells, float* acts, float* yhat) {
+  if (!c || !params || (n > 0 && !images)) return fail(TLB_ERR_ARG, "null argument");
+  if (n < 0) return fail(TLB_ERR_ARG, "negative count");
+  if (n == 0) return TLB_OK;
+  TLB_TRY(set_device(c));
+  float *d_img, *d_p, *d_cells = nullptr, *d_acts = nullptr, *d_yhat = nullptr, *d_tg = nullptr;
+  int32_t* d_lab = nullptr;
+  TLB_TRY(stage_in(c, 0, images, (size_t)n * 784, &d_img));
+  TLB_TRY(stage_out(c, 2, TLB_PSTRIDE, &d_p));
+  TLB_CUDA(cudaMemsetAsync(d_p, 0, TLB_PSTRIDE * sizeof(float), c->stream));
+  TLB_CUDA(cudaMemcpyAsync(d_p, params, TLB_NPARAM * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  if (targets) TLB_TRY(stage_in(c, 1, targets, (size_t)n * 10, &d_tg));
+  else if (labels) TLB_TRY(stage_in(c, 1, labels, (size_t)n, &d_lab));
+  // slot 3: cells rows [n][3904] (loss rides in column 3898); slot 4: acts; slot 5: yhat
+  if (cells) TLB_TRY(stage_out(c, 3, (size_t)n * TLB_PSTRIDE, &d_cells));
+  if (acts) TLB_TRY(stage_out(c, 4, (size_t)n * TLB_NACT, &d_acts));
+  if (yhat || cells) TLB_TRY(stage_out(c, 5, (size_t)n * 11, &d_yhat));
+  tlb::CellArgs a{};
+  a.images = d_img;
+  a.labels = d_lab;
+  a.targets = d_tg;
+  a.n = n;
+  a.params = d_p;
+  a.cells = d_cells;
+  a.losses = d_yhat ? d_yhat + n * 10 : nullptr;
+  a.acts = d_acts;
+  a.yhat = d_yhat;
+  TLB_CUDA(tlb::launch_cells(exact(c), a, plain_grid(c, n), c->stream));
+  if (cells) {
+    // rows of 3904 -> host cells of 3899 (3898 grads + loss)
+    TLB_CUDA(cudaMemcpy2DAsync(cells, TLB_CELL * sizeof(float), d_cells, TLB_PSTRIDE * sizeof(float),
+                               TLB_NPARAM * sizeof(float), (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+    TLB_CUDA(cudaMemcpy2DAsync(cells + TLB_NPARAM, TLB_CELL * sizeof(float), d_yhat + n * 10, sizeof(float),
+                               sizeof(float), (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (acts) TLB_CUDA(cudaMemcpyAsync(acts, d_acts, (size_t)n * TLB_NACT * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  if (yhat) TLB_CUDA(cudaMemcpyAsync(yhat, d_yhat, (size_t)n * 10 * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  TLB_CUDA(cudaStreamSynchronize(c->stream));
+  return TLB_OK;
+}
+
+int tlb_forward(tlb_ctx* c, const float* images, int64_t n, const float* params, float* yhat, float* acts) {
+  return run_cells(c, images, nullptr, nullptr, n, params, nullptr, acts, yhat);
+}
+
+int tlb_forward_backward(tlb_ctx* c, const float* images, const int32_t* labels, const float* targets, int64_t n,
+                         const float* params, float* cells, float* acts) {
+  if (!targets && !labels) return fail(TLB_ERR_ARG, "tlb_forward_backward: need labels or targets");
+  if (!cells) return fail(TLB_ERR_ARG, "tlb_forward_backward: null cells");
+  if (!targets)
+    for (int64_t i = 0; i < n; ++i)
+      if (labels[i] < 0 || labels[i] > 9)
+        return fail(TLB_ERR_VALUE, "one_hot: label " + std::to_string(labels[i]) + " out of range 0..9");
+  return run_cells(c, images, labels, targets, n, params, cells, acts, nullptr);
+}
+
+int tlb_evaluate(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n, const float* params,
+                 int32_t* pred, int64_t* correct) {
+  if (!c || !params) return fail(TLB_ERR_ARG, "tlb_evaluate: null argument");
+  if (n == 0) return fail(TLB_ERR_ERROR, "evaluate: empty dataset");
+  if (n < 0 || !images) return fail(TLB_ERR_ARG, "tlb_evaluate: bad dataset");
+  TLB_TRY(set_device(c));
+  float *d_img, *d_p;
+  int32_t *d_lab = nullptr, *d_pred = nullptr;
+  unsigned long long* d_cnt;
+  TLB_TRY(stage_in(c, 0, images, (size_t)n * 784, &d_img));
+  if (labels) TLB_TRY(stage_in(c, 1, labels, (size_t)n, &d_lab));
+  TLB_TRY(stage_out(c, 2, TLB_PSTRIDE, &d_p));
+  TLB_CUDA(cudaMemsetAsync(d_p, 0, TLB_PSTRIDE * sizeof(float), c->stream));
+  TLB_CUDA(cudaMemcpyAsync(d_p, params, TLB_NPARAM * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  if (pred) TLB_TRY(stage_out(c, 3, (size_t)n, &d_pred));
+  TLB_TRY(stage_out(c, 4, 1, &d_cnt));
+  TLB_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), c->stream));
+  TLB_TRY(tlb_evaluate_device(c, d_img, d_lab, n, d_p, d_pred, d_cnt));
+  if (pred) TLB_CUDA(cudaMemcpyAsync(pred, d_pred, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long cnt = 0;
+  TLB_TRY(fetch(c, &cnt, d_cnt, 1));
+  if (correct) *correct = (int64_t)cnt;
+  return TLB_OK;
+}
+
+int tlb_sgd_step(tlb_ctx* c, const float* params, const float* grads, float rate, int64_t batch, float* out) {
+  if (!c || !params || !grads || !out) return fail(TLB_ERR_ARG, "tlb_sgd_step: null argument");
+  if (batch < 1) return fail(TLB_ERR_ERROR, "sgd_step: batch must be >= 1");
+  TLB_TRY(set_device(c));
+  float *d_p, *d_g, *d_o;
+  TLB_TRY(stage_in(c, 0, params, TLB_NPARAM, &d_p));
+  TLB_TRY(stage_in(c, 1, grads, TLB_NPARAM, &d_g));
+  TLB_TRY(stage_out(c, 2, TLB_NPARAM, &d_o));
+  TLB_CUDA(tlb::launch_sgd(d_p, d_g, rate, batch, d_o, TLB_NPARAM, c->stream));
+  return fetch(c, out, d_o, TLB_NPARAM);
+}
+
+// ---- network, device buffers ----------------------------------------------------------------
+int tlb_train_device(tlb_ctx* c, const float* d_images, const int32_t* d_labels, int64_t n, float* d_params,
+                     float rate, int32_t epoch_begin, int32_t epochs, int64_t batch, double* d_epoch_loss) {
+  if (!c || !d_params || !d_epoch_loss) return fail(TLB_ERR_ARG, "tlb_train_device: null argument");
+  TLB_TRY(check_train_args(n, epochs, rate, batch));
+  if (epoch_begin < 0) return fail(TLB_ERR_ARG, "tlb_train_device: negative epoch_begin");
+  TLB_TRY(set_device(c));
+  return enqueue_train(c, d_images, d_labels, n, d_params, rate, epoch_begin, epochs, batch, d_epoch_loss);
+}
+
+int tlb_train_shard_device(tlb_ctx* c, const float* d_images, const int32_t* d_labels, int64_t n, int64_t batch,
+                           int64_t group, int64_t shard_lo, int64_t shard_hi, const float* d_params,
+                           float* d_grad_sum, double* d_loss_sum) {
+  if (!c || !d_params || !d_grad_sum || !d_loss_sum) return fail(TLB_ERR_ARG, "tlb_train_shard_device: null argument");
+  TLB_TRY(check_train_args(n, 1, 1.0f, batch));
+  const int64_t spe = (n + batch - 1) / batch;
+  if (group < 0 || group >= spe) return fail(TLB_ERR_ARG, "tlb_train_shard_device: group out of range");
+  if (shard_lo < 0 || shard_hi < shard_lo) return fail(TLB_ERR_ARG, "tlb_train_shard_device: bad shard");
+  TLB_TRY(set_device(c));
+  return enqueue_train(c, d_images, d_labels, n, const_cast<float*>(d_params), 1.0f, 0, 1, batch, nullptr, shard_lo,
+                       shard_hi, group, d_grad_sum, d_loss_sum);
+}
+
+int tlb_apply_sgd_device(tlb_ctx* c, float* d_params, const float* d_grad_sum, float rate, int64_t m) {
+  if (!c || !d_params || !d_grad_sum) return fail(TLB_ERR_ARG, "tlb_apply_sgd_device: null argument");
+  if (m < 1) return fail(TLB_ERR_ERROR, "sgd_step: batch must be >= 1");
+  TLB_TRY(set_device(c));
+  TLB_CUDA(tlb::launch_sgd(d_params, d_grad_sum, rate, m, d_params, TLB_NPARAM, c->stream));
+  return TLB_OK;
+}
+
+int tlb_evaluate_device(tlb_ctx* c, const float* d_images, const int32_t* d_labels, int64_t n, const float* d_params,
+                        int32_t* d_pred, unsigned long long* d_correct) {
+  if (!c || !d_params) return fail(TLB_ERR_ARG, "tlb_evaluate_device: null argument");
+  if (n <= 0) return TLB_OK;
+  TLB_TRY(set_device(c));
+  tlb::EvalArgs a{d_images, d_labels, n, d_params, d_pred, nullptr, d_correct};
+  TLB_CUDA(tlb::launch_eval(exact(c), a, plain_grid(c, n), c->stream));
+  return TLB_OK;
+}
+
+// ---- generic ops ----------------------------------------------------------------------------
+int tlb_nn_conv_shape(const int64_t* in, int ir, const int64_t* k, int kr, int64_t* out, int* orank) {
+  TLB_TRY(check_rank(ir, "conv"));
+  TLB_TRY(check_rank(kr, "conv"));
+  TLB_TRY(conv_shape(in, ir, k, kr, out));
+  if (orank) *orank = ir;
+  return TLB_OK;
+}
+
+int tlb_nn_mconv_shape(const int64_t* in, int ir, const int64_t* k, int kr, const int64_t* b, int br, int64_t* out,
+                       int* orank) {
+  TLB_TRY(check_rank(ir, "mconv"));
+  TLB_TRY(check_rank(kr, "mconv"));
+  int r = 0;
+  TLB_TRY(mconv_shape(in, ir, k, kr, b, br, out, &r));
+  if (orank) *orank = r;
+  return TLB_OK;
+}
+
+int tlb_nn_avgpool_shape(const int64_t* s, int r, int64_t* out, int* orank) {
+  TLB_TRY(check_rank(r, "avgpool"));
+  TLB_TRY(avgpool_shape(s, r, out));
+  if (orank) *orank = r;
+  return TLB_OK;
+}
+
+int tlb_nn_backavgpool_shape(const int64_t* s, int r, int64_t* out, int* orank) {
+  TLB_TRY(check_rank(r, "backavgpool"));
+  TLB_TRY(backavgpool_shape(s, r, out));
+  if (orank) *orank = r;
+  return TLB_OK;
+}
+
+int tlb_nn_backin_shape(const int64_t* d, int dr, const int64_t* k, int kr, const int64_t* in, int ir, int64_t* out,
+                        int* orank) {
+  TLB_TRY(check_rank(dr, "backin"));
+  TLB_TRY(backin_shape(d, dr, k, kr, in, ir, out));
+  if (orank) *orank = ir;
+  return TLB_OK;
+}
+
+static int run_conv(tlb_ctx* c, const float* in, const int64_t* is, int r, const float* k, const int64_t* ks,
+                    const float* b, int64_t nk, float* out) {
+  TLB_TRY(set_device(c));
+  int64_t os[8];
+  for (int a = 0; a < r; ++a) os[a] = is[a] - ks[a] + 1;
+  const int64_t nout = count_of(os, r) * nk;
+  float *d_in, *d_k, *d_b = nullptr, *d_o;
+  TLB_TRY(stage_in(c, 0, in, (size_t)count_of(is, r), &d_in));
+  TLB_TRY(stage_in(c, 1, k, (size_t)(count_of(ks, r) * nk), &d_k));
+  if (b) TLB_TRY(stage_in(c, 2, b, (size_t)nk, &d_b));
+  TLB_TRY(stage_out(c, 3, (size_t)nout, &d_o));
+  TLB_CUDA(tlb::nn_conv(d_in, is, d_k, ks, r, d_b, nk, d_o, c->stream));
+  return fetch(c, out, d_o, (size_t)nout);
+}
+
+int tlb_nn_conv(tlb_ctx* c, const float* in, const int64_t* is, int ir, const float* k, const int64_t* ks, int kr,
+                float* out) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  int64_t os[8];
+  int orank;
+  TLB_TRY(tlb_nn_conv_shape(is, ir, ks, kr, os, &orank));
+  return run_conv(c, in, is, ir, k, ks, nullptr, 1, out);
+}
+
+int tlb_nn_mconv(tlb_ctx* c, const float* in, const int64_t* is, int ir, const float* k, const int64_t* ks, int kr,
+                 const float* b, const int64_t* bs, int br, float* out) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  int64_t os[8];
+  int orank;
+  TLB_TRY(tlb_nn_mconv_shape(is, ir, ks, kr, bs, br, os, &orank));
+  return run_conv(c, in, is, ir, k, ks + 1, b, ks[0], out);
+}
+
+int tlb_nn_sigmoid(tlb_ctx* c, const float* x, int64_t n, float* out) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  TLB_TRY(set_device(c));
+  float *d_x, *d_o;
+  TLB_TRY(stage_in(c, 0, x, (size_t)n, &d_x));
+  TLB_TRY(stage_out(c, 1, (size_t)n, &d_o));
+  TLB_CUDA(tlb::nn_sigmoid(d_x, n, d_o, c->stream));
+  return fetch(c, out, d_o, (size_t)n);
+}
+
+int tlb_nn_backsigmoid(tlb_ctx* c, const float* d, const float* o, int64_t n, float* out) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  TLB_TRY(set_device(c));
+  float *d_d, *d_op, *d_o;
+  TLB_TRY(stage_in(c, 0, d, (size_t)n, &d_d));
+  TLB_TRY(stage_in(c, 1, o, (size_t)n, &d_op));
+  TLB_TRY(stage_out(c, 2, (size_t)n, &d_o));
+  TLB_CUDA(tlb::nn_backsigmoid(d_d, d_op, n, d_o, c->stream));
+  return fetch(c, out, d_o, (size_t)n);
+}
+
+int tlb_nn_avgpool(tlb_ctx* c, const float* in, const int64_t* s, int r, float* out) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  int64_t os[8];
+  int orank;
+  TLB_TRY(tlb_nn_avgpool_shape(s, r, os, &orank));
+  TLB_TRY(set_device(c));
+  float *d_in, *d_o;
+  const int64_t nout = count_of(os, r);
+  TLB_TRY(stage_in(c, 0, in, (size_t)count_of(s, r), &d_in));
+  TLB_TRY(stage_out(c, 1, (size_t)nout, &d_o));
+  TLB_CUDA(tlb::nn_avgpool(d_in, s, r, d_o, c->stream));
+  return fetch(c, out, d_o, (size_t)nout);
+}
+
+int tlb_nn_backavgpool(tlb_ctx* c, const float* d, const int64_t* s, int r, float* out) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  int64_t os[8];
+  int orank;
+  TLB_TRY(tlb_nn_backavgpool_shape(s, r, os, &orank));
+  TLB_TRY(set_device(c));
+  float *d_d, *d_o;
+  const int64_t nout = count_of(os, r);
+  TLB_TRY(stage_in(c, 0, d, (size_t)count_of(s, r), &d_d));
+  TLB_TRY(stage_out(c, 1, (size_t)nout, &d_o));
+  TLB_CUDA(tlb::nn_backavgpool(d_d, s, r, d_o, c->stream));
+  return fetch(c, out, d_o, (size_t)nout);
+}
+
+int tlb_nn_backweights(tlb_ctx* c, const float* d, const int64_t* ds, int dr, const float* in, const int64_t* is,
+                       int ir, float* out) {
+  // backweights(d_out, in) = conv(in, d_out) (nn.cpp:160)
+  return tlb_nn_conv(c, in, is, ir, d, ds, dr, out);
+}
+
+int tlb_nn_backbias(tlb_ctx* c, const float* d, int64_t n, float* out) {
+  if (!c || !out) return fail(TLB_ERR_ARG, "null argument");
+  TLB_TRY(set_device(c));
+  float *d_d, *d_o;
+  TLB_TRY(stage_in(c, 0, d, (size_t)n, &d_d));
+  TLB_TRY(stage_out(c, 1, 1, &d_o));
+  TLB_CUDA(tlb::nn_sum_all(d_d, n, d_o, c->stream));
+  return fetch(c, out, d_o, 1);
+}
+
+int tlb_nn_backin(tlb_ctx* c, const float* d, const int64_t* ds, int dr, const float* k, const int64_t* ks, int kr,
+                  const int64_t* is, int ir, float* out) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  int64_t os[8];
+  int orank;
+  TLB_TRY(tlb_nn_backin_shape(ds, dr, ks, kr, is, ir, os, &orank));
+  TLB_TRY(set_device(c));
+  float *d_d, *d_k, *d_o;
+  const int64_t nout = count_of(is, ir);
+  TLB_TRY(stage_in(c, 0, d, (size_t)count_of(ds, dr), &d_d));
+  TLB_TRY(stage_in(c, 1, k, (size_t)count_of(ks, kr), &d_k));
+  TLB_TRY(stage_out(c, 2, (size_t)nout, &d_o));
+  TLB_CUDA(tlb::nn_backin(d_d, ds, d_k, ks, ir, d_o, c->stream));
+  return fetch(c, out, d_o, (size_t)nout);
+}
+
+int tlb_expf_range(tlb_ctx* c, uint32_t start_bits, int64_t n, float* out) {
+  if (!c || !out) return fail(TLB_ERR_ARG, "null argument");
+  TLB_TRY(set_device(c));
+  float* d_o;
+  TLB_TRY(stage_out(c, 0, (size_t)n, &d_o));
+  TLB_CUDA(tlb::nn_expf_range(start_bits, n, d_o, c->stream));
+  return fetch(c, out, d_o, (size_t)n);
+}
+
+}  // extern "C"

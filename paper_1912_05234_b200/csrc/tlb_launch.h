@@ -1,0 +1,77 @@
+// tlb_launch.h -- internal kernel argument blocks and launchers (not part of the public C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace tlb {
+
+struct TrainArgs {
+  const float* images;    // [n][784] fp32, device
+  const int32_t* labels;  // [n]
+  int64_t n;
+  int64_t batch;
+  float rate;
+  int64_t step_begin, step_end;  // absolute step range (epoch * steps_per_epoch + group)
+  int64_t steps_per_epoch;
+  float* params;        // [3904] in/out
+  float* work;          // EXACT: [min(batch,n)][3904] example rows; fast: [grid][3904] CTA partials
+  float* losses;        // [min(batch,n)] per-example loss of the current group
+  double* epoch_loss;   // [epochs] running fp64 sum -> mean (network.cpp:239, 245)
+  unsigned int* barrier;
+  // Data-parallel shard mode (grad_out != nullptr): only examples [shard_lo, shard_hi) of each
+  // group are processed and, instead of the SGD update, their fixed-order gradient sum goes to
+  // grad_out[3898] and the fp64 loss sum to loss_out[0] (for the NCCL allreduce).
+  int64_t shard_lo, shard_hi;
+  float* grad_out;
+  double* loss_out;
+};
+
+struct CellArgs {
+  const float* images;
+  const int32_t* labels;  // one-hot targets from labels (mnist::one_hot) when targets == nullptr
+  const float* targets;   // [n][10] dense targets or nullptr
+  int64_t n;
+  const float* params;
+  float* cells;   // [n][3904] gradient rows (nullptr: forward only)
+  float* losses;  // [n] or nullptr
+  float* acts;    // [n][5290] c1,s1,c2,s2,out or nullptr
+  float* yhat;    // [n][10] or nullptr
+};
+
+struct EvalArgs {
+  const float* images;
+  const int32_t* labels;  // nullable
+  int64_t n;
+  const float* params;
+  int32_t* pred;   // nullable
+  float* yhat;     // nullable
+  unsigned long long* correct;  // nullable
+};
+
+size_t smem_bytes();
+int threads_per_cta();
+cudaError_t train_occupancy(bool exact, int* occ);
+cudaError_t eval_occupancy(bool exact, int* occ);
+cudaError_t launch_train(bool exact, const TrainArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_cells(bool exact, const CellArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_eval(bool exact, const EvalArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_sgd(const float* params, const float* grad, float rate, int64_t m, float* out, int n,
+                       cudaStream_t st);
+
+// Generic rank-polymorphic nn ops (nn_ops.cu).  Shapes are host arrays (rank <= 8).
+cudaError_t nn_conv(const float* in, const int64_t* is, const float* k, const int64_t* ks, int r,
+                    const float* bias, int64_t nk, float* out, cudaStream_t st);
+cudaError_t nn_sigmoid(const float* x, int64_t n, float* out, cudaStream_t st);
+cudaError_t nn_backsigmoid(const float* d, const float* o, int64_t n, float* out, cudaStream_t st);
+cudaError_t nn_avgpool(const float* in, const int64_t* s, int r, float* out, cudaStream_t st);
+cudaError_t nn_backavgpool(const float* d, const int64_t* s, int r, float* out, cudaStream_t st);
+cudaError_t nn_backin(const float* d, const int64_t* ds, const float* k, const int64_t* ks, int r, float* out,
+                      cudaStream_t st);
+cudaError_t nn_sum_all(const float* x, int64_t n, float* out, cudaStream_t st);
+cudaError_t nn_expf(const float* x, int64_t n, float* out, cudaStream_t st);
+cudaError_t nn_expf_range(uint32_t start_bits, int64_t n, float* out, cudaStream_t st);
+
+}  // namespace tlb

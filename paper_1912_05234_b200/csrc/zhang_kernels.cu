@@ -1,0 +1,290 @@
+// zhang_kernels.cu -- sm_100a kernels for the reference's hot path (net::train / forward / backward /
+// evaluate, proj/src/network.cpp:81-280) and their host-side launchers.
+//
+//  * train_kernel<EXACT>  persistent cooperative kernel: runs a whole range of SGD steps (epochs x
+//                         groups) in ONE launch.  Per step: each CTA takes a static_chunk of the
+//                         group's examples (runtime.cpp:138-145), runs forward+backward per image in
+//                         shared memory, writes its gradient rows (EXACT: one row per example, the
+//                         reference's parallel_build cell) or one per-CTA partial (fast); grid barrier;
+//                         fixed-order reduction + sgd_step over the 3,898 parameters and the fp64
+//                         epoch-loss sum (network.cpp:236-248); grid barrier.
+//  * cells_kernel<EXACT>  per-example forward(+backward) rows / activations (net::forward/backward).
+//  * eval_kernel<EXACT>   forward + argmax + correct count (net::predict / net::evaluate).
+//  * sgd_kernel           net::sgd_step on a reduced gradient (also the post-allreduce step of DP).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tlb_launch.h"
+#include "zhang_step.cuh"
+
+namespace tlb {
+
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------------------------------------------
+// Job iteration over (step, example) pairs owned by one CTA, used for the image prefetch ring.
+// ------------------------------------------------------------------------------------------------
+struct Job {
+  int64_t step, e, hi;
+};
+
+__device__ __forceinline__ int64_t group_size(const TrainArgs& a, int64_t st) {
+  const int64_t start = (st % a.steps_per_epoch) * a.batch;
+  const int64_t rem = a.n - start;
+  return rem < a.batch ? rem : a.batch;
+}
+
+// Examples of group `st` handled by this launch: the whole group, or the DP shard of it.
+__device__ __forceinline__ int64_t local_size(const TrainArgs& a, int64_t st) {
+  const int64_t m = group_size(a, st);
+  if (!a.grad_out) return m;
+  const int64_t hi = a.shard_hi < m ? a.shard_hi : m;
+  return hi > a.shard_lo ? hi - a.shard_lo : 0;
+}
+__device__ __forceinline__ int64_t local_offset(const TrainArgs& a) { return a.grad_out ? a.shard_lo : 0; }
+
+__device__ __forceinline__ bool first_job(const TrainArgs& a, int64_t from, Job& j) {
+  for (int64_t st = from; st < a.step_end; ++st) {
+    int64_t lo, hi;
+    static_chunk(local_size(a, st), gridDim.x, blockIdx.x, lo, hi);
+    if (lo < hi) {
+      j = Job{st, lo, hi};
+      return true;
+    }
+  }
+  return false;
+}
+
+__device__ __forceinline__ bool next_job(const TrainArgs& a, Job& j) {
+  if (j.e + 1 < j.hi) {
+    ++j.e;
+    return true;
+  }
+  return first_job(a, j.step + 1, j);
+}
+
+__device__ __forceinline__ const float* job_image(const TrainArgs& a, const Job& j) {
+  return a.images + ((j.step % a.steps_per_epoch) * a.batch + local_offset(a) + j.e) * kImg;
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
+  extern __shared__ __align__(128) float smem_raw[];
+  const Smem s = carve_smem(smem_raw);
+  smem_setup(s);
+  unsigned int target = 0;
+  const int G = gridDim.x;
+
+  Job pf;
+  bool pf_valid = first_job(a, a.step_begin, pf);
+  if (threadIdx.x == 0 && pf_valid) issue_image(s, 0, job_image(a, pf));
+  uint32_t consumed = 0;
+
+  for (int64_t st = a.step_begin; st < a.step_end; ++st) {
+    const int64_t ks = st % a.steps_per_epoch, start = ks * a.batch + local_offset(a);
+    const int64_t m = local_size(a, st);
+    int64_t lo, hi;
+    static_chunk(m, G, blockIdx.x, lo, hi);
+
+    // ---- phase 1: per-example forward + backward out of shared memory ----
+    load_params(s, a.params);
+    if constexpr (!EXACT)
+      for (int i = threadIdx.x; i < kPStride; i += blockDim.x) s.G[i] = 0.0f;
+    __syncthreads();
+    for (int64_t e = lo; e < hi; ++e) {
+      const int buf = consumed & 1;
+      mbar_wait(&s.bar[buf], (consumed >> 1) & 1);
+      if (pf_valid) {
+        Job nx = pf;
+        if (next_job(a, nx)) {
+          if (threadIdx.x == 0) issue_image(s, buf ^ 1, job_image(a, nx));
+          pf = nx;
+        } else {
+          pf_valid = false;
+        }
+      }
+      const int label = __ldg(a.labels + start + e);
+      forward_image<EXACT>(s, s.img + buf * kImg, label, nullptr, true);
+      if (threadIdx.x == 0) a.losses[e] = example_loss(s, label, nullptr);
+      backward_image<EXACT, !EXACT>(s, s.img + buf * kImg, EXACT ? a.work + e * kPStride : nullptr);
+      ++consumed;
+    }
+    if constexpr (!EXACT) {
+      if (lo < hi) {
+        float4* dst = reinterpret_cast<float4*>(a.work + (int64_t)blockIdx.x * kPStride);
+        const float4* src = reinterpret_cast<const float4*>(s.G);
+        for (int i = threadIdx.x; i < kPStride / 4; i += blockDim.x) __stcg(dst + i, src[i]);
+      }
+    }
+    grid_sync(a.barrier, target);
+
+    // ---- phase 2: fixed-order batch reduction + sgd_step (network.cpp:236-244) ----
+    int64_t nrows = m;
+    if constexpr (!EXACT) {
+      const int64_t block = (m + G - 1) / G;
+      nrows = (m + block - 1) / block;  // non-empty CTA partials, CTA order
+    }
+    const int64_t ep = st / a.steps_per_epoch;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= kNParam; j += G * blockDim.x) {
+      if (j < kNParam) {
+        float acc = 0.0f;
+#pragma unroll 8
+        for (int64_t r = 0; r < nrows; ++r) acc = fadd(acc, __ldcg(a.work + r * kPStride + j));
+        if (a.grad_out) {
+          a.grad_out[j] = acc;
+        } else {
+          const float w = __ldcg(a.params + j);
+          __stcg(a.params + j, fsub(w, fmul(a.rate, __fdiv_rn(acc, (float)m))));
+        }
+      } else if (a.grad_out) {
+        double l = 0.0;
+        for (int64_t e = 0; e < m; ++e) l = __dadd_rn(l, (double)__ldcg(a.losses + e));
+        a.loss_out[0] = l;
+      } else {
+        double l = ks == 0 ? 0.0 : a.epoch_loss[ep];
+        for (int64_t e = 0; e < m; ++e) l = __dadd_rn(l, (double)__ldcg(a.losses + e));
+        a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(l, (double)a.n) : l;
+      }
+    }
+    grid_sync(a.barrier, target);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Per-example forward(+backward) cells: net::forward / net::backward / net::loss for n images.
+// ------------------------------------------------------------------------------------------------
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads, 2) cells_kernel(CellArgs a) {
+  extern __shared__ __align__(128) float smem_raw[];
+  const Smem s = carve_smem(smem_raw);
+  smem_setup(s);
+  int64_t lo, hi;
+  static_chunk(a.n, gridDim.x, blockIdx.x, lo, hi);
+  load_params(s, a.params);
+  if (threadIdx.x == 0 && lo < hi) issue_image(s, 0, a.images + lo * kImg);
+  __syncthreads();
+  uint32_t k = 0;
+  for (int64_t e = lo; e < hi; ++e, ++k) {
+    const int buf = k & 1;
+    mbar_wait(&s.bar[buf], (k >> 1) & 1);
+    if (threadIdx.x == 0 && e + 1 < hi) issue_image(s, buf ^ 1, a.images + (e + 1) * kImg);
+    const float* y = a.targets ? a.targets + e * 10 : nullptr;
+    const int label = a.labels ? __ldg(a.labels + e) : -1;
+    const bool has_target = y != nullptr || a.labels != nullptr;
+    forward_image<EXACT>(s, s.img + buf * kImg, label, y, a.cells != nullptr);
+    if (a.acts) {
+      float* dst = a.acts + e * kNAct;
+      for (int i = threadIdx.x; i < kNAct; i += blockDim.x) {
+        float v;
+        if (i < kS1) v = s.c1[i];
+        else if (i < kC2) v = s.s1[i - kS1];
+        else if (i < kS2) v = s.c2[i - kC2];
+        else if (i < kOut) v = s.s2[i - kS2];
+        else v = s.out[i - kOut];
+        dst[i] = v;
+      }
+    }
+    if (threadIdx.x < 10 && a.yhat) a.yhat[e * 10 + threadIdx.x] = s.out[threadIdx.x];
+    if (threadIdx.x == 0 && a.losses && has_target) a.losses[e] = example_loss(s, label, y);
+    __syncthreads();
+    if (a.cells) {
+      backward_image<EXACT, false>(s, s.img + buf * kImg, a.cells + e * kPStride);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Forward + predict (+ correct count): net::evaluate (network.cpp:263-280).
+// ------------------------------------------------------------------------------------------------
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads, 2) eval_kernel(EvalArgs a) {
+  extern __shared__ __align__(128) float smem_raw[];
+  const Smem s = carve_smem(smem_raw);
+  smem_setup(s);
+  int64_t lo, hi;
+  static_chunk(a.n, gridDim.x, blockIdx.x, lo, hi);
+  load_params(s, a.params);
+  if (threadIdx.x == 0 && lo < hi) issue_image(s, 0, a.images + lo * kImg);
+  __syncthreads();
+  unsigned long long correct = 0;
+  uint32_t k = 0;
+  for (int64_t e = lo; e < hi; ++e, ++k) {
+    const int buf = k & 1;
+    mbar_wait(&s.bar[buf], (k >> 1) & 1);
+    if (threadIdx.x == 0 && e + 1 < hi) issue_image(s, buf ^ 1, a.images + (e + 1) * kImg);
+    forward_image<EXACT>(s, s.img + buf * kImg, -1, nullptr, false);
+    if (threadIdx.x < 10 && a.yhat) a.yhat[e * 10 + threadIdx.x] = s.out[threadIdx.x];
+    if (threadIdx.x == 0) {
+      int best = 0;  // net::predict (network.cpp:253-261): strict >, lowest index wins ties
+#pragma unroll
+      for (int i = 1; i < 10; ++i)
+        if (s.out[i] > s.out[best]) best = i;
+      if (a.pred) a.pred[e] = best;
+      if (a.labels) correct += (best == __ldg(a.labels + e));
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && a.correct && correct) atomicAdd(a.correct, correct);
+}
+
+// net::sgd_step (network.cpp:171-180): w - rate * (g / (float)m), elementwise.
+__global__ void sgd_kernel(const float* params, const float* grad, float rate, float m, float* out, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) out[j] = fsub(params[j], fmul(rate, __fdiv_rn(grad[j], m)));
+}
+
+// ------------------------------------------------------------------------------------------------
+// Host launchers
+// ------------------------------------------------------------------------------------------------
+size_t smem_bytes() { return kSmemBytes; }
+int threads_per_cta() { return kThreads; }
+
+template <class K>
+static cudaError_t prep(K kernel, int* occ) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kernel, kThreads, kSmemBytes);
+}
+
+cudaError_t train_occupancy(bool exact, int* occ) {
+  return exact ? prep(train_kernel<true>, occ) : prep(train_kernel<false>, occ);
+}
+
+cudaError_t launch_train(bool exact, const TrainArgs& a, int grid, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(a.barrier, 0, sizeof(unsigned int), st);
+  if (e != cudaSuccess) return e;
+  void* args[] = {const_cast<TrainArgs*>(&a)};
+  const void* fn = exact ? (const void*)train_kernel<true> : (const void*)train_kernel<false>;
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, kSmemBytes, st);
+}
+
+cudaError_t launch_cells(bool exact, const CellArgs& a, int grid, cudaStream_t st) {
+  int occ = 0;
+  cudaError_t e = exact ? prep(cells_kernel<true>, &occ) : prep(cells_kernel<false>, &occ);
+  if (e != cudaSuccess) return e;
+  if (exact) cells_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(a);
+  else cells_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_eval(bool exact, const EvalArgs& a, int grid, cudaStream_t st) {
+  int occ = 0;
+  cudaError_t e = exact ? prep(eval_kernel<true>, &occ) : prep(eval_kernel<false>, &occ);
+  if (e != cudaSuccess) return e;
+  if (exact) eval_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(a);
+  else eval_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t eval_occupancy(bool exact, int* occ) {
+  return exact ? prep(eval_kernel<true>, occ) : prep(eval_kernel<false>, occ);
+}
+
+cudaError_t launch_sgd(const float* params, const float* grad, float rate, int64_t m, float* out, int n,
+                       cudaStream_t st) {
+  sgd_kernel<<<(n + 255) / 256, 256, 0, st>>>(params, grad, rate, (float)m, out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace tlb
