@@ -186,7 +186,8 @@ def run_ours(args):
     B, n_per = args.batch, args.n
     n_total = n_per * world
     images, labels = synth_make_set(n_total, 1)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)  # a real stream: torch's default stream handle is 0
+    torch.cuda.set_stream(stream)
     ctx = Context(local, mode=args.mode)
     ctx.set_stream(stream.cuda_stream)
     if args.grid:

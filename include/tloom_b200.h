@@ -59,7 +59,8 @@ const char* tlb_version(void);
 /* ---- context: device, stream, mode, workspaces ------------------------------------------------ */
 int tlb_ctx_create(int device, tlb_ctx** out);
 int tlb_ctx_destroy(tlb_ctx* ctx);
-/* Use a caller-owned cudaStream_t (NULL = the context's own stream). */
+/* Enqueue on a caller-owned cudaStream_t (NULL = the legacy default stream).  A new context uses
+ * its own non-blocking stream. */
 int tlb_ctx_set_stream(tlb_ctx* ctx, void* cuda_stream);
 int tlb_ctx_set_mode(tlb_ctx* ctx, int mode);
 int tlb_ctx_get_mode(const tlb_ctx* ctx, int* mode);

@@ -318,7 +318,7 @@ int tlb_ctx_destroy(tlb_ctx* c) {
 
 int tlb_ctx_set_stream(tlb_ctx* c, void* stream) {
   if (!c) return fail(TLB_ERR_ARG, "null context");
-  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+  c->stream = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream, as in CUDA
   return TLB_OK;
 }
 

@@ -118,16 +118,37 @@ struct Box {
   int r;
 };
 
-// BackinBox::sum (nn.cpp:169-189): nested per-axis sums, innermost axis first, each from 0.0f.
-__device__ float box_sum(const Box& b, int axis, int64_t doff, int64_t koff) {
-  float acc = 0.0f;
-  if (axis == b.r - 1) {
-    for (int64_t u = 0; u < b.cnt[axis]; ++u) acc = __fadd_rn(acc, __fmul_rn(b.k[koff + u], b.d[doff - u]));
-    return acc;
+// BackinBox::sum (nn.cpp:169-189): nested per-axis sums, innermost axis first, each level starting
+// from 0.0f.  Iterative (explicit per-level accumulators) instead of device recursion.
+__device__ float box_sum(const Box& b, int64_t dbase, int64_t kbase) {
+  float acc[8];
+  int64_t u[8], doff[8], koff[8];
+  int l = 0;
+  acc[0] = 0.0f;
+  u[0] = 0;
+  doff[0] = dbase;
+  koff[0] = kbase;
+  for (;;) {
+    float done;
+    if (l == b.r - 1) {
+      float s = 0.0f;
+      for (int64_t v = 0; v < b.cnt[l]; ++v) s = __fadd_rn(s, __fmul_rn(b.k[koff[l] + v], b.d[doff[l] - v]));
+      done = s;
+    } else if (u[l] < b.cnt[l]) {
+      doff[l + 1] = doff[l] - u[l] * b.dst[l];
+      koff[l + 1] = koff[l] + u[l] * b.kst[l];
+      ++l;
+      acc[l] = 0.0f;
+      u[l] = 0;
+      continue;
+    } else {
+      done = acc[l];
+    }
+    if (l == 0) return done;
+    --l;
+    acc[l] = __fadd_rn(acc[l], done);
+    ++u[l];
   }
-  for (int64_t u = 0; u < b.cnt[axis]; ++u)
-    acc = __fadd_rn(acc, box_sum(b, axis + 1, doff - u * b.dst[axis], koff + u * b.kst[axis]));
-  return acc;
 }
 
 // backin (nn.cpp:193-217): clipped correlation of the error with the kernel.
@@ -157,7 +178,7 @@ __global__ void backin_kernel(const float* d, Shp ds, const float* k, Shp ks, Sh
       dbase += (i - off) * b.dst[a];
       kbase += off * b.kst[a];
     }
-    out[o] = box_sum(bb, 0, dbase, kbase);
+    out[o] = box_sum(bb, dbase, kbase);
   }
 }
 

@@ -68,6 +68,16 @@ __device__ __forceinline__ const float* job_image(const TrainArgs& a, const Job&
   return a.images + ((j.step % a.steps_per_epoch) * a.batch + local_offset(a) + j.e) * kImg;
 }
 
+// sgd_step (network.cpp:171-180) for one parameter, or the shard's gradient sum in DP mode.
+__device__ __forceinline__ void finish_param(const TrainArgs& a, int j, float acc, int64_t m) {
+  if (a.grad_out) {
+    a.grad_out[j] = acc;
+  } else {
+    const float w = __ldcg(a.params + j);
+    __stcg(a.params + j, fsub(w, fmul(a.rate, __fdiv_rn(acc, (float)m))));
+  }
+}
+
 template <bool EXACT>
 __global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
   extern __shared__ __align__(128) float smem_raw[];
@@ -120,29 +130,39 @@ __global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
     grid_sync(a.barrier, target);
 
     // ---- phase 2: fixed-order batch reduction + sgd_step (network.cpp:236-244) ----
-    int64_t nrows = m;
-    if constexpr (!EXACT) {
-      const int64_t block = (m + G - 1) / G;
-      nrows = (m + block - 1) / block;  // non-empty CTA partials, CTA order
-    }
     const int64_t ep = st / a.steps_per_epoch;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= kNParam; j += G * blockDim.x) {
-      if (j < kNParam) {
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gsz = G * blockDim.x;
+    if constexpr (EXACT) {
+      // the reference's order: acc = ((0 + g_0) + g_1) + ... over the group's examples
+      for (int j = gtid; j < kNParam; j += gsz) {
         float acc = 0.0f;
 #pragma unroll 8
-        for (int64_t r = 0; r < nrows; ++r) acc = fadd(acc, __ldcg(a.work + r * kPStride + j));
-        if (a.grad_out) {
-          a.grad_out[j] = acc;
-        } else {
-          const float w = __ldcg(a.params + j);
-          __stcg(a.params + j, fsub(w, fmul(a.rate, __fdiv_rn(acc, (float)m))));
-        }
-      } else if (a.grad_out) {
-        double l = 0.0;
+        for (int64_t r = 0; r < m; ++r) acc = fadd(acc, __ldcg(a.work + r * kPStride + j));
+        finish_param(a, j, acc, m);
+      }
+    } else {
+      // CTA partials in CTA order, 8 lanes per parameter + fixed shuffle tree (deterministic)
+      const int64_t block = (m + G - 1) / G;
+      const int64_t nrows = m > 0 ? (m + block - 1) / block : 0;
+      const int iters = (kNParam * 8 + gsz - 1) / gsz;
+      for (int itr = 0; itr < iters; ++itr) {
+        const int t = itr * gsz + gtid, j = t >> 3, l = t & 7;
+        float acc = 0.0f;
+        if (j < kNParam)
+          for (int64_t r = l; r < nrows; r += 8) acc += __ldcg(a.work + r * kPStride + j);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (j < kNParam && l == 0) finish_param(a, j, acc, m);
+      }
+    }
+    if (blockIdx.x == G - 1 && threadIdx.x == blockDim.x - 1) {
+      double l = 0.0;  // loss_sum += (double)cell[3898], example order (network.cpp:239-242)
+      if (a.grad_out) {
         for (int64_t e = 0; e < m; ++e) l = __dadd_rn(l, (double)__ldcg(a.losses + e));
         a.loss_out[0] = l;
       } else {
-        double l = ks == 0 ? 0.0 : a.epoch_loss[ep];
+        l = ks == 0 ? 0.0 : a.epoch_loss[ep];
         for (int64_t e = 0; e < m; ++e) l = __dadd_rn(l, (double)__ldcg(a.losses + e));
         a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(l, (double)a.n) : l;
       }

@@ -29,11 +29,13 @@ struct Smem {
   float* dz;
   float* red;
   float* G;
+  float* dzp;  // dz2 zero-padded by 4 on every side: [12][16][16]; border stays 0
   uint64_t* tab;
   uint64_t* bar;
 };
 
-constexpr int kSmemFloats = kPStride + 2 * kImg + 3456 + 864 + 768 + 192 + 16 + 16 + 1088 + kPStride;
+constexpr int kDzp = 12 * 16 * 16;
+constexpr int kSmemFloats = kPStride + 2 * kImg + 3456 + 864 + 768 + 192 + 16 + 16 + 1088 + kPStride + kDzp;
 constexpr size_t kSmemBytes = sizeof(float) * kSmemFloats + 32 * sizeof(uint64_t) + 2 * sizeof(uint64_t);
 
 __device__ __forceinline__ Smem carve_smem(float* base) {
@@ -49,14 +51,16 @@ __device__ __forceinline__ Smem carve_smem(float* base) {
   s.dz = p; p += 16;
   s.red = p; p += 1088;
   s.G = p; p += kPStride;
+  s.dzp = p; p += kDzp;
   s.tab = reinterpret_cast<uint64_t*>(p);
   s.bar = s.tab + 32;
   return s;
 }
 
-// One-time per-CTA setup: exp2 table, image mbarriers.
+// One-time per-CTA setup: exp2 table, zero padding of dz2, image mbarriers.
 __device__ __forceinline__ void smem_setup(const Smem& s) {
   if (threadIdx.x < 32) s.tab[threadIdx.x] = exp_tab_entry(threadIdx.x);
+  for (int i = threadIdx.x; i < kDzp; i += blockDim.x) s.dzp[i] = 0.0f;
   if (threadIdx.x == 0) {
     mbar_init(&s.bar[0], 1);
     mbar_init(&s.bar[1], 1);
@@ -261,29 +265,79 @@ __device__ __forceinline__ void stage_fc_back(const Smem& s, float* row) {
     for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
       for (int dx = 0; dx < 2; ++dx) {
-        const int e = (c * 8 + 2 * py + dy) * 8 + 2 * px + dx;
-        const float o = s.c2[e];
-        s.c2[e] = fmul(fmul(dc, o), fsub(1.0f, o));
+        const int y = 2 * py + dy, x = 2 * px + dx;
+        const float o = s.c2[(c * 8 + y) * 8 + x];
+        s.dzp[(c * 16 + y + 4) * 16 + x + 4] = fmul(fmul(dc, o), fsub(1.0f, o));
       }
   }
 }
 
 // C2 backward: g_k2 = conv(s1, dz2[i]) (64 taps, (y,x) row-major), g_b2 = sum_all(dz2[i]),
-// d_s1 = sum_i backin(dz2[i], k2[i], s1) with the reference's clipped nested sums, then
-// backavgpool + backsigmoid through c1 -> dz1 (in place over c1).
+// d_s1 = sum_i backin(dz2[i], k2[i], s1), then backavgpool + backsigmoid through c1 -> dz1 (in place).
+//
+// backin runs over the zero-padded dz2 (uniform 5x5 taps, register-blocked 4 outputs per thread).
+// The reference's clipped nested sums (nn.cpp:169-189: per i, row sums over u2 from 0, outer sum over
+// u1 from 0, then acc += per-i result) only ever see the padded zero products prepended or appended
+// to a row/outer sum, and x + (+-0) == x (with +0 + -0 == +0), so EXACT stays bit-identical while
+// executing 259,200 instead of 115,200 multiply-adds per image.
 template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
-  const float* dz2 = s.c2;
-  for (int it = threadIdx.x; it < 1236; it += blockDim.x) {
-    if (it < 360) {
-      const int i = it / 30, r = it - i * 30, c = r / 5, u = r - c * 5;
+  for (int it = threadIdx.x; it < 588; it += blockDim.x) {
+    if (it < 216) {
+      const int c = it / 36, r = it - c * 36, p = r / 3, qq = r - p * 3;
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll 1
+      for (int i = 0; i < 12; ++i) {
+        const float* kk = s.P + kK2 + (i * 6 + c) * 25;
+        float outer[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int u1 = 0; u1 < 5; ++u1) {
+          const float4* dp = reinterpret_cast<const float4*>(s.dzp + (i * 16 + p - u1 + 4) * 16 + 4 * qq);
+          const float4 a = dp[0], b = dp[1];
+          const float d[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+          float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+          for (int u2 = 0; u2 < 5; ++u2) {
+            const float w = kk[u1 * 5 + u2];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+              if constexpr (EXACT) rs[o] = mac<true>(rs[o], w, d[o - u2 + 4]);
+              else acc[o] = __fmaf_rn(w, d[o - u2 + 4], acc[o]);
+            }
+          }
+          if constexpr (EXACT) {
+#pragma unroll
+            for (int o = 0; o < 4; ++o) outer[o] = fadd(outer[o], rs[o]);
+          }
+        }
+        if constexpr (EXACT) {
+#pragma unroll
+          for (int o = 0; o < 4; ++o) acc[o] = fadd(acc[o], outer[o]);
+        }
+      }
+      // backavgpool (x0.25) + backsigmoid through c1 for the 2x8 block this thread owns
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy) {
+        float4* cp = reinterpret_cast<float4*>(s.c1 + (c * 24 + 2 * p + dy) * 24 + 8 * qq);
+        const float4 v0 = cp[0], v1 = cp[1];
+        float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          const float dc = fmul(acc[x >> 1], 0.25f);
+          cv[x] = fmul(fmul(dc, cv[x]), fsub(1.0f, cv[x]));
+        }
+        cp[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
+        cp[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+      }
+    } else if (it < 576) {
+      const int t = it - 216, i = t / 30, r = t - i * 30, c = r / 5, u = r - c * 5;
       float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll 2
       for (int y = 0; y < 8; ++y) {
         const float4* sp = reinterpret_cast<const float4*>(s.s1 + (c * 12 + u + y) * 12);
         const float4 a = sp[0], b = sp[1], cc = sp[2];
         const float sr[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, cc.x, cc.y, cc.z, cc.w};
-        const float4* dp = reinterpret_cast<const float4*>(dz2 + i * 64 + y * 8);
+        const float4* dp = reinterpret_cast<const float4*>(s.dzp + (i * 16 + y + 4) * 16 + 4);
         const float4 d0 = dp[0], d1 = dp[1];
         const float dr[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
 #pragma unroll
@@ -293,38 +347,17 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
       }
 #pragma unroll
       for (int v = 0; v < 5; ++v) put<ACCUM>(s, row, kK2 + ((i * 6 + c) * 5 + u) * 5 + v, acc[v]);
-    } else if (it < 372) {
-      const int i = it - 360;
-      float acc = 0.0f;
-#pragma unroll 8
-      for (int e = 0; e < 64; ++e) acc = fadd(acc, dz2[i * 64 + e]);
-      put<ACCUM>(s, row, kB2 + i, acc);
     } else {
-      const int o = it - 372, c = o / 144, rem = o - c * 144, p = rem / 12, q = rem - p * 12;
-      const int off1 = p < 8 ? 0 : p - 7, off2 = q < 8 ? 0 : q - 7;
-      const int cnt1 = min(min(8, p + 1), 5 - off1), cnt2 = min(min(8, q + 1), 5 - off2);
+      const int i = it - 576;
       float acc = 0.0f;
-#pragma unroll 1
-      for (int i = 0; i < 12; ++i) {
-        const float* kk = s.P + kK2 + (i * 6 + c) * 25 + off1 * 5 + off2;
-        const float* dd = dz2 + i * 64 + (p - off1) * 8 + (q - off2);
-        float outer = 0.0f;
-        for (int u1 = 0; u1 < cnt1; ++u1) {
-          float rsum = 0.0f;
-          for (int u2 = 0; u2 < cnt2; ++u2) rsum = mac<EXACT>(rsum, kk[u1 * 5 + u2], dd[-u1 * 8 - u2]);
-          outer = fadd(outer, rsum);
-        }
-        acc = fadd(acc, outer);
+#pragma unroll
+      for (int y = 0; y < 8; ++y) {
+        const float4* dp = reinterpret_cast<const float4*>(s.dzp + (i * 16 + y + 4) * 16 + 4);
+        const float4 d0 = dp[0], d1 = dp[1];
+        acc = fadd(fadd(fadd(fadd(acc, d0.x), d0.y), d0.z), d0.w);
+        acc = fadd(fadd(fadd(fadd(acc, d1.x), d1.y), d1.z), d1.w);
       }
-      const float dc = fmul(acc, 0.25f);
-#pragma unroll
-      for (int dy = 0; dy < 2; ++dy)
-#pragma unroll
-        for (int dx = 0; dx < 2; ++dx) {
-          const int e = (c * 24 + 2 * p + dy) * 24 + 2 * q + dx;
-          const float ov = s.c1[e];
-          s.c1[e] = fmul(fmul(dc, ov), fsub(1.0f, ov));
-        }
+      put<ACCUM>(s, row, kB2 + i, acc);
     }
   }
 }

@@ -1,0 +1,94 @@
+"""Data-parallel training across GPUs (one process per GPU, torch.distributed for the plumbing).
+
+The reference parallelises net::train over the examples of each SGD group with a static ceil-block
+split (runtime::parallel_build / static_chunk, runtime.cpp:138-191) and then reduces the per-example
+gradient cells in example order (network.cpp:236-243).  Across GPUs the same split becomes: rank r
+owns static_chunk(m, world, r) of every group, computes its shard's gradient sum on device
+(tlb_train_shard_device), one allreduce(sum) of the 3,898-float buffer crosses NVLink (NCCL), and every
+rank applies the identical sgd_step with the GLOBAL group size m (network.cpp:244).  The fp64 loss sum
+is kept per rank and reduced once per epoch.
+
+The host logic (grouping, sharding, collective, update) lives in ``train_epoch`` with a pluggable
+compute backend so it is exercised on CPU with gloo in tests/test_parallel.py.
+"""
+from __future__ import annotations
+
+from typing import Callable, Protocol
+
+import torch
+import torch.distributed as dist
+
+NPARAM, PSTRIDE = 3898, 3904
+
+
+def static_chunk(n: int, workers: int, w: int) -> tuple[int, int]:
+    """runtime::static_chunk (runtime.cpp:138-145): ceil-block split of [0, n)."""
+    if n < 0 or workers < 1 or w < 0 or w >= workers:
+        raise ValueError("static_chunk: invalid arguments")
+    block = (n + workers - 1) // workers
+    lo = min(w * block, n)
+    return lo, min(lo + block, n)
+
+
+def groups(n: int, batch: int) -> list[tuple[int, int]]:
+    """mnist::batches (mnist.cpp:169-185): consecutive groups [start, start+m) in dataset order."""
+    if batch < 1:
+        raise ValueError(f"batches: size must be >= 1, got {batch}")
+    return [(s, min(batch, n - s)) for s in range(0, n, batch)]
+
+
+class ShardBackend(Protocol):
+    def shard_grad(self, group: int, lo: int, hi: int, grad: torch.Tensor, loss: torch.Tensor) -> None:
+        """grad[:3898] = sum of the shard's gradient rows; loss[0] = fp64 sum of its losses."""
+
+    def apply(self, grad: torch.Tensor, rate: float, m: int) -> None:
+        """params -= rate * (grad / m)."""
+
+
+def train_epoch(backend: ShardBackend, n: int, batch: int, rate: float, grad: torch.Tensor,
+                loss: torch.Tensor, loss_acc: torch.Tensor, world: int, rank: int,
+                allreduce: Callable[[torch.Tensor], None]) -> None:
+    """One epoch of data-parallel net::train.  loss_acc (fp64, 1 element) accumulates this rank's
+    loss; the caller reduces it across ranks once per epoch."""
+    for g, (_, m) in enumerate(groups(n, batch)):
+        lo, hi = static_chunk(m, world, rank)
+        backend.shard_grad(g, lo, hi, grad, loss)
+        loss_acc += loss
+        allreduce(grad)
+        backend.apply(grad, rate, m)
+
+
+class DeviceBackend:
+    """Shard compute on the B200 through the C ABI (tlb_train_shard_device / tlb_apply_sgd_device)."""
+
+    def __init__(self, ctx, d_images: torch.Tensor, d_labels: torch.Tensor, n: int, batch: int,
+                 d_params: torch.Tensor):
+        self.ctx, self.x, self.y, self.n, self.batch, self.p = ctx, d_images, d_labels, n, batch, d_params
+
+    def shard_grad(self, group, lo, hi, grad, loss):
+        self.ctx.train_shard_device(self.x.data_ptr(), self.y.data_ptr(), self.n, self.batch, group, lo, hi,
+                                    self.p.data_ptr(), grad.data_ptr(), loss.data_ptr())
+
+    def apply(self, grad, rate, m):
+        self.ctx.apply_sgd_device(self.p.data_ptr(), grad.data_ptr(), rate, m)
+
+
+class DeviceShardStep:
+    """bench.py's N>1 step: weak scaling, one epoch per call, NCCL allreduce per group."""
+
+    def __init__(self, ctx, d_images, d_labels, n: int, global_batch: int, world: int, rank: int):
+        self.ctx, self.x, self.y, self.n, self.B = ctx, d_images, d_labels, n, global_batch
+        self.world, self.rank = world, rank
+        dev = d_images.device
+        self.grad = torch.zeros(PSTRIDE, device=dev)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.loss_acc = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.groups_per_epoch = len(groups(n, global_batch))
+
+    def epoch(self, d_params, rate: float, d_epoch_loss, e: int) -> None:
+        backend = DeviceBackend(self.ctx, self.x, self.y, self.n, self.B, d_params)
+        self.loss_acc.zero_()
+        train_epoch(backend, self.n, self.B, rate, self.grad, self.loss, self.loss_acc, self.world, self.rank,
+                    lambda t: dist.all_reduce(t, op=dist.ReduceOp.SUM))
+        dist.all_reduce(self.loss_acc, op=dist.ReduceOp.SUM)
+        d_epoch_loss[e : e + 1].copy_(self.loss_acc / self.n)

@@ -110,7 +110,7 @@ class Context:
         _check(self._L.tlb_ctx_set_mode(self._h, MODES[name]))
 
     def set_stream(self, cuda_stream_ptr: int) -> None:
-        _check(self._L.tlb_ctx_set_stream(self._h, C.c_void_p(cuda_stream_ptr or None)))
+        _check(self._L.tlb_ctx_set_stream(self._h, C.c_void_p(cuda_stream_ptr)))
 
     def set_grid(self, ctas: int) -> None:
         _check(self._L.tlb_ctx_set_grid(self._h, ctas))
