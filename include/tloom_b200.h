@@ -3,7 +3,7 @@
  *
  * This is the drop-in boundary for the reference's training path.  The reference
  * exposes it as the C++ headers proj/include/tloom/{nn,network,mnist}.hpp; our C++ mirror of those
- * headers (include/tloom/*.hpp, same names and exceptions) and any FFI binding (ctypes, cgo, JNI)
+ * headers (include/tloom/ *.hpp, same names and exceptions) and any FFI binding (ctypes, cgo, JNI)
  * sit on top of these entry points.  Plain pointers and sizes only; no torch or C++ types.
  *
  * Conventions
@@ -66,6 +66,9 @@ int tlb_ctx_set_mode(tlb_ctx* ctx, int mode);
 int tlb_ctx_get_mode(const tlb_ctx* ctx, int* mode);
 /* CTAs of the persistent train kernel (0 = auto); clamped to the co-resident maximum. */
 int tlb_ctx_set_grid(tlb_ctx* ctx, int ctas);
+/* Profiling hook: device buffer of [steps][16] uint64 clock64 stamps written by CTA 0 of the
+ * persistent train kernel at each stage boundary (NULL disables; see bench.py --trace). */
+int tlb_ctx_set_trace(tlb_ctx* ctx, void* d_trace);
 int tlb_ctx_info(const tlb_ctx* ctx, int* sm_count, int* train_ctas_per_sm, int* eval_ctas_per_sm,
                  int64_t* smem_bytes_per_cta);
 int tlb_synchronize(tlb_ctx* ctx);
@@ -93,6 +96,12 @@ int tlb_forward(tlb_ctx* ctx, const float* images, int64_t n, const float* param
 int tlb_forward_backward(tlb_ctx* ctx, const float* images, const int32_t* labels,
                          const float* targets, int64_t n, const float* params, float* cells,
                          float* acts);
+/* net::backward (network.cpp:145-169) from cached activations acts [n][TLB_NACT] (as returned by
+ * tlb_forward) and dense targets [n][10]: grads [n][TLB_NPARAM]. */
+int tlb_backward(tlb_ctx* ctx, const float* images, const float* acts, const float* targets, int64_t n,
+                 const float* params, float* grads);
+/* net::loss (network.cpp:97-109) for n rows: out[r] = 0.5f * sum_i (y[r][i] - yhat[r][i])^2. */
+int tlb_loss(tlb_ctx* ctx, const float* yhat, const float* y, int64_t n, float* out);
 /* net::predict / net::evaluate (network.cpp:253-280): pred [n] (nullable), correct count. */
 int tlb_evaluate(tlb_ctx* ctx, const float* images, const int32_t* labels, int64_t n,
                  const float* params, int32_t* pred, int64_t* correct);

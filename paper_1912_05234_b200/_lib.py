@@ -37,6 +37,7 @@ _SIGS = {
     "tlb_ctx_set_mode": (C.c_int, [vp, C.c_int]),
     "tlb_ctx_get_mode": (C.c_int, [vp, C.POINTER(C.c_int)]),
     "tlb_ctx_set_grid": (C.c_int, [vp, C.c_int]),
+    "tlb_ctx_set_trace": (C.c_int, [vp, vp]),
     "tlb_ctx_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), i64p]),
     "tlb_synchronize": (C.c_int, [vp]),
     "tlb_init_params": (C.c_int, [C.c_uint64, f32p]),
@@ -46,6 +47,8 @@ _SIGS = {
     "tlb_train": (C.c_int, [vp, f32p, i32p, C.c_int64, f32p, C.c_float, C.c_int32, C.c_int64, f64p, EPOCH_CB, vp]),
     "tlb_forward": (C.c_int, [vp, f32p, C.c_int64, f32p, f32p, f32p]),
     "tlb_forward_backward": (C.c_int, [vp, f32p, i32p, f32p, C.c_int64, f32p, f32p, f32p]),
+    "tlb_backward": (C.c_int, [vp, f32p, f32p, f32p, C.c_int64, f32p, f32p]),
+    "tlb_loss": (C.c_int, [vp, f32p, f32p, C.c_int64, f32p]),
     "tlb_evaluate": (C.c_int, [vp, f32p, i32p, C.c_int64, f32p, i32p, i64p]),
     "tlb_sgd_step": (C.c_int, [vp, f32p, f32p, C.c_float, C.c_int64, f32p]),
     "tlb_train_device": (C.c_int, [vp, vp, vp, C.c_int64, vp, C.c_float, C.c_int32, C.c_int32, C.c_int64, vp]),

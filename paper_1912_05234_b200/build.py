@@ -27,6 +27,12 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + os.pat
 CU_FLAGS = ARCH + COMMON + ["-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 SOURCES = ["zhang_kernels.cu", "nn_ops.cu", "capi.cu", "host_data.cpp"]
+# C++ mirror of the reference headers (include/tloom/*.hpp): plain host code, g++ -std=gnu++20
+HOST_SOURCES = ["host/tensor.cpp", "host/runtime.cpp", "host/nn.cpp", "host/network.cpp", "host/mnist.cpp",
+                "host/synth.cpp"]
+CXX = os.environ.get("CXX", "g++")
+CXX_FLAGS = ["-std=gnu++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
+             "-I" + os.path.join(CSRC, "host")]
 HEADERS = ["tlb_common.cuh", "zhang_step.cuh", "tlb_launch.h", "tlb_capi_internal.h"]
 
 
@@ -39,7 +45,17 @@ def _stale(target: str, deps: list[str]) -> bool:
 
 def _compile(src: str, force: bool) -> tuple[str, str]:
     path = os.path.join(CSRC, src)
-    obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+    obj = os.path.join(OBJ, os.path.splitext(src)[0].replace("/", "_") + ".o")
+    if src.startswith("host/"):
+        hdeps = [path, os.path.join(ROOT, "include", "tloom_b200.h"), os.path.join(CSRC, "host", "device.hpp")]
+        hdeps += [os.path.join(ROOT, "include", "tloom", h) for h in os.listdir(os.path.join(ROOT, "include", "tloom"))]
+        if not force and not _stale(obj, hdeps):
+            return obj, ""
+        cmd = [CXX] + CXX_FLAGS + ["-c", path, "-o", obj]
+        out = subprocess.run(cmd, capture_output=True, text=True)
+        if out.returncode != 0:
+            raise RuntimeError(f"g++ failed for {src}:\n{' '.join(cmd)}\n{out.stdout}\n{out.stderr}")
+        return obj, out.stderr
     deps = [path, os.path.join(ROOT, "include", "tloom_b200.h")] + [os.path.join(CSRC, h) for h in HEADERS]
     if not force and not _stale(obj, deps):
         return obj, ""
@@ -56,8 +72,8 @@ def _compile(src: str, force: bool) -> tuple[str, str]:
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
-    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        results = list(ex.map(lambda s: _compile(s, force), SOURCES))
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        results = list(ex.map(lambda s: _compile(s, force), SOURCES + HOST_SOURCES))
     objs = [r[0] for r in results]
     if verbose:
         for _, log in results:

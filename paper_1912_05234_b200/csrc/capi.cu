@@ -71,10 +71,11 @@ struct tlb_ctx {
   cudaStream_t own_stream = nullptr;
   int mode = TLB_MODE_EXACT;
   int grid_override = 0;
+  unsigned long long* trace = nullptr;  // device buffer for per-stage clock stamps (profiling)
   int occ_train[2] = {0, 0};
   int occ_eval[2] = {0, 0};
   DevBuf work, losses, barrier;    // persistent-train workspaces
-  DevBuf stage[6];                 // host-API staging buffers
+  DevBuf stage[8];                 // host-API staging buffers
 };
 
 namespace {
@@ -258,6 +259,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.shard_hi = shard_hi;
   a.grad_out = grad_out;
   a.loss_out = loss_out;
+  a.trace = c->trace;
   if (a.step_end <= a.step_begin) return TLB_OK;
   TLB_CUDA(tlb::launch_train(exact(c), a, grid, c->stream));
   return TLB_OK;
@@ -342,6 +344,12 @@ int tlb_ctx_set_grid(tlb_ctx* c, int ctas) {
   return TLB_OK;
 }
 
+int tlb_ctx_set_trace(tlb_ctx* c, void* d_trace) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  c->trace = static_cast<unsigned long long*>(d_trace);
+  return TLB_OK;
+}
+
 int tlb_ctx_info(const tlb_ctx* c, int* sm, int* occ_train, int* occ_eval, int64_t* smem) {
   if (!c) return fail(TLB_ERR_ARG, "null context");
   const int x = c->mode == TLB_MODE_EXACT ? 1 : 0;
@@ -396,7 +404,8 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
 }
 
 static int run_cells(tlb_ctx* c, const float* images, const int32_t* labels, const float* targets, int64_t n,
-                     const float* params, float* cells, float* acts, float* yhat) {
+                     const float* params, float* cells, float* acts, float* yhat, const float* acts_in = nullptr,
+                     float* grads_only = nullptr) {
   if (!c || !params || (n > 0 && !images)) return fail(TLB_ERR_ARG, "null argument");
   if (n < 0) return fail(TLB_ERR_ARG, "negative count");
   if (n == 0) return TLB_OK;
@@ -410,7 +419,9 @@ static int run_cells(tlb_ctx* c, const float* images, const int32_t* labels, con
   if (targets) TLB_TRY(stage_in(c, 1, targets, (size_t)n * 10, &d_tg));
   else if (labels) TLB_TRY(stage_in(c, 1, labels, (size_t)n, &d_lab));
   // slot 3: cells rows [n][3904] (loss rides in column 3898); slot 4: acts; slot 5: yhat
-  if (cells) TLB_TRY(stage_out(c, 3, (size_t)n * TLB_PSTRIDE, &d_cells));
+  if (cells || grads_only) TLB_TRY(stage_out(c, 3, (size_t)n * TLB_PSTRIDE, &d_cells));
+  float* d_acts_in = nullptr;
+  if (acts_in) TLB_TRY(stage_in(c, 6, acts_in, (size_t)n * TLB_NACT, &d_acts_in));
   if (acts) TLB_TRY(stage_out(c, 4, (size_t)n * TLB_NACT, &d_acts));
   if (yhat || cells) TLB_TRY(stage_out(c, 5, (size_t)n * 11, &d_yhat));
   tlb::CellArgs a{};
@@ -423,7 +434,11 @@ static int run_cells(tlb_ctx* c, const float* images, const int32_t* labels, con
   a.losses = d_yhat ? d_yhat + n * 10 : nullptr;
   a.acts = d_acts;
   a.yhat = d_yhat;
+  a.acts_in = d_acts_in;
   TLB_CUDA(tlb::launch_cells(exact(c), a, plain_grid(c, n), c->stream));
+  if (grads_only)
+    TLB_CUDA(cudaMemcpy2DAsync(grads_only, TLB_NPARAM * sizeof(float), d_cells, TLB_PSTRIDE * sizeof(float),
+                               TLB_NPARAM * sizeof(float), (size_t)n, cudaMemcpyDeviceToHost, c->stream));
   if (cells) {
     // rows of 3904 -> host cells of 3899 (3898 grads + loss)
     TLB_CUDA(cudaMemcpy2DAsync(cells, TLB_CELL * sizeof(float), d_cells, TLB_PSTRIDE * sizeof(float),
@@ -450,6 +465,24 @@ int tlb_forward_backward(tlb_ctx* c, const float* images, const int32_t* labels,
       if (labels[i] < 0 || labels[i] > 9)
         return fail(TLB_ERR_VALUE, "one_hot: label " + std::to_string(labels[i]) + " out of range 0..9");
   return run_cells(c, images, labels, targets, n, params, cells, acts, nullptr);
+}
+
+int tlb_backward(tlb_ctx* c, const float* images, const float* acts, const float* targets, int64_t n,
+                 const float* params, float* grads) {
+  if (!acts || !targets || !grads) return fail(TLB_ERR_ARG, "tlb_backward: null argument");
+  return run_cells(c, images, nullptr, targets, n, params, nullptr, nullptr, nullptr, acts, grads);
+}
+
+int tlb_loss(tlb_ctx* c, const float* yhat, const float* y, int64_t n, float* out) {
+  if (!c || !yhat || !y || !out) return fail(TLB_ERR_ARG, "tlb_loss: null argument");
+  if (n <= 0) return TLB_OK;
+  TLB_TRY(set_device(c));
+  float *d_h, *d_y, *d_o;
+  TLB_TRY(stage_in(c, 0, yhat, (size_t)n * 10, &d_h));
+  TLB_TRY(stage_in(c, 1, y, (size_t)n * 10, &d_y));
+  TLB_TRY(stage_out(c, 2, (size_t)n, &d_o));
+  TLB_CUDA(tlb::nn_loss(d_h, d_y, n, d_o, c->stream));
+  return fetch(c, out, d_o, (size_t)n);
 }
 
 int tlb_evaluate(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n, const float* params,

@@ -1,0 +1,249 @@
+// network.cpp -- tloom::net (include/tloom/network.hpp) over the C ABI.
+//
+// Parameter tensors travel as one flat fp32 buffer in write_flat order (reference network.cpp:186-193);
+// train / forward / backward / loss / sgd_step / evaluate run on the B200 (tlb_* entry points).
+// Argument checks and messages follow the reference (network.cpp:27-49, 83-85, 98-101, 211-214).
+#include "tloom/network.hpp"
+
+#include <bit>
+#include <cstring>
+#include <fstream>
+#include <iterator>
+
+#include "device.hpp"
+#include "tloom_b200.h"
+
+namespace tloom::net {
+
+namespace {
+
+const Shape kK1{6, 5, 5}, kB1{6}, kK2{12, 6, 5, 5}, kB2{12}, kFc{10, 12, 1, 4, 4}, kB{10}, kImage{28, 28};
+
+void expect(const Tensor& t, const Shape& s, const char* name) {
+  if (t.shape() != s)
+    throw ShapeError(std::string("params: ") + name + " has shape " + t.shape().str() + ", expected " + s.str());
+}
+
+std::vector<float> flat(const Params& p) {
+  std::vector<float> v;
+  v.reserve(TLB_NPARAM);
+  for (const Tensor* t : {&p.k1, &p.b1, &p.k2, &p.b2, &p.fc, &p.b}) v.insert(v.end(), t->data().begin(), t->data().end());
+  return v;
+}
+
+template <class T>
+T unflat(const float* v) {
+  const Shape* shapes[6] = {&kK1, &kB1, &kK2, &kB2, &kFc, &kB};
+  Tensor parts[6];
+  for (int i = 0; i < 6; ++i) {
+    const auto n = static_cast<std::size_t>(shapes[i]->count());
+    parts[i] = Tensor(*shapes[i], std::vector<float>(v, v + n));
+    v += n;
+  }
+  return T{parts[0], parts[1], parts[2], parts[3], parts[4], parts[5]};
+}
+
+std::vector<float> dataset_images(const mnist::MnistSet& data) {
+  const auto px = data.images.data();
+  return std::vector<float>(px.begin(), px.end());
+}
+
+std::vector<std::int32_t> dataset_labels(const mnist::MnistSet& data) {
+  return std::vector<std::int32_t>(data.labels.begin(), data.labels.end());
+}
+
+}  // namespace
+
+void Params::validate() const {
+  expect(k1, kK1, "k1");
+  expect(b1, kB1, "b1");
+  expect(k2, kK2, "k2");
+  expect(b2, kB2, "b2");
+  expect(fc, kFc, "fc");
+  expect(b, kB, "b");
+}
+
+Params Params::zeros() {
+  return Params{Tensor::zeros(kK1), Tensor::zeros(kB1), Tensor::zeros(kK2),
+                Tensor::zeros(kB2), Tensor::zeros(kFc), Tensor::zeros(kB)};
+}
+
+Params init_params(std::uint64_t seed) {
+  std::vector<float> v(TLB_NPARAM);
+  detail::check(tlb_init_params(seed, v.data()));
+  return unflat<Params>(v.data());
+}
+
+std::pair<Tensor, ActCache> forward(const Tensor& image, const Params& p) {
+  p.validate();
+  if (image.shape() != kImage)
+    throw ShapeError("forward: image has shape " + image.shape().str() + ", expected " + kImage.str());
+  const std::vector<float> w = flat(p);
+  std::vector<float> yhat(10), act(TLB_NACT);
+  {
+    auto dev = detail::device();
+    detail::check(tlb_forward(dev.ctx, image.data().data(), 1, w.data(), yhat.data(), act.data()));
+  }
+  ActCache c;
+  c.input = image;
+  const float* a = act.data();
+  c.c1 = Tensor(Shape{6, 24, 24}, std::vector<float>(a, a + 3456));
+  c.s1 = Tensor(Shape{6, 12, 12}, std::vector<float>(a + 3456, a + 4320));
+  c.c2 = Tensor(Shape{12, 1, 8, 8}, std::vector<float>(a + 4320, a + 5088));
+  c.s2 = Tensor(Shape{12, 1, 4, 4}, std::vector<float>(a + 5088, a + 5280));
+  c.out = Tensor(Shape{10, 1, 1, 1, 1}, std::vector<float>(a + 5280, a + 5290));
+  return {c.out.reshape(Shape{10}), c};
+}
+
+float loss(const Tensor& yhat, const Tensor& y) {
+  if (yhat.shape() != Shape{10} || y.shape() != Shape{10})
+    throw ShapeError("loss: shapes " + yhat.shape().str() + " and " + y.shape().str() + ", expected [10] and [10]");
+  float out = 0.0f;
+  auto dev = detail::device();
+  detail::check(tlb_loss(dev.ctx, yhat.data().data(), y.data().data(), 1, &out));
+  return out;
+}
+
+Grads backward(const ActCache& cache, const Params& p, const Tensor& y) {
+  p.validate();
+  if (y.shape() != Shape{10})
+    throw ShapeError("ew_map2: shapes [10] and " + y.shape().str() + " differ");
+  std::vector<float> act;
+  act.reserve(TLB_NACT);
+  for (const Tensor* t : {&cache.c1, &cache.s1, &cache.c2, &cache.s2, &cache.out})
+    act.insert(act.end(), t->data().begin(), t->data().end());
+  if (act.size() != TLB_NACT || cache.input.count() != 784)
+    throw ShapeError("backward: activation cache does not match the network signature");
+  const std::vector<float> w = flat(p);
+  std::vector<float> g(TLB_NPARAM);
+  {
+    auto dev = detail::device();
+    detail::check(tlb_backward(dev.ctx, cache.input.data().data(), act.data(), y.data().data(), 1, w.data(), g.data()));
+  }
+  return unflat<Grads>(g.data());
+}
+
+Params sgd_step(const Params& p, const Grads& acc, float rate, std::int64_t batch) {
+  if (batch < 1) throw Error("sgd_step: batch must be >= 1");
+  const std::vector<float> w = flat(p);
+  std::vector<float> g;
+  g.reserve(TLB_NPARAM);
+  for (const Tensor* t : {&acc.k1, &acc.b1, &acc.k2, &acc.b2, &acc.fc, &acc.b}) g.insert(g.end(), t->data().begin(), t->data().end());
+  if (g.size() != TLB_NPARAM || w.size() != TLB_NPARAM) throw ShapeError("sgd_step: parameter/gradient shapes differ");
+  std::vector<float> out(TLB_NPARAM);
+  auto dev = detail::device();
+  detail::check(tlb_sgd_step(dev.ctx, w.data(), g.data(), rate, batch, out.data()));
+  return unflat<Params>(out.data());
+}
+
+namespace {
+void epoch_trampoline(int epoch, double mean, void* user) {
+  (*static_cast<const std::function<void(int, double)>*>(user))(epoch, mean);
+}
+}  // namespace
+
+TrainResult train(const Params& p, const mnist::MnistSet& data, const Hyper& h,
+                  const std::function<void(int, double)>& on_epoch) {
+  p.validate();
+  if (data.size() == 0) throw Error("train: empty dataset");
+  if (h.epochs < 0) throw Error("train: negative epoch count");
+  if (!(h.rate > 0.0f)) throw Error("train: rate must be > 0");
+  if (h.batch < 1) throw Error("batches: size must be >= 1, got " + std::to_string(h.batch));
+  std::vector<float> w = flat(p);
+  const std::vector<float> images = dataset_images(data);
+  const std::vector<std::int32_t> labels = dataset_labels(data);
+  std::vector<double> losses(static_cast<std::size_t>(h.epochs));
+  {
+    auto dev = detail::device();
+    detail::check(tlb_train(dev.ctx, images.data(), labels.data(), data.size(), w.data(), h.rate, h.epochs, h.batch,
+                            losses.data(), on_epoch ? epoch_trampoline : nullptr,
+                            const_cast<std::function<void(int, double)>*>(&on_epoch)));
+  }
+  return TrainResult{unflat<Params>(w.data()), std::move(losses)};
+}
+
+int predict(const Tensor& yhat) {
+  if (yhat.shape() != Shape{10}) throw ShapeError("predict: shape " + yhat.shape().str() + ", expected [10]");
+  const auto v = yhat.data();
+  int best = 0;
+  for (int i = 1; i < 10; ++i)
+    if (v[static_cast<std::size_t>(i)] > v[static_cast<std::size_t>(best)]) best = i;
+  return best;
+}
+
+double evaluate(const Params& p, const mnist::MnistSet& data) {
+  p.validate();
+  if (data.size() == 0) throw Error("evaluate: empty dataset");
+  const std::vector<float> w = flat(p);
+  const std::vector<float> images = dataset_images(data);
+  const std::vector<std::int32_t> labels = dataset_labels(data);
+  std::int64_t correct = 0;
+  auto dev = detail::device();
+  detail::check(tlb_evaluate(dev.ctx, images.data(), labels.data(), data.size(), w.data(), nullptr, &correct));
+  return static_cast<double>(correct) / static_cast<double>(data.size());
+}
+
+// ---- TLM1 checkpoints (reference network.cpp:282-362): little-endian rank, extents, raw f32 ----
+namespace {
+
+void put_u32(std::vector<unsigned char>& o, std::uint32_t v) {
+  for (int i = 0; i < 4; ++i) o.push_back(static_cast<unsigned char>(v >> (8 * i)));
+}
+
+std::uint32_t get_u32(const std::vector<unsigned char>& b, std::size_t& at) {
+  if (at + 4 > b.size()) throw FormatError("checkpoint: truncated at byte " + std::to_string(at));
+  std::uint32_t v = 0;
+  for (int i = 0; i < 4; ++i) v |= static_cast<std::uint32_t>(b[at + static_cast<std::size_t>(i)]) << (8 * i);
+  at += 4;
+  return v;
+}
+
+Tensor get_tensor(const std::vector<unsigned char>& b, std::size_t& at, const Shape& want, const char* name) {
+  const std::uint32_t rank = get_u32(b, at);
+  if (rank > static_cast<std::uint32_t>(Shape::kMaxRank))
+    throw FormatError("checkpoint: tensor " + std::string(name) + " has rank " + std::to_string(rank));
+  std::vector<std::int64_t> ext(rank);
+  for (auto& e : ext) e = get_u32(b, at);
+  const Shape got{std::span<const std::int64_t>(ext)};
+  if (got != want)
+    throw FormatError("checkpoint: tensor " + std::string(name) + " has shape " + got.str() + ", expected " + want.str());
+  std::vector<float> v(static_cast<std::size_t>(got.count()));
+  for (auto& x : v) x = std::bit_cast<float>(get_u32(b, at));
+  return Tensor(got, std::move(v));
+}
+
+}  // namespace
+
+void save_params(const std::filesystem::path& path, const Params& p) {
+  p.validate();
+  std::vector<unsigned char> out{'T', 'L', 'M', '1'};
+  for (const Tensor* t : {&p.k1, &p.b1, &p.k2, &p.b2, &p.fc, &p.b}) {
+    put_u32(out, static_cast<std::uint32_t>(t->shape().rank()));
+    for (int a = 0; a < t->shape().rank(); ++a) put_u32(out, static_cast<std::uint32_t>(t->shape()[a]));
+    for (const float v : t->data()) put_u32(out, std::bit_cast<std::uint32_t>(v));
+  }
+  std::ofstream f(path, std::ios::binary | std::ios::trunc);
+  if (!f) throw FormatError("cannot open checkpoint for writing: " + path.string());
+  f.write(reinterpret_cast<const char*>(out.data()), static_cast<std::streamsize>(out.size()));
+  if (!f) throw FormatError("write failure on checkpoint: " + path.string());
+}
+
+Params load_params(const std::filesystem::path& path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw FormatError("cannot open checkpoint: " + path.string());
+  const std::vector<unsigned char> b((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+  if (f.bad()) throw FormatError("read failure on checkpoint: " + path.string());
+  if (b.size() < 4 || std::memcmp(b.data(), "TLM1", 4) != 0) throw FormatError("checkpoint: bad magic, expected \"TLM1\"");
+  std::size_t at = 4;
+  Params p;
+  p.k1 = get_tensor(b, at, kK1, "k1");
+  p.b1 = get_tensor(b, at, kB1, "b1");
+  p.k2 = get_tensor(b, at, kK2, "k2");
+  p.b2 = get_tensor(b, at, kB2, "b2");
+  p.fc = get_tensor(b, at, kFc, "fc");
+  p.b = get_tensor(b, at, kB, "b");
+  if (at != b.size()) throw FormatError("checkpoint: " + std::to_string(b.size() - at) + " trailing bytes");
+  return p;
+}
+
+}  // namespace tloom::net

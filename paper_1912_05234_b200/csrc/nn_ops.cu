@@ -182,6 +182,18 @@ __global__ void backin_kernel(const float* d, Shp ds, const float* k, Shp ks, Sh
   }
 }
 
+// net::loss (network.cpp:97-109) per row: 0.5f * sum_i (y_i - yhat_i)^2, i in order.
+__global__ void loss_kernel(const float* yhat, const float* y, int64_t n, float* out) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.0f;
+    for (int i = 0; i < 10; ++i) {
+      const float d = __fsub_rn(y[r * 10 + i], yhat[r * 10 + i]);
+      acc = __fadd_rn(acc, __fmul_rn(d, d));
+    }
+    out[r] = __fmul_rn(0.5f, acc);
+  }
+}
+
 // sum_all (tensor.cpp:310-314): sequential from 0.0f (one thread; exact order).
 __global__ void sum_all_kernel(const float* x, int64_t n, float* out) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -265,6 +277,11 @@ cudaError_t nn_backin(const float* d, const int64_t* ds, const float* k, const i
   const Shp O = mk(os, r);
   const int64_t n = shp_count(O);
   if (n > 0) backin_kernel<<<blocks_for(n), 128, 0, st>>>(d, mk(ds, r), k, mk(ks, r), O, out);
+  return cudaGetLastError();
+}
+
+cudaError_t nn_loss(const float* yhat, const float* y, int64_t n, float* out, cudaStream_t st) {
+  if (n > 0) loss_kernel<<<blocks_for(n), 256, 0, st>>>(yhat, y, n, out);
   return cudaGetLastError();
 }
 

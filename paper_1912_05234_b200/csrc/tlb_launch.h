@@ -27,6 +27,7 @@ struct TrainArgs {
   int64_t shard_lo, shard_hi;
   float* grad_out;
   double* loss_out;
+  unsigned long long* trace;  // optional [steps][16] clock64 stamps of CTA 0 (tlb_ctx_set_trace)
 };
 
 struct CellArgs {
@@ -38,6 +39,7 @@ struct CellArgs {
   float* cells;   // [n][3904] gradient rows (nullptr: forward only)
   float* losses;  // [n] or nullptr
   float* acts;    // [n][5290] c1,s1,c2,s2,out or nullptr
+  const float* acts_in;  // backward from cached activations (net::backward) instead of a forward pass
   float* yhat;    // [n][10] or nullptr
 };
 
@@ -70,6 +72,7 @@ cudaError_t nn_avgpool(const float* in, const int64_t* s, int r, float* out, cud
 cudaError_t nn_backavgpool(const float* d, const int64_t* s, int r, float* out, cudaStream_t st);
 cudaError_t nn_backin(const float* d, const int64_t* ds, const float* k, const int64_t* ks, int r, float* out,
                       cudaStream_t st);
+cudaError_t nn_loss(const float* yhat, const float* y, int64_t n, float* out, cudaStream_t st);
 cudaError_t nn_sum_all(const float* x, int64_t n, float* out, cudaStream_t st);
 cudaError_t nn_expf(const float* x, int64_t n, float* out, cudaStream_t st);
 cudaError_t nn_expf_range(uint32_t start_bits, int64_t n, float* out, cudaStream_t st);

@@ -81,10 +81,11 @@ __device__ __forceinline__ void finish_param(const TrainArgs& a, int j, float ac
 template <bool EXACT>
 __global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
   extern __shared__ __align__(128) float smem_raw[];
-  const Smem s = carve_smem(smem_raw);
+  Smem s = carve_smem(smem_raw);
   smem_setup(s);
   unsigned int target = 0;
   const int G = gridDim.x;
+  unsigned long long* const trace = blockIdx.x == 0 ? a.trace : nullptr;
 
   Job pf;
   bool pf_valid = first_job(a, a.step_begin, pf);
@@ -96,15 +97,19 @@ __global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
     const int64_t m = local_size(a, st);
     int64_t lo, hi;
     static_chunk(m, G, blockIdx.x, lo, hi);
+    s.tr = trace ? trace + (st - a.step_begin) * 16 : nullptr;
+    mark(s, 0);
 
     // ---- phase 1: per-example forward + backward out of shared memory ----
     load_params(s, a.params);
     if constexpr (!EXACT)
       for (int i = threadIdx.x; i < kPStride; i += blockDim.x) s.G[i] = 0.0f;
     __syncthreads();
+    mark(s, 1);
     for (int64_t e = lo; e < hi; ++e) {
       const int buf = consumed & 1;
       mbar_wait(&s.bar[buf], (consumed >> 1) & 1);
+      mark(s, 2);
       if (pf_valid) {
         Job nx = pf;
         if (next_job(a, nx)) {
@@ -127,7 +132,9 @@ __global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
         for (int i = threadIdx.x; i < kPStride / 4; i += blockDim.x) __stcg(dst + i, src[i]);
       }
     }
+    mark(s, 10);
     grid_sync(a.barrier, target);
+    mark(s, 11);
 
     // ---- phase 2: fixed-order batch reduction + sgd_step (network.cpp:236-244) ----
     const int64_t ep = st / a.steps_per_epoch;
@@ -167,7 +174,10 @@ __global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
         a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(l, (double)a.n) : l;
       }
     }
+    __syncthreads();
+    mark(s, 12);
     grid_sync(a.barrier, target);
+    mark(s, 13);
   }
 }
 
@@ -192,7 +202,26 @@ __global__ void __launch_bounds__(kThreads, 2) cells_kernel(CellArgs a) {
     const float* y = a.targets ? a.targets + e * 10 : nullptr;
     const int label = a.labels ? __ldg(a.labels + e) : -1;
     const bool has_target = y != nullptr || a.labels != nullptr;
-    forward_image<EXACT>(s, s.img + buf * kImg, label, y, a.cells != nullptr);
+    if (a.acts_in) {
+      // net::backward(cache, p, y): activations come from the caller's ActCache (network.cpp:145-169)
+      const float* src = a.acts_in + e * kNAct;
+      for (int i = threadIdx.x; i < kNAct; i += blockDim.x) {
+        const float v = src[i];
+        if (i < kS1) s.c1[i] = v;
+        else if (i < kC2) s.s1[i - kS1] = v;
+        else if (i < kS2) s.c2[i - kC2] = v;
+        else if (i < kOut) s.s2[i - kS2] = v;
+        else s.out[i - kOut] = v;
+      }
+      __syncthreads();
+      if (threadIdx.x < 10) {
+        const float o = s.out[threadIdx.x];
+        s.dz[threadIdx.x] = fmul(fmul(fsub(o, target_of(threadIdx.x, label, y)), o), fsub(1.0f, o));
+      }
+      __syncthreads();
+    } else {
+      forward_image<EXACT>(s, s.img + buf * kImg, label, y, a.cells != nullptr);
+    }
     if (a.acts) {
       float* dst = a.acts + e * kNAct;
       for (int i = threadIdx.x; i < kNAct; i += blockDim.x) {

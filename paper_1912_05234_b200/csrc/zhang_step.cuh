@@ -32,7 +32,13 @@ struct Smem {
   float* dzp;  // dz2 zero-padded by 4 on every side: [12][16][16]; border stays 0
   uint64_t* tab;
   uint64_t* bar;
+  unsigned long long* tr;  // optional per-stage clock64 trace (CTA 0 only), nullptr otherwise
 };
+
+// Profiling hook: stamp the SM clock after a stage (thread 0 of a traced CTA).
+__device__ __forceinline__ void mark(const Smem& s, int slot) {
+  if (s.tr && threadIdx.x == 0) s.tr[slot] = clock64();
+}
 
 constexpr int kDzp = 12 * 16 * 16;
 constexpr int kSmemFloats = kPStride + 2 * kImg + 3456 + 864 + 768 + 192 + 16 + 16 + 1088 + kPStride + kDzp;
@@ -54,6 +60,7 @@ __device__ __forceinline__ Smem carve_smem(float* base) {
   s.dzp = p; p += kDzp;
   s.tab = reinterpret_cast<uint64_t*>(p);
   s.bar = s.tab + 32;
+  s.tr = nullptr;
   return s;
 }
 
@@ -461,12 +468,16 @@ __device__ __forceinline__ void forward_image(const Smem& s, const float* img, i
                                               bool want_dz) {
   stage_conv1<EXACT>(s, img);
   __syncthreads();
+  mark(s, 3);
   stage_conv2<EXACT>(s);
   __syncthreads();
+  mark(s, 4);
   stage_pool2(s);
   __syncthreads();
+  mark(s, 5);
   stage_fc<EXACT>(s, label, y, want_dz);
   __syncthreads();
+  mark(s, 6);
 }
 
 // Whole backward pass (after forward_image with want_dz).  Ends with a __syncthreads.
@@ -474,10 +485,13 @@ template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void backward_image(const Smem& s, const float* img, float* row) {
   stage_fc_back<EXACT, ACCUM>(s, row);
   __syncthreads();
+  mark(s, 7);
   stage_conv2_back<EXACT, ACCUM>(s, row);
   __syncthreads();
+  mark(s, 8);
   stage_conv1_back<EXACT, ACCUM>(s, img, row);
   __syncthreads();
+  mark(s, 9);
 }
 
 }  // namespace tlb

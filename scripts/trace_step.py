@@ -1,0 +1,55 @@
+"""Per-stage timing of the persistent train kernel from CTA 0's clock64 stamps (one traced epoch).
+
+    python scripts/trace_step.py [--mode fast|exact] [--grid G] [--batch B]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1912_05234_b200 import Context  # noqa: E402
+from paper_1912_05234_b200.runtime import init_params, synth_make_set  # noqa: E402
+
+NAMES = ["params", "img_wait", "conv1", "conv2", "pool2", "fc", "fc_back", "conv2_back", "conv1_back",
+         "partial_out", "barrier1", "reduce_sgd", "barrier2"]
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--mode", default="fast")
+ap.add_argument("--grid", type=int, default=0)
+ap.add_argument("--batch", type=int, default=100)
+ap.add_argument("--n", type=int, default=10000)
+args = ap.parse_args()
+dev = torch.device("cuda:0")
+s = torch.cuda.Stream()
+torch.cuda.set_stream(s)
+x, y = synth_make_set(args.n, 1)
+ctx = Context(0, mode=args.mode)
+ctx.set_stream(s.cuda_stream)
+if args.grid:
+    ctx.set_grid(args.grid)
+d_x, d_y = torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev)
+d_p = torch.zeros(3904, device=dev)
+d_p[:3898] = torch.from_numpy(init_params(42)).to(dev)
+loss = torch.zeros(4, dtype=torch.float64, device=dev)
+steps = (args.n + args.batch - 1) // args.batch
+ctx.train_device(d_x.data_ptr(), d_y.data_ptr(), args.n, d_p.data_ptr(), 0.05, 0, 1, args.batch, loss.data_ptr())
+tr = torch.zeros(steps * 16, dtype=torch.int64, device=dev)
+ctx.set_trace(tr.data_ptr())
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(s)
+ctx.train_device(d_x.data_ptr(), d_y.data_ptr(), args.n, d_p.data_ptr(), 0.05, 1, 1, args.batch, loss.data_ptr())
+e1.record(s)
+torch.cuda.synchronize()
+t = tr.view(steps, 16).cpu().numpy().astype(np.int64)
+d = np.diff(t[:, :14], axis=1)  # stage durations (cycles)
+med = np.median(d[1:], axis=0)
+mhz = 1965.0
+out = {"mode": args.mode, "batch": args.batch, "epoch_ms": e0.elapsed_time(e1),
+       "step_us_median": float(np.median(t[1:, 13] - t[1:, 0]) / mhz),
+       "stage_us_median": {n: round(float(v) / mhz, 3) for n, v in zip(NAMES, med)},
+       "info": ctx.info()}
+print(json.dumps(out))

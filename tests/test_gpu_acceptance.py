@@ -1,0 +1,28 @@
+"""The reference's own release gate (proj/tests/acceptance.cpp + oracles.cpp, UNMODIFIED sources) compiled
+against this repo's C++ headers (include/tloom/*.hpp) and linked to libtloom_b200.so, i.e. every
+tloom::nn / tloom::net call inside it runs on the B200.  Built here by ``make -C oracle acceptance``
+(the sources only exist in this container); the binary travels to the GPU box in oracle/_ref/."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+EXE = os.path.join(ROOT, "oracle", "_ref", "acceptance_b200")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.skipif(not os.path.exists(EXE), reason="acceptance_b200 not built (needs /root/reference at build time)")
+def test_reference_acceptance_gate_on_b200():
+    env = dict(os.environ, LD_LIBRARY_PATH=os.path.join(ROOT, "paper_1912_05234_b200", "lib"))
+    out = subprocess.run([EXE], capture_output=True, text=True, timeout=900, env=env)
+    log = out.stdout + out.stderr
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "acceptance_b200.log"), "w") as f:
+        f.write(log)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("A")]
+    assert len(lines) == 7, log
+    assert not [l for l in lines if ": FAIL" in l], log
+    assert "ACCEPTANCE: 0 hard failure(s)" in out.stdout, log
+    assert out.returncode == 0, log
