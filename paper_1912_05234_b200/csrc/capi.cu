@@ -74,7 +74,7 @@ struct tlb_ctx {
   unsigned long long* trace = nullptr;  // device buffer for per-stage clock stamps (profiling)
   int occ_train[2] = {0, 0};
   int occ_eval[2] = {0, 0};
-  DevBuf work, losses, barrier;    // persistent-train workspaces
+  DevBuf work, losses, loss_part, barrier;  // persistent-train workspaces
   DevBuf stage[8];                 // host-API staging buffers
 };
 
@@ -236,6 +236,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   TLB_CUDA(c->work.ensure((size_t)rows * TLB_PSTRIDE * sizeof(float)));
   TLB_CUDA(c->losses.ensure((size_t)std::max<int64_t>(m_local, 1) * sizeof(float)));
   TLB_CUDA(c->barrier.ensure(sizeof(unsigned int)));
+  TLB_CUDA(c->loss_part.ensure((size_t)grid * sizeof(double)));
   tlb::TrainArgs a{};
   a.images = d_images;
   a.labels = d_labels;
@@ -253,6 +254,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.params = d_params;
   a.work = static_cast<float*>(c->work.p);
   a.losses = static_cast<float*>(c->losses.p);
+  a.loss_part = static_cast<double*>(c->loss_part.p);
   a.epoch_loss = d_epoch_loss;
   a.barrier = static_cast<unsigned int*>(c->barrier.p);
   a.shard_lo = shard_lo;
@@ -311,6 +313,7 @@ int tlb_ctx_destroy(tlb_ctx* c) {
   cudaStreamSynchronize(c->stream);
   c->work.release();
   c->losses.release();
+  c->loss_part.release();
   c->barrier.release();
   for (auto& s : c->stage) s.release();
   if (c->own_stream) cudaStreamDestroy(c->own_stream);

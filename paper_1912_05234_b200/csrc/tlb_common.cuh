@@ -59,9 +59,17 @@ __device__ __forceinline__ float glibc_expf(float x, const uint64_t* tab) {
   return __double2float_rn(y);
 }
 
-// nn::sigmoid (nn.cpp:127-129): 1.0f / (1.0f + expf(-x)), IEEE add and divide.
+// nn::sigmoid (nn.cpp:127-129): 1.0f / (1.0f + expf(-x)).  1.0f / y correctly rounded is exactly
+// the IEEE reciprocal __frcp_rn(y), so the divide costs a reciprocal, not a general division.
 __device__ __forceinline__ float sigmoid_ref(float x, const uint64_t* tab) {
-  return __fdiv_rn(1.0f, __fadd_rn(1.0f, glibc_expf(-x, tab)));
+  return __frcp_rn(__fadd_rn(1.0f, glibc_expf(-x, tab)));
+}
+
+// Mode-dependent logistic: EXACT = the reference's bits; fast = ex2.approx-based exp (a few ulp).
+template <bool EXACT>
+__device__ __forceinline__ float sigmoid_m(float x, const uint64_t* tab) {
+  if constexpr (EXACT) return sigmoid_ref(x, tab);
+  else return __frcp_rn(1.0f + __expf(-x));
 }
 
 // glibc's __exp2f_data.tab (N = 32): asuint64(2^(i/32)) - (i << 47); copied to shared memory.

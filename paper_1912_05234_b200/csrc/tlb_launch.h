@@ -18,7 +18,8 @@ struct TrainArgs {
   int64_t steps_per_epoch;
   float* params;        // [3904] in/out
   float* work;          // EXACT: [min(batch,n)][3904] example rows; fast: [grid][3904] CTA partials
-  float* losses;        // [min(batch,n)] per-example loss of the current group
+  float* losses;        // EXACT: [min(batch,n)] per-example loss of the current group
+  double* loss_part;    // fast: [grid] per-CTA fp64 loss partials
   double* epoch_loss;   // [epochs] running fp64 sum -> mean (network.cpp:239, 245)
   unsigned int* barrier;
   // Data-parallel shard mode (grad_out != nullptr): only examples [shard_lo, shard_hi) of each

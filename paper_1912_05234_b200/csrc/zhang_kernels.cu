@@ -78,6 +78,73 @@ __device__ __forceinline__ void finish_param(const TrainArgs& a, int j, float ac
   }
 }
 
+// Ordered reduction of this CTA's parameter slice over `nrows` gradient rows, then sgd_step.
+template <bool EXACT>
+__device__ __forceinline__ void reduce_slice(const Smem& s, const TrainArgs& a, int64_t nrows, int64_t m) {
+  int64_t j0, j1;
+  static_chunk(kNParam, gridDim.x, blockIdx.x, j0, j1);
+  constexpr int kLanes = EXACT ? 1 : 8;  // fast: 8 lanes per parameter + fixed shuffle tree
+  float* stage = s.c1;                   // c1|s1|c2|s2 are contiguous: 5,280 free floats
+  const int t = threadIdx.x, per = blockDim.x / kLanes;
+  for (int64_t jb = j0; jb < j1; jb += per) {
+    const int W = (int)min((int64_t)per, j1 - jb);
+    const int R = 5280 / W;
+    const int j = t / kLanes, l = t % kLanes;
+    float acc = 0.0f;
+    for (int64_t r0 = 0; r0 < nrows; r0 += R) {
+      const int rr = (int)min((int64_t)R, nrows - r0);
+      __syncthreads();
+      for (int idx = t; idx < rr * W; idx += blockDim.x) {
+        const int r = idx / W, c = idx - r * W;
+        stage[idx] = __ldcg(a.work + (r0 + r) * kPStride + jb + c);
+      }
+      __syncthreads();
+      if (j < W) {
+        if constexpr (EXACT) {
+#pragma unroll 4
+          for (int r = 0; r < rr; ++r) acc = fadd(acc, stage[r * W + j]);
+        } else {
+          for (int r = l; r < rr; r += kLanes) acc += stage[r * W + j];
+        }
+      }
+    }
+    if constexpr (!EXACT) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    }
+    if (j < W && l == 0) finish_param(a, (int)jb + j, acc, m);
+  }
+}
+
+// fp64 loss sum of the group (network.cpp:239-242).  EXACT: per-example losses in example order;
+// fast: per-CTA partial sums in CTA order.  Updates the epoch mean at the group that ends the epoch.
+template <bool EXACT>
+__device__ __forceinline__ void reduce_loss(const Smem& s, const TrainArgs& a, int64_t m, int64_t nrows, int64_t ks,
+                                            int64_t ep) {
+  double l = 0.0;
+  if (!a.grad_out && ks != 0) l = a.epoch_loss[ep];
+  if constexpr (EXACT) {
+    float* stage = s.red;
+    for (int64_t e0 = 0; e0 < m; e0 += 1024) {
+      const int n = (int)min((int64_t)1024, m - e0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) stage[i] = __ldcg(a.losses + e0 + i);
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int i = 0; i < n; ++i) l = __dadd_rn(l, (double)stage[i]);
+    }
+  } else {
+    if (threadIdx.x == 0)
+      for (int64_t r = 0; r < nrows; ++r) l = __dadd_rn(l, __ldcg(a.loss_part + r));
+  }
+  if (threadIdx.x == 0) {
+    if (a.grad_out) a.loss_out[0] = l;
+    else a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(l, (double)a.n) : l;
+  }
+}
+
+
 template <bool EXACT>
 __global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
   extern __shared__ __align__(128) float smem_raw[];
@@ -106,6 +173,7 @@ __global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
       for (int i = threadIdx.x; i < kPStride; i += blockDim.x) s.G[i] = 0.0f;
     __syncthreads();
     mark(s, 1);
+    double cta_loss = 0.0;  // fast mode: this CTA's losses, example order, fp64
     for (int64_t e = lo; e < hi; ++e) {
       const int buf = consumed & 1;
       mbar_wait(&s.bar[buf], (consumed >> 1) & 1);
@@ -121,7 +189,11 @@ __global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
       }
       const int label = __ldg(a.labels + start + e);
       forward_image<EXACT>(s, s.img + buf * kImg, label, nullptr, true);
-      if (threadIdx.x == 0) a.losses[e] = example_loss(s, label, nullptr);
+      if (threadIdx.x == 0) {
+        const float l = example_loss(s, label, nullptr);
+        if constexpr (EXACT) a.losses[e] = l;
+        else cta_loss = __dadd_rn(cta_loss, (double)l);
+      }
       backward_image<EXACT, !EXACT>(s, s.img + buf * kImg, EXACT ? a.work + e * kPStride : nullptr);
       ++consumed;
     }
@@ -130,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
         float4* dst = reinterpret_cast<float4*>(a.work + (int64_t)blockIdx.x * kPStride);
         const float4* src = reinterpret_cast<const float4*>(s.G);
         for (int i = threadIdx.x; i < kPStride / 4; i += blockDim.x) __stcg(dst + i, src[i]);
+        if (threadIdx.x == 0) a.loss_part[blockIdx.x] = cta_loss;
       }
     }
     mark(s, 10);
@@ -137,43 +210,15 @@ __global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
     mark(s, 11);
 
     // ---- phase 2: fixed-order batch reduction + sgd_step (network.cpp:236-244) ----
-    const int64_t ep = st / a.steps_per_epoch;
-    const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gsz = G * blockDim.x;
-    if constexpr (EXACT) {
-      // the reference's order: acc = ((0 + g_0) + g_1) + ... over the group's examples
-      for (int j = gtid; j < kNParam; j += gsz) {
-        float acc = 0.0f;
-#pragma unroll 8
-        for (int64_t r = 0; r < m; ++r) acc = fadd(acc, __ldcg(a.work + r * kPStride + j));
-        finish_param(a, j, acc, m);
-      }
-    } else {
-      // CTA partials in CTA order, 8 lanes per parameter + fixed shuffle tree (deterministic)
+    // CTA b owns parameters static_chunk(3898, G, b); its rows are staged through shared memory
+    // (the activation buffers are free now) so the ordered sums run out of SMEM, not L2.
+    int64_t nrows = m;  // EXACT: one row per example (reference order); fast: CTA partials in CTA order
+    if constexpr (!EXACT) {
       const int64_t block = (m + G - 1) / G;
-      const int64_t nrows = m > 0 ? (m + block - 1) / block : 0;
-      const int iters = (kNParam * 8 + gsz - 1) / gsz;
-      for (int itr = 0; itr < iters; ++itr) {
-        const int t = itr * gsz + gtid, j = t >> 3, l = t & 7;
-        float acc = 0.0f;
-        if (j < kNParam)
-          for (int64_t r = l; r < nrows; r += 8) acc += __ldcg(a.work + r * kPStride + j);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (j < kNParam && l == 0) finish_param(a, j, acc, m);
-      }
+      nrows = m > 0 ? (m + block - 1) / block : 0;
     }
-    if (blockIdx.x == G - 1 && threadIdx.x == blockDim.x - 1) {
-      double l = 0.0;  // loss_sum += (double)cell[3898], example order (network.cpp:239-242)
-      if (a.grad_out) {
-        for (int64_t e = 0; e < m; ++e) l = __dadd_rn(l, (double)__ldcg(a.losses + e));
-        a.loss_out[0] = l;
-      } else {
-        l = ks == 0 ? 0.0 : a.epoch_loss[ep];
-        for (int64_t e = 0; e < m; ++e) l = __dadd_rn(l, (double)__ldcg(a.losses + e));
-        a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(l, (double)a.n) : l;
-      }
-    }
+    reduce_slice<EXACT>(s, a, nrows, m);
+    if (blockIdx.x == G - 1) reduce_loss<EXACT>(s, a, m, nrows, ks, st / a.steps_per_epoch);
     __syncthreads();
     mark(s, 12);
     grid_sync(a.barrier, target);

@@ -133,8 +133,8 @@ __device__ __forceinline__ void stage_conv1(const Smem& s, const float* img) {
     float t0[8], t1[8];
 #pragma unroll
     for (int o = 0; o < 8; ++o) {
-      t0[o] = sigmoid_ref(fadd(a0[o], b), s.tab);
-      t1[o] = sigmoid_ref(fadd(a1[o], b), s.tab);
+      t0[o] = sigmoid_m<EXACT>(fadd(a0[o], b), s.tab);
+      t1[o] = sigmoid_m<EXACT>(fadd(a1[o], b), s.tab);
     }
     float4* d0 = reinterpret_cast<float4*>(s.c1 + (i * 24 + y0) * 24 + x0);
     float4* d1 = reinterpret_cast<float4*>(s.c1 + (i * 24 + y0 + 1) * 24 + x0);
@@ -176,7 +176,7 @@ __device__ __forceinline__ void stage_conv2(const Smem& s) {
     const float b = s.P[kB2 + i];
     float t[4];
 #pragma unroll
-    for (int o = 0; o < 4; ++o) t[o] = sigmoid_ref(fadd(acc[o], b), s.tab);
+    for (int o = 0; o < 4; ++o) t[o] = sigmoid_m<EXACT>(fadd(acc[o], b), s.tab);
     *reinterpret_cast<float4*>(s.c2 + (i * 8 + y) * 8 + 4 * xh) = make_float4(t[0], t[1], t[2], t[3]);
   }
 }
@@ -204,7 +204,7 @@ __device__ __forceinline__ void stage_fc(const Smem& s, int label, const float* 
       float acc = 0.0f;
 #pragma unroll 8
       for (int j = 0; j < 192; ++j) acc = mac<true>(acc, s.s2[j], w[j]);
-      const float o = sigmoid_ref(fadd(acc, s.P[kB + i]), s.tab);
+      const float o = sigmoid_m<EXACT>(fadd(acc, s.P[kB + i]), s.tab);
       s.out[i] = o;
       if (want_dz) s.dz[i] = fmul(fmul(fsub(o, target_of(i, label, y)), o), fsub(1.0f, o));
     }
@@ -218,7 +218,7 @@ __device__ __forceinline__ void stage_fc(const Smem& s, int label, const float* 
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
       if (lane == 0) {
-        const float o = sigmoid_ref(fadd(acc, s.P[kB + i]), s.tab);
+        const float o = sigmoid_m<EXACT>(fadd(acc, s.P[kB + i]), s.tab);
         s.out[i] = o;
         if (want_dz) s.dz[i] = fmul(fmul(fsub(o, target_of(i, label, y)), o), fsub(1.0f, o));
       }

@@ -21,7 +21,7 @@ def test_reference_acceptance_gate_on_b200():
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "acceptance_b200.log"), "w") as f:
         f.write(log)
-    lines = [l for l in out.stdout.splitlines() if l.startswith("A")]
+    lines = [l for l in out.stdout.splitlines() if l[:1] == "A" and l[1:2].isdigit()]
     assert len(lines) == 7, log
     assert not [l for l in lines if ": FAIL" in l], log
     assert "ACCEPTANCE: 0 hard failure(s)" in out.stdout, log
