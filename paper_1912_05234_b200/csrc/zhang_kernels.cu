@@ -94,9 +94,23 @@ __device__ __forceinline__ void reduce_slice(const Smem& s, const TrainArgs& a, 
     for (int64_t r0 = 0; r0 < nrows; r0 += R) {
       const int rr = (int)min((int64_t)R, nrows - r0);
       __syncthreads();
-      for (int idx = t; idx < rr * W; idx += blockDim.x) {
-        const int r = idx / W, c = idx - r * W;
-        stage[idx] = __ldcg(a.work + (r0 + r) * kPStride + jb + c);
+      // all of this thread's loads in flight before any shared store (L2 latency paid once)
+      constexpr int kBatch = 8;
+      for (int base = t; base < rr * W; base += kBatch * blockDim.x) {
+        float v[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const int idx = base + u * blockDim.x;
+          if (idx < rr * W) {
+            const int r = idx / W, c = idx - r * W;
+            v[u] = __ldcg(a.work + (r0 + r) * kPStride + jb + c);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const int idx = base + u * blockDim.x;
+          if (idx < rr * W) stage[idx] = v[u];
+        }
       }
       __syncthreads();
       if (j < W) {
