@@ -20,7 +20,6 @@
 
 namespace tlb {
 
-constexpr int kThreads = 256;
 
 // ------------------------------------------------------------------------------------------------
 // Job iteration over (step, example) pairs owned by one CTA, used for the image prefetch ring.
@@ -69,12 +68,12 @@ __device__ __forceinline__ const float* job_image(const TrainArgs& a, const Job&
 }
 
 // sgd_step (network.cpp:171-180) for one parameter, or the shard's gradient sum in DP mode.
-__device__ __forceinline__ void finish_param(const TrainArgs& a, int j, float acc, int64_t m) {
+// The step's weights are still in shared memory (loaded at the step start), so no L2 read here.
+__device__ __forceinline__ void finish_param(const Smem& s, const TrainArgs& a, int j, float acc, int64_t m) {
   if (a.grad_out) {
     a.grad_out[j] = acc;
   } else {
-    const float w = __ldcg(a.params + j);
-    __stcg(a.params + j, fsub(w, fmul(a.rate, __fdiv_rn(acc, (float)m))));
+    __stcg(a.params + j, fsub(s.P[j], fmul(a.rate, __fdiv_rn(acc, (float)m))));
   }
 }
 
@@ -95,7 +94,7 @@ __device__ __forceinline__ void reduce_slice(const Smem& s, const TrainArgs& a, 
       const int rr = (int)min((int64_t)R, nrows - r0);
       __syncthreads();
       // all of this thread's loads in flight before any shared store (L2 latency paid once)
-      constexpr int kBatch = 8;
+      constexpr int kBatch = 16;
       for (int base = t; base < rr * W; base += kBatch * blockDim.x) {
         float v[kBatch];
 #pragma unroll
@@ -113,6 +112,7 @@ __device__ __forceinline__ void reduce_slice(const Smem& s, const TrainArgs& a, 
         }
       }
       __syncthreads();
+      if (r0 == 0) mark(s, 14);
       if (j < W) {
         if constexpr (EXACT) {
 #pragma unroll 4
@@ -127,7 +127,8 @@ __device__ __forceinline__ void reduce_slice(const Smem& s, const TrainArgs& a, 
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     }
-    if (j < W && l == 0) finish_param(a, (int)jb + j, acc, m);
+    if (jb == j0) mark(s, 15);
+    if (j < W && l == 0) finish_param(s, a, (int)jb + j, acc, m);
   }
 }
 
@@ -160,7 +161,7 @@ __device__ __forceinline__ void reduce_loss(const Smem& s, const TrainArgs& a, i
 
 
 template <bool EXACT>
-__global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
   extern __shared__ __align__(128) float smem_raw[];
   Smem s = carve_smem(smem_raw);
   smem_setup(s);
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 2) train_kernel(TrainArgs a) {
 // Per-example forward(+backward) cells: net::forward / net::backward / net::loss for n images.
 // ------------------------------------------------------------------------------------------------
 template <bool EXACT>
-__global__ void __launch_bounds__(kThreads, 2) cells_kernel(CellArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) cells_kernel(CellArgs a) {
   extern __shared__ __align__(128) float smem_raw[];
   const Smem s = carve_smem(smem_raw);
   smem_setup(s);
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 2) cells_kernel(CellArgs a) {
         else if (i < kOut) s.s2[i - kS2] = v;
         else s.out[i - kOut] = v;
       }
+      if constexpr (EXACT) build_shifted(s, s.img + buf * kImg, threadIdx.x, blockDim.x);
       __syncthreads();
       if (threadIdx.x < 10) {
         const float o = s.out[threadIdx.x];
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 2) cells_kernel(CellArgs a) {
 // Forward + predict (+ correct count): net::evaluate (network.cpp:263-280).
 // ------------------------------------------------------------------------------------------------
 template <bool EXACT>
-__global__ void __launch_bounds__(kThreads, 2) eval_kernel(EvalArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) eval_kernel(EvalArgs a) {
   extern __shared__ __align__(128) float smem_raw[];
   const Smem s = carve_smem(smem_raw);
   smem_setup(s);

@@ -1,35 +1,43 @@
-// zhang_step.cuh -- one CTA runs the whole Zhang-CNN training cell of one image out of shared memory.
+// zhang_step.cuh -- one 512-thread CTA runs the whole Zhang-CNN training cell of one image out of
+// shared memory.
 //
 // Reference path (proj/src/network.cpp:81-169, kernels proj/src/nn.cpp:96-217):
 //   c1 = sigmoid(mconv(I,k1,b1)); s1 = avgpool(c1); c2 = sigmoid(mconv(s1,k2,b2)); s2 = avgpool(c2);
 //   out = sigmoid(mconv(s2,fc,b)); loss = 1/2 sum (y-out)^2; hand backprop FC -> C2 -> C1.
 //
-// Every stage below maps the reference's per-output computation onto CTA threads.  With EXACT=true
-// each output is produced by ONE thread in exactly the reference's summation order with separately
-// rounded products (no FMA), the glibc expf restatement and IEEE division, so results are bitwise
-// identical to the reference (SURVEY.md §8(a) numerics contract).  With EXACT=false the same stages
-// use FFMA and split the long C1 weight-gradient sums across threads (within the 1e-4 tolerance).
+// Every stage maps the reference's per-output computation onto CTA threads.  With EXACT=true each
+// output is produced in exactly the reference's summation order with separately rounded products (no
+// FMA), the glibc expf restatement and IEEE reciprocal, so results are bitwise identical to the
+// reference (SURVEY.md §8(a) numerics contract).  Where an output's order is a nested sum (backin), the
+// independent inner sums are computed by two lanes and handed over with warp shuffles, the ordered
+// outer chain staying on one lane.  With EXACT=false the same stages use FFMA and split long sums
+// across lanes (deterministic fixed trees; within the 1e-4 tolerance).
 //
-// Shared-memory working set per CTA (floats): params 3904 | image x2 1568 | c1 3456 | s1 864 |
-// c2 768 | s2 192 | out 16 | dz 16 | red 1088 | grad accumulator 3904  (= 63 KB + tables).
+// One CTA per SM (16 warps) keeps the latency-bound batch-100 step busy; shared memory per CTA is
+// ~125 KB (layout in carve_smem).
 #pragma once
 
 #include "tlb_common.cuh"
 
 namespace tlb {
 
+constexpr int kThreads = 512;
+
 struct Smem {
-  float* P;
+  float* P;    // parameters [3904]
+  float* Kp;   // k2 re-laid out with each (i,c,ky) row of 5 padded to 8: [12][6][5][8]
   float* img;  // two image buffers of kImg floats (double-buffered TMA ring)
-  float* c1;  // c1, then dz1 in place
-  float* s1;
-  float* c2;  // c2, then dz2 in place
+  float* sh;   // image shifted by v (0..4): sh[v][y][x] = I[y][x+v], x < 24: [5][28][24]
+  float* c1;   // c1, then dz1 in place        } c1|s1|c2|s2 contiguous (5,280 floats): reused as
+  float* s1;   //                               } the staging buffer of the batch reduction
+  float* c2;
   float* s2;
   float* out;
   float* dz;
-  float* red;
-  float* G;
   float* dzp;  // dz2 zero-padded by 4 on every side: [12][16][16]; border stays 0
+  float* fcp;  // EXACT FC products [10][192]
+  float* red;  // fast C1 weight-gradient partials [432][5]
+  float* G;    // fast per-CTA gradient accumulator [3904]
   uint64_t* tab;
   uint64_t* bar;
   unsigned long long* tr;  // optional per-stage clock64 trace (CTA 0 only), nullptr otherwise
@@ -47,24 +55,31 @@ __device__ __forceinline__ void mark(const Smem& s, int slot) {
   }
 }
 
+constexpr int kKp = 12 * 6 * 5 * 8;
+constexpr int kSh = 5 * 28 * 24;
 constexpr int kDzp = 12 * 16 * 16;
-constexpr int kSmemFloats = kPStride + 2 * kImg + 3456 + 864 + 768 + 192 + 16 + 16 + 1088 + kPStride + kDzp;
+constexpr int kRed = 432 * 5;
+constexpr int kSmemFloats =
+    kPStride + kKp + 2 * kImg + kSh + 3456 + 864 + 768 + 192 + 16 + 16 + kDzp + 1920 + kRed + kPStride;
 constexpr size_t kSmemBytes = sizeof(float) * kSmemFloats + 32 * sizeof(uint64_t) + 2 * sizeof(uint64_t);
 
 __device__ __forceinline__ Smem carve_smem(float* base) {
   Smem s;
   float* p = base;
   s.P = p; p += kPStride;
+  s.Kp = p; p += kKp;
   s.img = p; p += 2 * kImg;
+  s.sh = p; p += kSh;
   s.c1 = p; p += 3456;
   s.s1 = p; p += 864;
   s.c2 = p; p += 768;
   s.s2 = p; p += 192;
   s.out = p; p += 16;
   s.dz = p; p += 16;
-  s.red = p; p += 1088;
-  s.G = p; p += kPStride;
   s.dzp = p; p += kDzp;
+  s.fcp = p; p += 1920;
+  s.red = p; p += kRed;
+  s.G = p; p += kPStride;
   s.tab = reinterpret_cast<uint64_t*>(p);
   s.bar = s.tab + 32;
   s.tr = nullptr;
@@ -90,12 +105,12 @@ __device__ __forceinline__ void issue_image(const Smem& s, int buf, const float*
   tma_load_1d(s.img + buf * kImg, src, kImg * sizeof(float), &s.bar[buf]);
 }
 
-// Parameters (3,898 floats, padded) global -> shared.  __ldcg: other CTAs rewrote them in the
-// previous step's SGD phase, so bypass L1.
+// Parameters (3,898 floats, padded) global -> shared, then the padded k2 copy.  __ldcg: other CTAs
+// rewrote them in the previous step's SGD phase, so bypass L1.  Ends with __syncthreads.
 __device__ __forceinline__ void load_params(const Smem& s, const float* params) {
   const float4* src = reinterpret_cast<const float4*>(params);
   float4* dst = reinterpret_cast<float4*>(s.P);
-  constexpr int kBatch = 4;  // issue every load before the first shared store
+  constexpr int kBatch = 2;  // every load in flight before the first shared store
   for (int base = threadIdx.x; base < kPStride / 4; base += kBatch * blockDim.x) {
     float4 v[kBatch];
 #pragma unroll
@@ -105,96 +120,123 @@ __device__ __forceinline__ void load_params(const Smem& s, const float* params) 
     for (int u = 0; u < kBatch; ++u)
       if (base + u * (int)blockDim.x < kPStride / 4) dst[base + u * blockDim.x] = v[u];
   }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < kKp; idx += blockDim.x) {
+    const int row = idx >> 3, k = idx & 7;
+    s.Kp[idx] = k < 5 ? s.P[kK2 + row * 5 + k] : 0.0f;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float target_of(int i, int label, const float* y) {
+  return y ? y[i] : (i == label ? 1.0f : 0.0f);  // mnist::one_hot (mnist.cpp:161-167)
 }
 
 // ---------------------------------------------------------------------------------------------
 // Forward stages (net::forward, network.cpp:81-95)
 // ---------------------------------------------------------------------------------------------
 
-// C1: mconv(I,k1,b1) -> sigmoid -> avgpool, fused.  Item = (channel i, pooled row py, 8-wide
-// column strip xs): the thread computes the 2x8 conv outputs feeding 4 pooled outputs.
-// Per output: taps (ky,kx) row-major (nn.cpp:28-33), then + b1[i] (nn.cpp:123).
+// sh[v][y][x] = I[y][x+v] (x < 24): the EXACT C1 weight gradient reads each shifted row with two
+// aligned 128-bit loads instead of 24 scalar ones.
+__device__ __forceinline__ void build_shifted(const Smem& s, const float* img, int t0, int nt) {
+  for (int q = t0; q < kSh / 4; q += nt) {
+    const int v = q / 168, rem = q - v * 168, y = rem / 6, x4 = 4 * (rem - y * 6);
+    const float* srow = img + y * 28 + x4 + v;
+    *reinterpret_cast<float4*>(s.sh + (v * 28 + y) * 24 + x4) = make_float4(srow[0], srow[1], srow[2], srow[3]);
+  }
+}
+
+// C1: mconv(I,k1,b1) -> sigmoid -> avgpool.  Item = (channel i, conv row y, 8-wide strip xs); the
+// two rows of a pooling window sit on adjacent lanes and meet through a shuffle.  Per output: taps
+// (ky,kx) row-major (nn.cpp:28-33), then + b1[i] (nn.cpp:123); pool ((p00+p01)+p10)+p11, *0.25f.
+// Warps 13.5..15 meanwhile build the v-shifted image copies used by the C1 weight gradient.
 template <bool EXACT>
 __device__ __forceinline__ void stage_conv1(const Smem& s, const float* img) {
-  for (int it = threadIdx.x; it < 216; it += blockDim.x) {
-    const int i = it / 36, r = it - i * 36, py = r / 3, xs = r - py * 3;
-    const int y0 = 2 * py, x0 = 8 * xs;
+  const int it = threadIdx.x;
+  if (it < 448) {  // 14 full warps; items >= 432 are padding lanes (valid = false)
+    const bool valid = it < 432;
+    const int pair = (valid ? it : 0) >> 1, r = it & 1;
+    const int i = pair / 36, rem = pair - i * 36, py = rem / 3, xs = rem - py * 3;
+    const int y = 2 * py + r, x0 = 8 * xs;
     const float* k = s.P + kK1 + i * 25;
-    float a0[8], a1[8];
+    float a[8];
 #pragma unroll
-    for (int o = 0; o < 8; ++o) a0[o] = a1[o] = 0.0f;
+    for (int o = 0; o < 8; ++o) a[o] = 0.0f;
 #pragma unroll
-    for (int rr = 0; rr < 6; ++rr) {
-      const float4* src = reinterpret_cast<const float4*>(img + (y0 + rr) * 28 + x0);
+    for (int ky = 0; ky < 5; ++ky) {
+      const float4* src = reinterpret_cast<const float4*>(img + (y + ky) * 28 + x0);
       const float4 v0 = src[0], v1 = src[1], v2 = src[2];
       const float in[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
-      if (rr < 5) {
 #pragma unroll
-        for (int kx = 0; kx < 5; ++kx) {
-          const float w = k[rr * 5 + kx];
+      for (int kx = 0; kx < 5; ++kx) {
+        const float w = k[ky * 5 + kx];
 #pragma unroll
-          for (int o = 0; o < 8; ++o) a0[o] = mac<EXACT>(a0[o], in[o + kx], w);
-        }
-      }
-      if (rr >= 1) {
-#pragma unroll
-        for (int kx = 0; kx < 5; ++kx) {
-          const float w = k[(rr - 1) * 5 + kx];
-#pragma unroll
-          for (int o = 0; o < 8; ++o) a1[o] = mac<EXACT>(a1[o], in[o + kx], w);
-        }
+        for (int o = 0; o < 8; ++o) a[o] = mac<EXACT>(a[o], in[o + kx], w);
       }
     }
     const float b = s.P[kB1 + i];
-    float t0[8], t1[8];
+    float t[8], u[8];
 #pragma unroll
-    for (int o = 0; o < 8; ++o) {
-      t0[o] = sigmoid_m<EXACT>(fadd(a0[o], b), s.tab);
-      t1[o] = sigmoid_m<EXACT>(fadd(a1[o], b), s.tab);
+    for (int o = 0; o < 8; ++o) t[o] = sigmoid_m<EXACT>(fadd(a[o], b), s.tab);
+#pragma unroll
+    for (int o = 0; o < 8; ++o) u[o] = __shfl_xor_sync(0xffffffffu, t[o], 1);
+    if (valid) {
+      float4* d = reinterpret_cast<float4*>(s.c1 + (i * 24 + y) * 24 + x0);
+      d[0] = make_float4(t[0], t[1], t[2], t[3]);
+      d[1] = make_float4(t[4], t[5], t[6], t[7]);
+      float pv[2];
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2) {
+        const int px = 2 * r + k2;
+        const float t00 = r ? u[2 * px] : t[2 * px], t01 = r ? u[2 * px + 1] : t[2 * px + 1];
+        const float t10 = r ? t[2 * px] : u[2 * px], t11 = r ? t[2 * px + 1] : u[2 * px + 1];
+        pv[k2] = fmul(fadd(fadd(fadd(t00, t01), t10), t11), 0.25f);
+      }
+      *reinterpret_cast<float2*>(s.s1 + (i * 12 + py) * 12 + 4 * xs + 2 * r) = make_float2(pv[0], pv[1]);
     }
-    float4* d0 = reinterpret_cast<float4*>(s.c1 + (i * 24 + y0) * 24 + x0);
-    float4* d1 = reinterpret_cast<float4*>(s.c1 + (i * 24 + y0 + 1) * 24 + x0);
-    d0[0] = make_float4(t0[0], t0[1], t0[2], t0[3]);
-    d0[1] = make_float4(t0[4], t0[5], t0[6], t0[7]);
-    d1[0] = make_float4(t1[0], t1[1], t1[2], t1[3]);
-    d1[1] = make_float4(t1[4], t1[5], t1[6], t1[7]);
-    float pv[4];
-#pragma unroll
-    for (int px = 0; px < 4; ++px)  // avgpool (nn.cpp:144): ((p00+p01)+p10)+p11, then *0.25f
-      pv[px] = fmul(fadd(fadd(fadd(t0[2 * px], t0[2 * px + 1]), t1[2 * px]), t1[2 * px + 1]), 0.25f);
-    *reinterpret_cast<float4*>(s.s1 + (i * 12 + py) * 12 + 4 * xs) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+  } else if constexpr (EXACT) {
+    build_shifted(s, img, it - 448, blockDim.x - 448);
   }
 }
 
 // C2: mconv(s1,k2,b2) -> sigmoid.  Item = (kernel i, row y, 4-wide half-row xh); per output the
-// 150 taps run (c, ky, kx) row-major (nn.cpp:14-33).
+// 150 taps run (c, ky, kx) row-major.  Fast mode splits the channel sum over two lanes (c < 3 and
+// c >= 3) and combines them with a shuffle; EXACT keeps one ordered chain per output.
 template <bool EXACT>
 __device__ __forceinline__ void stage_conv2(const Smem& s) {
-  for (int it = threadIdx.x; it < 192; it += blockDim.x) {
-    const int i = it >> 4, r = it & 15, y = r >> 1, xh = r & 1;
-    const float* k = s.P + kK2 + i * 150;
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  constexpr int kSplit = EXACT ? 1 : 2;
+  const int it = threadIdx.x;
+  if (it >= 192 * kSplit) return;
+  const int item = it / kSplit, part = it % kSplit;
+  const int i = item >> 4, r = item & 15, y = r >> 1, xh = r & 1;
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  const int c0 = part * (6 / kSplit), c1 = c0 + 6 / kSplit;
 #pragma unroll 1
-    for (int c = 0; c < 6; ++c) {
+  for (int c = c0; c < c1; ++c) {
 #pragma unroll
-      for (int ky = 0; ky < 5; ++ky) {
-        const float4* src = reinterpret_cast<const float4*>(s.s1 + (c * 12 + y + ky) * 12 + 4 * xh);
-        const float4 v0 = src[0], v1 = src[1];
-        const float in[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    for (int ky = 0; ky < 5; ++ky) {
+      const float4* src = reinterpret_cast<const float4*>(s.s1 + (c * 12 + y + ky) * 12 + 4 * xh);
+      const float4 v0 = src[0], v1 = src[1];
+      const float in[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      const float4* wp = reinterpret_cast<const float4*>(s.Kp + ((i * 6 + c) * 5 + ky) * 8);
+      const float4 w0 = wp[0], w1 = wp[1];
+      const float w[5] = {w0.x, w0.y, w0.z, w0.w, w1.x};
 #pragma unroll
-        for (int kx = 0; kx < 5; ++kx) {
-          const float w = k[(c * 5 + ky) * 5 + kx];
+      for (int kx = 0; kx < 5; ++kx)
 #pragma unroll
-          for (int o = 0; o < 4; ++o) acc[o] = mac<EXACT>(acc[o], in[o + kx], w);
-        }
-      }
+        for (int o = 0; o < 4; ++o) acc[o] = mac<EXACT>(acc[o], in[o + kx], w[kx]);
     }
-    const float b = s.P[kB2 + i];
-    float t[4];
-#pragma unroll
-    for (int o = 0; o < 4; ++o) t[o] = sigmoid_m<EXACT>(fadd(acc[o], b), s.tab);
-    *reinterpret_cast<float4*>(s.c2 + (i * 8 + y) * 8 + 4 * xh) = make_float4(t[0], t[1], t[2], t[3]);
   }
+  if constexpr (!EXACT) {
+#pragma unroll
+    for (int o = 0; o < 4; ++o) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], 1);
+    if (part) return;
+  }
+  const float b = s.P[kB2 + i];
+  float t[4];
+#pragma unroll
+  for (int o = 0; o < 4; ++o) t[o] = sigmoid_m<EXACT>(fadd(acc[o], b), s.tab);
+  *reinterpret_cast<float4*>(s.c2 + (i * 8 + y) * 8 + 4 * xh) = make_float4(t[0], t[1], t[2], t[3]);
 }
 
 __device__ __forceinline__ void stage_pool2(const Smem& s) {
@@ -205,22 +247,25 @@ __device__ __forceinline__ void stage_pool2(const Smem& s) {
   }
 }
 
-__device__ __forceinline__ float target_of(int i, int label, const float* y) {
-  return y ? y[i] : (i == label ? 1.0f : 0.0f);  // mnist::one_hot (mnist.cpp:161-167)
-}
-
 // FC: out[i] = sigmoid(sum_j s2[j]*fc[i][j] + b[i]); also dz = backsigmoid(out - y, out)
-// (network.cpp:146-152, nn.cpp:131-133).  EXACT: one thread per output, j in order.
+// (network.cpp:146-152, nn.cpp:131-133).  EXACT: all 1,920 products in parallel, then one ordered
+// 192-term chain per output.  Fast: one warp per output with a shuffle tree.
 template <bool EXACT>
 __device__ __forceinline__ void stage_fc(const Smem& s, int label, const float* y, bool want_dz) {
   if constexpr (EXACT) {
+    for (int idx = threadIdx.x; idx < 1920; idx += blockDim.x)
+      s.fcp[idx] = fmul(s.s2[idx % 192], s.P[kFC + idx]);
+    __syncthreads();
     if (threadIdx.x < 10) {
       const int i = threadIdx.x;
-      const float* w = s.P + kFC + i * 192;
+      const float4* p4 = reinterpret_cast<const float4*>(s.fcp + i * 192);
       float acc = 0.0f;
 #pragma unroll 8
-      for (int j = 0; j < 192; ++j) acc = mac<true>(acc, s.s2[j], w[j]);
-      const float o = sigmoid_m<EXACT>(fadd(acc, s.P[kB + i]), s.tab);
+      for (int j = 0; j < 48; ++j) {
+        const float4 v = p4[j];
+        acc = fadd(fadd(fadd(fadd(acc, v.x), v.y), v.z), v.w);
+      }
+      const float o = sigmoid_m<true>(fadd(acc, s.P[kB + i]), s.tab);
       s.out[i] = o;
       if (want_dz) s.dz[i] = fmul(fmul(fsub(o, target_of(i, label, y)), o), fsub(1.0f, o));
     }
@@ -234,7 +279,7 @@ __device__ __forceinline__ void stage_fc(const Smem& s, int label, const float* 
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
       if (lane == 0) {
-        const float o = sigmoid_m<EXACT>(fadd(acc, s.P[kB + i]), s.tab);
+        const float o = sigmoid_m<false>(fadd(acc, s.P[kB + i]), s.tab);
         s.out[i] = o;
         if (want_dz) s.dz[i] = fmul(fmul(fsub(o, target_of(i, label, y)), o), fsub(1.0f, o));
       }
@@ -267,7 +312,7 @@ __device__ __forceinline__ void put(const Smem& s, float* row, int idx, float v)
 
 // FC backward: g_fc[i][j] = 0 + s2[j]*dz[i]; g_b = 0 + dz; d_s2[j] = sum_i fc[i][j]*dz[i]
 // (backin with singleton error, nn.cpp:193-217, summed over i as network.cpp:135-138), then
-// backavgpool (nn.cpp:148-158) and backsigmoid through c2 -> dz2 (in place over c2).
+// backavgpool (nn.cpp:148-158) and backsigmoid through c2 -> dz2 (into the padded buffer).
 template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void stage_fc_back(const Smem& s, float* row) {
   for (int idx = threadIdx.x; idx < 1930; idx += blockDim.x) {
@@ -288,72 +333,105 @@ __device__ __forceinline__ void stage_fc_back(const Smem& s, float* row) {
     for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
       for (int dx = 0; dx < 2; ++dx) {
-        const int y = 2 * py + dy, x = 2 * px + dx;
-        const float o = s.c2[(c * 8 + y) * 8 + x];
-        s.dzp[(c * 16 + y + 4) * 16 + x + 4] = fmul(fmul(dc, o), fsub(1.0f, o));
+        const int yy = 2 * py + dy, xx = 2 * px + dx;
+        const float o = s.c2[(c * 8 + yy) * 8 + xx];
+        s.dzp[(c * 16 + yy + 4) * 16 + xx + 4] = fmul(fmul(dc, o), fsub(1.0f, o));
       }
   }
 }
 
-// C2 backward: g_k2 = conv(s1, dz2[i]) (64 taps, (y,x) row-major), g_b2 = sum_all(dz2[i]),
-// d_s1 = sum_i backin(dz2[i], k2[i], s1), then backavgpool + backsigmoid through c1 -> dz1 (in place).
-//
-// backin runs over the zero-padded dz2 (uniform 5x5 taps, register-blocked 4 outputs per thread).
-// The reference's clipped nested sums (nn.cpp:169-189: per i, row sums over u2 from 0, outer sum over
-// u1 from 0, then acc += per-i result) only ever see the padded zero products prepended or appended
-// to a row/outer sum, and x + (+-0) == x (with +0 + -0 == +0), so EXACT stays bit-identical while
-// executing 259,200 instead of 115,200 multiply-adds per image.
+// backin per-kernel term b_i(c, p, 4qq+o), o < 4, over the zero-padded dz2 (uniform 5x5 taps).
+// The reference's clipped nested sums (nn.cpp:169-189: row sums over u2 from 0, outer sum over u1
+// from 0) only ever see the padded zero products prepended or appended to a row/outer sum, and
+// x + (+-0) == x (with +0 + -0 == +0), so EXACT stays bit-identical.  Fast: plain FFMA chain.
+template <bool EXACT>
+__device__ __forceinline__ void backin_term(const Smem& s, int i, int c, int p, int qq, float (&b)[4]) {
+  const float* kk = s.Kp + (i * 6 + c) * 40;
+#pragma unroll
+  for (int o = 0; o < 4; ++o) b[o] = 0.0f;
+#pragma unroll
+  for (int u1 = 0; u1 < 5; ++u1) {
+    const float4* dp = reinterpret_cast<const float4*>(s.dzp + (i * 16 + p - u1 + 4) * 16 + 4 * qq);
+    const float4 d0 = dp[0], d1 = dp[1];
+    const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+    const float4* wp = reinterpret_cast<const float4*>(kk + u1 * 8);
+    const float4 w0 = wp[0], w1 = wp[1];
+    const float w[5] = {w0.x, w0.y, w0.z, w0.w, w1.x};
+    float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int u2 = 0; u2 < 5; ++u2)
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        if constexpr (EXACT) rs[o] = mac<true>(rs[o], w[u2], d[o - u2 + 4]);
+        else b[o] = __fmaf_rn(w[u2], d[o - u2 + 4], b[o]);
+      }
+    if constexpr (EXACT) {
+#pragma unroll
+      for (int o = 0; o < 4; ++o) b[o] = fadd(b[o], rs[o]);
+    }
+  }
+}
+
+// C2 backward: d_s1 = sum_i backin(dz2[i], k2[i], s1) (+ backavgpool/backsigmoid through c1 -> dz1),
+// g_k2 = conv(s1, dz2[i]) (64 taps, (y,x) row-major), g_b2 = sum_all(dz2[i]).
+// backin items are lane pairs: the even lane runs kernels i = 0..5, the odd lane i = 6..11 and hands
+// its six per-kernel terms over by shuffle, so the ordered chain acc = (((0 + b_0) + b_1) + ... + b_11)
+// (network.cpp:135-138) stays exact on the even lane.
 template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
-  for (int it = threadIdx.x; it < 588; it += blockDim.x) {
-    if (it < 216) {
-      const int c = it / 36, r = it - c * 36, p = r / 3, qq = r - p * 3;
+  constexpr int kBackin = 448;  // 432 lane-pair items padded to whole warps
+  for (int it = threadIdx.x; it < kBackin + 372; it += blockDim.x) {
+    if (it < kBackin) {
+      const bool valid = it < 432;
+      const int pair = (valid ? it : 0) >> 1, half = it & 1;
+      const int c = pair / 36, r = pair - c * 36, p = r / 3, qq = r - p * 3;
       float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll 1
-      for (int i = 0; i < 12; ++i) {
-        const float* kk = s.P + kK2 + (i * 6 + c) * 25;
-        float outer[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      float mine[6][4];
 #pragma unroll
-        for (int u1 = 0; u1 < 5; ++u1) {
-          const float4* dp = reinterpret_cast<const float4*>(s.dzp + (i * 16 + p - u1 + 4) * 16 + 4 * qq);
-          const float4 a = dp[0], b = dp[1];
-          const float d[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-          float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      for (int k = 0; k < 6; ++k) {
+        float b[4];
+        backin_term<EXACT>(s, 6 * half + k, c, p, qq, b);
 #pragma unroll
-          for (int u2 = 0; u2 < 5; ++u2) {
-            const float w = kk[u1 * 5 + u2];
-#pragma unroll
-            for (int o = 0; o < 4; ++o) {
-              if constexpr (EXACT) rs[o] = mac<true>(rs[o], w, d[o - u2 + 4]);
-              else acc[o] = __fmaf_rn(w, d[o - u2 + 4], acc[o]);
-            }
-          }
-          if constexpr (EXACT) {
-#pragma unroll
-            for (int o = 0; o < 4; ++o) outer[o] = fadd(outer[o], rs[o]);
-          }
-        }
-        if constexpr (EXACT) {
-#pragma unroll
-          for (int o = 0; o < 4; ++o) acc[o] = fadd(acc[o], outer[o]);
+        for (int o = 0; o < 4; ++o) {
+          mine[k][o] = b[o];
+          if (!half) acc[o] = fadd(acc[o], b[o]);
         }
       }
-      // backavgpool (x0.25) + backsigmoid through c1 for the 2x8 block this thread owns
+      if constexpr (EXACT) {
 #pragma unroll
-      for (int dy = 0; dy < 2; ++dy) {
-        float4* cp = reinterpret_cast<float4*>(s.c1 + (c * 24 + 2 * p + dy) * 24 + 8 * qq);
-        const float4 v0 = cp[0], v1 = cp[1];
-        float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        for (int k = 0; k < 6; ++k)
 #pragma unroll
-        for (int x = 0; x < 8; ++x) {
-          const float dc = fmul(acc[x >> 1], 0.25f);
-          cv[x] = fmul(fmul(dc, cv[x]), fsub(1.0f, cv[x]));
-        }
-        cp[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
-        cp[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+          for (int o = 0; o < 4; ++o) {
+            const float v = __shfl_xor_sync(0xffffffffu, mine[k][o], 1);
+            acc[o] = fadd(acc[o], v);
+          }
+      } else {
+        float part[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+#pragma unroll
+          for (int o = 0; o < 4; ++o) part[o] += mine[k][o];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) acc[o] += __shfl_xor_sync(0xffffffffu, part[o], 1);
       }
-    } else if (it < 576) {
-      const int t = it - 216, i = t / 30, r = t - i * 30, c = r / 5, u = r - c * 5;
+      if (valid && !half) {
+        // backavgpool (x0.25) + backsigmoid through c1 for the 2x8 block this pair owns
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy) {
+          float4* cp = reinterpret_cast<float4*>(s.c1 + (c * 24 + 2 * p + dy) * 24 + 8 * qq);
+          const float4 v0 = cp[0], v1 = cp[1];
+          float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            const float dc = fmul(acc[x >> 1], 0.25f);
+            cv[x] = fmul(fmul(dc, cv[x]), fsub(1.0f, cv[x]));
+          }
+          cp[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
+          cp[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+        }
+      }
+    } else if (it < kBackin + 360) {
+      const int t = it - kBackin, i = t / 30, r = t - i * 30, c = r / 5, u = r - c * 5;
       float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll 2
       for (int y = 0; y < 8; ++y) {
@@ -371,7 +449,7 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
 #pragma unroll
       for (int v = 0; v < 5; ++v) put<ACCUM>(s, row, kK2 + ((i * 6 + c) * 5 + u) * 5 + v, acc[v]);
     } else {
-      const int i = it - 576;
+      const int i = it - kBackin - 360;
       float acc = 0.0f;
 #pragma unroll
       for (int y = 0; y < 8; ++y) {
@@ -386,7 +464,8 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
 }
 
 // C1 backward: g_k1[i][u][v] = sum_{y,x<24} I[u+y][v+x]*dz1[i][y][x]; g_b1[i] = sum dz1[i].
-// EXACT: one thread per output, 576 terms in order.  Fast: 4-row partials + fixed-order combine.
+// EXACT: one thread per output, the 576 terms in order, reading the v-shifted image copy so every
+// row is two aligned 128-bit loads.  Fast: 2-row partials (432 items) + fixed-order combine.
 template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img, float* row) {
   const float* dz1 = s.c1;
@@ -395,17 +474,17 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
       if (it < 150) {
         const int i = it / 25, r = it - i * 25, u = r / 5, v = r - u * 5;
         float acc = 0.0f;
-#pragma unroll 1
+#pragma unroll 2
         for (int y = 0; y < 24; ++y) {
-          const float* ir = img + (u + y) * 28 + v;
+          const float4* ip = reinterpret_cast<const float4*>(s.sh + (v * 28 + u + y) * 24);
           const float4* dp = reinterpret_cast<const float4*>(dz1 + (i * 24 + y) * 24);
 #pragma unroll
           for (int x4 = 0; x4 < 6; ++x4) {
-            const float4 d = dp[x4];
-            acc = mac<true>(acc, ir[4 * x4 + 0], d.x);
-            acc = mac<true>(acc, ir[4 * x4 + 1], d.y);
-            acc = mac<true>(acc, ir[4 * x4 + 2], d.z);
-            acc = mac<true>(acc, ir[4 * x4 + 3], d.w);
+            const float4 a = ip[x4], d = dp[x4];
+            acc = mac<true>(acc, a.x, d.x);
+            acc = mac<true>(acc, a.y, d.y);
+            acc = mac<true>(acc, a.z, d.z);
+            acc = mac<true>(acc, a.w, d.w);
           }
         }
         put<ACCUM>(s, row, kK1 + it, acc);
@@ -422,43 +501,43 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
       }
     }
   } else {
-    for (int it = threadIdx.x; it < 216; it += blockDim.x) {
-      if (it < 180) {
-        const int i = it / 30, r = it - i * 30, u = r / 6, yq = r - u * 6;
-        float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll 1
-        for (int y = 4 * yq; y < 4 * yq + 4; ++y) {
-          const float4* ip = reinterpret_cast<const float4*>(img + (u + y) * 28);
-          float ir[28];
+    const int it = threadIdx.x;
+    if (it < 360) {  // (i, u, 2-row chunk yc) -> partials for v = 0..4
+      const int i = it / 60, r = it - i * 60, u = r / 12, yc = r - u * 12;
+      float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-          for (int q = 0; q < 7; ++q) {
-            const float4 t = ip[q];
-            ir[4 * q] = t.x; ir[4 * q + 1] = t.y; ir[4 * q + 2] = t.z; ir[4 * q + 3] = t.w;
-          }
-          const float4* dp = reinterpret_cast<const float4*>(dz1 + (i * 24 + y) * 24);
+      for (int dy = 0; dy < 2; ++dy) {
+        const int y = 2 * yc + dy;
+        const float4* ip = reinterpret_cast<const float4*>(img + (u + y) * 28);
+        float ir[28];
 #pragma unroll
-          for (int x4 = 0; x4 < 6; ++x4) {
-            const float4 d = dp[x4];
-            const float dv[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-            for (int xx = 0; xx < 4; ++xx)
-#pragma unroll
-              for (int v = 0; v < 5; ++v) acc[v] = __fmaf_rn(ir[4 * x4 + xx + v], dv[xx], acc[v]);
-          }
+        for (int q = 0; q < 7; ++q) {
+          const float4 t = ip[q];
+          ir[4 * q] = t.x; ir[4 * q + 1] = t.y; ir[4 * q + 2] = t.z; ir[4 * q + 3] = t.w;
         }
+        const float4* dp = reinterpret_cast<const float4*>(dz1 + (i * 24 + y) * 24);
 #pragma unroll
-        for (int v = 0; v < 5; ++v) s.red[it * 5 + v] = acc[v];
-      } else {
-        const int j = it - 180, i = j / 6, yq = j - i * 6;
-        const float4* dp = reinterpret_cast<const float4*>(dz1 + i * 576 + yq * 96);
-        float acc = 0.0f;
-#pragma unroll 4
-        for (int e = 0; e < 24; ++e) {
-          const float4 d = dp[e];
-          acc += (d.x + d.y) + (d.z + d.w);
+        for (int x4 = 0; x4 < 6; ++x4) {
+          const float4 d = dp[x4];
+          const float dv[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+          for (int xx = 0; xx < 4; ++xx)
+#pragma unroll
+            for (int v = 0; v < 5; ++v) acc[v] = __fmaf_rn(ir[4 * x4 + xx + v], dv[xx], acc[v]);
         }
-        s.red[900 + j] = acc;
       }
+#pragma unroll
+      for (int v = 0; v < 5; ++v) s.red[it * 5 + v] = acc[v];
+    } else if (it < 432) {  // g_b1 partials: (i, 2-row chunk)
+      const int j = it - 360, i = j / 12, yc = j - i * 12;
+      const float4* dp = reinterpret_cast<const float4*>(dz1 + i * 576 + yc * 48);
+      float acc = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 12; ++e) {
+        const float4 d = dp[e];
+        acc += (d.x + d.y) + (d.z + d.w);
+      }
+      s.red[1800 + j] = acc;
     }
     __syncthreads();
     for (int t = threadIdx.x; t < 156; t += blockDim.x) {
@@ -466,12 +545,12 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
       if (t < 150) {
         const int i = t / 25, r = t - i * 25, u = r / 5, v = r - u * 5;
 #pragma unroll
-        for (int yq = 0; yq < 6; ++yq) acc += s.red[((i * 30) + u * 6 + yq) * 5 + v];
+        for (int yc = 0; yc < 12; ++yc) acc += s.red[((i * 5 + u) * 12 + yc) * 5 + v];
         put<ACCUM>(s, row, kK1 + t, acc);
       } else {
         const int i = t - 150;
 #pragma unroll
-        for (int yq = 0; yq < 6; ++yq) acc += s.red[900 + i * 6 + yq];
+        for (int yc = 0; yc < 12; ++yc) acc += s.red[1800 + i * 12 + yc];
         put<ACCUM>(s, row, kB1 + i, acc);
       }
     }

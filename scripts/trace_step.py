@@ -48,7 +48,10 @@ t = tr.view(steps, 16).cpu().numpy().astype(np.int64)
 d = np.diff(t[:, :14], axis=1)  # stage durations (cycles)
 med = np.median(d[1:], axis=0)
 mhz = 1965.0
-out = {"mode": args.mode, "batch": args.batch, "epoch_ms": e0.elapsed_time(e1),
+sub = np.median(t[1:, 14] - t[1:, 11]) / 1965.0, np.median(t[1:, 15] - t[1:, 14]) / 1965.0, np.median(t[1:, 12] - t[1:, 15]) / 1965.0
+out = {"reduce_split_us": {"stage_loads": round(float(sub[0]), 3), "accumulate": round(float(sub[1]), 3),
+                           "finish": round(float(sub[2]), 3)},
+       "mode": args.mode, "batch": args.batch, "epoch_ms": e0.elapsed_time(e1),
        "step_us_median": float(np.median(t[1:, 13] - t[1:, 0]) / mhz),
        "stage_us_median": {n: round(float(v) / mhz, 3) for n, v in zip(NAMES, med)},
        "info": ctx.info()}
