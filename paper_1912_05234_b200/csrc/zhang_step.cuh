@@ -34,9 +34,9 @@ struct Smem {
   float* s2;
   float* out;
   float* dz;
-  float* dzp;  // dz2 zero-padded by 4 on every side: [12][16][16]; border stays 0
+  float* dzp;  // dz2 zero-padded by 4 on every side: [12][16][16] (strided, see dzp_at); border stays 0
   float* fcp;  // EXACT FC products [10][192]
-  float* red;  // fast C1 weight-gradient partials [432][5]
+  float* red;  // fast C1 weight-gradient row partials [144][26]
   float* G;    // fast per-CTA gradient accumulator [3904]
   uint64_t* tab;
   uint64_t* bar;
@@ -56,9 +56,16 @@ __device__ __forceinline__ void mark(const Smem& s, int slot) {
 }
 
 constexpr int kKp = 12 * 6 * 5 * 8;
-constexpr int kSh = 5 * 28 * 24;
-constexpr int kDzp = 12 * 16 * 16;
-constexpr int kRed = 432 * 5;
+// Bank-conflict-free strides (in float4 units the plane/kernel strides are odd mod 8):
+constexpr int kShPlane = 28 * 24 + 4;   // shifted-image plane (v) stride
+constexpr int kSh = 5 * kShPlane + 4;   // (+4 keeps the next buffer 16-B aligned)
+constexpr int kDzpRow = 20;             // padded dz2 row: 16 used columns
+constexpr int kDzpK = 16 * kDzpRow + 4; // padded dz2 kernel (i) stride
+constexpr int kDzp = 12 * kDzpK;
+constexpr int kRed = 144 * 26;          // fast C1 weight-gradient row partials
+
+__device__ __forceinline__ int dzp_at(int i, int R, int col) { return i * kDzpK + R * kDzpRow + col; }
+__device__ __forceinline__ int sh_at(int v, int y) { return v * kShPlane + y * 24; }
 constexpr int kSmemFloats =
     kPStride + kKp + 2 * kImg + kSh + 3456 + 864 + 768 + 192 + 16 + 16 + kDzp + 1920 + kRed + kPStride;
 constexpr size_t kSmemBytes = sizeof(float) * kSmemFloats + 32 * sizeof(uint64_t) + 2 * sizeof(uint64_t);
@@ -142,7 +149,7 @@ __device__ __forceinline__ void build_shifted(const Smem& s, const float* img, i
   for (int q = t0; q < kSh / 4; q += nt) {
     const int v = q / 168, rem = q - v * 168, y = rem / 6, x4 = 4 * (rem - y * 6);
     const float* srow = img + y * 28 + x4 + v;
-    *reinterpret_cast<float4*>(s.sh + (v * 28 + y) * 24 + x4) = make_float4(srow[0], srow[1], srow[2], srow[3]);
+    *reinterpret_cast<float4*>(s.sh + sh_at(v, y) + x4) = make_float4(srow[0], srow[1], srow[2], srow[3]);
   }
 }
 
@@ -335,137 +342,215 @@ __device__ __forceinline__ void stage_fc_back(const Smem& s, float* row) {
       for (int dx = 0; dx < 2; ++dx) {
         const int yy = 2 * py + dy, xx = 2 * px + dx;
         const float o = s.c2[(c * 8 + yy) * 8 + xx];
-        s.dzp[(c * 16 + yy + 4) * 16 + xx + 4] = fmul(fmul(dc, o), fsub(1.0f, o));
+        s.dzp[dzp_at(c, yy + 4, xx + 4)] = fmul(fmul(dc, o), fsub(1.0f, o));
       }
   }
 }
 
-// backin per-kernel term b_i(c, p, 4qq+o), o < 4, over the zero-padded dz2 (uniform 5x5 taps).
-// The reference's clipped nested sums (nn.cpp:169-189: row sums over u2 from 0, outer sum over u1
-// from 0) only ever see the padded zero products prepended or appended to a row/outer sum, and
-// x + (+-0) == x (with +0 + -0 == +0), so EXACT stays bit-identical.  Fast: plain FFMA chain.
+// backin d_s1 = sum_i backin(dz2[i], k2[i], s1), then backavgpool + backsigmoid through c1 -> dz1.
+//
+// Lanes come in quads per item (channel c, output rows p0 = 2pp and p0+1, columns 4qq..4qq+3); lane s
+// of the quad owns kernels i = 3s..3s+2.  Per kernel it keeps the 25 weights in registers and streams
+// the six padded dz2 rows the two output rows need, so each loaded row feeds both rows' taps.
+// The reference's clipped nested sums (nn.cpp:169-189: per i, row sums over u2 from 0, outer sum over
+// u1 from 0) only ever see padded zero products prepended or appended to a row/outer sum, and
+// x + (+-0) == x (with +0 + -0 == +0), so the EXACT terms are bit-identical.  EXACT then hands the
+// per-kernel terms to lane 0 of the quad by shuffle, keeping acc = (((0 + b_0) + b_1) + ... + b_11)
+// (network.cpp:135-138) as one ordered chain; fast mode sums with FFMA and a fixed xor tree.
 template <bool EXACT>
-__device__ __forceinline__ void backin_term(const Smem& s, int i, int c, int p, int qq, float (&b)[4]) {
-  const float* kk = s.Kp + (i * 6 + c) * 40;
+__device__ __forceinline__ void backin_quad(const Smem& s, int lane_item, bool valid) {
+  const int item = valid ? lane_item >> 2 : 0, q4 = lane_item & 3;
+  const int c = item / 18, rem = item - c * 18, pp = rem / 3, qq = rem - pp * 3, p0 = 2 * pp;
+  float b[3][2][4];
 #pragma unroll
-  for (int o = 0; o < 4; ++o) b[o] = 0.0f;
+  for (int k = 0; k < 3; ++k) {
+    const int i = 3 * q4 + k;
+    float w[5][5];
 #pragma unroll
-  for (int u1 = 0; u1 < 5; ++u1) {
-    const float4* dp = reinterpret_cast<const float4*>(s.dzp + (i * 16 + p - u1 + 4) * 16 + 4 * qq);
-    const float4 d0 = dp[0], d1 = dp[1];
-    const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-    const float4* wp = reinterpret_cast<const float4*>(kk + u1 * 8);
-    const float4 w0 = wp[0], w1 = wp[1];
-    const float w[5] = {w0.x, w0.y, w0.z, w0.w, w1.x};
-    float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int u1 = 0; u1 < 5; ++u1) {
+      const float4* wp = reinterpret_cast<const float4*>(s.Kp + ((i * 6 + c) * 5 + u1) * 8);
+      const float4 w0 = wp[0], w1 = wp[1];
+      w[u1][0] = w0.x; w[u1][1] = w0.y; w[u1][2] = w0.z; w[u1][3] = w0.w; w[u1][4] = w1.x;
+    }
 #pragma unroll
-    for (int u2 = 0; u2 < 5; ++u2)
+    for (int orow = 0; orow < 2; ++orow)
 #pragma unroll
-      for (int o = 0; o < 4; ++o) {
-        if constexpr (EXACT) rs[o] = mac<true>(rs[o], w[u2], d[o - u2 + 4]);
-        else b[o] = __fmaf_rn(w[u2], d[o - u2 + 4], b[o]);
+      for (int o = 0; o < 4; ++o) b[k][orow][o] = 0.0f;
+    // padded rows R = p0 + rr, rr = 5..0: output row orow uses tap row u1 = orow + 4 - rr (ascending)
+#pragma unroll
+    for (int rr = 5; rr >= 0; --rr) {
+      const float4* dp = reinterpret_cast<const float4*>(s.dzp + dzp_at(i, p0 + rr, 4 * qq));
+      const float4 d0 = dp[0], d1 = dp[1];
+      const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+      for (int orow = 0; orow < 2; ++orow) {
+        const int u1 = orow + 4 - rr;
+        if (u1 < 0 || u1 > 4) continue;
+        if constexpr (EXACT) {
+          float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+          for (int u2 = 0; u2 < 5; ++u2)
+#pragma unroll
+            for (int o = 0; o < 4; ++o) rs[o] = mac<true>(rs[o], w[u1][u2], d[o - u2 + 4]);
+#pragma unroll
+          for (int o = 0; o < 4; ++o) b[k][orow][o] = fadd(b[k][orow][o], rs[o]);
+        } else {
+#pragma unroll
+          for (int u2 = 0; u2 < 5; ++u2)
+#pragma unroll
+            for (int o = 0; o < 4; ++o) b[k][orow][o] = __fmaf_rn(w[u1][u2], d[o - u2 + 4], b[k][orow][o]);
+        }
       }
-    if constexpr (EXACT) {
-#pragma unroll
-      for (int o = 0; o < 4; ++o) b[o] = fadd(b[o], rs[o]);
     }
   }
+  float acc[2][4];
+  if constexpr (EXACT) {
+    const int lead = (threadIdx.x & 31) & ~3;
+#pragma unroll
+    for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        float a = 0.0f;
+#pragma unroll
+        for (int src = 0; src < 4; ++src)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) a = fadd(a, __shfl_sync(0xffffffffu, b[k][orow][o], lead + src));
+        acc[orow][o] = a;
+      }
+  } else {
+#pragma unroll
+    for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        float a = (b[0][orow][o] + b[1][orow][o]) + b[2][orow][o];
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        acc[orow][o] = a;
+      }
+  }
+  if (valid && q4 == 0) {
+    // backavgpool (x0.25) + backsigmoid through c1 for the 4x8 block of c1 this quad owns
+#pragma unroll
+    for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy) {
+        float4* cp = reinterpret_cast<float4*>(s.c1 + (c * 24 + 2 * (p0 + orow) + dy) * 24 + 8 * qq);
+        const float4 v0 = cp[0], v1 = cp[1];
+        float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          const float dc = fmul(acc[orow][x >> 1], 0.25f);
+          cv[x] = fmul(fmul(dc, cv[x]), fsub(1.0f, cv[x]));
+        }
+        cp[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
+        cp[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+      }
+  }
 }
 
-// C2 backward: d_s1 = sum_i backin(dz2[i], k2[i], s1) (+ backavgpool/backsigmoid through c1 -> dz1),
-// g_k2 = conv(s1, dz2[i]) (64 taps, (y,x) row-major), g_b2 = sum_all(dz2[i]).
-// backin items are lane pairs: the even lane runs kernels i = 0..5, the odd lane i = 6..11 and hands
-// its six per-kernel terms over by shuffle, so the ordered chain acc = (((0 + b_0) + b_1) + ... + b_11)
-// (network.cpp:135-138) stays exact on the even lane.
+// g_k2[i][c][u][v] = sum_{y,x<8} s1[c][u+y][v+x] * dz2[i][y][x] (conv(s1, dz2[i]), nn.cpp:160;
+// 64 taps row-major) and g_b2[i] = sum_all(dz2[i]).  EXACT: one lane per (i,c,u), five ordered chains.
+template <bool ACCUM>
+__device__ __forceinline__ void gk2_exact(const Smem& s, float* row, int t) {
+  if (t < 360) {
+    const int i = t / 30, r = t - i * 30, c = r / 5, u = r - c * 5;
+    float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll 2
+    for (int y = 0; y < 8; ++y) {
+      const float4* sp = reinterpret_cast<const float4*>(s.s1 + (c * 12 + u + y) * 12);
+      const float4 a = sp[0], b = sp[1], cc = sp[2];
+      const float sr[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, cc.x, cc.y, cc.z, cc.w};
+      const float4* dp = reinterpret_cast<const float4*>(s.dzp + dzp_at(i, y + 4, 4));
+      const float4 d0 = dp[0], d1 = dp[1];
+      const float dr[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[v] = mac<true>(acc[v], sr[v + x], dr[x]);
+    }
+#pragma unroll
+    for (int v = 0; v < 5; ++v) put<ACCUM>(s, row, kK2 + ((i * 6 + c) * 5 + u) * 5 + v, acc[v]);
+  } else {
+    const int i = t - 360;
+    float acc = 0.0f;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      const float4* dp = reinterpret_cast<const float4*>(s.dzp + dzp_at(i, y + 4, 4));
+      const float4 d0 = dp[0], d1 = dp[1];
+      acc = fadd(fadd(fadd(fadd(acc, d0.x), d0.y), d0.z), d0.w);
+      acc = fadd(fadd(fadd(fadd(acc, d1.x), d1.y), d1.z), d1.w);
+    }
+    put<ACCUM>(s, row, kB2 + i, acc);
+  }
+}
+
+// Fast g_k2/g_b2: lane quads per (i, c) hold all 25 outputs; lane q of the quad takes rows y = 2q, 2q+1
+// and the quad combines with a fixed xor tree (each s1 row feeds 5 outputs x 8 taps from registers).
+template <bool ACCUM>
+__device__ __forceinline__ void gk2_fast(const Smem& s, float* row, int t) {
+  const int item = t >> 2, q4 = t & 3, i = item / 6, c = item - i * 6;
+  float acc[5][5];
+#pragma unroll
+  for (int u = 0; u < 5; ++u)
+#pragma unroll
+    for (int v = 0; v < 5; ++v) acc[u][v] = 0.0f;
+  float bsum = 0.0f;
+#pragma unroll
+  for (int dy = 0; dy < 2; ++dy) {
+    const int y = 2 * q4 + dy;
+    const float4* dp = reinterpret_cast<const float4*>(s.dzp + dzp_at(i, y + 4, 4));
+    const float4 d0 = dp[0], d1 = dp[1];
+    const float dr[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+    bsum += ((dr[0] + dr[1]) + (dr[2] + dr[3])) + ((dr[4] + dr[5]) + (dr[6] + dr[7]));
+#pragma unroll
+    for (int u = 0; u < 5; ++u) {
+      const float4* sp = reinterpret_cast<const float4*>(s.s1 + (c * 12 + u + y) * 12);
+      const float4 a = sp[0], b = sp[1], cc = sp[2];
+      const float sr[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[u][v] = __fmaf_rn(sr[v + x], dr[x], acc[u][v]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 5; ++u)
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      float a = acc[u][v];
+      a += __shfl_xor_sync(0xffffffffu, a, 1);
+      a += __shfl_xor_sync(0xffffffffu, a, 2);
+      acc[u][v] = a;
+    }
+  bsum += __shfl_xor_sync(0xffffffffu, bsum, 1);
+  bsum += __shfl_xor_sync(0xffffffffu, bsum, 2);
+  // spread the 25 puts over the quad's lanes (lane q writes outputs q, q+4, ...)
+#pragma unroll
+  for (int k = 0; k < 25; ++k)
+    if ((k & 3) == q4) put<ACCUM>(s, row, kK2 + (i * 6 + c) * 25 + k, acc[k / 5][k % 5]);
+  if (c == 0 && q4 == 0) put<ACCUM>(s, row, kB2 + i, bsum);
+}
+
+// C2 backward stage: backin quads (448 lanes incl. padding) + g_k2/g_b2 lanes.
 template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
-  constexpr int kBackin = 448;  // 432 lane-pair items padded to whole warps
-  for (int it = threadIdx.x; it < kBackin + 372; it += blockDim.x) {
+  constexpr int kBackin = 448;                   // 108 quads = 432 lanes, padded to 14 warps
+  constexpr int kGk2 = EXACT ? 372 : 288;        // exact: 360 (i,c,u) lanes + 12 g_b2; fast: 72 quads
+  for (int it = threadIdx.x; it < kBackin + kGk2; it += blockDim.x) {
     if (it < kBackin) {
-      const bool valid = it < 432;
-      const int pair = (valid ? it : 0) >> 1, half = it & 1;
-      const int c = pair / 36, r = pair - c * 36, p = r / 3, qq = r - p * 3;
-      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-      float mine[6][4];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        float b[4];
-        backin_term<EXACT>(s, 6 * half + k, c, p, qq, b);
-#pragma unroll
-        for (int o = 0; o < 4; ++o) {
-          mine[k][o] = b[o];
-          if (!half) acc[o] = fadd(acc[o], b[o]);
-        }
-      }
-      if constexpr (EXACT) {
-#pragma unroll
-        for (int k = 0; k < 6; ++k)
-#pragma unroll
-          for (int o = 0; o < 4; ++o) {
-            const float v = __shfl_xor_sync(0xffffffffu, mine[k][o], 1);
-            acc[o] = fadd(acc[o], v);
-          }
-      } else {
-        float part[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-        for (int k = 0; k < 6; ++k)
-#pragma unroll
-          for (int o = 0; o < 4; ++o) part[o] += mine[k][o];
-#pragma unroll
-        for (int o = 0; o < 4; ++o) acc[o] += __shfl_xor_sync(0xffffffffu, part[o], 1);
-      }
-      if (valid && !half) {
-        // backavgpool (x0.25) + backsigmoid through c1 for the 2x8 block this pair owns
-#pragma unroll
-        for (int dy = 0; dy < 2; ++dy) {
-          float4* cp = reinterpret_cast<float4*>(s.c1 + (c * 24 + 2 * p + dy) * 24 + 8 * qq);
-          const float4 v0 = cp[0], v1 = cp[1];
-          float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-          for (int x = 0; x < 8; ++x) {
-            const float dc = fmul(acc[x >> 1], 0.25f);
-            cv[x] = fmul(fmul(dc, cv[x]), fsub(1.0f, cv[x]));
-          }
-          cp[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
-          cp[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
-        }
-      }
-    } else if (it < kBackin + 360) {
-      const int t = it - kBackin, i = t / 30, r = t - i * 30, c = r / 5, u = r - c * 5;
-      float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll 2
-      for (int y = 0; y < 8; ++y) {
-        const float4* sp = reinterpret_cast<const float4*>(s.s1 + (c * 12 + u + y) * 12);
-        const float4 a = sp[0], b = sp[1], cc = sp[2];
-        const float sr[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, cc.x, cc.y, cc.z, cc.w};
-        const float4* dp = reinterpret_cast<const float4*>(s.dzp + (i * 16 + y + 4) * 16 + 4);
-        const float4 d0 = dp[0], d1 = dp[1];
-        const float dr[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-#pragma unroll
-        for (int x = 0; x < 8; ++x)
-#pragma unroll
-          for (int v = 0; v < 5; ++v) acc[v] = mac<EXACT>(acc[v], sr[v + x], dr[x]);
-      }
-#pragma unroll
-      for (int v = 0; v < 5; ++v) put<ACCUM>(s, row, kK2 + ((i * 6 + c) * 5 + u) * 5 + v, acc[v]);
+      backin_quad<EXACT>(s, it, it < 432);
+    } else if constexpr (EXACT) {
+      gk2_exact<ACCUM>(s, row, it - kBackin);
     } else {
-      const int i = it - kBackin - 360;
-      float acc = 0.0f;
-#pragma unroll
-      for (int y = 0; y < 8; ++y) {
-        const float4* dp = reinterpret_cast<const float4*>(s.dzp + (i * 16 + y + 4) * 16 + 4);
-        const float4 d0 = dp[0], d1 = dp[1];
-        acc = fadd(fadd(fadd(fadd(acc, d0.x), d0.y), d0.z), d0.w);
-        acc = fadd(fadd(fadd(fadd(acc, d1.x), d1.y), d1.z), d1.w);
-      }
-      put<ACCUM>(s, row, kB2 + i, acc);
+      gk2_fast<ACCUM>(s, row, it - kBackin);
     }
   }
 }
 
 // C1 backward: g_k1[i][u][v] = sum_{y,x<24} I[u+y][v+x]*dz1[i][y][x]; g_b1[i] = sum dz1[i].
-// EXACT: one thread per output, the 576 terms in order, reading the v-shifted image copy so every
-// row is two aligned 128-bit loads.  Fast: 2-row partials (432 items) + fixed-order combine.
+// EXACT: one lane per output, the 576 terms in order, reading the v-shifted image copy so every row
+// is aligned 128-bit loads.  Fast: one lane per (i, y) holds all 25 outputs (the dz1 row stays in
+// registers and feeds 5 image rows), then a fixed-order combine over the 24 row partials.
 template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img, float* row) {
   const float* dz1 = s.c1;
@@ -476,7 +561,7 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
         float acc = 0.0f;
 #pragma unroll 2
         for (int y = 0; y < 24; ++y) {
-          const float4* ip = reinterpret_cast<const float4*>(s.sh + (v * 28 + u + y) * 24);
+          const float4* ip = reinterpret_cast<const float4*>(s.sh + sh_at(v, u + y));
           const float4* dp = reinterpret_cast<const float4*>(dz1 + (i * 24 + y) * 24);
 #pragma unroll
           for (int x4 = 0; x4 < 6; ++x4) {
@@ -502,12 +587,22 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
     }
   } else {
     const int it = threadIdx.x;
-    if (it < 360) {  // (i, u, 2-row chunk yc) -> partials for v = 0..4
-      const int i = it / 60, r = it - i * 60, u = r / 12, yc = r - u * 12;
-      float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+    if (it < 144) {  // (i, y): 25 row-partials + the bias row-partial
+      const int i = it / 24, y = it - i * 24;
+      const float4* dp = reinterpret_cast<const float4*>(dz1 + (i * 24 + y) * 24);
+      float dr[24];
 #pragma unroll
-      for (int dy = 0; dy < 2; ++dy) {
-        const int y = 2 * yc + dy;
+      for (int q = 0; q < 6; ++q) {
+        const float4 t = dp[q];
+        dr[4 * q] = t.x; dr[4 * q + 1] = t.y; dr[4 * q + 2] = t.z; dr[4 * q + 3] = t.w;
+      }
+      float bias = 0.0f;
+#pragma unroll
+      for (int x = 0; x < 24; ++x) bias += dr[x];
+      float* out = s.red + it * 26;
+      out[25] = bias;
+#pragma unroll 1
+      for (int u = 0; u < 5; ++u) {
         const float4* ip = reinterpret_cast<const float4*>(img + (u + y) * 28);
         float ir[28];
 #pragma unroll
@@ -515,42 +610,27 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
           const float4 t = ip[q];
           ir[4 * q] = t.x; ir[4 * q + 1] = t.y; ir[4 * q + 2] = t.z; ir[4 * q + 3] = t.w;
         }
-        const float4* dp = reinterpret_cast<const float4*>(dz1 + (i * 24 + y) * 24);
+        float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-        for (int x4 = 0; x4 < 6; ++x4) {
-          const float4 d = dp[x4];
-          const float dv[4] = {d.x, d.y, d.z, d.w};
+        for (int x = 0; x < 24; ++x)
 #pragma unroll
-          for (int xx = 0; xx < 4; ++xx)
+          for (int v = 0; v < 5; ++v) acc[v] = __fmaf_rn(ir[x + v], dr[x], acc[v]);
 #pragma unroll
-            for (int v = 0; v < 5; ++v) acc[v] = __fmaf_rn(ir[4 * x4 + xx + v], dv[xx], acc[v]);
-        }
+        for (int v = 0; v < 5; ++v) out[u * 5 + v] = acc[v];
       }
-#pragma unroll
-      for (int v = 0; v < 5; ++v) s.red[it * 5 + v] = acc[v];
-    } else if (it < 432) {  // g_b1 partials: (i, 2-row chunk)
-      const int j = it - 360, i = j / 12, yc = j - i * 12;
-      const float4* dp = reinterpret_cast<const float4*>(dz1 + i * 576 + yc * 48);
-      float acc = 0.0f;
-#pragma unroll
-      for (int e = 0; e < 12; ++e) {
-        const float4 d = dp[e];
-        acc += (d.x + d.y) + (d.z + d.w);
-      }
-      s.red[1800 + j] = acc;
     }
     __syncthreads();
     for (int t = threadIdx.x; t < 156; t += blockDim.x) {
       float acc = 0.0f;
       if (t < 150) {
-        const int i = t / 25, r = t - i * 25, u = r / 5, v = r - u * 5;
-#pragma unroll
-        for (int yc = 0; yc < 12; ++yc) acc += s.red[((i * 5 + u) * 12 + yc) * 5 + v];
+        const int i = t / 25, k = t - i * 25;
+#pragma unroll 8
+        for (int y = 0; y < 24; ++y) acc += s.red[(i * 24 + y) * 26 + k];
         put<ACCUM>(s, row, kK1 + t, acc);
       } else {
         const int i = t - 150;
-#pragma unroll
-        for (int yc = 0; yc < 12; ++yc) acc += s.red[1800 + i * 12 + yc];
+#pragma unroll 8
+        for (int y = 0; y < 24; ++y) acc += s.red[(i * 24 + y) * 26 + 25];
         put<ACCUM>(s, row, kB1 + i, acc);
       }
     }
