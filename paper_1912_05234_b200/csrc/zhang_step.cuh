@@ -146,7 +146,7 @@ __device__ __forceinline__ float target_of(int i, int label, const float* y) {
 // sh[v][y][x] = I[y][x+v] (x < 24): the EXACT C1 weight gradient reads each shifted row with two
 // aligned 128-bit loads instead of 24 scalar ones.
 __device__ __forceinline__ void build_shifted(const Smem& s, const float* img, int t0, int nt) {
-  for (int q = t0; q < kSh / 4; q += nt) {
+  for (int q = t0; q < 5 * 28 * 6; q += nt) {  // 5 planes x 28 rows x 6 float4
     const int v = q / 168, rem = q - v * 168, y = rem / 6, x4 = 4 * (rem - y * 6);
     const float* srow = img + y * 28 + x4 + v;
     *reinterpret_cast<float4*>(s.sh + sh_at(v, y) + x4) = make_float4(srow[0], srow[1], srow[2], srow[3]);
