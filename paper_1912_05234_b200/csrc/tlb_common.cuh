@@ -146,9 +146,11 @@ __device__ __forceinline__ void grid_sync(unsigned int* counter, unsigned int& t
     __threadfence();
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
     unsigned int v;
-    do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+    while (v < target) {
+      __nanosleep(32);  // back off so 148 pollers do not starve the arrivals on the same L2 line
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-    } while (v < target);
+    }
   }
   __syncthreads();
 }

@@ -558,18 +558,36 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
     for (int it = threadIdx.x; it < 156; it += blockDim.x) {
       if (it < 150) {
         const int i = it / 25, r = it - i * 25, u = r / 5, v = r - u * 5;
+        const float4* ib = reinterpret_cast<const float4*>(s.sh + sh_at(v, u));
+        const float4* db = reinterpret_cast<const float4*>(dz1 + i * 576);
         float acc = 0.0f;
-#pragma unroll 2
-        for (int y = 0; y < 24; ++y) {
-          const float4* ip = reinterpret_cast<const float4*>(s.sh + sh_at(v, u + y));
-          const float4* dp = reinterpret_cast<const float4*>(dz1 + (i * 24 + y) * 24);
+        // software pipeline: row y+1 is in flight while the ordered chain consumes row y
+        float4 a[6], d[6];
 #pragma unroll
-          for (int x4 = 0; x4 < 6; ++x4) {
-            const float4 a = ip[x4], d = dp[x4];
-            acc = mac<true>(acc, a.x, d.x);
-            acc = mac<true>(acc, a.y, d.y);
-            acc = mac<true>(acc, a.z, d.z);
-            acc = mac<true>(acc, a.w, d.w);
+        for (int q = 0; q < 6; ++q) {
+          a[q] = ib[q];
+          d[q] = db[q];
+        }
+#pragma unroll 1
+        for (int y = 0; y < 24; ++y) {
+          const int yn = y + 1 < 24 ? y + 1 : y;
+          float4 an[6], dn[6];
+#pragma unroll
+          for (int q = 0; q < 6; ++q) {
+            an[q] = ib[yn * 6 + q];
+            dn[q] = db[yn * 6 + q];
+          }
+#pragma unroll
+          for (int q = 0; q < 6; ++q) {
+            acc = mac<true>(acc, a[q].x, d[q].x);
+            acc = mac<true>(acc, a[q].y, d[q].y);
+            acc = mac<true>(acc, a[q].z, d[q].z);
+            acc = mac<true>(acc, a[q].w, d[q].w);
+          }
+#pragma unroll
+          for (int q = 0; q < 6; ++q) {
+            a[q] = an[q];
+            d[q] = dn[q];
           }
         }
         put<ACCUM>(s, row, kK1 + it, acc);
