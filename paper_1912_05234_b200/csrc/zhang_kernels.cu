@@ -93,22 +93,23 @@ __device__ __forceinline__ void reduce_slice(const Smem& s, const TrainArgs& a, 
     for (int64_t r0 = 0; r0 < nrows; r0 += R) {
       const int rr = (int)min((int64_t)R, nrows - r0);
       __syncthreads();
-      // all of this thread's loads in flight before any shared store (L2 latency paid once)
-      constexpr int kBatch = 16;
-      for (int base = t; base < rr * W; base += kBatch * blockDim.x) {
-        float v[kBatch];
+      // thread -> (column c, first row); every load of a thread is in flight before its first
+      // shared store, so the L2 round trip is paid once per chunk (no per-element division)
+      const int step = blockDim.x / W, c = t % W, rt = t / W;
+      if (rt < step) {
+        constexpr int kBatch = 8;
+        for (int rb = rt; rb < rr; rb += kBatch * step) {
+          float v[kBatch];
 #pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          const int idx = base + u * blockDim.x;
-          if (idx < rr * W) {
-            const int r = idx / W, c = idx - r * W;
-            v[u] = __ldcg(a.work + (r0 + r) * kPStride + jb + c);
+          for (int u = 0; u < kBatch; ++u) {
+            const int rw = rb + u * step;
+            if (rw < rr) v[u] = __ldcg(a.work + (r0 + rw) * kPStride + jb + c);
           }
-        }
 #pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          const int idx = base + u * blockDim.x;
-          if (idx < rr * W) stage[idx] = v[u];
+          for (int u = 0; u < kBatch; ++u) {
+            const int rw = rb + u * step;
+            if (rw < rr) stage[rw * W + c] = v[u];
+          }
         }
       }
       __syncthreads();
@@ -150,8 +151,15 @@ __device__ __forceinline__ void reduce_loss(const Smem& s, const TrainArgs& a, i
         for (int i = 0; i < n; ++i) l = __dadd_rn(l, (double)stage[i]);
     }
   } else {
-    if (threadIdx.x == 0)
-      for (int64_t r = 0; r < nrows; ++r) l = __dadd_rn(l, __ldcg(a.loss_part + r));
+    double* stage = reinterpret_cast<double*>(s.red);  // fp64 CTA partials, staged in one round trip
+    for (int64_t r0 = 0; r0 < nrows; r0 += 512) {
+      const int n = (int)min((int64_t)512, nrows - r0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) stage[i] = __ldcg(a.loss_part + r0 + i);
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int i = 0; i < n; ++i) l = __dadd_rn(l, stage[i]);
+    }
   }
   if (threadIdx.x == 0) {
     if (a.grad_out) a.loss_out[0] = l;

@@ -349,22 +349,24 @@ __device__ __forceinline__ void stage_fc_back(const Smem& s, float* row) {
 
 // backin d_s1 = sum_i backin(dz2[i], k2[i], s1), then backavgpool + backsigmoid through c1 -> dz1.
 //
-// Lanes come in quads per item (channel c, output rows p0 = 2pp and p0+1, columns 4qq..4qq+3); lane s
-// of the quad owns kernels i = 3s..3s+2.  Per kernel it keeps the 25 weights in registers and streams
-// the six padded dz2 rows the two output rows need, so each loaded row feeds both rows' taps.
+// One lane per item (channel c, output rows p0 = 2pp and p0+1, columns 4qq..4qq+3) runs all twelve
+// kernels in order.  Per kernel it holds the 25 weights in registers and streams the six padded dz2
+// rows its two output rows need, so each loaded row feeds both rows' taps; lanes of a warp share the
+// dz2 rows (broadcast) across channels, which keeps shared-memory traffic ~4x below per-row tiling.
 // The reference's clipped nested sums (nn.cpp:169-189: per i, row sums over u2 from 0, outer sum over
-// u1 from 0) only ever see padded zero products prepended or appended to a row/outer sum, and
-// x + (+-0) == x (with +0 + -0 == +0), so the EXACT terms are bit-identical.  EXACT then hands the
-// per-kernel terms to lane 0 of the quad by shuffle, keeping acc = (((0 + b_0) + b_1) + ... + b_11)
-// (network.cpp:135-138) as one ordered chain; fast mode sums with FFMA and a fixed xor tree.
+// u1 from 0, then acc = acc + term over i as network.cpp:135-138) only ever see padded zero products
+// prepended or appended to a row/outer sum, and x + (+-0) == x (with +0 + -0 == +0), so EXACT stays
+// bit-identical.  Fast mode accumulates every tap with FFMA.
 template <bool EXACT>
-__device__ __forceinline__ void backin_quad(const Smem& s, int lane_item, bool valid) {
-  const int item = valid ? lane_item >> 2 : 0, q4 = lane_item & 3;
+__device__ __forceinline__ void backin_item(const Smem& s, int item) {
   const int c = item / 18, rem = item - c * 18, pp = rem / 3, qq = rem - pp * 3, p0 = 2 * pp;
-  float b[3][2][4];
+  float acc[2][4];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const int i = 3 * q4 + k;
+  for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+    for (int o = 0; o < 4; ++o) acc[orow][o] = 0.0f;
+#pragma unroll 1
+  for (int i = 0; i < 12; ++i) {
     float w[5][5];
 #pragma unroll
     for (int u1 = 0; u1 < 5; ++u1) {
@@ -372,10 +374,11 @@ __device__ __forceinline__ void backin_quad(const Smem& s, int lane_item, bool v
       const float4 w0 = wp[0], w1 = wp[1];
       w[u1][0] = w0.x; w[u1][1] = w0.y; w[u1][2] = w0.z; w[u1][3] = w0.w; w[u1][4] = w1.x;
     }
+    float outer[2][4];
 #pragma unroll
     for (int orow = 0; orow < 2; ++orow)
 #pragma unroll
-      for (int o = 0; o < 4; ++o) b[k][orow][o] = 0.0f;
+      for (int o = 0; o < 4; ++o) outer[orow][o] = 0.0f;
     // padded rows R = p0 + rr, rr = 5..0: output row orow uses tap row u1 = orow + 4 - rr (ascending)
 #pragma unroll
     for (int rr = 5; rr >= 0; --rr) {
@@ -393,59 +396,38 @@ __device__ __forceinline__ void backin_quad(const Smem& s, int lane_item, bool v
 #pragma unroll
             for (int o = 0; o < 4; ++o) rs[o] = mac<true>(rs[o], w[u1][u2], d[o - u2 + 4]);
 #pragma unroll
-          for (int o = 0; o < 4; ++o) b[k][orow][o] = fadd(b[k][orow][o], rs[o]);
+          for (int o = 0; o < 4; ++o) outer[orow][o] = fadd(outer[orow][o], rs[o]);
         } else {
 #pragma unroll
           for (int u2 = 0; u2 < 5; ++u2)
 #pragma unroll
-            for (int o = 0; o < 4; ++o) b[k][orow][o] = __fmaf_rn(w[u1][u2], d[o - u2 + 4], b[k][orow][o]);
+            for (int o = 0; o < 4; ++o) acc[orow][o] = __fmaf_rn(w[u1][u2], d[o - u2 + 4], acc[orow][o]);
         }
       }
     }
+    if constexpr (EXACT) {
+#pragma unroll
+      for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+        for (int o = 0; o < 4; ++o) acc[orow][o] = fadd(acc[orow][o], outer[orow][o]);
+    }
   }
-  float acc[2][4];
-  if constexpr (EXACT) {
-    const int lead = (threadIdx.x & 31) & ~3;
+  // backavgpool (x0.25) + backsigmoid through c1 for the 4x8 block of c1 this item owns
 #pragma unroll
-    for (int orow = 0; orow < 2; ++orow)
+  for (int orow = 0; orow < 2; ++orow)
 #pragma unroll
-      for (int o = 0; o < 4; ++o) {
-        float a = 0.0f;
+    for (int dy = 0; dy < 2; ++dy) {
+      float4* cp = reinterpret_cast<float4*>(s.c1 + (c * 24 + 2 * (p0 + orow) + dy) * 24 + 8 * qq);
+      const float4 v0 = cp[0], v1 = cp[1];
+      float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-        for (int src = 0; src < 4; ++src)
-#pragma unroll
-          for (int k = 0; k < 3; ++k) a = fadd(a, __shfl_sync(0xffffffffu, b[k][orow][o], lead + src));
-        acc[orow][o] = a;
+      for (int x = 0; x < 8; ++x) {
+        const float dc = fmul(acc[orow][x >> 1], 0.25f);
+        cv[x] = fmul(fmul(dc, cv[x]), fsub(1.0f, cv[x]));
       }
-  } else {
-#pragma unroll
-    for (int orow = 0; orow < 2; ++orow)
-#pragma unroll
-      for (int o = 0; o < 4; ++o) {
-        float a = (b[0][orow][o] + b[1][orow][o]) + b[2][orow][o];
-        a += __shfl_xor_sync(0xffffffffu, a, 1);
-        a += __shfl_xor_sync(0xffffffffu, a, 2);
-        acc[orow][o] = a;
-      }
-  }
-  if (valid && q4 == 0) {
-    // backavgpool (x0.25) + backsigmoid through c1 for the 4x8 block of c1 this quad owns
-#pragma unroll
-    for (int orow = 0; orow < 2; ++orow)
-#pragma unroll
-      for (int dy = 0; dy < 2; ++dy) {
-        float4* cp = reinterpret_cast<float4*>(s.c1 + (c * 24 + 2 * (p0 + orow) + dy) * 24 + 8 * qq);
-        const float4 v0 = cp[0], v1 = cp[1];
-        float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-        for (int x = 0; x < 8; ++x) {
-          const float dc = fmul(acc[orow][x >> 1], 0.25f);
-          cv[x] = fmul(fmul(dc, cv[x]), fsub(1.0f, cv[x]));
-        }
-        cp[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
-        cp[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
-      }
-  }
+      cp[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
+      cp[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+    }
 }
 
 // g_k2[i][c][u][v] = sum_{y,x<8} s1[c][u+y][v+x] * dz2[i][y][x] (conv(s1, dz2[i]), nn.cpp:160;
@@ -531,19 +513,18 @@ __device__ __forceinline__ void gk2_fast(const Smem& s, float* row, int t) {
   if (c == 0 && q4 == 0) put<ACCUM>(s, row, kB2 + i, bsum);
 }
 
-// C2 backward stage: backin quads (448 lanes incl. padding) + g_k2/g_b2 lanes.
+// C2 backward stage: backin items on warps 0-3 (108 lanes + padding) run concurrently with the
+// g_k2/g_b2 lanes on the following warps (both read dz2; disjoint outputs).
 template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
-  constexpr int kBackin = 448;                   // 108 quads = 432 lanes, padded to 14 warps
+  constexpr int kBackin = 128;                   // 108 items, padded to 4 whole warps
   constexpr int kGk2 = EXACT ? 372 : 288;        // exact: 360 (i,c,u) lanes + 12 g_b2; fast: 72 quads
-  for (int it = threadIdx.x; it < kBackin + kGk2; it += blockDim.x) {
-    if (it < kBackin) {
-      backin_quad<EXACT>(s, it, it < 432);
-    } else if constexpr (EXACT) {
-      gk2_exact<ACCUM>(s, row, it - kBackin);
-    } else {
-      gk2_fast<ACCUM>(s, row, it - kBackin);
-    }
+  const int it = threadIdx.x;
+  if (it < kBackin) {
+    if (it < 108) backin_item<EXACT>(s, it);
+  } else if (it < kBackin + kGk2) {
+    if constexpr (EXACT) gk2_exact<ACCUM>(s, row, it - kBackin);
+    else gk2_fast<ACCUM>(s, row, it - kBackin);
   }
 }
 
