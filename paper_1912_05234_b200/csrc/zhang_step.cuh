@@ -206,44 +206,59 @@ __device__ __forceinline__ void stage_conv1(const Smem& s, const float* img) {
   }
 }
 
-// C2: mconv(s1,k2,b2) -> sigmoid.  Item = (kernel i, row y, 4-wide half-row xh); per output the
-// 150 taps run (c, ky, kx) row-major.  Fast mode splits the channel sum over two lanes (c < 3 and
-// c >= 3) and combines them with a shuffle; EXACT keeps one ordered chain per output.
+// C2: mconv(s1,k2,b2) -> sigmoid -> avgpool.  One lane per output row (kernel i, row y, 8 columns):
+// per (c, ky) a lane loads the 12-float s1 row segment and the 5 weights and does 40 multiply-adds.
+// Per output the 150 taps run (c, ky, kx) row-major (nn.cpp:14-33).  Fast mode splits the channel
+// sum over a lane pair (c < 3, c >= 3) and combines with a shuffle; EXACT keeps one ordered chain.
+// The two rows of each pooling window are neighbouring lane groups and meet through a shuffle.
 template <bool EXACT>
 __device__ __forceinline__ void stage_conv2(const Smem& s) {
   constexpr int kSplit = EXACT ? 1 : 2;
   const int it = threadIdx.x;
-  if (it >= 192 * kSplit) return;
+  if (it >= 96 * kSplit) return;  // 3 (EXACT) / 6 (fast) whole warps
   const int item = it / kSplit, part = it % kSplit;
-  const int i = item >> 4, r = item & 15, y = r >> 1, xh = r & 1;
-  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  const int i = item >> 3, y = item & 7;
+  float acc[8];
+#pragma unroll
+  for (int o = 0; o < 8; ++o) acc[o] = 0.0f;
   const int c0 = part * (6 / kSplit), c1 = c0 + 6 / kSplit;
 #pragma unroll 1
   for (int c = c0; c < c1; ++c) {
 #pragma unroll
     for (int ky = 0; ky < 5; ++ky) {
-      const float4* src = reinterpret_cast<const float4*>(s.s1 + (c * 12 + y + ky) * 12 + 4 * xh);
-      const float4 v0 = src[0], v1 = src[1];
-      const float in[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      const float4* src = reinterpret_cast<const float4*>(s.s1 + (c * 12 + y + ky) * 12);
+      const float4 v0 = src[0], v1 = src[1], v2 = src[2];
+      const float in[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
       const float4* wp = reinterpret_cast<const float4*>(s.Kp + ((i * 6 + c) * 5 + ky) * 8);
       const float4 w0 = wp[0], w1 = wp[1];
       const float w[5] = {w0.x, w0.y, w0.z, w0.w, w1.x};
 #pragma unroll
       for (int kx = 0; kx < 5; ++kx)
 #pragma unroll
-        for (int o = 0; o < 4; ++o) acc[o] = mac<EXACT>(acc[o], in[o + kx], w[kx]);
+        for (int o = 0; o < 8; ++o) acc[o] = mac<EXACT>(acc[o], in[o + kx], w[kx]);
     }
   }
   if constexpr (!EXACT) {
 #pragma unroll
-    for (int o = 0; o < 4; ++o) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], 1);
-    if (part) return;
+    for (int o = 0; o < 8; ++o) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], 1);
   }
   const float b = s.P[kB2 + i];
-  float t[4];
+  float t[8], u[8];
 #pragma unroll
-  for (int o = 0; o < 4; ++o) t[o] = sigmoid_m<EXACT>(fadd(acc[o], b), s.tab);
-  *reinterpret_cast<float4*>(s.c2 + (i * 8 + y) * 8 + 4 * xh) = make_float4(t[0], t[1], t[2], t[3]);
+  for (int o = 0; o < 8; ++o) t[o] = sigmoid_m<EXACT>(fadd(acc[o], b), s.tab);
+#pragma unroll
+  for (int o = 0; o < 8; ++o) u[o] = __shfl_xor_sync(0xffffffffu, t[o], kSplit);  // row y ^ 1
+  if (part) return;
+  float4* d = reinterpret_cast<float4*>(s.c2 + (i * 8 + y) * 8);
+  d[0] = make_float4(t[0], t[1], t[2], t[3]);
+  d[1] = make_float4(t[4], t[5], t[6], t[7]);
+  if ((y & 1) == 0) {  // avgpool (nn.cpp:144): ((p00 + p01) + p10) + p11, then * 0.25f
+    float pv[4];
+#pragma unroll
+    for (int px = 0; px < 4; ++px)
+      pv[px] = fmul(fadd(fadd(fadd(t[2 * px], t[2 * px + 1]), u[2 * px]), u[2 * px + 1]), 0.25f);
+    *reinterpret_cast<float4*>(s.s2 + (i * 4 + (y >> 1)) * 4) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+  }
 }
 
 __device__ __forceinline__ void stage_pool2(const Smem& s) {
@@ -643,11 +658,9 @@ __device__ __forceinline__ void forward_image(const Smem& s, const float* img, i
   stage_conv1<EXACT>(s, img);
   __syncthreads();
   mark(s, 3);
-  stage_conv2<EXACT>(s);
+  stage_conv2<EXACT>(s);  // includes avgpool
   __syncthreads();
   mark(s, 4);
-  stage_pool2(s);
-  __syncthreads();
   mark(s, 5);
   stage_fc<EXACT>(s, label, y, want_dz);
   __syncthreads();
