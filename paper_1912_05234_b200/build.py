@@ -87,5 +87,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_stage_bench() -> str:
+    """Developer micro-benchmark of the per-image stages (not part of the library)."""
+    os.makedirs(OBJ, exist_ok=True)
+    exe = os.path.join(OBJ, "stage_bench")
+    cmd = [NVCC] + ARCH + COMMON + ["-Xptxas", "-v", "--expt-relaxed-constexpr", os.path.join(CSRC, "stage_bench.cu"),
+                                    "-o", exe]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError(f"stage_bench build failed:\n{out.stderr}")
+    return exe
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    if "--bench" in sys.argv:
+        print(build_stage_bench())

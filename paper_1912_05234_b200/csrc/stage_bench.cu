@@ -1,0 +1,137 @@
+// stage_bench.cu -- developer micro-benchmark for the per-image stages of zhang_step.cuh.
+//
+// One 512-thread CTA per SM (148 CTAs, like the batch-100 train kernel) repeats one stage `iters`
+// times on deterministic pseudo-random shared-memory contents; thread 0 measures clock64 across the
+// loop.  Prints one JSON line per (mode, stage, variant) with the median cycles and us per call.
+// Not part of the product library; build: python -m paper_1912_05234_b200.build --bench
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include "zhang_step.cuh"
+
+using namespace tlb;
+
+enum Stage { kConv1, kConv2V0, kConv2V1, kFc, kFcBack, kC2BackV0, kC2BackV1, kC1Back, kForward, kBackwardV0,
+             kBackwardV1, kNumStages };
+static const char* kNames[kNumStages] = {"conv1", "conv2_v0_halves", "conv2_v1_rows", "fc", "fc_back",
+                                         "conv2_back_v0_quads", "conv2_back_v1_items", "conv1_back",
+                                         "forward_image", "backward_v0", "backward_v1"};
+
+__device__ __forceinline__ float hrand(unsigned int x) {  // deterministic value in [0, 1)
+  x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+  return (x >> 8) * (1.0f / 16777216.0f);
+}
+
+__device__ void fill(const Smem& s) {
+  const int t = threadIdx.x, n = blockDim.x;
+  for (int i = t; i < kPStride; i += n) s.P[i] = i < kNParam ? (hrand(i) - 0.5f) * 0.2f : 0.0f;
+  for (int i = t; i < 2 * kImg; i += n) s.img[i] = hrand(i + 10000);
+  for (int i = t; i < 3456; i += n) s.c1[i] = 0.3f + 0.4f * hrand(i + 20000);
+  for (int i = t; i < 864; i += n) s.s1[i] = 0.3f + 0.4f * hrand(i + 30000);
+  for (int i = t; i < 768; i += n) s.c2[i] = 0.3f + 0.4f * hrand(i + 40000);
+  for (int i = t; i < 192; i += n) s.s2[i] = 0.3f + 0.4f * hrand(i + 50000);
+  if (t < 16) { s.out[t] = 0.5f; s.dz[t] = (hrand(t + 60000) - 0.5f) * 0.1f; }
+  for (int i = t; i < kPStride; i += n) s.G[i] = 0.0f;
+  __syncthreads();
+  for (int idx = t; idx < kKp; idx += n) {
+    const int row = idx >> 3, k = idx & 7;
+    s.Kp[idx] = k < 5 ? s.P[kK2 + row * 5 + k] : 0.0f;
+  }
+  for (int q = t; q < 12 * 64; q += n) {
+    const int i = q >> 6, y = (q >> 3) & 7, x = q & 7;
+    s.dzp[dzp_at(i, y + 4, x + 4)] = (hrand(q + 70000) - 0.5f) * 0.01f;
+  }
+  build_shifted(s, s.img, t, n);
+  __syncthreads();
+}
+
+template <bool EXACT, int STAGE>
+__device__ __forceinline__ void run_stage(const Smem& s, float* row) {
+  constexpr bool A = !EXACT;
+  if constexpr (STAGE == kConv1) stage_conv1<EXACT>(s, s.img);
+  else if constexpr (STAGE == kConv2V0) stage_conv2<EXACT, 0>(s);
+  else if constexpr (STAGE == kConv2V1) stage_conv2<EXACT, 1>(s);
+  else if constexpr (STAGE == kFc) stage_fc<EXACT>(s, 3, nullptr, true);
+  else if constexpr (STAGE == kFcBack) stage_fc_back<EXACT, A>(s, row);
+  else if constexpr (STAGE == kC2BackV0) stage_conv2_back<EXACT, A, 0>(s, row);
+  else if constexpr (STAGE == kC2BackV1) stage_conv2_back<EXACT, A, 1>(s, row);
+  else if constexpr (STAGE == kC1Back) stage_conv1_back<EXACT, A>(s, s.img, row);
+  else if constexpr (STAGE == kForward) forward_image<EXACT>(s, s.img, 3, nullptr, true);
+  else if constexpr (STAGE == kBackwardV0) {
+    stage_fc_back<EXACT, A>(s, row);
+    __syncthreads();
+    stage_conv2_back<EXACT, A, 0>(s, row);
+    __syncthreads();
+    stage_conv1_back<EXACT, A>(s, s.img, row);
+  } else {
+    stage_fc_back<EXACT, A>(s, row);
+    __syncthreads();
+    stage_conv2_back<EXACT, A, 1>(s, row);
+    __syncthreads();
+    stage_conv1_back<EXACT, A>(s, s.img, row);
+  }
+}
+
+template <bool EXACT, int STAGE>
+__global__ void __launch_bounds__(kThreads, 1) stage_kernel(float* rows, unsigned long long* cycles, int iters) {
+  extern __shared__ __align__(128) float smem_raw[];
+  const Smem s = carve_smem(smem_raw);
+  smem_setup(s);
+  fill(s);
+  float* row = rows + (size_t)blockIdx.x * kPStride;
+  run_stage<EXACT, STAGE>(s, row);  // warm-up
+  __syncthreads();
+  const unsigned long long t0 = clock64();
+  for (int k = 0; k < iters; ++k) {
+    run_stage<EXACT, STAGE>(s, row);
+    __syncthreads();
+  }
+  const unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
+template <bool EXACT, int STAGE>
+void measure(float* rows, unsigned long long* d_cycles, int sms, int iters, double mhz) {
+  auto k = stage_kernel<EXACT, STAGE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  k<<<sms, kThreads, kSmemBytes>>>(rows, d_cycles, iters);
+  cudaError_t e = cudaDeviceSynchronize();
+  std::vector<unsigned long long> c(sms);
+  cudaMemcpy(c.data(), d_cycles, sms * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  std::sort(c.begin(), c.end());
+  const double med = (double)c[sms / 2] / iters, mx = (double)c[sms - 1] / iters;
+  printf("{\"mode\": \"%s\", \"stage\": \"%s\", \"cycles\": %.0f, \"us\": %.3f, \"us_max_cta\": %.3f, \"err\": \"%s\"}\n",
+         EXACT ? "exact" : "fast", kNames[STAGE], med, med / mhz, mx / mhz, cudaGetErrorString(e));
+}
+
+template <bool EXACT>
+void all(float* rows, unsigned long long* d_cycles, int sms, int iters, double mhz) {
+  measure<EXACT, kConv1>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kConv2V0>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kConv2V1>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kFc>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kFcBack>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kC2BackV0>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kC2BackV1>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kC1Back>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kForward>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kBackwardV0>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kBackwardV1>(rows, d_cycles, sms, iters, mhz);
+}
+
+int main(int argc, char** argv) {
+  const int iters = argc > 1 ? atoi(argv[1]) : 100;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  float* rows;
+  unsigned long long* d_cycles;
+  cudaMalloc(&rows, (size_t)sms * kPStride * sizeof(float));
+  cudaMalloc(&d_cycles, sms * sizeof(unsigned long long));
+  const double mhz = 1965.0;
+  all<false>(rows, d_cycles, sms, iters, mhz);
+  all<true>(rows, d_cycles, sms, iters, mhz);
+  return 0;
+}

@@ -212,7 +212,7 @@ __device__ __forceinline__ void stage_conv1(const Smem& s, const float* img) {
 // sum over a lane pair (c < 3, c >= 3) and combines with a shuffle; EXACT keeps one ordered chain.
 // The two rows of each pooling window are neighbouring lane groups and meet through a shuffle.
 template <bool EXACT>
-__device__ __forceinline__ void stage_conv2(const Smem& s) {
+__device__ __forceinline__ void stage_conv2_rows(const Smem& s) {
   constexpr int kSplit = EXACT ? 1 : 2;
   const int it = threadIdx.x;
   if (it >= 96 * kSplit) return;  // 3 (EXACT) / 6 (fast) whole warps
@@ -261,7 +261,60 @@ __device__ __forceinline__ void stage_conv2(const Smem& s) {
   }
 }
 
+// C2 variant with 4-output lanes (kernel i, row y, half-row xh): twice the lanes of stage_conv2_rows,
+// so more warps hide the shared-memory latency.  Pool partner (row y^1) is lane ^ (2*kSplit).
+template <bool EXACT>
+__device__ __forceinline__ void stage_conv2_halves(const Smem& s) {
+  constexpr int kSplit = EXACT ? 1 : 2;
+  const int it = threadIdx.x;
+  if (it >= 192 * kSplit) return;  // 6 (EXACT) / 12 (fast) whole warps
+  const int item = it / kSplit, part = it % kSplit;
+  const int xh = item & 1, y = (item >> 1) & 7, i = item >> 4;
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  const int c0 = part * (6 / kSplit), c1 = c0 + 6 / kSplit;
+#pragma unroll 1
+  for (int c = c0; c < c1; ++c) {
+#pragma unroll
+    for (int ky = 0; ky < 5; ++ky) {
+      const float4* src = reinterpret_cast<const float4*>(s.s1 + (c * 12 + y + ky) * 12 + 4 * xh);
+      const float4 v0 = src[0], v1 = src[1];
+      const float in[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      const float4* wp = reinterpret_cast<const float4*>(s.Kp + ((i * 6 + c) * 5 + ky) * 8);
+      const float4 w0 = wp[0], w1 = wp[1];
+      const float w[5] = {w0.x, w0.y, w0.z, w0.w, w1.x};
+#pragma unroll
+      for (int kx = 0; kx < 5; ++kx)
+#pragma unroll
+        for (int o = 0; o < 4; ++o) acc[o] = mac<EXACT>(acc[o], in[o + kx], w[kx]);
+    }
+  }
+  if constexpr (!EXACT) {
+#pragma unroll
+    for (int o = 0; o < 4; ++o) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], 1);
+  }
+  const float b = s.P[kB2 + i];
+  float t[4], u[4];
+#pragma unroll
+  for (int o = 0; o < 4; ++o) t[o] = sigmoid_m<EXACT>(fadd(acc[o], b), s.tab);
+#pragma unroll
+  for (int o = 0; o < 4; ++o) u[o] = __shfl_xor_sync(0xffffffffu, t[o], 2 * kSplit);  // row y ^ 1
+  if (part) return;
+  *reinterpret_cast<float4*>(s.c2 + (i * 8 + y) * 8 + 4 * xh) = make_float4(t[0], t[1], t[2], t[3]);
+  if ((y & 1) == 0) {  // avgpool (nn.cpp:144): ((p00 + p01) + p10) + p11, then * 0.25f
+    const float p0 = fmul(fadd(fadd(fadd(t[0], t[1]), u[0]), u[1]), 0.25f);
+    const float p1 = fmul(fadd(fadd(fadd(t[2], t[3]), u[2]), u[3]), 0.25f);
+    *reinterpret_cast<float2*>(s.s2 + (i * 4 + (y >> 1)) * 4 + 2 * xh) = make_float2(p0, p1);
+  }
+}
+
+template <bool EXACT, int V>
+__device__ __forceinline__ void stage_conv2(const Smem& s) {
+  if constexpr (V == 0) stage_conv2_halves<EXACT>(s);
+  else stage_conv2_rows<EXACT>(s);
+}
+
 __device__ __forceinline__ void stage_pool2(const Smem& s) {
+
   for (int t = threadIdx.x; t < 192; t += blockDim.x) {
     const int c = t >> 4, py = (t >> 2) & 3, px = t & 3;
     const float* q = s.c2 + (c * 8 + 2 * py) * 8 + 2 * px;
@@ -445,6 +498,99 @@ __device__ __forceinline__ void backin_item(const Smem& s, int item) {
     }
 }
 
+// backin variant: lane quads split the twelve kernels 3 per lane; EXACT hands the per-kernel terms to
+// lane 0 of the quad by shuffle so the ordered chain over i stays on one lane.
+template <bool EXACT>
+__device__ __forceinline__ void backin_quad(const Smem& s, int lane_item, bool valid) {
+  const int item = valid ? lane_item >> 2 : 0, q4 = lane_item & 3;
+  const int c = item / 18, rem = item - c * 18, pp = rem / 3, qq = rem - pp * 3, p0 = 2 * pp;
+  float b[3][2][4];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int i = 3 * q4 + k;
+    float w[5][5];
+#pragma unroll
+    for (int u1 = 0; u1 < 5; ++u1) {
+      const float4* wp = reinterpret_cast<const float4*>(s.Kp + ((i * 6 + c) * 5 + u1) * 8);
+      const float4 w0 = wp[0], w1 = wp[1];
+      w[u1][0] = w0.x; w[u1][1] = w0.y; w[u1][2] = w0.z; w[u1][3] = w0.w; w[u1][4] = w1.x;
+    }
+#pragma unroll
+    for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+      for (int o = 0; o < 4; ++o) b[k][orow][o] = 0.0f;
+    // padded rows R = p0 + rr, rr = 5..0: output row orow uses tap row u1 = orow + 4 - rr (ascending)
+#pragma unroll
+    for (int rr = 5; rr >= 0; --rr) {
+      const float4* dp = reinterpret_cast<const float4*>(s.dzp + dzp_at(i, p0 + rr, 4 * qq));
+      const float4 d0 = dp[0], d1 = dp[1];
+      const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+      for (int orow = 0; orow < 2; ++orow) {
+        const int u1 = orow + 4 - rr;
+        if (u1 < 0 || u1 > 4) continue;
+        if constexpr (EXACT) {
+          float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+          for (int u2 = 0; u2 < 5; ++u2)
+#pragma unroll
+            for (int o = 0; o < 4; ++o) rs[o] = mac<true>(rs[o], w[u1][u2], d[o - u2 + 4]);
+#pragma unroll
+          for (int o = 0; o < 4; ++o) b[k][orow][o] = fadd(b[k][orow][o], rs[o]);
+        } else {
+#pragma unroll
+          for (int u2 = 0; u2 < 5; ++u2)
+#pragma unroll
+            for (int o = 0; o < 4; ++o) b[k][orow][o] = __fmaf_rn(w[u1][u2], d[o - u2 + 4], b[k][orow][o]);
+        }
+      }
+    }
+  }
+  float acc[2][4];
+  if constexpr (EXACT) {
+    const int lead = (threadIdx.x & 31) & ~3;
+#pragma unroll
+    for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        float a = 0.0f;
+#pragma unroll
+        for (int src = 0; src < 4; ++src)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) a = fadd(a, __shfl_sync(0xffffffffu, b[k][orow][o], lead + src));
+        acc[orow][o] = a;
+      }
+  } else {
+#pragma unroll
+    for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        float a = (b[0][orow][o] + b[1][orow][o]) + b[2][orow][o];
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        acc[orow][o] = a;
+      }
+  }
+  if (valid && q4 == 0) {
+    // backavgpool (x0.25) + backsigmoid through c1 for the 4x8 block of c1 this quad owns
+#pragma unroll
+    for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy) {
+        float4* cp = reinterpret_cast<float4*>(s.c1 + (c * 24 + 2 * (p0 + orow) + dy) * 24 + 8 * qq);
+        const float4 v0 = cp[0], v1 = cp[1];
+        float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          const float dc = fmul(acc[orow][x >> 1], 0.25f);
+          cv[x] = fmul(fmul(dc, cv[x]), fsub(1.0f, cv[x]));
+        }
+        cp[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
+        cp[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+      }
+  }
+}
+
 // g_k2[i][c][u][v] = sum_{y,x<8} s1[c][u+y][v+x] * dz2[i][y][x] (conv(s1, dz2[i]), nn.cpp:160;
 // 64 taps row-major) and g_b2[i] = sum_all(dz2[i]).  EXACT: one lane per (i,c,u), five ordered chains.
 template <bool ACCUM>
@@ -528,18 +674,31 @@ __device__ __forceinline__ void gk2_fast(const Smem& s, float* row, int t) {
   if (c == 0 && q4 == 0) put<ACCUM>(s, row, kB2 + i, bsum);
 }
 
-// C2 backward stage: backin items on warps 0-3 (108 lanes + padding) run concurrently with the
-// g_k2/g_b2 lanes on the following warps (both read dz2; disjoint outputs).
-template <bool EXACT, bool ACCUM>
+// C2 backward stage.  V = 0: backin lane quads on warps 0-13 (432 lanes), then the g_k2/g_b2 lanes;
+// V = 1: one backin lane per item on warps 0-3, concurrent with the g_k2/g_b2 lanes on warps 4+.
+template <bool EXACT, bool ACCUM, int V>
 __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
-  constexpr int kBackin = 128;                   // 108 items, padded to 4 whole warps
-  constexpr int kGk2 = EXACT ? 372 : 288;        // exact: 360 (i,c,u) lanes + 12 g_b2; fast: 72 quads
-  const int it = threadIdx.x;
-  if (it < kBackin) {
-    if (it < 108) backin_item<EXACT>(s, it);
-  } else if (it < kBackin + kGk2) {
-    if constexpr (EXACT) gk2_exact<ACCUM>(s, row, it - kBackin);
-    else gk2_fast<ACCUM>(s, row, it - kBackin);
+  constexpr int kGk2 = EXACT ? 372 : 288;  // exact: 360 (i,c,u) lanes + 12 g_b2; fast: 72 quads
+  if constexpr (V == 0) {
+    constexpr int kBackin = 448;  // 108 quads = 432 lanes, padded to 14 warps
+    for (int it = threadIdx.x; it < kBackin + kGk2; it += blockDim.x) {
+      if (it < kBackin) {
+        backin_quad<EXACT>(s, it, it < 432);
+      } else if constexpr (EXACT) {
+        gk2_exact<ACCUM>(s, row, it - kBackin);
+      } else {
+        gk2_fast<ACCUM>(s, row, it - kBackin);
+      }
+    }
+  } else {
+    constexpr int kBackin = 128;  // 108 items, padded to 4 whole warps
+    const int it = threadIdx.x;
+    if (it < kBackin) {
+      if (it < 108) backin_item<EXACT>(s, it);
+    } else if (it < kBackin + kGk2) {
+      if constexpr (EXACT) gk2_exact<ACCUM>(s, row, it - kBackin);
+      else gk2_fast<ACCUM>(s, row, it - kBackin);
+    }
   }
 }
 
@@ -651,6 +810,13 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
   }
 }
 
+// Stage variants used by the product kernels (chosen with paper_1912_05234_b200/csrc/stage_bench.cu).
+template <bool EXACT>
+struct StageCfg {
+  static constexpr int conv2 = 0;
+  static constexpr int conv2_back = EXACT ? 1 : 0;
+};
+
 // Whole forward pass of one image (image already in shared memory).
 template <bool EXACT>
 __device__ __forceinline__ void forward_image(const Smem& s, const float* img, int label, const float* y,
@@ -658,7 +824,7 @@ __device__ __forceinline__ void forward_image(const Smem& s, const float* img, i
   stage_conv1<EXACT>(s, img);
   __syncthreads();
   mark(s, 3);
-  stage_conv2<EXACT>(s);  // includes avgpool
+  stage_conv2<EXACT, StageCfg<EXACT>::conv2>(s);  // includes avgpool
   __syncthreads();
   mark(s, 4);
   mark(s, 5);
@@ -673,7 +839,7 @@ __device__ __forceinline__ void backward_image(const Smem& s, const float* img, 
   stage_fc_back<EXACT, ACCUM>(s, row);
   __syncthreads();
   mark(s, 7);
-  stage_conv2_back<EXACT, ACCUM>(s, row);
+  stage_conv2_back<EXACT, ACCUM, StageCfg<EXACT>::conv2_back>(s, row);
   __syncthreads();
   mark(s, 8);
   stage_conv1_back<EXACT, ACCUM>(s, img, row);
