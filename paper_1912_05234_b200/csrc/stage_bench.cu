@@ -77,8 +77,7 @@ __device__ __forceinline__ void run_stage(const Smem& s, float* row) {
 
 template <bool EXACT, int STAGE>
 __global__ void __launch_bounds__(kThreads, 1) stage_kernel(float* rows, unsigned long long* cycles, int iters) {
-  extern __shared__ __align__(128) float smem_raw[];
-  const Smem s = carve_smem(smem_raw);
+  const Smem s = carve_smem(tlb_smem);
   smem_setup(s);
   fill(s);
   float* row = rows + (size_t)blockIdx.x * kPStride;

@@ -170,8 +170,7 @@ __device__ __forceinline__ void reduce_loss(const Smem& s, const TrainArgs& a, i
 
 template <bool EXACT>
 __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
-  extern __shared__ __align__(128) float smem_raw[];
-  Smem s = carve_smem(smem_raw);
+  Smem s = carve_smem(tlb_smem);
   smem_setup(s);
   unsigned int target = 0;
   const int G = gridDim.x;
@@ -254,8 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
 // ------------------------------------------------------------------------------------------------
 template <bool EXACT>
 __global__ void __launch_bounds__(kThreads, 1) cells_kernel(CellArgs a) {
-  extern __shared__ __align__(128) float smem_raw[];
-  const Smem s = carve_smem(smem_raw);
+  const Smem s = carve_smem(tlb_smem);
   smem_setup(s);
   int64_t lo, hi;
   static_chunk(a.n, gridDim.x, blockIdx.x, lo, hi);
@@ -317,8 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1) cells_kernel(CellArgs a) {
 // ------------------------------------------------------------------------------------------------
 template <bool EXACT>
 __global__ void __launch_bounds__(kThreads, 1) eval_kernel(EvalArgs a) {
-  extern __shared__ __align__(128) float smem_raw[];
-  const Smem s = carve_smem(smem_raw);
+  const Smem s = carve_smem(tlb_smem);
   smem_setup(s);
   int64_t lo, hi;
   static_chunk(a.n, gridDim.x, blockIdx.x, lo, hi);

@@ -70,6 +70,9 @@ constexpr int kSmemFloats =
     kPStride + kKp + 2 * kImg + kSh + 3456 + 864 + 768 + 192 + 16 + 16 + kDzp + 1920 + kRed + kPStride;
 constexpr size_t kSmemBytes = sizeof(float) * kSmemFloats + 32 * sizeof(uint64_t) + 2 * sizeof(uint64_t);
 
+// The CTA's dynamic shared memory (one declaration for every kernel and stage).
+extern __shared__ __align__(128) float tlb_smem[];
+
 __device__ __forceinline__ Smem carve_smem(float* base) {
   Smem s;
   float* p = base;
@@ -92,6 +95,8 @@ __device__ __forceinline__ Smem carve_smem(float* base) {
   s.tr = nullptr;
   return s;
 }
+
+__device__ __forceinline__ Smem smem_view() { return carve_smem(tlb_smem); }
 
 // One-time per-CTA setup: exp2 table, zero padding of dz2, image mbarriers.
 __device__ __forceinline__ void smem_setup(const Smem& s) {
@@ -817,18 +822,42 @@ struct StageCfg {
   static constexpr int conv2_back = EXACT ? 1 : 0;
 };
 
+// ---------------------------------------------------------------------------------------------
+// Out-of-line stage entry points.  Each stage is compiled as its own function so the register
+// allocator schedules it without the persistent kernel's long-lived state (step/job/prefetch
+// bookkeeping) occupying registers; the stages re-derive the shared-memory map themselves.
+// ---------------------------------------------------------------------------------------------
+template <bool EXACT>
+__device__ __noinline__ void call_conv1(const float* img) { stage_conv1<EXACT>(smem_view(), img); }
+template <bool EXACT>
+__device__ __noinline__ void call_conv2() { stage_conv2<EXACT, StageCfg<EXACT>::conv2>(smem_view()); }
+template <bool EXACT>
+__device__ __noinline__ void call_fc(int label, const float* y, bool want_dz) {
+  stage_fc<EXACT>(smem_view(), label, y, want_dz);
+}
+template <bool EXACT, bool ACCUM>
+__device__ __noinline__ void call_fc_back(float* row) { stage_fc_back<EXACT, ACCUM>(smem_view(), row); }
+template <bool EXACT, bool ACCUM>
+__device__ __noinline__ void call_conv2_back(float* row) {
+  stage_conv2_back<EXACT, ACCUM, StageCfg<EXACT>::conv2_back>(smem_view(), row);
+}
+template <bool EXACT, bool ACCUM>
+__device__ __noinline__ void call_conv1_back(const float* img, float* row) {
+  stage_conv1_back<EXACT, ACCUM>(smem_view(), img, row);
+}
+
 // Whole forward pass of one image (image already in shared memory).
 template <bool EXACT>
 __device__ __forceinline__ void forward_image(const Smem& s, const float* img, int label, const float* y,
                                               bool want_dz) {
-  stage_conv1<EXACT>(s, img);
+  call_conv1<EXACT>(img);
   __syncthreads();
   mark(s, 3);
-  stage_conv2<EXACT, StageCfg<EXACT>::conv2>(s);  // includes avgpool
+  call_conv2<EXACT>();  // includes avgpool
   __syncthreads();
   mark(s, 4);
   mark(s, 5);
-  stage_fc<EXACT>(s, label, y, want_dz);
+  call_fc<EXACT>(label, y, want_dz);
   __syncthreads();
   mark(s, 6);
 }
@@ -836,13 +865,13 @@ __device__ __forceinline__ void forward_image(const Smem& s, const float* img, i
 // Whole backward pass (after forward_image with want_dz).  Ends with a __syncthreads.
 template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void backward_image(const Smem& s, const float* img, float* row) {
-  stage_fc_back<EXACT, ACCUM>(s, row);
+  call_fc_back<EXACT, ACCUM>(row);
   __syncthreads();
   mark(s, 7);
-  stage_conv2_back<EXACT, ACCUM, StageCfg<EXACT>::conv2_back>(s, row);
+  call_conv2_back<EXACT, ACCUM>(row);
   __syncthreads();
   mark(s, 8);
-  stage_conv1_back<EXACT, ACCUM>(s, img, row);
+  call_conv1_back<EXACT, ACCUM>(img, row);
   __syncthreads();
   mark(s, 9);
 }
