@@ -22,6 +22,10 @@
 namespace tlb {
 
 constexpr int kThreads = 512;
+#ifndef TLB_EXACT_C1_PIPELINED
+#define TLB_EXACT_C1_PIPELINED 1
+#endif
+constexpr bool kExactC1Pipelined = TLB_EXACT_C1_PIPELINED;
 
 struct Smem {
   float* P;    // parameters [3904]
@@ -38,6 +42,7 @@ struct Smem {
   float* fcp;  // EXACT FC products [10][192]
   float* red;  // fast C1 weight-gradient row partials [144][26]
   float* G;    // fast per-CTA gradient accumulator [3904]
+  float* prod; // EXACT C1 weight-gradient product ring [2][150][48]
   uint64_t* tab;
   uint64_t* bar;
   unsigned long long* tr;  // optional per-stage clock64 trace (CTA 0 only), nullptr otherwise
@@ -63,11 +68,13 @@ constexpr int kDzpRow = 20;             // padded dz2 row: 16 used columns
 constexpr int kDzpK = 16 * kDzpRow + 4; // padded dz2 kernel (i) stride
 constexpr int kDzp = 12 * kDzpK;
 constexpr int kRed = 144 * 26;          // fast C1 weight-gradient row partials
+constexpr int kProdChunk = 150 * 48;    // EXACT C1 weight-gradient products of 2 image rows
 
 __device__ __forceinline__ int dzp_at(int i, int R, int col) { return i * kDzpK + R * kDzpRow + col; }
 __device__ __forceinline__ int sh_at(int v, int y) { return v * kShPlane + y * 24; }
 constexpr int kSmemFloats =
-    kPStride + kKp + 2 * kImg + kSh + 3456 + 864 + 768 + 192 + 16 + 16 + kDzp + 1920 + kRed + kPStride;
+    kPStride + kKp + 2 * kImg + kSh + 3456 + 864 + 768 + 192 + 16 + 16 + kDzp + 1920 + kRed + kPStride +
+    2 * kProdChunk;
 constexpr size_t kSmemBytes = sizeof(float) * kSmemFloats + 32 * sizeof(uint64_t) + 2 * sizeof(uint64_t);
 
 // The CTA's dynamic shared memory (one declaration for every kernel and stage).
@@ -90,6 +97,7 @@ __device__ __forceinline__ Smem carve_smem(float* base) {
   s.fcp = p; p += 1920;
   s.red = p; p += kRed;
   s.G = p; p += kPStride;
+  s.prod = p; p += 2 * kProdChunk;
   s.tab = reinterpret_cast<uint64_t*>(p);
   s.bar = s.tab + 32;
   s.tr = nullptr;
@@ -97,6 +105,14 @@ __device__ __forceinline__ Smem carve_smem(float* base) {
 }
 
 __device__ __forceinline__ Smem smem_view() { return carve_smem(tlb_smem); }
+
+// Named CTA barriers (id 0 is __syncthreads): producers arrive, consumers sync (or vice versa).
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // One-time per-CTA setup: exp2 table, zero padding of dz2, image mbarriers.
 __device__ __forceinline__ void smem_setup(const Smem& s) {
@@ -430,62 +446,52 @@ __device__ __forceinline__ void stage_fc_back(const Smem& s, float* row) {
 // u1 from 0, then acc = acc + term over i as network.cpp:135-138) only ever see padded zero products
 // prepended or appended to a row/outer sum, and x + (+-0) == x (with +0 + -0 == +0), so EXACT stays
 // bit-identical.  Fast mode accumulates every tap with FFMA.
+// backin term of kernel i for the 2x4 output tile (p0.., 4qq..): ordered nested sums (EXACT) into
+// b[orow][o], or FFMA accumulation straight into acc (fast).
 template <bool EXACT>
-__device__ __forceinline__ void backin_item(const Smem& s, int item) {
-  const int c = item / 18, rem = item - c * 18, pp = rem / 3, qq = rem - pp * 3, p0 = 2 * pp;
-  float acc[2][4];
+__device__ __forceinline__ void backin_kernel_term(const Smem& s, int i, int c, int p0, int qq, float (&b)[2][4],
+                                                   float (&acc)[2][4]) {
+  float w[5][5];
+#pragma unroll
+  for (int u1 = 0; u1 < 5; ++u1) {
+    const float4* wp = reinterpret_cast<const float4*>(s.Kp + ((i * 6 + c) * 5 + u1) * 8);
+    const float4 w0 = wp[0], w1 = wp[1];
+    w[u1][0] = w0.x; w[u1][1] = w0.y; w[u1][2] = w0.z; w[u1][3] = w0.w; w[u1][4] = w1.x;
+  }
 #pragma unroll
   for (int orow = 0; orow < 2; ++orow)
 #pragma unroll
-    for (int o = 0; o < 4; ++o) acc[orow][o] = 0.0f;
-#pragma unroll 1
-  for (int i = 0; i < 12; ++i) {
-    float w[5][5];
+    for (int o = 0; o < 4; ++o) b[orow][o] = 0.0f;
+  // padded rows R = p0 + rr, rr = 5..0: output row orow uses tap row u1 = orow + 4 - rr (ascending)
 #pragma unroll
-    for (int u1 = 0; u1 < 5; ++u1) {
-      const float4* wp = reinterpret_cast<const float4*>(s.Kp + ((i * 6 + c) * 5 + u1) * 8);
-      const float4 w0 = wp[0], w1 = wp[1];
-      w[u1][0] = w0.x; w[u1][1] = w0.y; w[u1][2] = w0.z; w[u1][3] = w0.w; w[u1][4] = w1.x;
-    }
-    float outer[2][4];
+  for (int rr = 5; rr >= 0; --rr) {
+    const float4* dp = reinterpret_cast<const float4*>(s.dzp + dzp_at(i, p0 + rr, 4 * qq));
+    const float4 d0 = dp[0], d1 = dp[1];
+    const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
 #pragma unroll
-    for (int orow = 0; orow < 2; ++orow)
+    for (int orow = 0; orow < 2; ++orow) {
+      const int u1 = orow + 4 - rr;
+      if (u1 < 0 || u1 > 4) continue;
+      if constexpr (EXACT) {
+        float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-      for (int o = 0; o < 4; ++o) outer[orow][o] = 0.0f;
-    // padded rows R = p0 + rr, rr = 5..0: output row orow uses tap row u1 = orow + 4 - rr (ascending)
+        for (int u2 = 0; u2 < 5; ++u2)
 #pragma unroll
-    for (int rr = 5; rr >= 0; --rr) {
-      const float4* dp = reinterpret_cast<const float4*>(s.dzp + dzp_at(i, p0 + rr, 4 * qq));
-      const float4 d0 = dp[0], d1 = dp[1];
-      const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+          for (int o = 0; o < 4; ++o) rs[o] = mac<true>(rs[o], w[u1][u2], d[o - u2 + 4]);
 #pragma unroll
-      for (int orow = 0; orow < 2; ++orow) {
-        const int u1 = orow + 4 - rr;
-        if (u1 < 0 || u1 > 4) continue;
-        if constexpr (EXACT) {
-          float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int o = 0; o < 4; ++o) b[orow][o] = fadd(b[orow][o], rs[o]);
+      } else {
 #pragma unroll
-          for (int u2 = 0; u2 < 5; ++u2)
+        for (int u2 = 0; u2 < 5; ++u2)
 #pragma unroll
-            for (int o = 0; o < 4; ++o) rs[o] = mac<true>(rs[o], w[u1][u2], d[o - u2 + 4]);
-#pragma unroll
-          for (int o = 0; o < 4; ++o) outer[orow][o] = fadd(outer[orow][o], rs[o]);
-        } else {
-#pragma unroll
-          for (int u2 = 0; u2 < 5; ++u2)
-#pragma unroll
-            for (int o = 0; o < 4; ++o) acc[orow][o] = __fmaf_rn(w[u1][u2], d[o - u2 + 4], acc[orow][o]);
-        }
+          for (int o = 0; o < 4; ++o) acc[orow][o] = __fmaf_rn(w[u1][u2], d[o - u2 + 4], acc[orow][o]);
       }
     }
-    if constexpr (EXACT) {
-#pragma unroll
-      for (int orow = 0; orow < 2; ++orow)
-#pragma unroll
-        for (int o = 0; o < 4; ++o) acc[orow][o] = fadd(acc[orow][o], outer[orow][o]);
-    }
   }
-  // backavgpool (x0.25) + backsigmoid through c1 for the 4x8 block of c1 this item owns
+}
+
+// backavgpool (x0.25) + backsigmoid through c1 for the 4x8 block of c1 owned by a backin tile.
+__device__ __forceinline__ void backin_to_dz1(const Smem& s, int c, int p0, int qq, const float (&acc)[2][4]) {
 #pragma unroll
   for (int orow = 0; orow < 2; ++orow)
 #pragma unroll
@@ -501,6 +507,78 @@ __device__ __forceinline__ void backin_item(const Smem& s, int item) {
       cp[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
       cp[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
     }
+}
+
+// backin d_s1 = sum_i backin(dz2[i], k2[i], s1), then backavgpool + backsigmoid through c1 -> dz1.
+//
+// Item = (channel c, output rows p0 = 2pp and p0+1, columns 4qq..4qq+3); NSPLIT lanes share an item,
+// lane `part` running kernels [part*12/NSPLIT, (part+1)*12/NSPLIT).  Per kernel a lane holds the 25
+// weights in registers and streams the six padded dz2 rows the two output rows need, so each loaded
+// row feeds both rows' taps; lanes of a warp share the dz2 rows (broadcast) across channels.
+// The reference's clipped nested sums (nn.cpp:169-189: per i, row sums over u2 from 0, outer sum over
+// u1 from 0, then acc = acc + term over i as network.cpp:135-138) only ever see padded zero products
+// prepended or appended to a row/outer sum, and x + (+-0) == x (with +0 + -0 == +0), so EXACT stays
+// bit-identical; with NSPLIT = 2 the second lane's six per-kernel terms reach the first lane by
+// shuffle, in kernel order.  Fast mode accumulates every tap with FFMA and combines with one xor.
+template <bool EXACT, int NSPLIT>
+__device__ __forceinline__ void backin_tile(const Smem& s, int lane_item, bool valid) {
+  const int item = valid ? lane_item / NSPLIT : 0, part = lane_item % NSPLIT;
+  const int c = item / 18, rem = item - c * 18, pp = rem / 3, qq = rem - pp * 3, p0 = 2 * pp;
+  constexpr int KPL = 12 / NSPLIT;  // kernels per lane
+  float acc[2][4];
+#pragma unroll
+  for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+    for (int o = 0; o < 4; ++o) acc[orow][o] = 0.0f;
+  if constexpr (NSPLIT == 1) {
+#pragma unroll 1
+    for (int i = 0; i < 12; ++i) {
+      float b[2][4];
+      backin_kernel_term<EXACT>(s, i, c, p0, qq, b, acc);
+      if constexpr (EXACT) {
+#pragma unroll
+        for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+          for (int o = 0; o < 4; ++o) acc[orow][o] = fadd(acc[orow][o], b[orow][o]);
+      }
+    }
+  } else {
+    float mine[KPL][2][4];
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) {
+      backin_kernel_term<EXACT>(s, part * KPL + k, c, p0, qq, mine[k], acc);
+      if constexpr (EXACT) {
+        if (part == 0) {
+#pragma unroll
+          for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+            for (int o = 0; o < 4; ++o) acc[orow][o] = fadd(acc[orow][o], mine[k][orow][o]);
+        }
+      }
+    }
+    if constexpr (EXACT) {
+#pragma unroll
+      for (int k = 0; k < KPL; ++k)
+#pragma unroll
+        for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+          for (int o = 0; o < 4; ++o) {
+            const float v = __shfl_xor_sync(0xffffffffu, mine[k][orow][o], 1);
+            acc[orow][o] = fadd(acc[orow][o], v);
+          }
+    } else {
+#pragma unroll
+      for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+        for (int o = 0; o < 4; ++o) acc[orow][o] += __shfl_xor_sync(0xffffffffu, acc[orow][o], 1);
+    }
+  }
+  if (valid && part == 0) backin_to_dz1(s, c, p0, qq, acc);
+}
+
+template <bool EXACT>
+__device__ __forceinline__ void backin_item(const Smem& s, int item) {
+  backin_tile<EXACT, 1>(s, item, true);
 }
 
 // backin variant: lane quads split the twelve kernels 3 per lane; EXACT hands the per-kernel terms to
@@ -695,7 +773,7 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
         gk2_fast<ACCUM>(s, row, it - kBackin);
       }
     }
-  } else {
+  } else if constexpr (V == 1) {
     constexpr int kBackin = 128;  // 108 items, padded to 4 whole warps
     const int it = threadIdx.x;
     if (it < kBackin) {
@@ -704,6 +782,18 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
       if constexpr (EXACT) gk2_exact<ACCUM>(s, row, it - kBackin);
       else gk2_fast<ACCUM>(s, row, it - kBackin);
     }
+  } else {
+    // V = 2: lane pairs per backin item (224 lanes = 7 warps) beside the g_k2/g_b2 lanes
+    constexpr int kBackin = 224;
+    for (int it = threadIdx.x; it < kBackin + kGk2; it += blockDim.x) {
+      if (it < kBackin) {
+        backin_tile<EXACT, 2>(s, it, it < 216);
+      } else if constexpr (EXACT) {
+        gk2_exact<ACCUM>(s, row, it - kBackin);
+      } else {
+        gk2_fast<ACCUM>(s, row, it - kBackin);
+      }
+    }
   }
 }
 
@@ -711,10 +801,66 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
 // EXACT: one lane per output, the 576 terms in order, reading the v-shifted image copy so every row
 // is aligned 128-bit loads.  Fast: one lane per (i, y) holds all 25 outputs (the dz1 row stays in
 // registers and feeds 5 image rows), then a fixed-order combine over the 24 row partials.
+// EXACT C1 weight gradient as a producer/consumer pipeline: warps 5-15 compute the products
+// I[u+y][v+x] * dz1[i][y][x] of two image rows at a time into a double-buffered ring (128-bit loads
+// from the shifted image); lanes 0-149 of warps 0-4 then run the 150 ordered 576-term chains over
+// the ring (one 128-bit shared load per four adds) and lanes 150-155 the six bias chains.  Named
+// barriers 1/2 (ring slot full) and 3/4 (slot free) hand the slots over; the chains see exactly the
+// reference's sequence (y, x) row-major of separately rounded products.
+template <bool ACCUM>
+__device__ __forceinline__ void conv1_back_exact_pipelined(const Smem& s, float* row) {
+  constexpr int kChunks = 12, kConsumers = 160, kAll = 512;
+  const float* dz1 = s.c1;
+  const int t = threadIdx.x;
+  if (t >= kConsumers) {  // producers
+    const int pt = t - kConsumers, np = kAll - kConsumers;
+    for (int ch = 0; ch < kChunks; ++ch) {
+      const int slot = ch & 1;
+      if (ch >= 2) named_sync(3 + slot, kAll);  // wait until the consumers freed this slot
+      float* P = s.prod + slot * kProdChunk;
+      for (int q = pt; q < 150 * 12; q += np) {  // q -> (output o, row r of the chunk, 4 columns)
+        const int o = q / 12, k4 = q - o * 12, r = k4 / 6, x4 = k4 - r * 6;
+        const int i = o / 25, uv = o - i * 25, u = uv / 5, v = uv - u * 5, y = 2 * ch + r;
+        const float4 a = reinterpret_cast<const float4*>(s.sh + sh_at(v, u + y))[x4];
+        const float4 d = reinterpret_cast<const float4*>(dz1 + (i * 24 + y) * 24)[x4];
+        reinterpret_cast<float4*>(P + o * 48)[k4] =
+            make_float4(fmul(a.x, d.x), fmul(a.y, d.y), fmul(a.z, d.z), fmul(a.w, d.w));
+      }
+      named_arrive(1 + slot, kAll);  // slot full
+    }
+  } else {  // consumers: 150 weight chains + 6 bias chains
+    float acc = 0.0f;
+    for (int ch = 0; ch < kChunks; ++ch) {
+      const int slot = ch & 1;
+      named_sync(1 + slot, kAll);
+      if (t < 150) {
+        const float4* P = reinterpret_cast<const float4*>(s.prod + slot * kProdChunk + t * 48);
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+          const float4 v = P[k];
+          acc = fadd(fadd(fadd(fadd(acc, v.x), v.y), v.z), v.w);
+        }
+      } else if (t < 156) {
+        const float4* d = reinterpret_cast<const float4*>(dz1 + ((t - 150) * 24 + 2 * ch) * 24);
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+          const float4 v = d[k];
+          acc = fadd(fadd(fadd(fadd(acc, v.x), v.y), v.z), v.w);
+        }
+      }
+      if (ch + 2 < kChunks) named_arrive(3 + slot, kAll);  // slot free for chunk ch + 2
+    }
+    if (t < 150) put<ACCUM>(s, row, kK1 + t, acc);
+    else if (t < 156) put<ACCUM>(s, row, kB1 + t - 150, acc);
+  }
+}
+
 template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img, float* row) {
   const float* dz1 = s.c1;
-  if constexpr (EXACT) {
+  if constexpr (EXACT && kExactC1Pipelined) {
+    conv1_back_exact_pipelined<ACCUM>(s, row);
+  } else if constexpr (EXACT) {
     for (int it = threadIdx.x; it < 156; it += blockDim.x) {
       if (it < 150) {
         const int i = it / 25, r = it - i * 25, u = r / 5, v = r - u * 5;
@@ -818,8 +964,8 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
 // Stage variants used by the product kernels (chosen with paper_1912_05234_b200/csrc/stage_bench.cu).
 template <bool EXACT>
 struct StageCfg {
-  static constexpr int conv2 = 0;
-  static constexpr int conv2_back = EXACT ? 1 : 0;
+  static constexpr int conv2 = EXACT ? 0 : 1;
+  static constexpr int conv2_back = EXACT ? 1 : 2;
 };
 
 // ---------------------------------------------------------------------------------------------
