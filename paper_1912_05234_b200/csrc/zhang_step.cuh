@@ -813,19 +813,39 @@ __device__ __forceinline__ void conv1_back_exact_pipelined(const Smem& s, float*
   const float* dz1 = s.c1;
   const int t = threadIdx.x;
   if (t >= kConsumers) {  // producers
+    // each producer lane owns up to 6 fixed (output o, row r, 4-column group) slots; per chunk the
+    // image/dz1 rows advance by two, so all 12 loads of a chunk are issued before the first multiply
     const int pt = t - kConsumers, np = kAll - kConsumers;
+    int aoff[6], doff[6], poff[6];
+    bool on[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const int q = pt + k * np;  // q -> (output o, row r of the chunk, 4-column group x4)
+      on[k] = q < 150 * 12;
+      const int qq = on[k] ? q : 0;
+      const int o = qq / 12, k4 = qq - o * 12, r = k4 / 6, x4 = k4 - r * 6;
+      const int i = o / 25, uv = o - i * 25, u = uv / 5, v = uv - u * 5;
+      aoff[k] = sh_at(v, u + r) + 4 * x4;
+      doff[k] = (i * 24 + r) * 24 + 4 * x4;
+      poff[k] = o * 48 + 4 * k4;
+    }
     for (int ch = 0; ch < kChunks; ++ch) {
       const int slot = ch & 1;
       if (ch >= 2) named_sync(3 + slot, kAll);  // wait until the consumers freed this slot
       float* P = s.prod + slot * kProdChunk;
-      for (int q = pt; q < 150 * 12; q += np) {  // q -> (output o, row r of the chunk, 4 columns)
-        const int o = q / 12, k4 = q - o * 12, r = k4 / 6, x4 = k4 - r * 6;
-        const int i = o / 25, uv = o - i * 25, u = uv / 5, v = uv - u * 5, y = 2 * ch + r;
-        const float4 a = reinterpret_cast<const float4*>(s.sh + sh_at(v, u + y))[x4];
-        const float4 d = reinterpret_cast<const float4*>(dz1 + (i * 24 + y) * 24)[x4];
-        reinterpret_cast<float4*>(P + o * 48)[k4] =
-            make_float4(fmul(a.x, d.x), fmul(a.y, d.y), fmul(a.z, d.z), fmul(a.w, d.w));
+      float4 a[6], d[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        if (on[k]) {
+          a[k] = *reinterpret_cast<const float4*>(s.sh + aoff[k] + ch * 48);
+          d[k] = *reinterpret_cast<const float4*>(dz1 + doff[k] + ch * 48);
+        }
       }
+#pragma unroll
+      for (int k = 0; k < 6; ++k)
+        if (on[k])
+          *reinterpret_cast<float4*>(P + poff[k]) =
+              make_float4(fmul(a[k].x, d[k].x), fmul(a[k].y, d[k].y), fmul(a[k].z, d[k].z), fmul(a[k].w, d[k].w));
       named_arrive(1 + slot, kAll);  // slot full
     }
   } else {  // consumers: 150 weight chains + 6 bias chains
