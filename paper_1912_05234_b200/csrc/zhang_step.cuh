@@ -42,7 +42,7 @@ struct Smem {
   float* fcp;  // EXACT FC products [10][192]
   float* red;  // fast C1 weight-gradient row partials [144][26]
   float* G;    // fast per-CTA gradient accumulator [3904]
-  float* prod; // EXACT C1 weight-gradient product ring [2][150][48]
+  float* prod; // EXACT C1 weight-gradient product ring [2][150][52]
   uint64_t* tab;
   uint64_t* bar;
   unsigned long long* tr;  // optional per-stage clock64 trace (CTA 0 only), nullptr otherwise
@@ -68,7 +68,8 @@ constexpr int kDzpRow = 20;             // padded dz2 row: 16 used columns
 constexpr int kDzpK = 16 * kDzpRow + 4; // padded dz2 kernel (i) stride
 constexpr int kDzp = 12 * kDzpK;
 constexpr int kRed = 144 * 26;          // fast C1 weight-gradient row partials
-constexpr int kProdChunk = 150 * 48;    // EXACT C1 weight-gradient products of 2 image rows
+constexpr int kProdRow = 52;            // 48 products + 4 pad: odd float4 stride, conflict-free reads
+constexpr int kProdChunk = 150 * kProdRow;  // EXACT C1 weight-gradient products of 2 image rows
 
 __device__ __forceinline__ int dzp_at(int i, int R, int col) { return i * kDzpK + R * kDzpRow + col; }
 __device__ __forceinline__ int sh_at(int v, int y) { return v * kShPlane + y * 24; }
@@ -827,7 +828,7 @@ __device__ __forceinline__ void conv1_back_exact_pipelined(const Smem& s, float*
       const int i = o / 25, uv = o - i * 25, u = uv / 5, v = uv - u * 5;
       aoff[k] = sh_at(v, u + r) + 4 * x4;
       doff[k] = (i * 24 + r) * 24 + 4 * x4;
-      poff[k] = o * 48 + 4 * k4;
+      poff[k] = o * kProdRow + 4 * k4;
     }
     for (int ch = 0; ch < kChunks; ++ch) {
       const int slot = ch & 1;
@@ -854,7 +855,7 @@ __device__ __forceinline__ void conv1_back_exact_pipelined(const Smem& s, float*
       const int slot = ch & 1;
       named_sync(1 + slot, kAll);
       if (t < 150) {
-        const float4* P = reinterpret_cast<const float4*>(s.prod + slot * kProdChunk + t * 48);
+        const float4* P = reinterpret_cast<const float4*>(s.prod + slot * kProdChunk + t * kProdRow);
 #pragma unroll
         for (int k = 0; k < 12; ++k) {
           const float4 v = P[k];
