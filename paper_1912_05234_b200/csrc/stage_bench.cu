@@ -14,10 +14,10 @@
 
 using namespace tlb;
 
-enum Stage { kConv1, kConv2V0, kConv2V1, kFc, kFcBack, kC2BackV0, kC2BackV1, kC2BackV2, kC1Back, kForward,
+enum Stage { kConv1, kConv2V0, kConv2V1, kFc, kFcBack, kC2BackV0, kC2BackV1, kC2BackV2, kC2BackV3, kC1Back, kForward,
              kBackwardV0, kBackwardV1, kNumStages };
 static const char* kNames[kNumStages] = {"conv1", "conv2_v0_halves", "conv2_v1_rows", "fc", "fc_back",
-                                         "conv2_back_v0_quads", "conv2_back_v1_items", "conv2_back_v2_pairs", "conv1_back",
+                                         "conv2_back_v0_quads", "conv2_back_v1_items", "conv2_back_v2_pairs", "conv2_back_v3_ws", "conv1_back",
                                          "forward_image", "backward_v0", "backward_v1"};
 
 __device__ __forceinline__ float hrand(unsigned int x) {  // deterministic value in [0, 1)
@@ -59,6 +59,7 @@ __device__ __forceinline__ void run_stage(const Smem& s, float* row) {
   else if constexpr (STAGE == kC2BackV0) stage_conv2_back<EXACT, A, 0>(s, row);
   else if constexpr (STAGE == kC2BackV1) stage_conv2_back<EXACT, A, 1>(s, row);
   else if constexpr (STAGE == kC2BackV2) stage_conv2_back<EXACT, A, 2>(s, row);
+  else if constexpr (STAGE == kC2BackV3) stage_conv2_back<EXACT, A, 3>(s, row);
   else if constexpr (STAGE == kC1Back) stage_conv1_back<EXACT, A>(s, s.img, row);
   else if constexpr (STAGE == kForward) forward_image<EXACT>(s, s.img, 3, nullptr, true);
   else if constexpr (STAGE == kBackwardV0) {
@@ -117,6 +118,7 @@ void all(float* rows, unsigned long long* d_cycles, int sms, int iters, double m
   measure<EXACT, kC2BackV0>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kC2BackV1>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kC2BackV2>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kC2BackV3>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kC1Back>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kForward>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kBackwardV0>(rows, d_cycles, sms, iters, mhz);

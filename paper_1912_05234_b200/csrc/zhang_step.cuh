@@ -22,10 +22,6 @@
 namespace tlb {
 
 constexpr int kThreads = 512;
-#ifndef TLB_EXACT_C1_PIPELINED
-#define TLB_EXACT_C1_PIPELINED 1
-#endif
-constexpr bool kExactC1Pipelined = TLB_EXACT_C1_PIPELINED;
 
 struct Smem {
   float* P;    // parameters [3904]
@@ -42,7 +38,7 @@ struct Smem {
   float* fcp;  // EXACT FC products [10][192]
   float* red;  // fast C1 weight-gradient row partials [144][26]
   float* G;    // fast per-CTA gradient accumulator [3904]
-  float* prod; // EXACT C1 weight-gradient product ring [2][150][52]
+  float* term; // backin per-kernel terms b_i(c, p, q): [12][6][12][12]
   uint64_t* tab;
   uint64_t* bar;
   unsigned long long* tr;  // optional per-stage clock64 trace (CTA 0 only), nullptr otherwise
@@ -68,14 +64,13 @@ constexpr int kDzpRow = 20;             // padded dz2 row: 16 used columns
 constexpr int kDzpK = 16 * kDzpRow + 4; // padded dz2 kernel (i) stride
 constexpr int kDzp = 12 * kDzpK;
 constexpr int kRed = 144 * 26;          // fast C1 weight-gradient row partials
-constexpr int kProdRow = 52;            // 48 products + 4 pad: odd float4 stride, conflict-free reads
-constexpr int kProdChunk = 150 * kProdRow;  // EXACT C1 weight-gradient products of 2 image rows
+constexpr int kTerm = 12 * 864;         // backin per-kernel terms
 
 __device__ __forceinline__ int dzp_at(int i, int R, int col) { return i * kDzpK + R * kDzpRow + col; }
 __device__ __forceinline__ int sh_at(int v, int y) { return v * kShPlane + y * 24; }
 constexpr int kSmemFloats =
     kPStride + kKp + 2 * kImg + kSh + 3456 + 864 + 768 + 192 + 16 + 16 + kDzp + 1920 + kRed + kPStride +
-    2 * kProdChunk;
+    kTerm;
 constexpr size_t kSmemBytes = sizeof(float) * kSmemFloats + 32 * sizeof(uint64_t) + 2 * sizeof(uint64_t);
 
 // The CTA's dynamic shared memory (one declaration for every kernel and stage).
@@ -98,7 +93,7 @@ __device__ __forceinline__ Smem carve_smem(float* base) {
   s.fcp = p; p += 1920;
   s.red = p; p += kRed;
   s.G = p; p += kPStride;
-  s.prod = p; p += 2 * kProdChunk;
+  s.term = p; p += kTerm;
   s.tab = reinterpret_cast<uint64_t*>(p);
   s.bar = s.tab + 32;
   s.tr = nullptr;
@@ -758,6 +753,94 @@ __device__ __forceinline__ void gk2_fast(const Smem& s, float* row, int t) {
   if (c == 0 && q4 == 0) put<ACCUM>(s, row, kB2 + i, bsum);
 }
 
+// Weight-stationary backin.  Lane -> kernel pair (i, c) (seven lanes per pair, 504 lanes): the 25
+// weights of k2[i][c] stay in registers while the lane walks its output tiles (2 rows x 4 columns of
+// d_s1[c]), streaming six padded dz2[i] rows per tile.  Each tile's per-kernel term b_i (EXACT: the
+// reference's nested row/outer sums; fast: FFMA) goes to term[i][c][p][q]; backin_combine then forms
+// acc = (((0 + b_0) + b_1) + ... + b_11) per output in kernel order (network.cpp:135-138).
+template <bool EXACT>
+__device__ __forceinline__ void backin_ws(const Smem& s) {
+  const int t = threadIdx.x;
+  if (t >= 504) return;
+  const int pair = t / 7, sub = t - pair * 7, i = pair / 6, c = pair - i * 6;
+  float w[5][5];
+#pragma unroll
+  for (int u1 = 0; u1 < 5; ++u1)
+#pragma unroll
+    for (int u2 = 0; u2 < 5; ++u2) w[u1][u2] = s.Kp[((i * 6 + c) * 5 + u1) * 8 + u2];
+  float* term = s.term + (i * 6 + c) * 144;
+#pragma unroll 1
+  for (int tile = sub; tile < 18; tile += 7) {
+    const int pp = tile / 3, qq = tile - pp * 3, p0 = 2 * pp;
+    float b[2][4];
+#pragma unroll
+    for (int orow = 0; orow < 2; ++orow)
+#pragma unroll
+      for (int o = 0; o < 4; ++o) b[orow][o] = 0.0f;
+    float d[6][8];
+#pragma unroll
+    for (int rr = 0; rr < 6; ++rr) {  // all six rows in flight before the first multiply
+      const float4* dp = reinterpret_cast<const float4*>(s.dzp + dzp_at(i, p0 + rr, 4 * qq));
+      const float4 d0 = dp[0], d1 = dp[1];
+      d[rr][0] = d0.x; d[rr][1] = d0.y; d[rr][2] = d0.z; d[rr][3] = d0.w;
+      d[rr][4] = d1.x; d[rr][5] = d1.y; d[rr][6] = d1.z; d[rr][7] = d1.w;
+    }
+    // padded rows R = p0 + rr: output row orow uses tap row u1 = orow + 4 - rr, ascending as rr falls
+#pragma unroll
+    for (int rr = 5; rr >= 0; --rr) {
+#pragma unroll
+      for (int orow = 0; orow < 2; ++orow) {
+        const int u1 = orow + 4 - rr;
+        if (u1 < 0 || u1 > 4) continue;
+        float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int u2 = 0; u2 < 5; ++u2)
+#pragma unroll
+          for (int o = 0; o < 4; ++o) {
+            if constexpr (EXACT) rs[o] = mac<true>(rs[o], w[u1][u2], d[rr][o - u2 + 4]);
+            else b[orow][o] = __fmaf_rn(w[u1][u2], d[rr][o - u2 + 4], b[orow][o]);
+          }
+        if constexpr (EXACT) {
+#pragma unroll
+          for (int o = 0; o < 4; ++o) b[orow][o] = fadd(b[orow][o], rs[o]);
+        }
+      }
+    }
+#pragma unroll
+    for (int orow = 0; orow < 2; ++orow)
+      *reinterpret_cast<float4*>(term + (p0 + orow) * 12 + 4 * qq) =
+          make_float4(b[orow][0], b[orow][1], b[orow][2], b[orow][3]);
+  }
+}
+
+// d_s1[c][p][4qq..4qq+3] = ordered sum of the twelve kernel terms, then backavgpool + backsigmoid
+// through c1 -> dz1 for the 2x8 block of c1 it feeds.  216 lanes (c, p, qq).
+__device__ __forceinline__ void backin_combine(const Smem& s, int it) {
+  const int c = it / 36, r = it - c * 36, p = r / 3, qq = r - p * 3;
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int i = 0; i < 12; ++i) {
+    const float4 v = *reinterpret_cast<const float4*>(s.term + (i * 6 + c) * 144 + p * 12 + 4 * qq);
+    acc[0] = fadd(acc[0], v.x);
+    acc[1] = fadd(acc[1], v.y);
+    acc[2] = fadd(acc[2], v.z);
+    acc[3] = fadd(acc[3], v.w);
+  }
+#pragma unroll
+  for (int dy = 0; dy < 2; ++dy) {
+    float4* cp = reinterpret_cast<float4*>(s.c1 + (c * 24 + 2 * p + dy) * 24 + 8 * qq);
+    const float4 v0 = cp[0], v1 = cp[1];
+    float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      const float dc = fmul(acc[x >> 1], 0.25f);
+      cv[x] = fmul(fmul(dc, cv[x]), fsub(1.0f, cv[x]));
+    }
+    cp[0] = make_float4(cv[0], cv[1], cv[2], cv[3]);
+    cp[1] = make_float4(cv[4], cv[5], cv[6], cv[7]);
+  }
+}
+
 // C2 backward stage.  V = 0: backin lane quads on warps 0-13 (432 lanes), then the g_k2/g_b2 lanes;
 // V = 1: one backin lane per item on warps 0-3, concurrent with the g_k2/g_b2 lanes on warps 4+.
 template <bool EXACT, bool ACCUM, int V>
@@ -783,6 +866,21 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
       if constexpr (EXACT) gk2_exact<ACCUM>(s, row, it - kBackin);
       else gk2_fast<ACCUM>(s, row, it - kBackin);
     }
+  } else if constexpr (V == 3) {
+    // V = 3: weight-stationary backin over all lanes, then the ordered kernel combine (224 lanes)
+    // beside the g_k2/g_b2 lanes.
+    backin_ws<EXACT>(s);
+    __syncthreads();
+    constexpr int kComb = 224;  // 216 (c, p, qq) lanes padded to 7 warps
+    for (int it = threadIdx.x; it < kComb + kGk2; it += blockDim.x) {
+      if (it < kComb) {
+        if (it < 216) backin_combine(s, it);
+      } else if constexpr (EXACT) {
+        gk2_exact<ACCUM>(s, row, it - kComb);
+      } else {
+        gk2_fast<ACCUM>(s, row, it - kComb);
+      }
+    }
   } else {
     // V = 2: lane pairs per backin item (224 lanes = 7 warps) beside the g_k2/g_b2 lanes
     constexpr int kBackin = 224;
@@ -802,86 +900,10 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
 // EXACT: one lane per output, the 576 terms in order, reading the v-shifted image copy so every row
 // is aligned 128-bit loads.  Fast: one lane per (i, y) holds all 25 outputs (the dz1 row stays in
 // registers and feeds 5 image rows), then a fixed-order combine over the 24 row partials.
-// EXACT C1 weight gradient as a producer/consumer pipeline: warps 5-15 compute the products
-// I[u+y][v+x] * dz1[i][y][x] of two image rows at a time into a double-buffered ring (128-bit loads
-// from the shifted image); lanes 0-149 of warps 0-4 then run the 150 ordered 576-term chains over
-// the ring (one 128-bit shared load per four adds) and lanes 150-155 the six bias chains.  Named
-// barriers 1/2 (ring slot full) and 3/4 (slot free) hand the slots over; the chains see exactly the
-// reference's sequence (y, x) row-major of separately rounded products.
-template <bool ACCUM>
-__device__ __forceinline__ void conv1_back_exact_pipelined(const Smem& s, float* row) {
-  constexpr int kChunks = 12, kConsumers = 160, kAll = 512;
-  const float* dz1 = s.c1;
-  const int t = threadIdx.x;
-  if (t >= kConsumers) {  // producers
-    // each producer lane owns up to 6 fixed (output o, row r, 4-column group) slots; per chunk the
-    // image/dz1 rows advance by two, so all 12 loads of a chunk are issued before the first multiply
-    const int pt = t - kConsumers, np = kAll - kConsumers;
-    int aoff[6], doff[6], poff[6];
-    bool on[6];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) {
-      const int q = pt + k * np;  // q -> (output o, row r of the chunk, 4-column group x4)
-      on[k] = q < 150 * 12;
-      const int qq = on[k] ? q : 0;
-      const int o = qq / 12, k4 = qq - o * 12, r = k4 / 6, x4 = k4 - r * 6;
-      const int i = o / 25, uv = o - i * 25, u = uv / 5, v = uv - u * 5;
-      aoff[k] = sh_at(v, u + r) + 4 * x4;
-      doff[k] = (i * 24 + r) * 24 + 4 * x4;
-      poff[k] = o * kProdRow + 4 * k4;
-    }
-    for (int ch = 0; ch < kChunks; ++ch) {
-      const int slot = ch & 1;
-      if (ch >= 2) named_sync(3 + slot, kAll);  // wait until the consumers freed this slot
-      float* P = s.prod + slot * kProdChunk;
-      float4 a[6], d[6];
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        if (on[k]) {
-          a[k] = *reinterpret_cast<const float4*>(s.sh + aoff[k] + ch * 48);
-          d[k] = *reinterpret_cast<const float4*>(dz1 + doff[k] + ch * 48);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 6; ++k)
-        if (on[k])
-          *reinterpret_cast<float4*>(P + poff[k]) =
-              make_float4(fmul(a[k].x, d[k].x), fmul(a[k].y, d[k].y), fmul(a[k].z, d[k].z), fmul(a[k].w, d[k].w));
-      named_arrive(1 + slot, kAll);  // slot full
-    }
-  } else {  // consumers: 150 weight chains + 6 bias chains
-    float acc = 0.0f;
-    for (int ch = 0; ch < kChunks; ++ch) {
-      const int slot = ch & 1;
-      named_sync(1 + slot, kAll);
-      if (t < 150) {
-        const float4* P = reinterpret_cast<const float4*>(s.prod + slot * kProdChunk + t * kProdRow);
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-          const float4 v = P[k];
-          acc = fadd(fadd(fadd(fadd(acc, v.x), v.y), v.z), v.w);
-        }
-      } else if (t < 156) {
-        const float4* d = reinterpret_cast<const float4*>(dz1 + ((t - 150) * 24 + 2 * ch) * 24);
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-          const float4 v = d[k];
-          acc = fadd(fadd(fadd(fadd(acc, v.x), v.y), v.z), v.w);
-        }
-      }
-      if (ch + 2 < kChunks) named_arrive(3 + slot, kAll);  // slot free for chunk ch + 2
-    }
-    if (t < 150) put<ACCUM>(s, row, kK1 + t, acc);
-    else if (t < 156) put<ACCUM>(s, row, kB1 + t - 150, acc);
-  }
-}
-
 template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img, float* row) {
   const float* dz1 = s.c1;
-  if constexpr (EXACT && kExactC1Pipelined) {
-    conv1_back_exact_pipelined<ACCUM>(s, row);
-  } else if constexpr (EXACT) {
+  if constexpr (EXACT) {
     for (int it = threadIdx.x; it < 156; it += blockDim.x) {
       if (it < 150) {
         const int i = it / 25, r = it - i * 25, u = r / 5, v = r - u * 5;
