@@ -60,7 +60,8 @@ constexpr int kKp = 12 * 6 * 5 * 8;
 // Bank-conflict-free strides (in float4 units the plane/kernel strides are odd mod 8):
 constexpr int kShPlane = 28 * 24 + 4;   // shifted-image plane (v) stride
 constexpr int kSh = 5 * kShPlane + 4;   // (+4 keeps the next buffer 16-B aligned)
-constexpr int kDzpRow = 20;             // padded dz2 row: 16 used columns
+constexpr int kDzpRow = 24;             // padded dz2 row: 16 used columns (6 float4: neighbouring
+                                        // backin tiles land in different bank groups)
 constexpr int kDzpK = 16 * kDzpRow + 4; // padded dz2 kernel (i) stride
 constexpr int kDzp = 12 * kDzpK;
 constexpr int kRed = 144 * 26;          // fast C1 weight-gradient row partials
@@ -753,16 +754,18 @@ __device__ __forceinline__ void gk2_fast(const Smem& s, float* row, int t) {
   if (c == 0 && q4 == 0) put<ACCUM>(s, row, kB2 + i, bsum);
 }
 
-// Weight-stationary backin.  Lane -> kernel pair (i, c) (seven lanes per pair, 504 lanes): the 25
-// weights of k2[i][c] stay in registers while the lane walks its output tiles (2 rows x 4 columns of
-// d_s1[c]), streaming six padded dz2[i] rows per tile.  Each tile's per-kernel term b_i (EXACT: the
-// reference's nested row/outer sums; fast: FFMA) goes to term[i][c][p][q]; backin_combine then forms
-// acc = (((0 + b_0) + b_1) + ... + b_11) per output in kernel order (network.cpp:135-138).
+// Weight-stationary backin.  Lane t < 504 -> kernel i = t / 42, channel c = t % 6 and tile group
+// tg = (t % 42) / 6; it keeps the 25 weights of k2[i][c] in registers and walks tiles tg, tg+7, tg+14
+// (2 rows x 4 columns of d_s1[c]), streaming six padded dz2[i] rows per tile.  The six lanes of a
+// tile differ only in c, so each quarter-warp reads at most two distinct rows (broadcast).  Each
+// tile's per-kernel term b_i (EXACT: the reference's nested row/outer sums; fast: FFMA) goes to
+// term[i][c][p][q]; backin_combine then forms acc = (((0 + b_0) + b_1) + ... + b_11) per output in
+// kernel order (network.cpp:135-138).
 template <bool EXACT>
 __device__ __forceinline__ void backin_ws(const Smem& s) {
   const int t = threadIdx.x;
   if (t >= 504) return;
-  const int pair = t / 7, sub = t - pair * 7, i = pair / 6, c = pair - i * 6;
+  const int i = t / 42, r = t - i * 42, sub = r / 6, c = r - sub * 6;
   float w[5][5];
 #pragma unroll
   for (int u1 = 0; u1 < 5; ++u1)
