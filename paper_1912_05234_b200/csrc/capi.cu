@@ -3,6 +3,7 @@
 // Owns the per-context device workspaces and maps the reference API (tloom::nn / tloom::net,
 // proj/include/tloom/{nn,network}.hpp) onto the sm_100a kernels.  Argument checks reproduce the
 // reference's error conditions and messages (nn.cpp:37-94, network.cpp:209-214, mnist.cpp:169-170).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -76,6 +77,13 @@ struct tlb_ctx {
   int occ_eval[2] = {0, 0};
   DevBuf work, losses, loss_part, barrier;  // persistent-train workspaces
   DevBuf stage[8];                 // host-API staging buffers
+  // Overlapped ingestion for tlb_train: the dataset is copied chunk by chunk on `copy_stream` while
+  // the train kernel runs; a stream memory operation raises ready[k] to the call's token after
+  // chunk k lands (the kernel polls it before the image's TMA load).
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_gate = nullptr;
+  DevBuf ready;
+  unsigned int ready_token = 0;
 };
 
 namespace {
@@ -213,6 +221,37 @@ int plain_grid(tlb_ctx* c, int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(n, cap));
 }
 
+// cuStreamWriteValue32 through the runtime's driver entry point (no link-time libcuda dependency).
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn write_value32() {
+  static WriteValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<WriteValue32Fn>(p);
+  }();
+  return fn;
+}
+
+// Upload n images on the copy stream in chunks of `chunk` images, raising ready[k] to `token` after
+// chunk k.  The copy stream first waits for all earlier work on the context stream (buffer reuse).
+int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t chunk, unsigned int token) {
+  TLB_CUDA(cudaEventRecord(c->copy_gate, c->stream));
+  TLB_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));
+  unsigned int* flags = static_cast<unsigned int*>(c->ready.p);
+  for (int64_t k = 0, lo = 0; lo < n; ++k, lo += chunk) {
+    const int64_t cnt = std::min(chunk, n - lo);
+    TLB_CUDA(cudaMemcpyAsync(dev + lo * 784, host + lo * 784, (size_t)cnt * 784 * sizeof(float),
+                             cudaMemcpyHostToDevice, c->copy_stream));
+    const CUresult r = write_value32()(reinterpret_cast<CUstream>(c->copy_stream),
+                                       reinterpret_cast<CUdeviceptr>(flags + k), token, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) return fail(TLB_ERR_CUDA, "cuStreamWriteValue32 failed: " + std::to_string((int)r));
+  }
+  return TLB_OK;
+}
+
 int check_train_args(int64_t n, int32_t epochs, float rate, int64_t batch) {
   // network.cpp:211-214 then mnist::batches (mnist.cpp:170)
   if (n == 0) return fail(TLB_ERR_ERROR, "train: empty dataset");
@@ -227,7 +266,8 @@ int check_train_args(int64_t n, int32_t epochs, float rate, int64_t batch) {
 int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, int64_t n, float* d_params,
                   float rate, int32_t epoch_begin, int32_t epochs, int64_t batch, double* d_epoch_loss,
                   int64_t shard_lo = 0, int64_t shard_hi = 0, int64_t group = -1, float* grad_out = nullptr,
-                  double* loss_out = nullptr) {
+                  double* loss_out = nullptr, const unsigned int* ready = nullptr, unsigned int token = 0,
+                  int64_t chunk = 1) {
   const int64_t spe = (n + batch - 1) / batch;
   const int64_t m_max = std::min<int64_t>(batch, n);
   const int64_t m_local = grad_out ? std::max<int64_t>(0, std::min(shard_hi, m_max) - shard_lo) : m_max;
@@ -262,6 +302,10 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.grad_out = grad_out;
   a.loss_out = loss_out;
   a.trace = c->trace;
+  a.ready = ready;
+  a.ready_token = token;
+  a.chunk = chunk;
+  a.ready_step_end = a.step_begin + spe;  // only the call's first epoch can outrun the copies
   if (a.step_end <= a.step_begin) return TLB_OK;
   TLB_CUDA(tlb::launch_train(exact(c), a, grid, c->stream));
   return TLB_OK;
@@ -302,6 +346,12 @@ int tlb_ctx_create(int device, tlb_ctx** out) {
     delete c;
     return fail(TLB_ERR_CUDA, std::string("tlb_ctx_create: ") + cudaGetErrorString(e));
   }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->copy_gate, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(TLB_ERR_CUDA, std::string("tlb_ctx_create: ") + cudaGetErrorString(e));
+  }
   c->stream = c->own_stream;
   *out = c;
   return TLB_OK;
@@ -316,6 +366,10 @@ int tlb_ctx_destroy(tlb_ctx* c) {
   c->loss_part.release();
   c->barrier.release();
   for (auto& s : c->stage) s.release();
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  c->ready.release();
+  if (c->copy_gate) cudaEventDestroy(c->copy_gate);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return TLB_OK;
@@ -384,17 +438,42 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   int32_t* d_lab;
   float* d_p;
   double* d_loss;
-  TLB_TRY(stage_in(c, 0, images, (size_t)n * 784, &d_img));
+  // The dataset streams in on the copy stream while the first epoch already trains on the chunks
+  // that have landed (chunk = whole SGD groups, >= 256 KiB); labels/params are tiny and go first.
+  const int64_t per = std::max<int64_t>(1, (256 * 1024 + 784 * 4 - 1) / (784 * 4));
+  const int64_t chunk = ((per + batch - 1) / batch) * batch;
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  const bool overlap = write_value32() != nullptr;
+  TLB_TRY(stage_out(c, 0, (size_t)n * 784, &d_img));
+  if (overlap) {
+    if ((size_t)nchunks * sizeof(unsigned int) > c->ready.cap) {
+      TLB_CUDA(cudaStreamSynchronize(c->copy_stream));
+      TLB_CUDA(c->ready.ensure((size_t)nchunks * sizeof(unsigned int)));
+      TLB_CUDA(cudaMemset(c->ready.p, 0, c->ready.cap));
+      c->ready_token = 0;
+    }
+    if (++c->ready_token == 0) {  // wrapped: restart the token sequence from clean flags
+      TLB_CUDA(cudaStreamSynchronize(c->copy_stream));
+      TLB_CUDA(cudaMemset(c->ready.p, 0, c->ready.cap));
+      c->ready_token = 1;
+    }
+    TLB_TRY(ingest_images(c, images, d_img, n, chunk, c->ready_token));
+  } else if (n) {
+    TLB_CUDA(cudaMemcpyAsync(d_img, images, (size_t)n * 784 * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  }
+  const unsigned int* rdy = overlap ? static_cast<const unsigned int*>(c->ready.p) : nullptr;
   TLB_TRY(stage_in(c, 1, labels, (size_t)n, &d_lab));
   TLB_TRY(stage_out(c, 2, TLB_PSTRIDE, &d_p));
   TLB_CUDA(cudaMemsetAsync(d_p, 0, TLB_PSTRIDE * sizeof(float), c->stream));
   TLB_CUDA(cudaMemcpyAsync(d_p, params, TLB_NPARAM * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   TLB_TRY(stage_out(c, 3, (size_t)epochs, &d_loss));
   if (!on_epoch) {
-    TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, 0, epochs, batch, d_loss));
+    TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, 0, epochs, batch, d_loss, 0, 0, -1, nullptr, nullptr,
+                          rdy, c->ready_token, chunk));
   } else {
     for (int32_t e = 0; e < epochs; ++e) {
-      TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, e, 1, batch, d_loss));
+      TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, e, 1, batch, d_loss, 0, 0, -1, nullptr, nullptr,
+                            e == 0 ? rdy : nullptr, c->ready_token, chunk));
       double mean = 0.0;
       TLB_TRY(fetch(c, &mean, d_loss + e, 1));
       on_epoch(e + 1, mean, user);
@@ -403,6 +482,7 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   TLB_CUDA(cudaMemcpyAsync(params, d_p, TLB_NPARAM * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
   if (epoch_loss) TLB_CUDA(cudaMemcpyAsync(epoch_loss, d_loss, epochs * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   TLB_CUDA(cudaStreamSynchronize(c->stream));
+  if (overlap) TLB_CUDA(cudaStreamSynchronize(c->copy_stream));
   return TLB_OK;
 }
 

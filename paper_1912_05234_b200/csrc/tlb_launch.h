@@ -29,6 +29,13 @@ struct TrainArgs {
   float* grad_out;
   double* loss_out;
   unsigned long long* trace;  // optional [steps][16] clock64 stamps of CTA 0 (tlb_ctx_set_trace)
+  // Overlapped ingestion (tlb_train on host buffers): images arrive in chunks of `chunk` images on a
+  // copy stream; ready[k] >= ready_token once chunk k is resident.  Steps < ready_step_end poll the
+  // flag before the image's TMA load; nullptr = every image already resident.
+  const unsigned int* ready;
+  unsigned int ready_token;
+  int64_t chunk;
+  int64_t ready_step_end;
 };
 
 struct CellArgs {

@@ -63,8 +63,31 @@ __device__ __forceinline__ bool next_job(const TrainArgs& a, Job& j) {
   return first_job(a, j.step + 1, j);
 }
 
+__device__ __forceinline__ int64_t job_index(const TrainArgs& a, const Job& j) {
+  return (j.step % a.steps_per_epoch) * a.batch + local_offset(a) + j.e;
+}
+
 __device__ __forceinline__ const float* job_image(const TrainArgs& a, const Job& j) {
-  return a.images + ((j.step % a.steps_per_epoch) * a.batch + local_offset(a) + j.e) * kImg;
+  return a.images + job_index(a, j) * kImg;
+}
+
+// Overlapped ingestion: wait (thread 0) until the copy stream has landed the chunk holding this job's
+// image.  The flag is written by a stream memory operation after the chunk's copy completes.
+__device__ __forceinline__ void wait_ready(const TrainArgs& a, const Job& j) {
+  if (!a.ready || j.step >= a.ready_step_end) return;
+  const unsigned int* f = a.ready + job_index(a, j) / a.chunk;
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  while ((int)(v - a.ready_token) < 0) {
+    __nanosleep(256);
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // the TMA read below follows the flag
+}
+
+__device__ __forceinline__ void issue_job(const Smem& s, const TrainArgs& a, int buf, const Job& j) {
+  wait_ready(a, j);
+  issue_image(s, buf, job_image(a, j));
 }
 
 // sgd_step (network.cpp:171-180) for one parameter, or the shard's gradient sum in DP mode.
@@ -178,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
 
   Job pf;
   bool pf_valid = first_job(a, a.step_begin, pf);
-  if (threadIdx.x == 0 && pf_valid) issue_image(s, 0, job_image(a, pf));
+  if (threadIdx.x == 0 && pf_valid) issue_job(s, a, 0, pf);
   uint32_t consumed = 0;
 
   for (int64_t st = a.step_begin; st < a.step_end; ++st) {
@@ -203,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
       if (pf_valid) {
         Job nx = pf;
         if (next_job(a, nx)) {
-          if (threadIdx.x == 0) issue_image(s, buf ^ 1, job_image(a, nx));
+          if (threadIdx.x == 0) issue_job(s, a, buf ^ 1, nx);
           pf = nx;
         } else {
           pf_valid = false;

@@ -1011,7 +1011,7 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
 template <bool EXACT>
 struct StageCfg {
   static constexpr int conv2 = EXACT ? 0 : 1;
-  static constexpr int conv2_back = EXACT ? 1 : 2;
+  static constexpr int conv2_back = 1;
 };
 
 // ---------------------------------------------------------------------------------------------

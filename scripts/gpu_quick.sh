@@ -3,7 +3,7 @@
 TAG=${1:-q}
 OUT=gpurun_out
 mkdir -p $OUT
-timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu_$TAG.log
+timeout 900 python -u -m pytest tests -m gpu -x -v --timeout 300 > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu_$TAG.log
 for M in fast exact; do
   timeout 300 python scripts/trace_step.py --mode $M > $OUT/trace_${M}_$TAG.json 2>&1
 done

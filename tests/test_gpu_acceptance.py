@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.skipif(not os.path.exists(EXE), reason="acceptance_b200 not built (needs /root/reference at build time)")
 def test_reference_acceptance_gate_on_b200():
     env = dict(os.environ, LD_LIBRARY_PATH=os.path.join(ROOT, "paper_1912_05234_b200", "lib"))
-    out = subprocess.run([EXE], capture_output=True, text=True, timeout=900, env=env)
+    out = subprocess.run([EXE], capture_output=True, text=True, timeout=300, env=env)
     log = out.stdout + out.stderr
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "acceptance_b200.log"), "w") as f:
