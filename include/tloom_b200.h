@@ -69,6 +69,9 @@ int tlb_ctx_set_grid(tlb_ctx* ctx, int ctas);
 /* Profiling hook: device buffer of [steps][16] uint64 clock64 stamps written by CTA 0 of the
  * persistent train kernel at each stage boundary (NULL disables; see bench.py --trace). */
 int tlb_ctx_set_trace(tlb_ctx* ctx, void* d_trace);
+/* Fast mode, groups of <= 8 x (co-resident clusters) examples: 1 (default) runs the clustered train
+ * kernel (DSMEM gradient pre-reduction, one grid barrier per step); 0 forces the flat kernel. */
+int tlb_ctx_set_cluster(tlb_ctx* ctx, int enable);
 int tlb_ctx_info(const tlb_ctx* ctx, int* sm_count, int* train_ctas_per_sm, int* eval_ctas_per_sm,
                  int64_t* smem_bytes_per_cta);
 int tlb_synchronize(tlb_ctx* ctx);

@@ -38,6 +38,7 @@ _SIGS = {
     "tlb_ctx_get_mode": (C.c_int, [vp, C.POINTER(C.c_int)]),
     "tlb_ctx_set_grid": (C.c_int, [vp, C.c_int]),
     "tlb_ctx_set_trace": (C.c_int, [vp, vp]),
+    "tlb_ctx_set_cluster": (C.c_int, [vp, C.c_int]),
     "tlb_ctx_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), i64p]),
     "tlb_synchronize": (C.c_int, [vp]),
     "tlb_init_params": (C.c_int, [C.c_uint64, f32p]),

@@ -75,6 +75,8 @@ struct tlb_ctx {
   unsigned long long* trace = nullptr;  // device buffer for per-stage clock stamps (profiling)
   int occ_train[2] = {0, 0};
   int occ_eval[2] = {0, 0};
+  int max_clusters = 0;    // co-resident 8-CTA clusters of train_cluster_kernel (0 = unavailable)
+  bool use_cluster = true;
   DevBuf work, losses, loss_part, barrier;  // persistent-train workspaces
   DevBuf stage[8];                 // host-API staging buffers
   // Overlapped ingestion for tlb_train: the dataset is copied chunk by chunk on `copy_stream` while
@@ -271,12 +273,17 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   const int64_t spe = (n + batch - 1) / batch;
   const int64_t m_max = std::min<int64_t>(batch, n);
   const int64_t m_local = grad_out ? std::max<int64_t>(0, std::min(shard_hi, m_max) - shard_lo) : m_max;
-  const int grid = train_grid(c, std::max<int64_t>(m_local, 1));
+  // Clustered fast kernel: one example per CTA per step, every CTA co-resident.
+  const int csz = tlb::cluster_size();
+  const int clusters = (int)((std::max<int64_t>(m_local, 1) + csz - 1) / csz);
+  const bool clustered = !exact(c) && !grad_out && c->use_cluster && c->grid_override == 0 &&
+                         c->max_clusters > 0 && clusters <= c->max_clusters;
+  const int grid = clustered ? clusters * csz : train_grid(c, std::max<int64_t>(m_local, 1));
   const int64_t rows = exact(c) ? std::max<int64_t>(m_local, 1) : grid;
-  TLB_CUDA(c->work.ensure((size_t)rows * TLB_PSTRIDE * sizeof(float)));
+  TLB_CUDA(c->work.ensure(clustered ? tlb::cluster_work_bytes() : (size_t)rows * TLB_PSTRIDE * sizeof(float)));
   TLB_CUDA(c->losses.ensure((size_t)std::max<int64_t>(m_local, 1) * sizeof(float)));
-  TLB_CUDA(c->barrier.ensure(sizeof(unsigned int)));
-  TLB_CUDA(c->loss_part.ensure((size_t)grid * sizeof(double)));
+  TLB_CUDA(c->barrier.ensure(tlb::cluster_size() * sizeof(unsigned int)));
+  TLB_CUDA(c->loss_part.ensure((size_t)(clustered ? 2 * clusters : grid) * sizeof(double)));
   tlb::TrainArgs a{};
   a.images = d_images;
   a.labels = d_labels;
@@ -307,7 +314,8 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.chunk = chunk;
   a.ready_step_end = a.step_begin + spe;  // only the call's first epoch can outrun the copies
   if (a.step_end <= a.step_begin) return TLB_OK;
-  TLB_CUDA(tlb::launch_train(exact(c), a, grid, c->stream));
+  if (clustered) TLB_CUDA(tlb::launch_train_cluster(a, clusters, c->stream));
+  else TLB_CUDA(tlb::launch_train(exact(c), a, grid, c->stream));
   return TLB_OK;
 }
 
@@ -345,6 +353,10 @@ int tlb_ctx_create(int device, tlb_ctx** out) {
   if (e != cudaSuccess) {
     delete c;
     return fail(TLB_ERR_CUDA, std::string("tlb_ctx_create: ") + cudaGetErrorString(e));
+  }
+  if (e == cudaSuccess && tlb::cluster_train_capacity(&c->max_clusters) != cudaSuccess) {
+    (void)cudaGetLastError();  // no cluster launch on this device: the flat kernel is used
+    c->max_clusters = 0;
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->copy_gate, cudaEventDisableTiming);
@@ -398,6 +410,12 @@ int tlb_ctx_get_mode(const tlb_ctx* c, int* mode) {
 int tlb_ctx_set_grid(tlb_ctx* c, int ctas) {
   if (!c) return fail(TLB_ERR_ARG, "null context");
   c->grid_override = std::max(0, ctas);
+  return TLB_OK;
+}
+
+int tlb_ctx_set_cluster(tlb_ctx* c, int enable) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  c->use_cluster = enable != 0;
   return TLB_OK;
 }
 

@@ -272,6 +272,162 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------------
+// train_cluster_kernel: the fast-mode persistent train kernel for groups that fit one image per CTA
+// (batch <= grid).  CTAs form clusters of 8 (distributed shared memory); per step:
+//   1. each CTA runs forward+backward of its image, accumulating the gradient in its shared G;
+//   2. CTA q pushes slice r (488 floats) of its G into the receive buffer of owner CTA r (DSMEM
+//      stores); cluster barrier; owner r sums the 8 received slices in rank order;
+//   3. owner r adds its cluster partial into ONE global accumulator as 2^-40 fixed point
+//      (red.global.add.u64: integer addition is associative, so the sum is the same whatever order
+//      the clusters arrive in -- deterministic run to run), then bumps the slice-r arrival counter;
+//   4. owner r of every cluster waits until all clusters have arrived on slice r (no grid-wide
+//      barrier: only the 8-way slice counter), reads the slice total and applies sgd_step
+//      (network.cpp:171-180) to its copy of slice r;
+//   5. owner r pushes its updated slice into every CTA of its cluster (DSMEM); cluster barrier.
+// The parameters never round-trip through L2 between steps.  Accumulators are triple-buffered by
+// step; buffer (s+1) % 3 is zeroed by cluster 0 during step s before it signals step s (every CTA
+// that adds into it in step s+1 has observed that signal).  Not the reference's example-order chain:
+// EXACT mode keeps train_kernel<true>.
+// ------------------------------------------------------------------------------------------------
+constexpr int kCluster = 8;
+constexpr int kSlice = kPStride / kCluster;  // 488 floats per owner CTA
+constexpr int kSlice4 = kSlice / 4;
+static_assert(kSlice % 4 == 0, "slice must be float4-aligned");
+constexpr double kFix = 1099511627776.0;  // 2^40: gradient sums |g| < 2^23 (sigmoid-bounded terms)
+constexpr double kUnfix = 1.0 / kFix;
+// Cluster-kernel global workspace (in TrainArgs::work): [3][kPStride] u64 gradient accumulators,
+// [3] u64 loss accumulators, [kCluster] u32 slice arrival counters (zeroed by the host per launch).
+constexpr int64_t kAccWords = 3 * (int64_t)kPStride + 3;
+
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a) {
+  static_assert(StageCfg<false>::conv2_back != 3, "the DSMEM receive buffer reuses the backin term buffer");
+  Smem s = carve_smem(tlb_smem);
+  float* const rx = s.term;   // [8 source ranks][488]: slices pushed to this CTA (it owns slice `rank`)
+  __shared__ double loss_sh;  // this CTA's fp64 loss sum of the step (read by rank 0 over DSMEM)
+  smem_setup(s);
+  const uint32_t rank = cluster_rank(), cid = cluster_id(), ncl = cluster_count();
+  const int G = gridDim.x;
+  unsigned long long* const acc = reinterpret_cast<unsigned long long*>(a.work);  // [3][kPStride]
+  unsigned long long* const lacc = acc + 3 * kPStride;                             // [3]
+  unsigned int* const cnt = a.barrier;  // [kCluster] slice arrival counters
+  unsigned long long* const trace = blockIdx.x == 0 ? a.trace : nullptr;
+
+  Job pf;
+  bool pf_valid = first_job(a, a.step_begin, pf);
+  if (threadIdx.x == 0 && pf_valid) issue_job(s, a, 0, pf);
+  uint32_t consumed = 0;
+  load_params(s, a.params);  // once: afterwards the parameters live in shared memory
+
+  for (int64_t st = a.step_begin; st < a.step_end; ++st) {
+    const int64_t ls = st - a.step_begin;  // local step: accumulator buffer ls % 3
+    const int64_t ks = st % a.steps_per_epoch, start = ks * a.batch;
+    const int64_t m = local_size(a, st);
+    int64_t lo, hi;
+    static_chunk(m, G, blockIdx.x, lo, hi);
+    s.tr = trace ? trace + ls * 16 : nullptr;
+    mark(s, 0);
+    for (int i = threadIdx.x; i < kPStride; i += blockDim.x) s.G[i] = 0.0f;
+    __syncthreads();
+    mark(s, 1);
+    double cta_loss = 0.0;
+    for (int64_t e = lo; e < hi; ++e) {
+      const int buf = consumed & 1;
+      mbar_wait(&s.bar[buf], (consumed >> 1) & 1);
+      mark(s, 2);
+      if (pf_valid) {
+        Job nx = pf;
+        if (next_job(a, nx)) {
+          if (threadIdx.x == 0) issue_job(s, a, buf ^ 1, nx);
+          pf = nx;
+        } else {
+          pf_valid = false;
+        }
+      }
+      const int label = __ldg(a.labels + start + e);
+      forward_image<false>(s, s.img + buf * kImg, label, nullptr, true);
+      if (threadIdx.x == 0) cta_loss = __dadd_rn(cta_loss, (double)example_loss(s, label, nullptr));
+      backward_image<false, true>(s, s.img + buf * kImg, nullptr);
+      ++consumed;
+    }
+    // ---- 2. push slice q of G to its owner q; owner sums the 8 received slices (rank order) ----
+    if (threadIdx.x == 0) loss_sh = cta_loss;
+    for (int i = threadIdx.x; i < kCluster * kSlice4; i += blockDim.x) {
+      const int q = i / kSlice4, o = 4 * (i - q * kSlice4);
+      dsmem_st4(dsmem_map(rx + (int)rank * kSlice + o, q), *reinterpret_cast<const float4*>(s.G + q * kSlice + o));
+    }
+    mark(s, 9);
+    cluster_sync_all();  // every pushed slice has landed
+    mark(s, 10);
+    const int b = (int)(ls % 3), bn = (int)((ls + 1) % 3);
+    const int j = (int)rank * kSlice + (int)threadIdx.x;  // this thread's parameter (threads < 488)
+    if (threadIdx.x < kSlice) {
+      float sum = rx[threadIdx.x];
+#pragma unroll
+      for (int q = 1; q < kCluster; ++q) sum += rx[q * kSlice + threadIdx.x];
+      red_add_u64(acc + b * kPStride + j, __double2ll_rn((double)sum * kFix));
+      if (cid == 0) acc[bn * kPStride + j] = 0ull;  // next step's accumulator
+    }
+    if (rank == 0 && threadIdx.x == kSlice) {
+      double l = 0.0;
+      for (int q = 0; q < kCluster; ++q) l = __dadd_rn(l, dsmem_ld_f64(dsmem_map(&loss_sh, q)));
+      red_add_u64(lacc + b, __double2ll_rn(l * kFix));
+      if (cid == 0) lacc[bn] = 0ull;
+    }
+    __syncthreads();
+    mark(s, 14);
+    // ---- 3/4. arrival on slice `rank`, then wait for every cluster's contribution ----
+    if (threadIdx.x == 0) {
+      __threadfence();
+      unsigned int* c = cnt + rank;
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(c) : "memory");
+      const unsigned int want = (unsigned int)((ls + 1) * ncl);
+      unsigned int v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+      while ((int)(v - want) < 0) {
+        __nanosleep(32);
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+      }
+    }
+    __syncthreads();
+    mark(s, 11);
+    if (threadIdx.x < kSlice) {
+      const long long t = (long long)__ldcg(acc + b * kPStride + j);
+      if (j < kNParam) {
+        const float gsum = (float)((double)t * kUnfix);
+        s.P[j] = fsub(s.P[j], fmul(a.rate, __fdiv_rn(gsum, (float)m)));
+        if (cid == 0) __stcg(a.params + j, s.P[j]);
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == kSlice) {
+      const int64_t ep = st / a.steps_per_epoch;
+      const double l = (double)(long long)__ldcg(lacc + b) * kUnfix;
+      const double run = (ks != 0 ? a.epoch_loss[ep] : 0.0) + l;
+      a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(run, (double)a.n) : run;
+    }
+    __syncthreads();
+    mark(s, 12);
+    // ---- 5. push the updated slice into the other CTAs of the cluster ----
+    for (int i = threadIdx.x; i < (kCluster - 1) * kSlice4; i += blockDim.x) {
+      const int qi = i / kSlice4, q = qi < (int)rank ? qi : qi + 1;
+      const int o = (int)rank * kSlice + 4 * (i - qi * kSlice4);
+      dsmem_st4(dsmem_map(s.P + o, q), *reinterpret_cast<const float4*>(s.P + o));
+    }
+    cluster_sync_all();  // every owner's slice has landed everywhere
+    mark(s, 15);
+    for (int idx = threadIdx.x; idx < kKp; idx += blockDim.x) {
+      const int row = idx >> 3, k = idx & 7;
+      s.Kp[idx] = k < 5 ? s.P[kK2 + row * 5 + k] : 0.0f;
+    }
+    __syncthreads();
+    mark(s, 13);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
 // Per-example forward(+backward) cells: net::forward / net::backward / net::loss for n images.
 // ------------------------------------------------------------------------------------------------
 template <bool EXACT>
@@ -395,6 +551,56 @@ cudaError_t launch_train(bool exact, const TrainArgs& a, int grid, cudaStream_t 
   void* args[] = {const_cast<TrainArgs*>(&a)};
   const void* fn = exact ? (const void*)train_kernel<true> : (const void*)train_kernel<false>;
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, kSmemBytes, st);
+}
+
+cudaError_t cluster_train_capacity(int* max_clusters) {
+  *max_clusters = 0;
+  cudaError_t e = cudaFuncSetAttribute(train_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kCluster);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(max_clusters, train_cluster_kernel, &cfg);
+}
+
+int cluster_size() { return kCluster; }
+size_t cluster_work_bytes() { return kAccWords * sizeof(unsigned long long); }
+
+// Grid = clusters * 8 CTAs, all co-resident (clusters <= cluster_train_capacity): the kernel's grid
+// barrier needs co-residency, which the cooperative attribute also asserts where the driver allows it.
+cudaError_t launch_train_cluster(const TrainArgs& a, int clusters, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(a.barrier, 0, kCluster * sizeof(unsigned int), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(a.work, 0, kAccWords * sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * kCluster);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  e = cudaLaunchKernelEx(&cfg, train_cluster_kernel, a);
+  if (e == cudaErrorInvalidValue || e == cudaErrorNotSupported) {  // cooperative + cluster refused
+    (void)cudaGetLastError();
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, train_cluster_kernel, a);
+  }
+  return e;
 }
 
 cudaError_t launch_cells(bool exact, const CellArgs& a, int grid, cudaStream_t st) {

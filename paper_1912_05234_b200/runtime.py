@@ -115,6 +115,10 @@ class Context:
     def set_grid(self, ctas: int) -> None:
         _check(self._L.tlb_ctx_set_grid(self._h, ctas))
 
+    def set_cluster(self, enable: bool) -> None:
+        """Fast mode: clustered train kernel (DSMEM pre-reduction) when the group fits (default on)."""
+        _check(self._L.tlb_ctx_set_cluster(self._h, 1 if enable else 0))
+
     def set_trace(self, d_trace_ptr: int) -> None:
         """Per-stage clock64 stamps of CTA 0 into a device buffer of [steps][16] uint64 (0 disables)."""
         _check(self._L.tlb_ctx_set_trace(self._h, C.c_void_p(d_trace_ptr or None)))

@@ -252,6 +252,28 @@ def test_full_protocol_fast_within_tolerance(golden, zhang_sets):
         assert np.array_equal(bits(p2), bits(p3)) and list(l2) == list(l3)
 
 
+@pytest.mark.parametrize("n,batch,epochs", [(3, 100, 1), (64, 8, 2), (250, 100, 2), (256, 64, 1), (97, 9, 1),
+                                            (1040, 1040, 1)])
+@pytest.mark.parametrize("cluster", [True, False])
+def test_train_fast_vs_oracle(orc, small, zhang_sets, n, batch, epochs, cluster):
+    """FAST mode, clustered (DSMEM pre-reduction, one grid barrier) and flat kernels: ragged last groups,
+    batch > n, group sizes that fill 1..13 clusters partially, and a group larger than the clustered
+    kernel's capacity (falls back to the flat kernel).  Within 1e-4 relative of the reference order;
+    deterministic run to run."""
+    from paper_1912_05234_b200 import Context
+    (tr_x, tr_y), _ = zhang_sets
+    x, y = (tr_x, tr_y) if n > len(small[1]) else small
+    p0 = orc.init_params(42)
+    want_p, want_l = orc.train(x[:n], y[:n], p0, epochs=epochs, batch=batch)
+    with Context(0, mode="fast") as fctx:
+        fctx.set_cluster(cluster)
+        got_p, got_l = fctx.train(p0, x[:n], y[:n], epochs=epochs, batch=batch)
+        again_p, again_l = fctx.train(p0, x[:n], y[:n], epochs=epochs, batch=batch)
+    assert rel_err(got_l, want_l) <= REL_TOL
+    assert rel_err(got_p, want_p, floor=1e-3) <= REL_TOL, rel_err(got_p, want_p, floor=1e-3)
+    assert np.array_equal(bits(got_p), bits(again_p)) and list(got_l) == list(again_l)
+
+
 def test_evaluate_golden_params(ctx, golden, zhang_sets):
     _, (te_x, te_y) = zhang_sets
     acc, pred = ctx.evaluate(golden["final_params"], te_x, te_y, return_pred=True)
