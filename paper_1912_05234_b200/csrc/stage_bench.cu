@@ -29,7 +29,7 @@ __device__ void fill(const Smem& s) {
   const int t = threadIdx.x, n = blockDim.x;
   for (int i = t; i < kPStride; i += n) s.P[i] = i < kNParam ? (hrand(i) - 0.5f) * 0.2f : 0.0f;
   for (int i = t; i < 2 * kImg; i += n) s.img[i] = hrand(i + 10000);
-  for (int i = t; i < 3456; i += n) s.c1[i] = 0.3f + 0.4f * hrand(i + 20000);
+  for (int i = t; i < kC1Floats; i += n) s.c1[i] = 0.3f + 0.4f * hrand(i + 20000);
   for (int i = t; i < 864; i += n) s.s1[i] = 0.3f + 0.4f * hrand(i + 30000);
   for (int i = t; i < 768; i += n) s.c2[i] = 0.3f + 0.4f * hrand(i + 40000);
   for (int i = t; i < 192; i += n) s.s2[i] = 0.3f + 0.4f * hrand(i + 50000);

@@ -108,7 +108,7 @@ __device__ __forceinline__ void reduce_slice(const Smem& s, const TrainArgs& a, 
   int64_t j0, j1;
   static_chunk(kNParam, gridDim.x, blockIdx.x, j0, j1);
   constexpr int kLanes = EXACT ? 1 : 8;  // fast: 8 lanes per parameter + fixed shuffle tree
-  float* stage = s.c1;                   // c1|s1|c2|s2 are contiguous: 5,280 free floats
+  float* stage = s.c1;                   // c1|s1|c2|s2 are contiguous: >= 5,280 free floats
   const int t = threadIdx.x, per = blockDim.x / kLanes;
   for (int64_t jb = j0; jb < j1; jb += per) {
     const int W = (int)min((int64_t)per, j1 - jb);
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1) cells_kernel(CellArgs a) {
       const float* src = a.acts_in + e * kNAct;
       for (int i = threadIdx.x; i < kNAct; i += blockDim.x) {
         const float v = src[i];
-        if (i < kS1) s.c1[i] = v;
+        if (i < kS1) s.c1[(i / 576) * kC1Plane + i % 576] = v;
         else if (i < kC2) s.s1[i - kS1] = v;
         else if (i < kS2) s.c2[i - kC2] = v;
         else if (i < kOut) s.s2[i - kS2] = v;
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1) cells_kernel(CellArgs a) {
       float* dst = a.acts + e * kNAct;
       for (int i = threadIdx.x; i < kNAct; i += blockDim.x) {
         float v;
-        if (i < kS1) v = s.c1[i];
+        if (i < kS1) v = s.c1[(i / 576) * kC1Plane + i % 576];
         else if (i < kC2) v = s.s1[i - kS1];
         else if (i < kS2) v = s.c2[i - kC2];
         else if (i < kOut) v = s.s2[i - kS2];

@@ -68,9 +68,14 @@ constexpr int kRed = 144 * 26;          // fast C1 weight-gradient row partials
 constexpr int kTerm = 12 * 864;         // backin per-kernel terms
 
 __device__ __forceinline__ int dzp_at(int i, int R, int col) { return i * kDzpK + R * kDzpRow + col; }
+// c1 / dz1 channel planes padded 576 -> 580 floats: the six channel rows of one y start in six different
+// bank groups (580 mod 32 = 4), so the C1 weight-gradient lanes read them conflict-free.
+constexpr int kC1Plane = 580;
+constexpr int kC1Floats = 6 * kC1Plane;
+__device__ __forceinline__ int c1_at(int i, int y, int x) { return i * kC1Plane + y * 24 + x; }
 __device__ __forceinline__ int sh_at(int v, int y) { return v * kShPlane + y * 24; }
 constexpr int kSmemFloats =
-    kPStride + kKp + 2 * kImg + kSh + 3456 + 864 + 768 + 192 + 16 + 16 + kDzp + 1920 + kRed + kPStride +
+    kPStride + kKp + 2 * kImg + kSh + kC1Floats + 864 + 768 + 192 + 16 + 16 + kDzp + 1920 + kRed + kPStride +
     kTerm;
 constexpr size_t kSmemBytes = sizeof(float) * kSmemFloats + 32 * sizeof(uint64_t) + 2 * sizeof(uint64_t);
 
@@ -84,7 +89,7 @@ __device__ __forceinline__ Smem carve_smem(float* base) {
   s.Kp = p; p += kKp;
   s.img = p; p += 2 * kImg;
   s.sh = p; p += kSh;
-  s.c1 = p; p += 3456;
+  s.c1 = p; p += kC1Floats;
   s.s1 = p; p += 864;
   s.c2 = p; p += 768;
   s.s2 = p; p += 192;
@@ -206,7 +211,7 @@ __device__ __forceinline__ void stage_conv1(const Smem& s, const float* img) {
 #pragma unroll
     for (int o = 0; o < 8; ++o) u[o] = __shfl_xor_sync(0xffffffffu, t[o], 1);
     if (valid) {
-      float4* d = reinterpret_cast<float4*>(s.c1 + (i * 24 + y) * 24 + x0);
+      float4* d = reinterpret_cast<float4*>(s.c1 + c1_at(i, y, x0));
       d[0] = make_float4(t[0], t[1], t[2], t[3]);
       d[1] = make_float4(t[4], t[5], t[6], t[7]);
       float pv[2];
@@ -493,7 +498,7 @@ __device__ __forceinline__ void backin_to_dz1(const Smem& s, int c, int p0, int 
   for (int orow = 0; orow < 2; ++orow)
 #pragma unroll
     for (int dy = 0; dy < 2; ++dy) {
-      float4* cp = reinterpret_cast<float4*>(s.c1 + (c * 24 + 2 * (p0 + orow) + dy) * 24 + 8 * qq);
+      float4* cp = reinterpret_cast<float4*>(s.c1 + c1_at(c, 2 * (p0 + orow) + dy, 8 * qq));
       const float4 v0 = cp[0], v1 = cp[1];
       float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
@@ -657,7 +662,7 @@ __device__ __forceinline__ void backin_quad(const Smem& s, int lane_item, bool v
     for (int orow = 0; orow < 2; ++orow)
 #pragma unroll
       for (int dy = 0; dy < 2; ++dy) {
-        float4* cp = reinterpret_cast<float4*>(s.c1 + (c * 24 + 2 * (p0 + orow) + dy) * 24 + 8 * qq);
+        float4* cp = reinterpret_cast<float4*>(s.c1 + c1_at(c, 2 * (p0 + orow) + dy, 8 * qq));
         const float4 v0 = cp[0], v1 = cp[1];
         float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
@@ -831,7 +836,7 @@ __device__ __forceinline__ void backin_combine(const Smem& s, int it) {
   }
 #pragma unroll
   for (int dy = 0; dy < 2; ++dy) {
-    float4* cp = reinterpret_cast<float4*>(s.c1 + (c * 24 + 2 * p + dy) * 24 + 8 * qq);
+    float4* cp = reinterpret_cast<float4*>(s.c1 + c1_at(c, 2 * p + dy, 8 * qq));
     const float4 v0 = cp[0], v1 = cp[1];
     float cv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
@@ -909,9 +914,11 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
   if constexpr (EXACT) {
     for (int it = threadIdx.x; it < 156; it += blockDim.x) {
       if (it < 150) {
-        const int i = it / 25, r = it - i * 25, u = r / 5, v = r - u * 5;
+        // lane = (u, v) major, i minor: a warp reads ~6 shifted-image rows and the 6 dz1 channel rows
+        // of one y, each in its own bank group (conflict-free 128-bit loads)
+        const int i = it % 6, r = it / 6, u = r / 5, v = r - u * 5;
         const float4* ib = reinterpret_cast<const float4*>(s.sh + sh_at(v, u));
-        const float4* db = reinterpret_cast<const float4*>(dz1 + i * 576);
+        const float4* db = reinterpret_cast<const float4*>(dz1 + i * kC1Plane);
         float acc = 0.0f;
         // software pipeline: row y+1 is in flight while the ordered chain consumes row y
         float4 a[6], d[6];
@@ -942,10 +949,10 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
             d[q] = dn[q];
           }
         }
-        put<ACCUM>(s, row, kK1 + it, acc);
+        put<ACCUM>(s, row, kK1 + i * 25 + r, acc);
       } else {
         const int i = it - 150;
-        const float4* dp = reinterpret_cast<const float4*>(dz1 + i * 576);
+        const float4* dp = reinterpret_cast<const float4*>(dz1 + i * kC1Plane);
         float acc = 0.0f;
 #pragma unroll 4
         for (int e = 0; e < 144; ++e) {
@@ -959,7 +966,7 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
     const int it = threadIdx.x;
     if (it < 144) {  // (i, y): 25 row-partials + the bias row-partial
       const int i = it / 24, y = it - i * 24;
-      const float4* dp = reinterpret_cast<const float4*>(dz1 + (i * 24 + y) * 24);
+      const float4* dp = reinterpret_cast<const float4*>(dz1 + c1_at(i, y, 0));
       float dr[24];
 #pragma unroll
       for (int q = 0; q < 6; ++q) {
