@@ -158,6 +158,10 @@ class Reference:
         L.ref_last_error.restype = C.c_char_p
         L.ref_set_workers.argtypes = [C.c_int]
         L.ref_init_params.argtypes = [C.c_uint64, _f32p]
+        L.ref_save_params.argtypes = [C.c_char_p, _f32p]
+        L.ref_load_params.argtypes = [C.c_char_p, _f32p]
+        L.ref_load_set.argtypes = [C.c_char_p, C.c_char_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.ref_load_set.restype = C.c_int64
         L.ref_make_digits.argtypes = [C.c_int64, C.c_uint64, _u8p, _i32p]
         L.ref_make_set.argtypes = [C.c_int64, C.c_uint64, _f32p, _i32p]
         L.ref_forward.argtypes = [_f32p, _f32p, _f32p]
@@ -181,6 +185,23 @@ class Reference:
 
     def set_workers(self, w: int):
         self._check(self.L.ref_set_workers(w))
+
+    def save_params(self, path: str, params) -> None:
+        self._check(self.L.ref_save_params(path.encode(), fp(np.ascontiguousarray(params, np.float32))))
+
+    def load_params(self, path: str) -> np.ndarray:
+        p = np.zeros(NPARAM, np.float32)
+        self._check(self.L.ref_load_params(path.encode(), fp(p)))
+        return p
+
+    def load_set(self, images_path: str, labels_path: str, limit: int = -1):
+        n = self.L.ref_load_set(images_path.encode(), labels_path.encode(), limit, None, None)
+        if n < 0:
+            self._check(-n)
+        x = np.zeros((max(n, 1), 784), np.float32)
+        y = np.zeros(max(n, 1), np.int32)
+        self.L.ref_load_set(images_path.encode(), labels_path.encode(), limit, x.ctypes.data, y.ctypes.data)
+        return x[:n], y[:n]
 
     def init_params(self, seed: int) -> np.ndarray:
         p = np.zeros(NPARAM, np.float32)

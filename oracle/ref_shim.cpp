@@ -89,6 +89,38 @@ int ref_set_workers(int workers) {
 
 void ref_init_params(uint64_t seed, float* out) { params_to(net::init_params(seed), out); }
 
+// TLM1 checkpoint round trip through the reference's own codec (network.cpp:282-362).
+int ref_save_params(const char* path, const float* params) {
+  try {
+    net::save_params(path, params_from(params));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_load_params(const char* path, float* out) {
+  try {
+    params_to(net::load_params(path), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// mnist::load_set of IDX files (mnist.cpp:126-154) -> images [n][784], labels [n]; returns n.
+int64_t ref_load_set(const char* images_path, const char* labels_path, int64_t limit, float* images, int32_t* labels) {
+  try {
+    const mnist::MnistSet s = mnist::load_set(images_path, labels_path, limit);
+    if (images) copy_out(s.images, images);
+    if (labels)
+      for (int64_t i = 0; i < s.size(); ++i) labels[i] = s.labels[static_cast<std::size_t>(i)];
+    return s.size();
+  } catch (const std::exception& e) {
+    return -fail(e);
+  }
+}
+
 void ref_make_digits(int64_t n, uint64_t seed, uint8_t* px, int32_t* labels) {
   const synth::Corpus c = synth::make_digits(n, seed);
   std::memcpy(px, c.pixels.data(), c.pixels.size());

@@ -87,6 +87,28 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+TOOLS = {"tensorloom": "tools/tensorloom_cli.cpp", "tensorloom-datagen": "tools/datagen.cpp"}
+BINDIR = os.path.join(PKG, "bin")
+
+
+def build_tools(force: bool = False) -> list[str]:
+    """The reference's CLI tools (proj/tools/) rebuilt over the C++ mirror + libtloom_b200.so."""
+    os.makedirs(BINDIR, exist_ok=True)
+    outs = []
+    for name, src in TOOLS.items():
+        path = os.path.join(PKG, src)
+        exe = os.path.join(BINDIR, name)
+        deps = [path, LIB] + [os.path.join(ROOT, "include", "tloom", h) for h in os.listdir(os.path.join(ROOT, "include", "tloom"))]
+        if force or _stale(exe, deps):
+            cmd = [CXX, "-std=gnu++20", "-O2", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"), path, "-o", exe,
+                   "-L" + LIBDIR, "-ltloom_b200", "-Wl,-rpath,$ORIGIN/../lib", "-lpthread"]
+            out = subprocess.run(cmd, capture_output=True, text=True)
+            if out.returncode != 0:
+                raise RuntimeError(f"tool build failed for {name}:\n{' '.join(cmd)}\n{out.stderr}")
+        outs.append(exe)
+    return outs
+
+
 def build_stage_bench() -> str:
     """Developer micro-benchmark of the per-image stages (not part of the library)."""
     os.makedirs(OBJ, exist_ok=True)
@@ -101,5 +123,6 @@ def build_stage_bench() -> str:
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_tools(force="--force" in sys.argv))
     if "--bench" in sys.argv:
         print(build_stage_bench())
