@@ -159,6 +159,34 @@ int tlb_nn_backavgpool_shape(const int64_t* shape, int rank, int64_t* out_shape,
 int tlb_nn_backin_shape(const int64_t* d_shape, int d_rank, const int64_t* k_shape, int k_rank,
                         const int64_t* in_shape, int in_rank, int64_t* out_shape, int* out_rank);
 
+/* ---- Widened CNN (BASELINE.json configs[4]): conv1 32@5x5 -> sigmoid -> avgpool -> conv2 64@32x5x5 ->
+ * sigmoid -> avgpool -> FC 10 from [64,1,13,13], 64x64 inputs, 160,266 parameters in write_flat order
+ * (k1 [32,5,5], b1 [32], k2 [64,32,5,5], b2 [64], fc [10,64,1,13,13], b [10]).  Same group semantics
+ * as tlb_train (network.cpp:209-251: per-example gradients summed over the group, sgd_step) built from
+ * the shape-polymorphic nn:: operators (nn.cpp:96-217); the reference has no widened net::train, the
+ * oracle is the composition of its operators (oracle/widened.py).  engine selects the GEMM engine of
+ * the three conv2 contractions: TLB_WIDE_FP32 (register-tiled FFMA on the CUDA cores) or
+ * TLB_WIDE_TC (tcgen05 tensor cores, 3xTF32 split = fp32-level accuracy).  Deterministic, within the
+ * 1e-4 relative tolerance of the reference composition (not bitwise). */
+#define TLB_WIDE_NPARAM 160266
+#define TLB_WIDE_IMG 4096 /* 64 x 64 */
+#define TLB_WIDE_FP32 0
+#define TLB_WIDE_TC 1
+/* init_params rule (network.cpp:56-79) with the widened fans: k1 (25, 3600), k2 (800, 676), fc (10816, 1). */
+int tlb_wide_init_params(uint64_t seed, float* params_out);
+/* n synthetic 64x64 inputs: synth::make_digits(n, seed) glyphs centred at offset 18, / 255.0f. */
+int tlb_wide_make_set(int64_t n, uint64_t seed, float* images_out, int32_t* labels_out);
+int tlb_wide_train(tlb_ctx* ctx, const float* images, const int32_t* labels, int64_t n, float* params, float rate,
+                   int32_t epochs, int64_t batch, double* epoch_loss, int engine);
+int tlb_wide_train_device(tlb_ctx* ctx, const float* d_images, const int32_t* d_labels, int64_t n, float* d_params,
+                          float rate, int32_t epoch_begin, int32_t epochs, int64_t batch, double* d_epoch_loss,
+                          int engine);
+/* Forward only (inference): yhat [n][10]. */
+int tlb_wide_forward(tlb_ctx* ctx, const float* images, int64_t n, const float* params, float* yhat, int engine);
+/* Benchmark hook: re-run one conv2 contraction (0 forward, 1 weight gradient, 2 backin) of the last
+ * trained group on the context's workspaces with the given engine. */
+int tlb_wide_gemm_device(tlb_ctx* ctx, int which, int engine);
+
 /* Test hook: device glibc-expf restatement over float bit patterns [start, start+n). */
 int tlb_expf_range(tlb_ctx* ctx, uint32_t start_bits, int64_t n, float* out);
 

@@ -26,14 +26,14 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + os.pat
           "-I" + CSRC]
 CU_FLAGS = ARCH + COMMON + ["-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
-SOURCES = ["zhang_kernels.cu", "nn_ops.cu", "capi.cu", "host_data.cpp"]
+SOURCES = ["zhang_kernels.cu", "nn_ops.cu", "wide_kernels.cu", "wide_tc.cu", "capi.cu", "host_data.cpp"]
 # C++ mirror of the reference headers (include/tloom/*.hpp): plain host code, g++ -std=gnu++20
 HOST_SOURCES = ["host/tensor.cpp", "host/runtime.cpp", "host/nn.cpp", "host/network.cpp", "host/mnist.cpp",
                 "host/synth.cpp"]
 CXX = os.environ.get("CXX", "g++")
 CXX_FLAGS = ["-std=gnu++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
              "-I" + os.path.join(CSRC, "host")]
-HEADERS = ["tlb_common.cuh", "zhang_step.cuh", "tlb_launch.h", "tlb_capi_internal.h"]
+HEADERS = ["tlb_common.cuh", "zhang_step.cuh", "tlb_launch.h", "tlb_capi_internal.h", "wide_kernels.cuh"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

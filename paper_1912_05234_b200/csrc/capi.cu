@@ -15,6 +15,7 @@
 #include "tlb_capi_internal.h"
 #include "tlb_launch.h"
 #include "tloom_b200.h"
+#include "wide_kernels.cuh"
 
 namespace tlb {
 
@@ -86,6 +87,10 @@ struct tlb_ctx {
   cudaEvent_t copy_gate = nullptr;
   DevBuf ready;
   unsigned int ready_token = 0;
+  // Widened-network workspaces (capacity `wide_cap` images) and the last group's arguments.
+  DevBuf wide[12];
+  int64_t wide_cap = 0;
+  tlb::wide::StepArgs wide_last{};
 };
 
 namespace {
@@ -380,6 +385,7 @@ int tlb_ctx_destroy(tlb_ctx* c) {
   for (auto& s : c->stage) s.release();
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   c->ready.release();
+  for (auto& w : c->wide) w.release();
   if (c->copy_gate) cudaEventDestroy(c->copy_gate);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -817,6 +823,136 @@ int tlb_nn_backin(tlb_ctx* c, const float* d, const int64_t* ds, int dr, const f
   TLB_TRY(stage_out(c, 2, (size_t)nout, &d_o));
   TLB_CUDA(tlb::nn_backin(d_d, ds, d_k, ks, ir, d_o, c->stream));
   return fetch(c, out, d_o, (size_t)nout);
+}
+
+// ---- widened CNN (BASELINE configs[4]) -------------------------------------------------------------------
+namespace {
+namespace W = tlb::wide;
+
+int wide_ws(tlb_ctx* c, int64_t m, W::StepArgs& a) {
+  if (m > c->wide_cap) {
+    const size_t f = sizeof(float);
+    const size_t sizes[10] = {(size_t)m * W::kC1N * W::kC1W * W::kC1W * f, (size_t)m * W::kC1N * W::kS1Pos * f,
+                              (size_t)m * W::kC2N * W::kC2Pos * f,        (size_t)m * W::kS2Len * f,
+                              (size_t)m * W::kClasses * f,                (size_t)m * f,
+                              (size_t)m * W::kC2N * W::kC2Pos * f,        (size_t)42 * W::kGk2Rows * W::kC2N * f,
+                              (size_t)m * W::kC1N * 26 * f,               (size_t)(W::kNParam + 64) * f};
+    for (int i = 0; i < 10; ++i) {
+      c->wide[i].release();
+      TLB_CUDA(c->wide[i].ensure(sizes[i]));
+    }
+    c->wide_cap = m;
+  }
+  a.c1 = static_cast<float*>(c->wide[0].p);
+  a.s1 = static_cast<float*>(c->wide[1].p);
+  a.c2 = static_cast<float*>(c->wide[2].p);
+  a.s2 = static_cast<float*>(c->wide[3].p);
+  a.dz = static_cast<float*>(c->wide[4].p);
+  a.loss = static_cast<float*>(c->wide[5].p);
+  a.dz2 = static_cast<float*>(c->wide[6].p);
+  a.part = static_cast<float*>(c->wide[7].p);
+  a.part1 = static_cast<float*>(c->wide[8].p);
+  a.grad = static_cast<float*>(c->wide[9].p);
+  return TLB_OK;
+}
+
+int check_engine(int engine) {
+  if (engine != TLB_WIDE_FP32 && engine != TLB_WIDE_TC)
+    return fail(TLB_ERR_ARG, "unknown GEMM engine " + std::to_string(engine));
+  return TLB_OK;
+}
+
+int wide_enqueue(tlb_ctx* c, const float* d_images, const int32_t* d_labels, int64_t n, float* d_params, float rate,
+                 int32_t epoch_begin, int32_t epochs, int64_t batch, double* d_epoch_loss, int engine) {
+  const int64_t spe = (n + batch - 1) / batch;
+  W::StepArgs a{};
+  TLB_TRY(wide_ws(c, std::min(batch, n), a));
+  a.params = d_params;
+  a.rate = rate;
+  a.tensor = engine == TLB_WIDE_TC;
+  a.n_total = (double)n;
+  for (int32_t e = epoch_begin; e < epoch_begin + epochs; ++e)
+    for (int64_t s = 0; s < spe; ++s) {
+      const int64_t lo = s * batch;
+      a.m = std::min(batch, n - lo);
+      a.images = d_images + lo * W::kImgW * W::kImgW;
+      a.labels = d_labels + lo;
+      a.epoch_loss = d_epoch_loss ? d_epoch_loss + e : nullptr;
+      a.first = s == 0;
+      a.last = s == spe - 1;
+      TLB_CUDA(W::step(a, c->stream));
+      c->wide_last = a;
+    }
+  return TLB_OK;
+}
+}  // namespace
+
+int tlb_wide_train_device(tlb_ctx* c, const float* d_images, const int32_t* d_labels, int64_t n, float* d_params,
+                          float rate, int32_t epoch_begin, int32_t epochs, int64_t batch, double* d_epoch_loss,
+                          int engine) {
+  if (!c || !d_params || !d_images || !d_labels) return fail(TLB_ERR_ARG, "tlb_wide_train_device: null argument");
+  TLB_TRY(check_train_args(n, epochs, rate, batch));
+  TLB_TRY(check_engine(engine));
+  TLB_TRY(set_device(c));
+  return wide_enqueue(c, d_images, d_labels, n, d_params, rate, epoch_begin, epochs, batch, d_epoch_loss, engine);
+}
+
+int tlb_wide_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n, float* params, float rate,
+                   int32_t epochs, int64_t batch, double* epoch_loss, int engine) {
+  if (!c || !params) return fail(TLB_ERR_ARG, "tlb_wide_train: null argument");
+  TLB_TRY(check_train_args(n, epochs, rate, batch));
+  TLB_TRY(check_engine(engine));
+  if (!images || !labels) return fail(TLB_ERR_ARG, "tlb_wide_train: null dataset");
+  for (int64_t i = 0; i < n; ++i)
+    if (labels[i] < 0 || labels[i] > 9)
+      return fail(TLB_ERR_VALUE, "one_hot: label " + std::to_string(labels[i]) + " out of range 0..9");
+  TLB_TRY(set_device(c));
+  if (epochs == 0) return TLB_OK;
+  float *d_img, *d_p;
+  int32_t* d_lab;
+  double* d_loss;
+  TLB_TRY(stage_in(c, 0, images, (size_t)n * W::kImgW * W::kImgW, &d_img));
+  TLB_TRY(stage_in(c, 1, labels, (size_t)n, &d_lab));
+  TLB_TRY(stage_in(c, 2, params, (size_t)W::kNParam, &d_p));
+  TLB_TRY(stage_out(c, 3, (size_t)epochs, &d_loss));
+  TLB_TRY(wide_enqueue(c, d_img, d_lab, n, d_p, rate, 0, epochs, batch, d_loss, engine));
+  TLB_CUDA(cudaMemcpyAsync(params, d_p, W::kNParam * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  if (epoch_loss) TLB_CUDA(cudaMemcpyAsync(epoch_loss, d_loss, epochs * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  TLB_CUDA(cudaStreamSynchronize(c->stream));
+  return TLB_OK;
+}
+
+int tlb_wide_forward(tlb_ctx* c, const float* images, int64_t n, const float* params, float* yhat, int engine) {
+  if (!c || !params || !yhat || (n > 0 && !images)) return fail(TLB_ERR_ARG, "tlb_wide_forward: null argument");
+  if (n < 0) return fail(TLB_ERR_ARG, "negative count");
+  TLB_TRY(check_engine(engine));
+  if (n == 0) return TLB_OK;
+  TLB_TRY(set_device(c));
+  float *d_img, *d_p, *d_y;
+  TLB_TRY(stage_in(c, 0, images, (size_t)n * W::kImgW * W::kImgW, &d_img));
+  TLB_TRY(stage_in(c, 2, params, (size_t)W::kNParam, &d_p));
+  TLB_TRY(stage_out(c, 3, (size_t)n * W::kClasses, &d_y));
+  const int64_t chunk = 256;
+  W::StepArgs a{};
+  TLB_TRY(wide_ws(c, std::min(chunk, n), a));
+  a.params = d_p;
+  a.tensor = engine == TLB_WIDE_TC;
+  for (int64_t lo = 0; lo < n; lo += chunk) {
+    a.m = std::min(chunk, n - lo);
+    a.images = d_img + lo * W::kImgW * W::kImgW;
+    TLB_CUDA(W::forward(a, d_y + lo * W::kClasses, c->stream));
+  }
+  return fetch(c, yhat, d_y, (size_t)n * W::kClasses);
+}
+
+int tlb_wide_gemm_device(tlb_ctx* c, int which, int engine) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  TLB_TRY(check_engine(engine));
+  if (which < 0 || which > 2) return fail(TLB_ERR_ARG, "tlb_wide_gemm_device: which must be 0, 1 or 2");
+  if (c->wide_last.m <= 0) return fail(TLB_ERR_ERROR, "tlb_wide_gemm_device: no widened group trained yet");
+  TLB_TRY(set_device(c));
+  TLB_CUDA(W::gemm_only(which, engine == TLB_WIDE_TC, c->wide_last, c->stream));
+  return TLB_OK;
 }
 
 int tlb_expf_range(tlb_ctx* c, uint32_t start_bits, int64_t n, float* out) {

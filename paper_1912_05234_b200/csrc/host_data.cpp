@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <random>
 #include <string>
+#include <vector>
 
 #include "tlb_capi_internal.h"
 #include "tloom_b200.h"
@@ -105,6 +106,45 @@ extern "C" int tlb_validate_set(const float* images, const int32_t* labels, int6
     if (labels[i] < 0 || labels[i] > 9)
       return tlb::fail(TLB_ERR_VALUE, "dataset: label " + std::to_string(labels[i]) + " at index " +
                                           std::to_string(i) + " out of range 0..9");
+  }
+  return TLB_OK;
+}
+
+// ---- widened CNN (BASELINE configs[4]) host data ------------------------------------------------------
+// init_params (network.cpp:56-79) with the widened shapes: k1 [32,5,5] fan (25, 60*60), k2 [64,32,5,5]
+// fan (32*25, 26*26), fc [10,64,1,13,13] fan (64*13*13, 1); fill order k1, k2, fc from one mt19937_64
+// stream; biases zero.  Offsets follow write_flat order (k1, b1, k2, b2, fc, b).
+extern "C" int tlb_wide_init_params(uint64_t seed, float* p) {
+  if (!p) return tlb::fail(TLB_ERR_ARG, "tlb_wide_init_params: null output");
+  std::mt19937_64 rng(seed);
+  std::fill(p, p + TLB_WIDE_NPARAM, 0.0f);
+  struct Fill {
+    int off, count, fan_in, fan_out;
+  };
+  const Fill fills[3] = {{0, 800, 25, 3600}, {832, 51200, 800, 676}, {52096, 108160, 10816, 1}};
+  for (const Fill& f : fills) {
+    const float limit = std::sqrt(6.0f / static_cast<float>(f.fan_in + f.fan_out));
+    for (int i = 0; i < f.count; ++i) {
+      const float u = static_cast<float>(rng() >> 40) * 0x1p-24f;
+      p[f.off + i] = (u * 2.0f - 1.0f) * limit;
+    }
+  }
+  return TLB_OK;
+}
+
+extern "C" int tlb_wide_make_set(int64_t n, uint64_t seed, float* images, int32_t* labels) {
+  if (n < 0) return tlb::fail(TLB_ERR_ERROR, "make_digits: negative count");
+  if (n > 0 && (!images || !labels)) return tlb::fail(TLB_ERR_ARG, "tlb_wide_make_set: null output");
+  std::vector<uint8_t> px((size_t)n * 784);
+  std::vector<int32_t> lab((size_t)n);
+  const int rc = tlb_synth_make_digits(n, seed, px.data(), lab.data());
+  if (rc != TLB_OK) return rc;
+  std::fill(images, images + (size_t)n * TLB_WIDE_IMG, 0.0f);
+  for (int64_t i = 0; i < n; ++i) {
+    labels[i] = lab[(size_t)i];
+    for (int y = 0; y < 28; ++y)
+      for (int x = 0; x < 28; ++x)
+        images[(size_t)i * TLB_WIDE_IMG + (y + 18) * 64 + x + 18] = static_cast<float>(px[(size_t)i * 784 + y * 28 + x]) / 255.0f;
   }
   return TLB_OK;
 }

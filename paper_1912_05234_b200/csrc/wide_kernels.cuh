@@ -1,0 +1,171 @@
+// wide_kernels.cuh -- shapes, parameter layout, GEMM operand functors and the step driver of the widened
+// CNN (BASELINE.json configs[4]); see wide_kernels.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tlb {
+namespace wide {
+
+// ---- network shape (composition of nn.cpp operators) ----------------------
+constexpr int kImgW = 64;                       // input [64,64]
+constexpr int kC1N = 32, kC1W = 60;             // c1 [32,60,60]
+constexpr int kS1W = 30, kS1Pos = kS1W * kS1W;  // s1 [32,30,30]
+constexpr int kC2N = 64, kC2W = 26, kC2Pos = kC2W * kC2W;  // c2 [64,1,26,26]
+constexpr int kS2Len = kC2N * 13 * 13;          // s2 [64,1,13,13] = 10,816
+constexpr int kClasses = 10;
+constexpr int kK2Slice = kC1N * 25;             // 800 = one conv2 kernel [32,5,5]
+constexpr int kGk2Rows = kK2Slice + 1;          // + the all-ones row that yields g_b2
+
+// ---- flat parameter / gradient layout, write_flat order k1,b1,k2,b2,fc,b (network.cpp:186-193) -------
+constexpr int kOffK1 = 0;
+constexpr int kOffB1 = kOffK1 + kC1N * 25;        // 800
+constexpr int kOffK2 = kOffB1 + kC1N;             // 832
+constexpr int kOffB2 = kOffK2 + kC2N * kK2Slice;  // 52,032
+constexpr int kOffFC = kOffB2 + kC2N;             // 52,096
+constexpr int kOffBF = kOffFC + kClasses * kS2Len; // 160,256
+constexpr int kNParam = kOffBF + kClasses;        // 160,266
+
+constexpr int64_t kFlopPerTrainImage = 2LL * 109918080;  // 109,918,080 MAC
+constexpr int64_t kFlopPerFwdImage = 2LL * (2880000 + 34611200 + 108160);
+
+__device__ __forceinline__ float sigmoid_fast(float x) { return __frcp_rn(1.0f + __expf(-x)); }
+
+// ---- GEMM operand functors: D[m][n] = sum_k a(m,k) * b(n,k) over this split's k range ------------------
+// conv2 forward: m = (b, y, x) over 26x26 outputs, n = kernel i, k = (c, ky, kx); epilogue + b2, sigmoid.
+struct OpConv2Fwd {
+  static constexpr bool kAContigM = true;
+  static constexpr int N = kC2N;
+  const float* s1;
+  const float* p;
+  float* c2;
+  int64_t M;
+  __device__ __forceinline__ void k_range(int, int64_t& k0, int64_t& k1) const {
+    k0 = 0;
+    k1 = kK2Slice;
+  }
+  __device__ __forceinline__ float a(int64_t m, int64_t k) const {
+    const unsigned mm = (unsigned)m, b = mm / kC2Pos, pos = mm - b * kC2Pos, y = pos / kC2W, x = pos - y * kC2W;
+    const unsigned kk = (unsigned)k, c = kk / 25, r = kk - c * 25, ky = r / 5, kx = r - ky * 5;
+    return s1[(size_t)((b * kC1N + c) * kS1W + y + ky) * kS1W + x + kx];
+  }
+  __device__ __forceinline__ float b(int n, int64_t k) const { return p[kOffK2 + n * kK2Slice + (int)k]; }
+  __device__ __forceinline__ void store(int, int64_t m, int n, float v) const {
+    const unsigned mm = (unsigned)m, b = mm / kC2Pos, pos = mm - b * kC2Pos;
+    c2[(size_t)(b * kC2N + n) * kC2Pos + pos] = sigmoid_fast(v + p[kOffB2 + n]);
+  }
+};
+
+// conv2 weight gradient (+ bias via the all-ones row m = 800): m = (c, ky, kx), n = i, k = (b, y, x);
+// split-K partials part[z][m][n] reduced in fixed split order.
+struct OpGk2 {
+  static constexpr bool kAContigM = false;
+  static constexpr int N = kC2N;
+  static constexpr int64_t M = kGk2Rows;
+  const float* s1;
+  const float* dz2;
+  float* part;
+  int64_t K;
+  int splits;
+  __device__ __forceinline__ void k_range(int z, int64_t& k0, int64_t& k1) const {
+    const int64_t chunk = ((K + splits - 1) / splits + 31) / 32 * 32;
+    k0 = (int64_t)z * chunk;
+    k1 = k0 + chunk < K ? k0 + chunk : K;
+  }
+  __device__ __forceinline__ float a(int64_t m, int64_t k) const {
+    if (m == kK2Slice) return 1.0f;
+    const unsigned kk = (unsigned)k, b = kk / kC2Pos, pos = kk - b * kC2Pos, y = pos / kC2W, x = pos - y * kC2W;
+    const unsigned mm = (unsigned)m, c = mm / 25, r = mm - c * 25, ky = r / 5, kx = r - ky * 5;
+    return s1[(size_t)((b * kC1N + c) * kS1W + y + ky) * kS1W + x + kx];
+  }
+  __device__ __forceinline__ float b(int n, int64_t k) const {
+    const unsigned kk = (unsigned)k, b = kk / kC2Pos;
+    return dz2[(size_t)(b * kC2N + n) * kC2Pos + (kk - b * kC2Pos)];
+  }
+  __device__ __forceinline__ void store(int z, int64_t m, int n, float v) const {
+    part[((int64_t)z * kGk2Rows + m) * kC2N + n] = v;
+  }
+};
+
+// conv2 backin: m = (b, p, q) over the 30x30 s1 plane, n = channel c, k = (i, u, v) over the 64 kernels'
+// 5x5 taps; a = dz2[b,i,p-u,q-v] (zero outside, the reference's clipped sums, nn.cpp:169-189).  Epilogue:
+// backavgpool (x0.25) + backsigmoid through c1 -> dz1, written in place over c1.
+struct OpBackin {
+  static constexpr bool kAContigM = true;
+  static constexpr int N = kC1N;
+  const float* dz2;
+  const float* p;
+  float* c1;
+  int64_t M;
+  __device__ __forceinline__ void k_range(int, int64_t& k0, int64_t& k1) const {
+    k0 = 0;
+    k1 = (int64_t)kC2N * 25;
+  }
+  __device__ __forceinline__ float a(int64_t m, int64_t k) const {
+    const unsigned mm = (unsigned)m, b = mm / kS1Pos, r = mm - b * kS1Pos, pp = r / kS1W, q = r - pp * kS1W;
+    const unsigned kk = (unsigned)k, i = kk / 25, u = kk - i * 25, u1 = u / 5, u2 = u - u1 * 5;
+    const unsigned y = pp - u1, x = q - u2;  // wraps to a huge value when negative
+    return (y < (unsigned)kC2W && x < (unsigned)kC2W) ? dz2[(size_t)(b * kC2N + i) * kC2Pos + y * kC2W + x] : 0.0f;
+  }
+  __device__ __forceinline__ float b(int n, int64_t k) const {
+    const unsigned kk = (unsigned)k, i = kk / 25, u = kk - i * 25;
+    return p[kOffK2 + (i * kC1N + n) * 25 + u];
+  }
+  __device__ __forceinline__ void store(int, int64_t m, int n, float v) const {
+    const unsigned mm = (unsigned)m, b = mm / kS1Pos, r = mm - b * kS1Pos, pp = r / kS1W, q = r - pp * kS1W;
+    const float dc = v * 0.25f;
+    float* base = c1 + (size_t)((b * kC1N + n) * kC1W + 2 * pp) * kC1W + 2 * q;
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx) {
+        const float o = base[dy * kC1W + dx];
+        base[dy * kC1W + dx] = (dc * o) * (1.0f - o);
+      }
+  }
+};
+
+inline int gk2_splits(int64_t m) {
+  const int64_t k = m * kC2Pos;
+  int64_t s = k / 2048;
+  if (s > 42) s = 42;
+  return s < 1 ? 1 : (int)s;
+}
+
+// ---- one SGD group ------------------------------------------------------------------------------------
+struct StepArgs {
+  const float* images;    // [m][64*64] of this group
+  const int32_t* labels;  // [m]
+  float* params;          // [kNParam]
+  int64_t m;
+  float rate;
+  bool tensor;            // GEMM engine: tcgen05 3xTF32 (true) or FP32 CUDA cores (false)
+  // workspaces (capacity >= m images)
+  float* c1;   // [m][32][60][60], dz1 in place
+  float* s1;   // [m][32][30][30]
+  float* c2;   // [m][64][26][26]
+  float* s2;   // [m][10816]
+  float* dz;   // [m][10]
+  float* loss; // [m]
+  float* dz2;  // [m][64][26][26]
+  float* part;   // [42][801][64] split-K partials of g_k2
+  float* part1;  // [m][32][26] conv1 gradient partials
+  float* grad;   // [kNParam]
+  double* epoch_loss;  // running fp64 epoch loss (nullable)
+  int first, last;
+  double n_total;
+};
+
+cudaError_t step(const StepArgs& a, cudaStream_t st);
+cudaError_t forward(const StepArgs& a, float* yhat, cudaStream_t st);
+cudaError_t gemm_only(int which, bool tensor, const StepArgs& a, cudaStream_t st);
+
+// tcgen05 engine (wide_tc.cu)
+cudaError_t tc_gemm(const OpConv2Fwd& op, int splits, cudaStream_t st);
+cudaError_t tc_gemm(const OpGk2& op, int splits, cudaStream_t st);
+cudaError_t tc_gemm(const OpBackin& op, int splits, cudaStream_t st);
+
+}  // namespace wide
+}  // namespace tlb

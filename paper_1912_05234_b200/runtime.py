@@ -70,6 +70,25 @@ def validate_set(images: np.ndarray, labels: np.ndarray) -> None:
     _check(_lib.lib().tlb_validate_set(_fp(images), _ip(labels), len(labels)))
 
 
+WIDE_NPARAM, WIDE_IMG = 160266, 4096
+WIDE_ENGINES = {"fp32": 0, "tc": 1}
+
+
+def wide_init_params(seed: int = 42) -> np.ndarray:
+    """Widened CNN (BASELINE configs[4]) parameters: network.cpp:56-79's rule with the widened fans."""
+    p = np.zeros(WIDE_NPARAM, np.float32)
+    _check(_lib.lib().tlb_wide_init_params(seed, _fp(p)))
+    return p
+
+
+def wide_make_set(n: int, seed: int):
+    """n 64x64 inputs (synth::make_digits glyphs centred on a zero canvas, /255) and labels."""
+    im = np.zeros((max(n, 1), WIDE_IMG), np.float32)
+    lab = np.zeros(max(n, 1), np.int32)
+    _check(_lib.lib().tlb_wide_make_set(n, seed, _fp(im), _ip(lab)))
+    return im[:n], lab[:n]
+
+
 class Context:
     """One device context of the CUDA library (tlb_ctx)."""
 
@@ -186,6 +205,31 @@ class Context:
                      epochs: int, batch: int, d_epoch_loss: int) -> None:
         _check(self._L.tlb_train_device(self._h, d_images, d_labels, n, d_params, rate, epoch_begin, epochs,
                                         batch, d_epoch_loss))
+
+    # ---- widened CNN (BASELINE configs[4]) ------------------------------------------------------------
+    def wide_train(self, params, images, labels, rate: float = 0.05, epochs: int = 1, batch: int = 100,
+                   engine: str = "tc"):
+        p = np.array(params, np.float32, copy=True)
+        images, labels = _f32(images), np.ascontiguousarray(labels, np.int32)
+        losses = np.zeros(max(epochs, 1), np.float64)
+        _check(self._L.tlb_wide_train(self._h, _fp(images), _ip(labels), len(labels), _fp(p), rate, epochs, batch,
+                                      losses.ctypes.data_as(_lib.f64p), WIDE_ENGINES[engine]))
+        return p, losses[: max(epochs, 0)]
+
+    def wide_train_device(self, d_images: int, d_labels: int, n: int, d_params: int, rate: float, epoch_begin: int,
+                          epochs: int, batch: int, d_epoch_loss: int, engine: str = "tc") -> None:
+        _check(self._L.tlb_wide_train_device(self._h, d_images, d_labels, n, d_params, rate, epoch_begin, epochs,
+                                             batch, d_epoch_loss, WIDE_ENGINES[engine]))
+
+    def wide_forward(self, images, params, engine: str = "tc") -> np.ndarray:
+        images = _f32(images).reshape(-1, WIDE_IMG)
+        n = images.shape[0]
+        yhat = np.zeros((max(n, 1), 10), np.float32)
+        _check(self._L.tlb_wide_forward(self._h, _fp(images), n, _fp(_f32(params)), _fp(yhat), WIDE_ENGINES[engine]))
+        return yhat[:n]
+
+    def wide_gemm_device(self, which: int, engine: str) -> None:
+        _check(self._L.tlb_wide_gemm_device(self._h, which, WIDE_ENGINES[engine]))
 
     def train_shard_device(self, d_images: int, d_labels: int, n: int, batch: int, group: int, shard_lo: int,
                            shard_hi: int, d_params: int, d_grad_sum: int, d_loss_sum: int) -> None:
