@@ -835,12 +835,13 @@ int wide_ws(tlb_ctx* c, int64_t m, W::StepArgs& a) {
     const size_t sizes[10] = {(size_t)m * W::kC1N * W::kC1W * W::kC1W * f, (size_t)m * W::kC1N * W::kS1Pos * f,
                               (size_t)m * W::kC2N * W::kC2Pos * f,        (size_t)m * W::kS2Len * f,
                               (size_t)m * W::kClasses * f,                (size_t)m * f,
-                              (size_t)m * W::kC2N * W::kC2Pos * f,        (size_t)42 * W::kGk2Rows * W::kC2N * f,
+                              (size_t)m * W::kC2N * W::kDzPlane * f,      (size_t)42 * W::kGk2Rows * W::kC2N * f,
                               (size_t)m * W::kC1N * 26 * f,               (size_t)(W::kNParam + 64) * f};
     for (int i = 0; i < 10; ++i) {
       c->wide[i].release();
       TLB_CUDA(c->wide[i].ensure(sizes[i]));
     }
+    TLB_CUDA(cudaMemset(c->wide[6].p, 0, sizes[6]));  // dz2's zero border (interior rewritten per group)
     c->wide_cap = m;
   }
   a.c1 = static_cast<float*>(c->wide[0].p);

@@ -244,9 +244,9 @@ __global__ void __launch_bounds__(512) fc_kernel(const float* __restrict__ c2, c
     for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
       for (int dx = 0; dx < 2; ++dx) {
-        const int64_t idx = ((int64_t)b * kC2N + i) * kC2Pos + (2 * py + dy) * kC2W + 2 * px + dx;
-        const float o = c2[idx];
-        dz2[idx] = (dc * o) * (1.0f - o);
+        const float o = c2[((int64_t)b * kC2N + i) * kC2Pos + (2 * py + dy) * kC2W + 2 * px + dx];
+        dz2[((int64_t)b * kC2N + i) * kDzPlane + (2 * py + dy + kDzPad) * kDzW + 2 * px + dx + kDzPad] =
+            (dc * o) * (1.0f - o);
       }
   }
 }

@@ -33,28 +33,51 @@ constexpr int64_t kFlopPerFwdImage = 2LL * (2880000 + 34611200 + 108160);
 
 __device__ __forceinline__ float sigmoid_fast(float x) { return __frcp_rn(1.0f + __expf(-x)); }
 
-// ---- GEMM operand functors: D[m][n] = sum_k a(m,k) * b(n,k) over this split's k range ------------------
+// dz2 is stored zero-padded by 4 on every side ([m][64][34][34]) so the backin gather needs no bounds
+// checks (the reference's clipped sums, nn.cpp:169-189, only ever drop zero products).
+constexpr int kDzPad = 4, kDzW = kC2W + 2 * kDzPad, kDzPlane = kDzW * kDzW;  // 34, 1156
+
+// ---- GEMM operand functors: D[m][n] = sum_k A[m][k] * B[n][k] over this split's k range ----------------
+// Every operand is separable: A[m][k] = Aptr[a_row(m) + a_col(k)], B[n][k] = Bptr[b_row(n) + b_col(k)], so
+// the producers compute a row base once per tile and look column offsets up (kKTab > 0: K is static and
+// the offsets are tabulated in shared memory once per CTA).  a(m,k)/b(n,k) are the generic forms.
+template <class Op>
+struct SepOps {
+  __device__ __forceinline__ static float a(const Op& o, int64_t m, int64_t k) {
+    return o.a_ones(m) ? 1.0f : o.A[o.a_row(m) + o.a_col(k)];
+  }
+  __device__ __forceinline__ static float b(const Op& o, int n, int64_t k) { return o.B[o.b_row(n) + o.b_col(k)]; }
+};
+
 // conv2 forward: m = (b, y, x) over 26x26 outputs, n = kernel i, k = (c, ky, kx); epilogue + b2, sigmoid.
 struct OpConv2Fwd {
   static constexpr bool kAContigM = true;
   static constexpr int N = kC2N;
-  const float* s1;
-  const float* p;
+  static constexpr int kKTab = kK2Slice;
+  const float* A;  // s1
+  const float* B;  // params (k2 rows)
   float* c2;
   int64_t M;
   __device__ __forceinline__ void k_range(int, int64_t& k0, int64_t& k1) const {
     k0 = 0;
     k1 = kK2Slice;
   }
-  __device__ __forceinline__ float a(int64_t m, int64_t k) const {
+  __device__ __forceinline__ bool a_ones(int64_t) const { return false; }
+  __device__ __forceinline__ int64_t a_row(int64_t m) const {
     const unsigned mm = (unsigned)m, b = mm / kC2Pos, pos = mm - b * kC2Pos, y = pos / kC2W, x = pos - y * kC2W;
-    const unsigned kk = (unsigned)k, c = kk / 25, r = kk - c * 25, ky = r / 5, kx = r - ky * 5;
-    return s1[(size_t)((b * kC1N + c) * kS1W + y + ky) * kS1W + x + kx];
+    return (int64_t)b * (kC1N * kS1Pos) + y * kS1W + x;
   }
-  __device__ __forceinline__ float b(int n, int64_t k) const { return p[kOffK2 + n * kK2Slice + (int)k]; }
+  __device__ __forceinline__ int a_col(int64_t k) const {
+    const unsigned kk = (unsigned)k, c = kk / 25, r = kk - c * 25, ky = r / 5, kx = r - ky * 5;
+    return (int)(c * kS1Pos + ky * kS1W + kx);
+  }
+  __device__ __forceinline__ int64_t b_row(int n) const { return kOffK2 + n * kK2Slice; }
+  __device__ __forceinline__ int b_col(int64_t k) const { return (int)k; }
+  __device__ __forceinline__ float a(int64_t m, int64_t k) const { return SepOps<OpConv2Fwd>::a(*this, m, k); }
+  __device__ __forceinline__ float b(int n, int64_t k) const { return SepOps<OpConv2Fwd>::b(*this, n, k); }
   __device__ __forceinline__ void store(int, int64_t m, int n, float v) const {
     const unsigned mm = (unsigned)m, b = mm / kC2Pos, pos = mm - b * kC2Pos;
-    c2[(size_t)(b * kC2N + n) * kC2Pos + pos] = sigmoid_fast(v + p[kOffB2 + n]);
+    c2[(size_t)(b * kC2N + n) * kC2Pos + pos] = sigmoid_fast(v + B[kOffB2 + n]);
   }
 };
 
@@ -63,9 +86,10 @@ struct OpConv2Fwd {
 struct OpGk2 {
   static constexpr bool kAContigM = false;
   static constexpr int N = kC2N;
+  static constexpr int kKTab = 0;
   static constexpr int64_t M = kGk2Rows;
-  const float* s1;
-  const float* dz2;
+  const float* A;  // s1
+  const float* B;  // dz2 (padded)
   float* part;
   int64_t K;
   int splits;
@@ -74,45 +98,58 @@ struct OpGk2 {
     k0 = (int64_t)z * chunk;
     k1 = k0 + chunk < K ? k0 + chunk : K;
   }
-  __device__ __forceinline__ float a(int64_t m, int64_t k) const {
-    if (m == kK2Slice) return 1.0f;
-    const unsigned kk = (unsigned)k, b = kk / kC2Pos, pos = kk - b * kC2Pos, y = pos / kC2W, x = pos - y * kC2W;
+  __device__ __forceinline__ bool a_ones(int64_t m) const { return m == kK2Slice; }
+  __device__ __forceinline__ int64_t a_row(int64_t m) const {
     const unsigned mm = (unsigned)m, c = mm / 25, r = mm - c * 25, ky = r / 5, kx = r - ky * 5;
-    return s1[(size_t)((b * kC1N + c) * kS1W + y + ky) * kS1W + x + kx];
+    return c * kS1Pos + ky * kS1W + kx;
   }
-  __device__ __forceinline__ float b(int n, int64_t k) const {
-    const unsigned kk = (unsigned)k, b = kk / kC2Pos;
-    return dz2[(size_t)(b * kC2N + n) * kC2Pos + (kk - b * kC2Pos)];
+  __device__ __forceinline__ int64_t a_col(int64_t k) const {
+    const unsigned kk = (unsigned)k, b = kk / kC2Pos, pos = kk - b * kC2Pos, y = pos / kC2W, x = pos - y * kC2W;
+    return (int64_t)b * (kC1N * kS1Pos) + y * kS1W + x;
   }
+  __device__ __forceinline__ int64_t b_row(int n) const { return (int64_t)n * kDzPlane + kDzPad * kDzW + kDzPad; }
+  __device__ __forceinline__ int64_t b_col(int64_t k) const {
+    const unsigned kk = (unsigned)k, b = kk / kC2Pos, pos = kk - b * kC2Pos, y = pos / kC2W, x = pos - y * kC2W;
+    return (int64_t)b * (kC2N * kDzPlane) + y * kDzW + x;
+  }
+  __device__ __forceinline__ float a(int64_t m, int64_t k) const { return SepOps<OpGk2>::a(*this, m, k); }
+  __device__ __forceinline__ float b(int n, int64_t k) const { return SepOps<OpGk2>::b(*this, n, k); }
   __device__ __forceinline__ void store(int z, int64_t m, int n, float v) const {
     part[((int64_t)z * kGk2Rows + m) * kC2N + n] = v;
   }
 };
 
 // conv2 backin: m = (b, p, q) over the 30x30 s1 plane, n = channel c, k = (i, u, v) over the 64 kernels'
-// 5x5 taps; a = dz2[b,i,p-u,q-v] (zero outside, the reference's clipped sums, nn.cpp:169-189).  Epilogue:
-// backavgpool (x0.25) + backsigmoid through c1 -> dz1, written in place over c1.
+// 5x5 taps; A = padded dz2[b, i, p+4-u, q+4-v].  Epilogue: backavgpool (x0.25) + backsigmoid through c1
+// -> dz1, written in place over c1.
 struct OpBackin {
   static constexpr bool kAContigM = true;
   static constexpr int N = kC1N;
-  const float* dz2;
-  const float* p;
+  static constexpr int kKTab = kC2N * 25;
+  const float* A;  // dz2 (padded)
+  const float* B;  // params (k2)
   float* c1;
   int64_t M;
   __device__ __forceinline__ void k_range(int, int64_t& k0, int64_t& k1) const {
     k0 = 0;
     k1 = (int64_t)kC2N * 25;
   }
-  __device__ __forceinline__ float a(int64_t m, int64_t k) const {
+  __device__ __forceinline__ bool a_ones(int64_t) const { return false; }
+  __device__ __forceinline__ int64_t a_row(int64_t m) const {
     const unsigned mm = (unsigned)m, b = mm / kS1Pos, r = mm - b * kS1Pos, pp = r / kS1W, q = r - pp * kS1W;
-    const unsigned kk = (unsigned)k, i = kk / 25, u = kk - i * 25, u1 = u / 5, u2 = u - u1 * 5;
-    const unsigned y = pp - u1, x = q - u2;  // wraps to a huge value when negative
-    return (y < (unsigned)kC2W && x < (unsigned)kC2W) ? dz2[(size_t)(b * kC2N + i) * kC2Pos + y * kC2W + x] : 0.0f;
+    return (int64_t)b * (kC2N * kDzPlane) + (pp + kDzPad) * kDzW + q + kDzPad;
   }
-  __device__ __forceinline__ float b(int n, int64_t k) const {
-    const unsigned kk = (unsigned)k, i = kk / 25, u = kk - i * 25;
-    return p[kOffK2 + (i * kC1N + n) * 25 + u];
+  __device__ __forceinline__ int a_col(int64_t k) const {
+    const int kk = (int)k, i = kk / 25, u = kk - i * 25, u1 = u / 5, u2 = u - u1 * 5;
+    return i * kDzPlane - u1 * kDzW - u2;
   }
+  __device__ __forceinline__ int64_t b_row(int n) const { return kOffK2 + n * 25; }
+  __device__ __forceinline__ int b_col(int64_t k) const {
+    const int kk = (int)k, i = kk / 25, u = kk - i * 25;
+    return i * kK2Slice + u;
+  }
+  __device__ __forceinline__ float a(int64_t m, int64_t k) const { return SepOps<OpBackin>::a(*this, m, k); }
+  __device__ __forceinline__ float b(int n, int64_t k) const { return SepOps<OpBackin>::b(*this, n, k); }
   __device__ __forceinline__ void store(int, int64_t m, int n, float v) const {
     const unsigned mm = (unsigned)m, b = mm / kS1Pos, r = mm - b * kS1Pos, pp = r / kS1W, q = r - pp * kS1W;
     const float dc = v * 0.25f;
@@ -149,7 +186,7 @@ struct StepArgs {
   float* s2;   // [m][10816]
   float* dz;   // [m][10]
   float* loss; // [m]
-  float* dz2;  // [m][64][26][26]
+  float* dz2;  // [m][64][34][34], zero border of 4 (kDzPad)
   float* part;   // [42][801][64] split-K partials of g_k2
   float* part1;  // [m][32][26] conv1 gradient partials
   float* grad;   // [kNParam]

@@ -31,6 +31,7 @@ struct TcCfg {
   static constexpr int kBBytes = N * kBK * 4;
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
   static constexpr int kSmem = kStages * kStageBytes + 1024;  // + alignment slack (SW128 atoms: 1 KB)
+  // + the column-offset tables of ops with a static K (int32 A and B offsets)
   static constexpr int kTmemCols = N < 32 ? 32 : N;
   // kind::tf32 instruction descriptor: D f32 (bits 4-5 = 1), A/B tf32 (bits 7-9, 10-12 = 2), both
   // K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28.
@@ -87,9 +88,15 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
 __device__ __forceinline__ uint32_t sw128_off(int r, int j) { return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4)); }
 
 template <class Op>
+constexpr int tc_smem_bytes() {
+  return TcCfg<Op::N>::kSmem + 2 * Op::kKTab * (int)sizeof(int);
+}
+
+template <class Op>
 __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(Op op) {
   constexpr int N = Op::N;
   using Cfg = TcCfg<N>;
+  constexpr int kTab = Op::kKTab > 0 ? Op::kKTab : 1;
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
   __shared__ uint64_t full[kStages], empty[kStages], done;
   __shared__ uint32_t tmem_slot;
@@ -100,6 +107,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(Op op) {
   op.k_range(blockIdx.z, k0, k1);
   const int nchunks = k1 > k0 ? (int)((k1 - k0 + kBK - 1) / kBK) : 0;
 
+  int* const acol = reinterpret_cast<int*>(base + kStages * Cfg::kStageBytes);  // [kKTab] when K is static
+  int* const bcol = acol + kTab;
+  if constexpr (Op::kKTab > 0) {
+    for (int k = tid; k < Op::kKTab; k += blockDim.x) {
+      acol[k] = (int)op.a_col(k);
+      bcol[k] = (int)op.b_col(k);
+    }
+  }
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], kProducers);
@@ -127,19 +142,32 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(Op op) {
     const int ra_r = tid & (kBM - 1), ra_kh = tid >> 7;
     const int rb_r = tid % N, rb_part = tid / N;
     const int64_t m = m0 + ra_r;
-    const bool mv = m < op.M;
+    const bool mv = m < op.M, ones = op.a_ones(m);
+    const float* __restrict__ Ap = op.A + (mv && !ones ? op.a_row(m) : 0);
+    const float* __restrict__ Bp = op.B + op.b_row(rb_r);
     float va[16], vb[kBElems];
+    // A[m][k] = Ap[col(k)], B[n][k] = Bp[col(k)]: one add + one load per element
     auto gather = [&](int c, float (&a)[16], float (&b)[kBElems]) {
       const int64_t kb = k0 + (int64_t)c * kBK;
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const int64_t k = kb + ra_kh * 16 + e;
-        a[e] = (mv && k < k1) ? op.a(m, k) : 0.0f;
+        float v = 0.0f;
+        if (mv && k < k1) {
+          if constexpr (Op::kKTab > 0) v = ones ? 1.0f : Ap[acol[k]];
+          else v = ones ? 1.0f : Ap[op.a_col(k)];
+        }
+        a[e] = v;
       }
 #pragma unroll
       for (int e = 0; e < kBElems; ++e) {
         const int64_t k = kb + rb_part * kBElems + e;
-        b[e] = k < k1 ? op.b(rb_r, k) : 0.0f;
+        float v = 0.0f;
+        if (k < k1) {
+          if constexpr (Op::kKTab > 0) v = Bp[bcol[k]];
+          else v = Bp[op.b_col(k)];
+        }
+        b[e] = v;
       }
     };
     if (nchunks > 0) gather(0, va, vb);
@@ -225,15 +253,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(Op op) {
 
 template <class Op>
 cudaError_t launch_tc(const Op& op, int splits, cudaStream_t st) {
-  using Cfg = TcCfg<Op::N>;
+  constexpr int kSmem = tc_smem_bytes<Op>();
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const dim3 grid((unsigned)((op.M + kBM - 1) / kBM), 1, (unsigned)splits);
-  tc_gemm_kernel<Op><<<grid, kThreadsTC, Cfg::kSmem, st>>>(op);
+  tc_gemm_kernel<Op><<<grid, kThreadsTC, kSmem, st>>>(op);
   return cudaGetLastError();
 }
 
