@@ -832,12 +832,13 @@ namespace W = tlb::wide;
 int wide_ws(tlb_ctx* c, int64_t m, W::StepArgs& a) {
   if (m > c->wide_cap) {
     const size_t f = sizeof(float);
-    const size_t sizes[10] = {(size_t)m * W::kC1N * W::kC1W * W::kC1W * f, (size_t)m * W::kC1N * W::kS1Pos * f,
+    const size_t sizes[12] = {(size_t)m * W::kC1N * W::kC1W * W::kC1W * f, (size_t)m * W::kC1N * W::kS1Pos * f,
                               (size_t)m * W::kC2N * W::kC2Pos * f,        (size_t)m * W::kS2Len * f,
                               (size_t)m * W::kClasses * f,                (size_t)m * f,
                               (size_t)m * W::kC2N * W::kDzPlane * f,      (size_t)42 * W::kGk2Rows * W::kC2N * f,
-                              (size_t)m * W::kC1N * 26 * f,               (size_t)(W::kNParam + 64) * f};
-    for (int i = 0; i < 10; ++i) {
+                              (size_t)m * W::kC1N * 26 * f,               (size_t)(W::kNParam + 64) * f,
+                              (size_t)m * W::kC2N * W::kC2Pos * f,        W::kBImgBytes};
+    for (int i = 0; i < 12; ++i) {
       c->wide[i].release();
       TLB_CUDA(c->wide[i].ensure(sizes[i]));
     }
@@ -854,6 +855,8 @@ int wide_ws(tlb_ctx* c, int64_t m, W::StepArgs& a) {
   a.part = static_cast<float*>(c->wide[7].p);
   a.part1 = static_cast<float*>(c->wide[8].p);
   a.grad = static_cast<float*>(c->wide[9].p);
+  a.dz2t = static_cast<float*>(c->wide[10].p);
+  a.bimg = static_cast<float*>(c->wide[11].p);
   return TLB_OK;
 }
 

@@ -187,7 +187,7 @@ cudaError_t simt_gemm(const Op& op, int splits, cudaStream_t st) {
 __global__ void __launch_bounds__(512) fc_kernel(const float* __restrict__ c2, const float* __restrict__ p,
                                                  const int32_t* __restrict__ labels, float* __restrict__ s2g,
                                                  float* __restrict__ dzg, float* __restrict__ lossg,
-                                                 float* __restrict__ dz2) {
+                                                 float* __restrict__ dz2, float* __restrict__ dz2t, int64_t m) {
   __shared__ float s2[kS2Len];
   __shared__ float red[16][kClasses];
   __shared__ float dz[kClasses];
@@ -244,9 +244,11 @@ __global__ void __launch_bounds__(512) fc_kernel(const float* __restrict__ c2, c
     for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
       for (int dx = 0; dx < 2; ++dx) {
-        const float o = c2[((int64_t)b * kC2N + i) * kC2Pos + (2 * py + dy) * kC2W + 2 * px + dx];
-        dz2[((int64_t)b * kC2N + i) * kDzPlane + (2 * py + dy + kDzPad) * kDzW + 2 * px + dx + kDzPad] =
-            (dc * o) * (1.0f - o);
+        const int pos = (2 * py + dy) * kC2W + 2 * px + dx;
+        const float o = c2[((int64_t)b * kC2N + i) * kC2Pos + pos];
+        const float v = (dc * o) * (1.0f - o);
+        dz2[((int64_t)b * kC2N + i) * kDzPlane + (2 * py + dy + kDzPad) * kDzW + 2 * px + dx + kDzPad] = v;
+        dz2t[(int64_t)i * (m * kC2Pos) + (int64_t)b * kC2Pos + pos] = v;
       }
   }
 }
@@ -348,17 +350,17 @@ cudaError_t step(const StepArgs& a, cudaStream_t st) {
   cudaError_t e;
   conv1_kernel<<<dim3((unsigned)m, kC1N / kC1Group), 256, 0, st>>>(a.images, a.params, a.c1, a.s1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  OpConv2Fwd f{a.s1, a.params, a.c2, m * kC2Pos};
+  OpConv2Fwd f{a.s1, a.params, a.c2, m * kC2Pos, a.bimg};
   if ((e = a.tensor ? tc_gemm(f, 1, st) : simt_gemm<OpConv2Fwd, 64>(f, 1, st)) != cudaSuccess) return e;
-  fc_kernel<<<(unsigned)m, 512, 0, st>>>(a.c2, a.params, a.labels, a.s2, a.dz, a.loss, a.dz2);
+  fc_kernel<<<(unsigned)m, 512, 0, st>>>(a.c2, a.params, a.labels, a.s2, a.dz, a.loss, a.dz2, a.dz2t, m);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   gfc_kernel<<<(kClasses * kS2Len + kClasses + 255) / 256, 256, 0, st>>>(a.s2, a.dz, m, a.grad);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  OpGk2 gk{a.s1, a.dz2, a.part, m * kC2Pos, gk2_splits(m)};
+  OpGk2 gk{a.s1, a.dz2t, a.part, m * kC2Pos, gk2_splits(m)};
   if ((e = a.tensor ? tc_gemm(gk, gk.splits, st) : simt_gemm<OpGk2, 64>(gk, gk.splits, st)) != cudaSuccess) return e;
   gk2_reduce_kernel<<<(kGk2Rows * kC2N + 255) / 256, 256, 0, st>>>(a.part, gk.splits, a.grad);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  OpBackin bi{a.dz2, a.params, a.c1, m * kS1Pos};
+  OpBackin bi{a.dz2, a.params, a.c1, m * kS1Pos, a.bimg};
   if ((e = a.tensor ? tc_gemm(bi, 1, st) : simt_gemm<OpBackin, 32>(bi, 1, st)) != cudaSuccess) return e;
   gk1_kernel<<<dim3((unsigned)m, kC1N), 256, 0, st>>>(a.images, a.c1, a.part1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -415,7 +417,7 @@ cudaError_t forward(const StepArgs& a, float* yhat, cudaStream_t st) {
   conv1_kernel<<<dim3((unsigned)m, kC1N / kC1Group), 256, 0, st>>>(a.images, a.params, a.c1, a.s1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  OpConv2Fwd f{a.s1, a.params, a.c2, m * kC2Pos};
+  OpConv2Fwd f{a.s1, a.params, a.c2, m * kC2Pos, a.bimg};
   if ((e = a.tensor ? tc_gemm(f, 1, st) : simt_gemm<OpConv2Fwd, 64>(f, 1, st)) != cudaSuccess) return e;
   fc_forward_kernel<<<(unsigned)m, 512, 0, st>>>(a.c2, a.params, yhat);
   return cudaGetLastError();
@@ -426,14 +428,14 @@ cudaError_t forward(const StepArgs& a, float* yhat, cudaStream_t st) {
 cudaError_t gemm_only(int which, bool tensor, const StepArgs& a, cudaStream_t st) {
   const int64_t m = a.m;
   if (which == 0) {
-    OpConv2Fwd f{a.s1, a.params, a.c2, m * kC2Pos};
+    OpConv2Fwd f{a.s1, a.params, a.c2, m * kC2Pos, a.bimg};
     return tensor ? tc_gemm(f, 1, st) : simt_gemm<OpConv2Fwd, 64>(f, 1, st);
   }
   if (which == 1) {
-    OpGk2 gk{a.s1, a.dz2, a.part, m * kC2Pos, gk2_splits(m)};
+    OpGk2 gk{a.s1, a.dz2t, a.part, m * kC2Pos, gk2_splits(m)};
     return tensor ? tc_gemm(gk, gk.splits, st) : simt_gemm<OpGk2, 64>(gk, gk.splits, st);
   }
-  OpBackin bi{a.dz2, a.params, a.c1, m * kS1Pos};
+  OpBackin bi{a.dz2, a.params, a.c1, m * kS1Pos, a.bimg};
   return tensor ? tc_gemm(bi, 1, st) : simt_gemm<OpBackin, 32>(bi, 1, st);
 }
 

@@ -54,10 +54,13 @@ struct OpConv2Fwd {
   static constexpr bool kAContigM = true;
   static constexpr int N = kC2N;
   static constexpr int kKTab = kK2Slice;
+  static constexpr bool kBImage = true;   // B (the weights) is the same for every tile: pre-split image
+  static constexpr bool kBDense = false;
   const float* A;  // s1
   const float* B;  // params (k2 rows)
   float* c2;
   int64_t M;
+  const float* Bimg;  // tensor-core engine: per-chunk hi|lo swizzled B stages (tc_prepare_b)
   __device__ __forceinline__ void k_range(int, int64_t& k0, int64_t& k1) const {
     k0 = 0;
     k1 = kK2Slice;
@@ -87,9 +90,11 @@ struct OpGk2 {
   static constexpr bool kAContigM = false;
   static constexpr int N = kC2N;
   static constexpr int kKTab = 0;
+  static constexpr bool kBImage = false;
+  static constexpr bool kBDense = true;   // B rows contiguous and 16-B aligned: float4 gathers
   static constexpr int64_t M = kGk2Rows;
   const float* A;  // s1
-  const float* B;  // dz2 (padded)
+  const float* B;  // dz2t: [64][K] = dz2 transposed to (i, (b, y, x)), written by fc_kernel
   float* part;
   int64_t K;
   int splits;
@@ -107,11 +112,24 @@ struct OpGk2 {
     const unsigned kk = (unsigned)k, b = kk / kC2Pos, pos = kk - b * kC2Pos, y = pos / kC2W, x = pos - y * kC2W;
     return (int64_t)b * (kC1N * kS1Pos) + y * kS1W + x;
   }
-  __device__ __forceinline__ int64_t b_row(int n) const { return (int64_t)n * kDzPlane + kDzPad * kDzW + kDzPad; }
-  __device__ __forceinline__ int64_t b_col(int64_t k) const {
-    const unsigned kk = (unsigned)k, b = kk / kC2Pos, pos = kk - b * kC2Pos, y = pos / kC2W, x = pos - y * kC2W;
-    return (int64_t)b * (kC2N * kDzPlane) + y * kDzW + x;
+  // a_col of 16 consecutive k: decompose the first, then step x -> y -> image with carries
+  __device__ __forceinline__ void a_cols16(int64_t k, int64_t (&o)[16]) const {
+    const unsigned kk = (unsigned)k;
+    unsigned b = kk / kC2Pos, pos = kk - b * kC2Pos, y = pos / kC2W, x = pos - y * kC2W;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      o[e] = (int64_t)b * (kC1N * kS1Pos) + y * kS1W + x;
+      if (++x == (unsigned)kC2W) {
+        x = 0;
+        if (++y == (unsigned)kC2W) {
+          y = 0;
+          ++b;
+        }
+      }
+    }
   }
+  __device__ __forceinline__ int64_t b_row(int n) const { return (int64_t)n * K; }
+  __device__ __forceinline__ int64_t b_col(int64_t k) const { return k; }
   __device__ __forceinline__ float a(int64_t m, int64_t k) const { return SepOps<OpGk2>::a(*this, m, k); }
   __device__ __forceinline__ float b(int n, int64_t k) const { return SepOps<OpGk2>::b(*this, n, k); }
   __device__ __forceinline__ void store(int z, int64_t m, int n, float v) const {
@@ -126,10 +144,13 @@ struct OpBackin {
   static constexpr bool kAContigM = true;
   static constexpr int N = kC1N;
   static constexpr int kKTab = kC2N * 25;
+  static constexpr bool kBImage = true;
+  static constexpr bool kBDense = false;
   const float* A;  // dz2 (padded)
   const float* B;  // params (k2)
   float* c1;
   int64_t M;
+  const float* Bimg;
   __device__ __forceinline__ void k_range(int, int64_t& k0, int64_t& k1) const {
     k0 = 0;
     k1 = (int64_t)kC2N * 25;
@@ -187,6 +208,8 @@ struct StepArgs {
   float* dz;   // [m][10]
   float* loss; // [m]
   float* dz2;  // [m][64][34][34], zero border of 4 (kDzPad)
+  float* dz2t; // [64][m*676]: dz2 transposed (the conv2 weight-gradient GEMM's B operand)
+  float* bimg; // tensor-core engine: pre-split B stage images (<= 400 KB)
   float* part;   // [42][801][64] split-K partials of g_k2
   float* part1;  // [m][32][26] conv1 gradient partials
   float* grad;   // [kNParam]
@@ -200,6 +223,7 @@ cudaError_t forward(const StepArgs& a, float* yhat, cudaStream_t st);
 cudaError_t gemm_only(int which, bool tensor, const StepArgs& a, cudaStream_t st);
 
 // tcgen05 engine (wide_tc.cu)
+constexpr size_t kBImgBytes = 50 * 2 * 32 * 32 * 4;  // max over ops: chunks x (hi|lo) x N x 32 fp32
 cudaError_t tc_gemm(const OpConv2Fwd& op, int splits, cudaStream_t st);
 cudaError_t tc_gemm(const OpGk2& op, int splits, cudaStream_t st);
 cudaError_t tc_gemm(const OpBackin& op, int splits, cudaStream_t st);

@@ -22,7 +22,7 @@ namespace tlb {
 namespace wide {
 namespace {
 
-constexpr int kBM = 128, kBK = 32, kStages = 4;
+constexpr int kBM = 128, kBK = 32, kStages = 2;  // 2 stages x 2 CTAs per SM: twice the gathers in flight
 constexpr int kProducers = 256, kThreadsTC = kProducers + 32;
 
 template <int N>
@@ -89,18 +89,24 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int j) { return (uint32_t)(
 
 template <class Op>
 constexpr int tc_smem_bytes() {
-  return TcCfg<Op::N>::kSmem + 2 * Op::kKTab * (int)sizeof(int);
+  return kStages * TcCfg<Op::N>::kStageBytes + 2 * (Op::kKTab > 0 ? Op::kKTab : 1) * (int)sizeof(int) +
+         (2 * kStages + 2) * 8;
 }
 
 template <class Op>
-__global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(Op op) {
+__global__ void __launch_bounds__(kThreadsTC, 2) tc_gemm_kernel(Op op) {
   constexpr int N = Op::N;
   using Cfg = TcCfg<N>;
   constexpr int kTab = Op::kKTab > 0 ? Op::kKTab : 1;
+  // Dynamic shared memory only (no static __shared__), so the window starts 1024-B aligned and every
+  // pointer below stays in the shared state space (LDS/STS, not generic LD/ST):
+  //   [stages x (Ahi|Alo|Bhi|Blo)] [A/B column tables] [mbarriers full/empty/done] [TMEM slot]
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
-  __shared__ uint64_t full[kStages], empty[kStages], done;
-  __shared__ uint32_t tmem_slot;
-  uint8_t* const base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* const base = tc_smem_raw;
+  uint64_t* const full = reinterpret_cast<uint64_t*>(base + kStages * Cfg::kStageBytes + 2 * kTab * sizeof(int));
+  uint64_t* const empty = full + kStages;
+  uint64_t* const done_bar = empty + kStages;
+  uint32_t* const tmem_slot_p = reinterpret_cast<uint32_t*>(done_bar + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t m0 = (int64_t)blockIdx.x * kBM;
   int64_t k0, k1;
@@ -117,21 +123,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(Op op) {
   }
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], kProducers);
+      mbar_init(&full[s], kProducers + (Op::kBImage ? 1 : 0));  // + the B image's expect_tx arrival
       mbar_init(&empty[s], 1);
     }
-    mbar_init(&done, 1);
+    mbar_init(done_bar, 1);
     fence_barrier_init();
   }
   if (warp == 8) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot_p)),
                  "r"(Cfg::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_slot;
+  const uint32_t tmem = *tmem_slot_p;
 
   if (warp < 8) {
     // ---- producers: thread t owns A row t % 128 (16 of the chunk's 32 k) and B row t % N (32*N/256 k).
@@ -140,34 +146,47 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(Op op) {
     constexpr int kPerRowB = kProducers / N;  // threads per B row (4 or 8)
     constexpr int kBElems = kBK / kPerRowB;   // B elements per thread per chunk (8 or 4)
     const int ra_r = tid & (kBM - 1), ra_kh = tid >> 7;
-    const int rb_r = tid % N, rb_part = tid / N;
+    // B row / part: dense rows take consecutive threads along the row (coalesced float4 gathers)
+    const int rb_r = Op::kBDense ? tid / kPerRowB : tid % N, rb_part = Op::kBDense ? tid % kPerRowB : tid / N;
     const int64_t m = m0 + ra_r;
     const bool mv = m < op.M, ones = op.a_ones(m);
     const float* __restrict__ Ap = op.A + (mv && !ones ? op.a_row(m) : 0);
     const float* __restrict__ Bp = op.B + op.b_row(rb_r);
+    const int64_t kbeg = k0, kend = k1;
     float va[16], vb[kBElems];
     // A[m][k] = Ap[col(k)], B[n][k] = Bp[col(k)]: one add + one load per element
     auto gather = [&](int c, float (&a)[16], float (&b)[kBElems]) {
-      const int64_t kb = k0 + (int64_t)c * kBK;
+      const int64_t kb = kbeg + (int64_t)c * kBK;
+      int64_t ac[16];
+      if constexpr (Op::kKTab == 0) op.a_cols16(kb + ra_kh * 16, ac);  // one decomposition, then a walk
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const int64_t k = kb + ra_kh * 16 + e;
         float v = 0.0f;
-        if (mv && k < k1) {
+        if (mv && k < kend) {
           if constexpr (Op::kKTab > 0) v = ones ? 1.0f : Ap[acol[k]];
-          else v = ones ? 1.0f : Ap[op.a_col(k)];
+          else v = ones ? 1.0f : Ap[ac[e]];
         }
         a[e] = v;
       }
+      if constexpr (Op::kBDense) {
 #pragma unroll
-      for (int e = 0; e < kBElems; ++e) {
-        const int64_t k = kb + rb_part * kBElems + e;
-        float v = 0.0f;
-        if (k < k1) {
-          if constexpr (Op::kKTab > 0) v = Bp[bcol[k]];
-          else v = Bp[op.b_col(k)];
+        for (int e = 0; e < kBElems; e += 4) {
+          const int64_t k = kb + rb_part * kBElems + e;  // K, split bounds and row starts are multiples of 4
+          const float4 v = k < kend ? __ldg(reinterpret_cast<const float4*>(Bp + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          b[e] = v.x; b[e + 1] = v.y; b[e + 2] = v.z; b[e + 3] = v.w;
         }
-        b[e] = v;
+      } else if constexpr (!Op::kBImage) {
+#pragma unroll
+        for (int e = 0; e < kBElems; ++e) {
+          const int64_t k = kb + rb_part * kBElems + e;
+          float v = 0.0f;
+          if (k < kend) {
+            if constexpr (Op::kKTab > 0) v = Bp[bcol[k]];
+            else v = Bp[op.b_col(k)];
+          }
+          b[e] = v;
+        }
       }
     };
     if (nchunks > 0) gather(0, va, vb);
@@ -178,6 +197,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(Op op) {
       if (c >= kStages) mbar_wait(&empty[s], ((c / kStages) - 1) & 1);
       uint8_t* st = base + s * Cfg::kStageBytes;
       uint8_t *ahi = st, *alo = st + Cfg::kABytes, *bhi = st + 2 * Cfg::kABytes, *blo = bhi + Cfg::kBBytes;
+      if constexpr (Op::kBImage) {
+        if (tid == 0) {  // the pre-split B stage (hi|lo, already swizzled) by one 1-D TMA bulk copy
+          mbar_arrive_expect_tx(&full[s], 2 * Cfg::kBBytes);
+          tma_load_1d(bhi, reinterpret_cast<const uint8_t*>(op.Bimg) + (size_t)c * 2 * Cfg::kBBytes, 2 * Cfg::kBBytes,
+                      &full[s]);
+        }
+      }
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
         float h[4], l[4];
@@ -188,7 +214,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(Op op) {
         *reinterpret_cast<float4*>(alo + o) = make_float4(l[0], l[1], l[2], l[3]);
       }
 #pragma unroll
-      for (int jj = 0; jj < kBElems / 4; ++jj) {
+      for (int jj = 0; jj < (Op::kBImage ? 0 : kBElems / 4); ++jj) {
         float h[4], l[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) split_tf32(vb[4 * jj + e], h[e], l[e]);
@@ -220,12 +246,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(Op op) {
       }
       mma_commit(&empty[s]);
     }
-    mma_commit(&done);
+    mma_commit(done_bar);
   }
 
   // ---- epilogue (warps 0-3: TMEM lanes 32w..32w+31 = tile rows) ----
   if (warp < 4) {
-    mbar_wait(&done, 0);
+    mbar_wait(done_bar, 0);
     tc_fence_after();
     const int r = warp * 32 + lane;
     const int64_t m = m0 + r;
@@ -251,8 +277,39 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(Op op) {
   }
 }
 
+// B stage images for ops whose B (the conv2 weights) is shared by every tile: chunk c, row n, k-in-chunk kk
+// -> hi|lo fp32 at the SWIZZLE_128B position the UMMA descriptor expects.  Rebuilt per group (the weights
+// change every SGD step); 51,200 elements.
+template <class Op>
+__global__ void bimg_kernel(Op op, int64_t K) {
+  constexpr int N = Op::N;
+  using Cfg = TcCfg<N>;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nch = (K + kBK - 1) / kBK;
+  if (t >= nch * N * kBK) return;
+  const int kk = (int)(t % kBK), n = (int)((t / kBK) % N);
+  const int64_t c = t / ((int64_t)kBK * N), k = c * kBK + kk;
+  const float v = k < K ? op.B[op.b_row(n) + op.b_col(k)] : 0.0f;
+  float hi, lo;
+  split_tf32(v, hi, lo);
+  uint8_t* img = reinterpret_cast<uint8_t*>(const_cast<float*>(op.Bimg)) + (size_t)c * 2 * Cfg::kBBytes;
+  const uint32_t off = sw128_off(n, kk >> 2) + (kk & 3) * 4;
+  *reinterpret_cast<float*>(img + off) = hi;
+  *reinterpret_cast<float*>(img + Cfg::kBBytes + off) = lo;
+}
+
 template <class Op>
 cudaError_t launch_tc(const Op& op, int splits, cudaStream_t st) {
+  if constexpr (Op::kBImage) {
+    int64_t k0 = 0, K = 0;
+    // static K: the op's k_range does not depend on the split
+    K = Op::kKTab;
+    (void)k0;
+    const int64_t total = ((K + kBK - 1) / kBK) * Op::N * kBK;
+    bimg_kernel<Op><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(op, K);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   constexpr int kSmem = tc_smem_bytes<Op>();
   static bool attr = false;
   if (!attr) {
