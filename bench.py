@@ -167,6 +167,23 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def ncu_traffic(mode: str, batch: int, n: int, world: int):
+    """DRAM bytes per launch (read + write) of the train kernel from the committed `ncu --set full` capture
+    of this exact workload (profiles/r1/ncu_train_cluster_keymetrics.csv: fast mode, batch 100, 10k images,
+    one epoch per launch); None for any other configuration."""
+    path = os.path.join(ROOT, "profiles", "r1", "ncu_train_cluster_keymetrics.csv")
+    if not (mode == "fast" and batch == 100 and n == 10000 and world == 1 and os.path.exists(path)):
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    import csv
+    with open(path) as f:
+        for row in csv.DictReader(f):
+            if row["metric"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                total += float(row["value"]) * scale.get(row["unit"], 1)
+    return total
+
+
 # ---- our arm ----------------------------------------------------------------------------------------
 def run_ours(args):
     import torch
@@ -267,7 +284,9 @@ def run_ours(args):
                    "l2": "flushed between timed steps (256 MiB write outside the event pair)"},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp32_peak, "traffic": None,
+                     "frac": achieved / fp32_peak, "traffic": ncu_traffic(args.mode, B, n_per, world),
+                     "traffic_note": "DRAM bytes/launch from profiles/r1/ncu_train_cluster_keymetrics.csv; "
+                                     f"algorithmic input bytes/launch = {n_per * 3136}",
                      "per_launch": f"{n_per} images x {FLOP_PER_TRAIN_IMAGE} algorithmic FLOP",
                      "peak_source": f"{info['sm_count']} SMs x 128 FP32 lanes x 2 x sm_max_mhz {max_mhz} "
                                     "(MEASURED_PEAKS.json clocks); FFMA-bound path (no HBM/tensor bound)"},
