@@ -72,6 +72,10 @@ int tlb_ctx_set_trace(tlb_ctx* ctx, void* d_trace);
 /* Fast mode, groups of <= 8 x (co-resident clusters) examples: 1 (default) runs the clustered train
  * kernel (DSMEM gradient pre-reduction, one grid barrier per step); 0 forces the flat kernel. */
 int tlb_ctx_set_cluster(tlb_ctx* ctx, int enable);
+/* CTA size of the flat train / forward kernels: 0 = automatic (default: 256 = two independent CTAs per SM
+ * whose barrier stalls overlap once a launch has more than one item per SM, else 512), or forced 256 / 512.
+ * Env TLB_FAST_THREADS. */
+int tlb_ctx_set_threads(tlb_ctx* ctx, int threads);
 int tlb_ctx_info(const tlb_ctx* ctx, int* sm_count, int* train_ctas_per_sm, int* eval_ctas_per_sm,
                  int64_t* smem_bytes_per_cta);
 int tlb_synchronize(tlb_ctx* ctx);

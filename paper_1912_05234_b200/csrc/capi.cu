@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -74,8 +75,13 @@ struct tlb_ctx {
   int mode = TLB_MODE_EXACT;
   int grid_override = 0;
   unsigned long long* trace = nullptr;  // device buffer for per-stage clock stamps (profiling)
-  int occ_train[2] = {0, 0};
-  int occ_eval[2] = {0, 0};
+  // CTAs per SM of the flat train / forward kernels, [mode: 0 fast, 1 exact][CTA size: 0 = 256, 1 = 512]
+  int occ_train[2][2] = {{0, 0}, {0, 0}};
+  int occ_eval[2][2] = {{0, 0}, {0, 0}};
+  // CTA size of the flat kernels: 0 = automatic (256 = two independent CTAs per SM once the work exceeds
+  // one item per SM -- their barrier stalls overlap, +26-30% measured; 512 for small launches, where the
+  // per-item latency decides), else forced (tlb_ctx_set_threads / TLB_FAST_THREADS).
+  int threads_override = 0;
   int max_clusters = 0;    // co-resident 8-CTA clusters of train_cluster_kernel (0 = unavailable)
   bool use_cluster = true;
   DevBuf work, losses, loss_part, barrier;  // persistent-train workspaces
@@ -214,16 +220,21 @@ int fetch(tlb_ctx* c, T* host, const T* dev, size_t count) {
   return TLB_OK;
 }
 
-int train_grid(tlb_ctx* c, int64_t m_max) {
-  const int occ = c->occ_train[exact(c) ? 1 : 0];
+int pick_threads(const tlb_ctx* c, int64_t items) {
+  if (c->threads_override) return c->threads_override;
+  return items > c->sm_count ? 256 : 512;
+}
+
+int train_grid(tlb_ctx* c, int64_t m_max, int threads) {
+  const int occ = c->occ_train[exact(c) ? 1 : 0][threads == 256 ? 0 : 1];
   const int coop = std::max(1, occ * c->sm_count);
   if (c->grid_override > 0) return std::min(c->grid_override, coop);
   const int64_t want = std::max<int64_t>(c->sm_count, std::min<int64_t>(m_max, coop));
   return (int)std::min<int64_t>(want, coop);
 }
 
-int plain_grid(tlb_ctx* c, int64_t n) {
-  const int occ = c->occ_eval[exact(c) ? 1 : 0];
+int plain_grid(tlb_ctx* c, int64_t n, int threads = 512) {
+  const int occ = c->occ_eval[exact(c) ? 1 : 0][threads == 256 ? 0 : 1];
   const int64_t cap = (int64_t)std::max(1, occ) * c->sm_count;
   return (int)std::max<int64_t>(1, std::min<int64_t>(n, cap));
 }
@@ -283,7 +294,8 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   const int clusters = (int)((std::max<int64_t>(m_local, 1) + csz - 1) / csz);
   const bool clustered = !exact(c) && !grad_out && c->use_cluster && c->grid_override == 0 &&
                          c->max_clusters > 0 && clusters <= c->max_clusters;
-  const int grid = clustered ? clusters * csz : train_grid(c, std::max<int64_t>(m_local, 1));
+  const int threads = pick_threads(c, m_local);
+  const int grid = clustered ? clusters * csz : train_grid(c, std::max<int64_t>(m_local, 1), threads);
   const int64_t rows = exact(c) ? std::max<int64_t>(m_local, 1) : grid;
   TLB_CUDA(c->work.ensure(clustered ? tlb::cluster_work_bytes() : (size_t)rows * TLB_PSTRIDE * sizeof(float)));
   TLB_CUDA(c->losses.ensure((size_t)std::max<int64_t>(m_local, 1) * sizeof(float)));
@@ -320,7 +332,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.ready_step_end = a.step_begin + spe;  // only the call's first epoch can outrun the copies
   if (a.step_end <= a.step_begin) return TLB_OK;
   if (clustered) TLB_CUDA(tlb::launch_train_cluster(a, clusters, c->stream));
-  else TLB_CUDA(tlb::launch_train(exact(c), a, grid, c->stream));
+  else TLB_CUDA(tlb::launch_train(exact(c), a, grid, threads, c->stream));
   return TLB_OK;
 }
 
@@ -351,10 +363,12 @@ int tlb_ctx_create(int device, tlb_ctx** out) {
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
   cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = tlb::train_occupancy(false, &c->occ_train[0]);
-  if (e == cudaSuccess) e = tlb::train_occupancy(true, &c->occ_train[1]);
-  if (e == cudaSuccess) e = tlb::eval_occupancy(false, &c->occ_eval[0]);
-  if (e == cudaSuccess) e = tlb::eval_occupancy(true, &c->occ_eval[1]);
+  if (const char* t = getenv("TLB_FAST_THREADS")) c->threads_override = atoi(t) == 256 ? 256 : atoi(t) == 512 ? 512 : 0;
+  for (int x = 0; x < 2; ++x)
+    for (int t = 0; t < 2; ++t) {
+      if (e == cudaSuccess) e = tlb::train_occupancy(x == 1, t ? 512 : 256, &c->occ_train[x][t]);
+      if (e == cudaSuccess) e = tlb::eval_occupancy(x == 1, t ? 512 : 256, &c->occ_eval[x][t]);
+    }
   if (e != cudaSuccess) {
     delete c;
     return fail(TLB_ERR_CUDA, std::string("tlb_ctx_create: ") + cudaGetErrorString(e));
@@ -419,6 +433,14 @@ int tlb_ctx_set_grid(tlb_ctx* c, int ctas) {
   return TLB_OK;
 }
 
+int tlb_ctx_set_threads(tlb_ctx* c, int threads) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  if (threads != 0 && threads != 256 && threads != 512)
+    return fail(TLB_ERR_ARG, "tlb_ctx_set_threads: 0 (automatic), 256 or 512");
+  c->threads_override = threads;
+  return TLB_OK;
+}
+
 int tlb_ctx_set_cluster(tlb_ctx* c, int enable) {
   if (!c) return fail(TLB_ERR_ARG, "null context");
   c->use_cluster = enable != 0;
@@ -435,8 +457,8 @@ int tlb_ctx_info(const tlb_ctx* c, int* sm, int* occ_train, int* occ_eval, int64
   if (!c) return fail(TLB_ERR_ARG, "null context");
   const int x = c->mode == TLB_MODE_EXACT ? 1 : 0;
   if (sm) *sm = c->sm_count;
-  if (occ_train) *occ_train = c->occ_train[x];
-  if (occ_eval) *occ_eval = c->occ_eval[x];
+  if (occ_train) *occ_train = c->occ_train[x][1];
+  if (occ_eval) *occ_eval = c->occ_eval[x][1];
   if (smem) *smem = (int64_t)tlb::smem_bytes();
   return TLB_OK;
 }
@@ -666,7 +688,8 @@ int tlb_evaluate_device(tlb_ctx* c, const float* d_images, const int32_t* d_labe
   if (n <= 0) return TLB_OK;
   TLB_TRY(set_device(c));
   tlb::EvalArgs a{d_images, d_labels, n, d_params, d_pred, nullptr, d_correct};
-  TLB_CUDA(tlb::launch_eval(exact(c), a, plain_grid(c, n), c->stream));
+  const int threads = pick_threads(c, n);
+  TLB_CUDA(tlb::launch_eval(exact(c), a, plain_grid(c, n, threads), threads, c->stream));
   return TLB_OK;
 }
 

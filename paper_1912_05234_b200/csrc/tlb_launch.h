@@ -63,15 +63,15 @@ struct EvalArgs {
 
 size_t smem_bytes();
 int threads_per_cta();
-cudaError_t train_occupancy(bool exact, int* occ);
-cudaError_t eval_occupancy(bool exact, int* occ);
-cudaError_t launch_train(bool exact, const TrainArgs& a, int grid, cudaStream_t st);
+cudaError_t train_occupancy(bool exact, int threads, int* occ);
+cudaError_t eval_occupancy(bool exact, int threads, int* occ);
+cudaError_t launch_train(bool exact, const TrainArgs& a, int grid, int threads, cudaStream_t st);
 cudaError_t cluster_train_capacity(int* max_clusters);
 int cluster_size();
 size_t cluster_work_bytes();
 cudaError_t launch_train_cluster(const TrainArgs& a, int clusters, cudaStream_t st);
 cudaError_t launch_cells(bool exact, const CellArgs& a, int grid, cudaStream_t st);
-cudaError_t launch_eval(bool exact, const EvalArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_eval(bool exact, const EvalArgs& a, int grid, int threads, cudaStream_t st);
 cudaError_t launch_sgd(const float* params, const float* grad, float rate, int64_t m, float* out, int n,
                        cudaStream_t st);
 

@@ -166,7 +166,7 @@ __device__ __forceinline__ void reduce_loss(const Smem& s, const TrainArgs& a, i
   double l = 0.0;
   if (!a.grad_out && ks != 0) l = a.epoch_loss[ep];
   if constexpr (EXACT) {
-    float* stage = s.red;
+    float* stage = s.c1;  // activations are dead after the backward pass (s.red is fast-mode only)
     for (int64_t e0 = 0; e0 < m; e0 += 1024) {
       const int n = (int)min((int64_t)1024, m - e0);
       __syncthreads();
@@ -176,7 +176,7 @@ __device__ __forceinline__ void reduce_loss(const Smem& s, const TrainArgs& a, i
         for (int i = 0; i < n; ++i) l = __dadd_rn(l, (double)stage[i]);
     }
   } else {
-    double* stage = reinterpret_cast<double*>(s.red);  // fp64 CTA partials, staged in one round trip
+    double* stage = reinterpret_cast<double*>(s.c1);  // fp64 CTA partials, staged in one round trip
     for (int64_t r0 = 0; r0 < nrows; r0 += 512) {
       const int n = (int)min((int64_t)512, nrows - r0);
       __syncthreads();
@@ -536,23 +536,27 @@ __global__ void sgd_kernel(const float* params, const float* grad, float rate, f
 size_t smem_bytes() { return kSmemBytes; }
 int threads_per_cta() { return kThreads; }
 
+// Dynamic shared memory actually used by a kernel: the prefix (fast), prefix + EXACT tail, or all.
 template <class K>
-static cudaError_t prep(K kernel, int* occ) {
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+static cudaError_t prep(K kernel, int* occ, int threads, size_t smem) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kernel, kThreads, kSmemBytes);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kernel, threads, smem);
 }
 
-cudaError_t train_occupancy(bool exact, int* occ) {
-  return exact ? prep(train_kernel<true>, occ) : prep(train_kernel<false>, occ);
+cudaError_t train_occupancy(bool exact, int threads, int* occ) {
+  return exact ? prep(train_kernel<true>, occ, threads, kSmemExactBytes)
+               : prep(train_kernel<false>, occ, threads, kSmemFastBytes);
 }
 
-cudaError_t launch_train(bool exact, const TrainArgs& a, int grid, cudaStream_t st) {
+// 256-thread CTAs (two per SM: the stages loop over their lanes) or 512 (one per SM).
+cudaError_t launch_train(bool exact, const TrainArgs& a, int grid, int threads, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(a.barrier, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return e;
   void* args[] = {const_cast<TrainArgs*>(&a)};
   const void* fn = exact ? (const void*)train_kernel<true> : (const void*)train_kernel<false>;
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, kSmemBytes, st);
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, exact ? kSmemExactBytes : kSmemFastBytes,
+                                     st);
 }
 
 cudaError_t cluster_train_capacity(int* max_clusters) {
@@ -606,24 +610,26 @@ cudaError_t launch_train_cluster(const TrainArgs& a, int clusters, cudaStream_t 
 
 cudaError_t launch_cells(bool exact, const CellArgs& a, int grid, cudaStream_t st) {
   int occ = 0;
-  cudaError_t e = exact ? prep(cells_kernel<true>, &occ) : prep(cells_kernel<false>, &occ);
+  cudaError_t e = exact ? prep(cells_kernel<true>, &occ, kThreads, kSmemExactBytes)
+                        : prep(cells_kernel<false>, &occ, kThreads, kSmemFastBytes);
   if (e != cudaSuccess) return e;
-  if (exact) cells_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(a);
-  else cells_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(a);
+  if (exact) cells_kernel<true><<<grid, kThreads, kSmemExactBytes, st>>>(a);
+  else cells_kernel<false><<<grid, kThreads, kSmemFastBytes, st>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_eval(bool exact, const EvalArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_eval(bool exact, const EvalArgs& a, int grid, int threads, cudaStream_t st) {
   int occ = 0;
-  cudaError_t e = exact ? prep(eval_kernel<true>, &occ) : prep(eval_kernel<false>, &occ);
+  cudaError_t e = eval_occupancy(exact, threads, &occ);
   if (e != cudaSuccess) return e;
-  if (exact) eval_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(a);
-  else eval_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(a);
+  if (exact) eval_kernel<true><<<grid, threads, kSmemExactBytes, st>>>(a);
+  else eval_kernel<false><<<grid, threads, kSmemFastBytes, st>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t eval_occupancy(bool exact, int* occ) {
-  return exact ? prep(eval_kernel<true>, occ) : prep(eval_kernel<false>, occ);
+cudaError_t eval_occupancy(bool exact, int threads, int* occ) {
+  return exact ? prep(eval_kernel<true>, occ, threads, kSmemExactBytes)
+               : prep(eval_kernel<false>, occ, threads, kSmemFastBytes);
 }
 
 cudaError_t launch_sgd(const float* params, const float* grad, float rate, int64_t m, float* out, int n,

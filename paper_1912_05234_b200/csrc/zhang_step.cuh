@@ -74,10 +74,20 @@ constexpr int kC1Plane = 580;
 constexpr int kC1Floats = 6 * kC1Plane;
 __device__ __forceinline__ int c1_at(int i, int y, int x) { return i * kC1Plane + y * 24 + x; }
 __device__ __forceinline__ int sh_at(int v, int y) { return v * kShPlane + y * 24; }
-constexpr int kSmemFloats =
-    kPStride + kKp + 2 * kImg + kSh + kC1Floats + 864 + 768 + 192 + 16 + 16 + kDzp + 1920 + kRed + kPStride +
-    kTerm;
-constexpr size_t kSmemBytes = sizeof(float) * kSmemFloats + 32 * sizeof(uint64_t) + 2 * sizeof(uint64_t);
+// Shared-memory layout: a prefix every kernel uses, then a mode tail -- fast kernels: the C1 row partials
+// and the per-CTA gradient accumulator; EXACT kernels: the shifted image copies and the FC products (the
+// two tails alias: no kernel uses both) -- then the clustered kernel's DSMEM receive buffer (`term`).
+// Kernels allocate only what they touch, so both the fast and the EXACT flat kernels fit two CTAs per SM.
+constexpr int kPrefixFloats = kPStride + kKp + 2 * kImg + kC1Floats + 864 + 768 + 192 + 16 + 16 + kDzp;
+constexpr size_t kPrefixBytes = ((sizeof(float) * kPrefixFloats + 34 * sizeof(uint64_t)) + 15) / 16 * 16;
+constexpr int kFastTailFloats = kRed + kPStride;
+constexpr int kExactTailFloats = kSh + 1920;
+constexpr int kTailFloats = kFastTailFloats > kExactTailFloats ? kFastTailFloats : kExactTailFloats;
+constexpr size_t kSmemFastBytes = kPrefixBytes + sizeof(float) * kFastTailFloats;
+constexpr size_t kSmemExactBytes = kPrefixBytes + sizeof(float) * kExactTailFloats;
+constexpr size_t kSmemBytes = kPrefixBytes + sizeof(float) * (kTailFloats + kTerm);  // clustered kernel
+template <bool EXACT>
+constexpr size_t smem_bytes_for() { return EXACT ? kSmemExactBytes : kSmemFastBytes; }
 
 // The CTA's dynamic shared memory (one declaration for every kernel and stage).
 extern __shared__ __align__(128) float tlb_smem[];
@@ -88,7 +98,6 @@ __device__ __forceinline__ Smem carve_smem(float* base) {
   s.P = p; p += kPStride;
   s.Kp = p; p += kKp;
   s.img = p; p += 2 * kImg;
-  s.sh = p; p += kSh;
   s.c1 = p; p += kC1Floats;
   s.s1 = p; p += 864;
   s.c2 = p; p += 768;
@@ -96,12 +105,14 @@ __device__ __forceinline__ Smem carve_smem(float* base) {
   s.out = p; p += 16;
   s.dz = p; p += 16;
   s.dzp = p; p += kDzp;
-  s.fcp = p; p += 1920;
-  s.red = p; p += kRed;
-  s.G = p; p += kPStride;
-  s.term = p; p += kTerm;
   s.tab = reinterpret_cast<uint64_t*>(p);
   s.bar = s.tab + 32;
+  float* const tail = base + kPrefixBytes / sizeof(float);
+  s.red = tail;                   // fast tail
+  s.G = tail + kRed;
+  s.sh = tail;                    // EXACT tail (aliases the fast tail)
+  s.fcp = tail + kSh;
+  s.term = tail + kTailFloats;    // clustered-kernel tail
   s.tr = nullptr;
   return s;
 }
@@ -182,8 +193,9 @@ __device__ __forceinline__ void build_shifted(const Smem& s, const float* img, i
 // Warps 13.5..15 meanwhile build the v-shifted image copies used by the C1 weight gradient.
 template <bool EXACT>
 __device__ __forceinline__ void stage_conv1(const Smem& s, const float* img) {
-  const int it = threadIdx.x;
-  if (it < 448) {  // 14 full warps; items >= 432 are padding lanes (valid = false)
+  // 448 item lanes (14 full warps; items >= 432 are padding lanes, valid = false); with fewer threads
+  // than items the lanes loop (whole warps per round, so the pool shuffle stays warp-uniform).
+  for (int it = threadIdx.x; it < 448; it += blockDim.x) {
     const bool valid = it < 432;
     const int pair = (valid ? it : 0) >> 1, r = it & 1;
     const int i = pair / 36, rem = pair - i * 36, py = rem / 3, xs = rem - py * 3;
@@ -224,8 +236,13 @@ __device__ __forceinline__ void stage_conv1(const Smem& s, const float* img) {
       }
       *reinterpret_cast<float2*>(s.s1 + (i * 12 + py) * 12 + 4 * xs + 2 * r) = make_float2(pv[0], pv[1]);
     }
-  } else if constexpr (EXACT) {
-    build_shifted(s, img, it - 448, blockDim.x - 448);
+  }
+  if constexpr (EXACT) {  // warps 14-15 of a 512-thread CTA, else every thread after its conv1 items
+    if (blockDim.x > 448) {
+      if (threadIdx.x >= 448) build_shifted(s, img, threadIdx.x - 448, blockDim.x - 448);
+    } else {
+      build_shifted(s, img, threadIdx.x, blockDim.x);
+    }
   }
 }
 
@@ -867,12 +884,14 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
     }
   } else if constexpr (V == 1) {
     constexpr int kBackin = 128;  // 108 items, padded to 4 whole warps
-    const int it = threadIdx.x;
-    if (it < kBackin) {
-      if (it < 108) backin_item<EXACT>(s, it);
-    } else if (it < kBackin + kGk2) {
-      if constexpr (EXACT) gk2_exact<ACCUM>(s, row, it - kBackin);
-      else gk2_fast<ACCUM>(s, row, it - kBackin);
+    for (int it = threadIdx.x; it < kBackin + kGk2; it += blockDim.x) {
+      if (it < kBackin) {
+        if (it < 108) backin_item<EXACT>(s, it);
+      } else if constexpr (EXACT) {
+        gk2_exact<ACCUM>(s, row, it - kBackin);
+      } else {
+        gk2_fast<ACCUM>(s, row, it - kBackin);
+      }
     }
   } else if constexpr (V == 3) {
     // V = 3: weight-stationary backin over all lanes, then the ordered kernel combine (224 lanes)

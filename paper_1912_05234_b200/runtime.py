@@ -134,6 +134,10 @@ class Context:
     def set_grid(self, ctas: int) -> None:
         _check(self._L.tlb_ctx_set_grid(self._h, ctas))
 
+    def set_threads(self, threads: int) -> None:
+        """CTA size of the flat train / forward kernels: 0 automatic (default), 256 (two CTAs per SM) or 512."""
+        _check(self._L.tlb_ctx_set_threads(self._h, threads))
+
     def set_cluster(self, enable: bool) -> None:
         """Fast mode: clustered train kernel (DSMEM pre-reduction) when the group fits (default on)."""
         _check(self._L.tlb_ctx_set_cluster(self._h, 1 if enable else 0))

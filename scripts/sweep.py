@@ -55,6 +55,7 @@ def main():
     ap.add_argument("--modes", default="fast,exact")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.json"))
     ap.add_argument("--max-batch", type=int, default=262144)
+    ap.add_argument("--threads", type=int, default=0, help="fast mode CTA size (256 = two CTAs per SM; 0 = library default)")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     stream = torch.cuda.Stream()
@@ -71,6 +72,9 @@ def main():
     for mode in args.modes.split(","):
         ctx = Context(0, mode=mode)
         ctx.set_stream(stream.cuda_stream)
+        if args.threads:
+            ctx.set_threads(args.threads)
+        thr = args.threads or "auto"
         peak = peak_tflops(ctx.info()["sm_count"])
         # ---- configs[3]: batch sweep -------------------------------------------------------------
         B = 1024
@@ -89,7 +93,7 @@ def main():
                 run()
             ms = timed(stream, run, 5, flush)
             ips = n / (ms / 1e3)
-            emit({"config": "batch_sweep", "mode": mode, "batch": B, "images_per_launch": n, "ms": ms,
+            emit({"config": "batch_sweep", "mode": mode, "threads": thr, "batch": B, "images_per_launch": n, "ms": ms,
                   "images_per_s": ips, "tflops": ips * TRAIN_FLOP / 1e12,
                   "fp32_roofline_frac": ips * TRAIN_FLOP / 1e12 / peak, "loss": float(loss[0])})
             del d_x, d_y
@@ -114,7 +118,7 @@ def main():
             ips = N / (ms / 1e3)
             p = pred[: min(N, 10000)].cpu().numpy()
             exact_pred = bool(np.array_equal(p, golden_pred[: len(p)].astype(np.int32)))
-            emit({"config": "inference", "mode": mode, "images": N, "ms": ms, "images_per_s": ips,
+            emit({"config": "inference", "mode": mode, "threads": thr, "images": N, "ms": ms, "images_per_s": ips,
                   "tflops": ips * FWD_FLOP / 1e12, "fp32_roofline_frac": ips * FWD_FLOP / 1e12 / peak,
                   "accuracy": int(cnt.item()) / N, "pred_equal_reference": exact_pred})
             del d_x, d_y

@@ -203,6 +203,23 @@ def test_train_exact_bitwise_vs_oracle(ctx, orc, small, n, batch, epochs):
     assert list(got_l) == list(want_l)
 
 
+@pytest.mark.parametrize("threads", [256, 512])
+def test_train_exact_bitwise_cta_sizes(orc, small, threads):
+    """EXACT mode is bitwise at both CTA sizes of the flat kernel (256 = two CTAs per SM, stages looping
+    over their lanes), including a group larger than the SM count (the automatic 256-thread choice)."""
+    from paper_1912_05234_b200 import Context
+    x, y = small
+    p0 = orc.init_params(42)
+    want_p, want_l = orc.train(x[:256], y[:256], p0, epochs=1, batch=200)
+    with Context(0, mode="exact") as c:
+        c.set_threads(threads)
+        got_p, got_l = c.train(p0, x[:256], y[:256], epochs=1, batch=200)
+        yhat = c.forward(x[:8], got_p)
+    assert np.array_equal(bits(got_p), bits(want_p)) and list(got_l) == list(want_l)
+    for i in range(8):
+        assert np.array_equal(bits(yhat[i]), bits(orc.forward(x[i], got_p)[5280:5290]))
+
+
 def test_train_on_epoch_callback(ctx, orc, small):
     x, y = small
     seen = []
@@ -255,7 +272,7 @@ def test_full_protocol_fast_within_tolerance(golden, zhang_sets):
 @pytest.mark.parametrize("n,batch,epochs", [(3, 100, 1), (64, 8, 2), (250, 100, 2), (256, 64, 1), (97, 9, 1),
                                             (1040, 1040, 1)])
 @pytest.mark.parametrize("cluster", [True, False])
-def test_train_fast_vs_oracle(orc, small, zhang_sets, n, batch, epochs, cluster):
+def test_train_fast_vs_oracle(orc, small, zhang_sets, n, batch, epochs, cluster):  # flat: auto CTA size
     """FAST mode, clustered (DSMEM pre-reduction, one grid barrier) and flat kernels: ragged last groups,
     batch > n, group sizes that fill 1..13 clusters partially, and a group larger than the clustered
     kernel's capacity (falls back to the flat kernel).  Within 1e-4 relative of the reference order;
