@@ -292,8 +292,8 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   // Clustered fast kernel: one example per CTA per step, every CTA co-resident.
   const int csz = tlb::cluster_size();
   const int clusters = (int)((std::max<int64_t>(m_local, 1) + csz - 1) / csz);
-  const bool clustered = !exact(c) && !grad_out && c->use_cluster && c->grid_override == 0 &&
-                         c->max_clusters > 0 && clusters <= c->max_clusters;
+  const bool clustered = !exact(c) && c->use_cluster && c->grid_override == 0 && c->max_clusters > 0 &&
+                         clusters <= c->max_clusters;
   const int threads = pick_threads(c, m_local);
   const int grid = clustered ? clusters * csz : train_grid(c, std::max<int64_t>(m_local, 1), threads);
   const int64_t rows = exact(c) ? std::max<int64_t>(m_local, 1) : grid;

@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
 
   for (int64_t st = a.step_begin; st < a.step_end; ++st) {
     const int64_t ls = st - a.step_begin;  // local step: accumulator buffer ls % 3
-    const int64_t ks = st % a.steps_per_epoch, start = ks * a.batch;
+    const int64_t ks = st % a.steps_per_epoch, start = ks * a.batch + local_offset(a);
     const int64_t m = local_size(a, st);
     int64_t lo, hi;
     static_chunk(m, G, blockIdx.x, lo, hi);
@@ -400,15 +400,23 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       const long long t = (long long)__ldcg(acc + b * kPStride + j);
       if (j < kNParam) {
         const float gsum = (float)((double)t * kUnfix);
-        s.P[j] = fsub(s.P[j], fmul(a.rate, __fdiv_rn(gsum, (float)m)));
-        if (cid == 0) __stcg(a.params + j, s.P[j]);
+        if (a.grad_out) {  // data-parallel shard: the shard's gradient sum goes to the allreduce
+          if (cid == 0) a.grad_out[j] = gsum;
+        } else {
+          s.P[j] = fsub(s.P[j], fmul(a.rate, __fdiv_rn(gsum, (float)m)));
+          if (cid == 0) __stcg(a.params + j, s.P[j]);
+        }
       }
     }
     if (blockIdx.x == 0 && threadIdx.x == kSlice) {
-      const int64_t ep = st / a.steps_per_epoch;
       const double l = (double)(long long)__ldcg(lacc + b) * kUnfix;
-      const double run = (ks != 0 ? a.epoch_loss[ep] : 0.0) + l;
-      a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(run, (double)a.n) : run;
+      if (a.grad_out) {
+        a.loss_out[0] = l;
+      } else {
+        const int64_t ep = st / a.steps_per_epoch;
+        const double run = (ks != 0 ? a.epoch_loss[ep] : 0.0) + l;
+        a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(run, (double)a.n) : run;
+      }
     }
     __syncthreads();
     mark(s, 12);

@@ -306,7 +306,11 @@ def test_evaluate_ties_and_label_zero(ctx):
 
 # ---- data-parallel shard path ---------------------------------------------------------------------
 def test_dp_shards_sum_to_the_full_group(orc, small):
-    """Shard gradient sums (the NCCL allreduce operands) recombine to the full-group step."""
+    """Shard gradient sums (the NCCL allreduce operands) recombine to the full-group sum, which is the
+    reference's example-order sum (bitwise in EXACT mode); groups 0 and 1 (shard offsets into the group);
+    then the post-allreduce sgd_step equals one reference step."""
+    import ctypes as C
+
     import torch
     from paper_1912_05234_b200 import Context
     x, y = small
@@ -316,43 +320,47 @@ def test_dp_shards_sum_to_the_full_group(orc, small):
     d_x = torch.from_numpy(x[:n]).to(dev)
     d_y = torch.from_numpy(y[:n]).to(dev)
     for mode in ("exact", "fast"):
-        with Context(0, mode=mode) as c:
-            c.set_stream(torch.cuda.current_stream().cuda_stream)
-            d_p = torch.zeros(3904, device=dev)
-            d_p[:3898] = torch.from_numpy(p0).to(dev)
-            gs = []
-            for lo, hi in [(0, 50), (50, 100)]:
-                g = torch.zeros(3904, device=dev)
-                ls = torch.zeros(1, dtype=torch.float64, device=dev)
-                c.train_shard_device(d_x.data_ptr(), d_y.data_ptr(), n, batch, 0, lo, hi, d_p.data_ptr(),
-                                     g.data_ptr(), ls.data_ptr())
-                gs.append((g, ls))
-            full = torch.zeros(3904, device=dev)
-            fl = torch.zeros(1, dtype=torch.float64, device=dev)
-            c.train_shard_device(d_x.data_ptr(), d_y.data_ptr(), n, batch, 0, 0, 100, d_p.data_ptr(),
-                                 full.data_ptr(), fl.data_ptr())
-            torch.cuda.synchronize()
-            s = (gs[0][0] + gs[1][0]).cpu().numpy()[:3898]
-            f = full.cpu().numpy()[:3898]
-            np.testing.assert_allclose(s, f, rtol=1e-4, atol=1e-6)
-            assert abs(float(gs[0][1] + gs[1][1]) - float(fl)) <= 1e-9 * abs(float(fl))
-            if mode == "exact":  # full-group shard == the reference's example-order sum
-                rows = np.stack([orc.cell(x[i], p0, int(y[i])) for i in range(100)])
+        for group, cuts in ((0, [(0, 50), (50, 100)]), (1, [(0, 30), (30, 100)])):
+            with Context(0, mode=mode) as c:
+                c.set_stream(torch.cuda.current_stream().cuda_stream)
+                d_p = torch.zeros(3904, device=dev)
+                d_p[:3898] = torch.from_numpy(p0).to(dev)
+                gs = []
+                for lo, hi in cuts:
+                    g = torch.zeros(3904, device=dev)
+                    ls = torch.zeros(1, dtype=torch.float64, device=dev)
+                    c.train_shard_device(d_x.data_ptr(), d_y.data_ptr(), n, batch, group, lo, hi, d_p.data_ptr(),
+                                         g.data_ptr(), ls.data_ptr())
+                    gs.append((g, ls))
+                full = torch.zeros(3904, device=dev)
+                fl = torch.zeros(1, dtype=torch.float64, device=dev)
+                c.train_shard_device(d_x.data_ptr(), d_y.data_ptr(), n, batch, group, 0, 100, d_p.data_ptr(),
+                                     full.data_ptr(), fl.data_ptr())
+                torch.cuda.synchronize()
+                s = (gs[0][0] + gs[1][0]).cpu().numpy()[:3898]
+                f = full.cpu().numpy()[:3898]
+                np.testing.assert_allclose(s, f, rtol=1e-4, atol=1e-6)
+                assert abs(float(gs[0][1] + gs[1][1]) - float(fl)) <= 1e-9 * abs(float(fl))
+                rows = np.stack([orc.cell(x[group * batch + e], p0, int(y[group * batch + e])) for e in range(batch)])
                 acc = np.zeros(3898, np.float32)
                 for r in rows:
                     acc = (acc + r[:3898]).astype(np.float32)
-                assert np.array_equal(bits(f), bits(acc))
-            # apply the update and compare with one reference step
-            c.apply_sgd_device(d_p.data_ptr(), full.data_ptr(), 0.05, 100)
-            torch.cuda.synchronize()
-            want_p = p0.copy()
-            loss = np.zeros(1)
-            import ctypes as C
-            orc.L.orc_train_group(x.ctypes.data_as(C.POINTER(C.c_float)), y.ctypes.data_as(C.POINTER(C.c_int32)),
-                                  0, 100, want_p.ctypes.data_as(C.POINTER(C.c_float)), 0.05,
-                                  loss.ctypes.data_as(C.POINTER(C.c_double)), 4)
-            got_p = d_p.cpu().numpy()[:3898]
-            if mode == "exact":
-                assert np.array_equal(bits(got_p), bits(want_p))
-            else:
-                assert rel_err(got_p, want_p, floor=1e-3) <= REL_TOL
+                want_l = float(np.sum(rows[:, 3898].astype(np.float64)))
+                if mode == "exact":
+                    assert np.array_equal(bits(f), bits(acc))
+                else:
+                    np.testing.assert_allclose(f, acc, rtol=1e-4, atol=1e-6)
+                assert abs(float(fl) - want_l) <= 1e-6 * abs(want_l)
+                # apply the update and compare with one reference step of that group
+                c.apply_sgd_device(d_p.data_ptr(), full.data_ptr(), 0.05, 100)
+                torch.cuda.synchronize()
+                want_p = p0.copy()
+                loss = np.zeros(1)
+                orc.L.orc_train_group(x.ctypes.data_as(C.POINTER(C.c_float)), y.ctypes.data_as(C.POINTER(C.c_int32)),
+                                      group * batch, 100, want_p.ctypes.data_as(C.POINTER(C.c_float)), 0.05,
+                                      loss.ctypes.data_as(C.POINTER(C.c_double)), 4)
+                got_p = d_p.cpu().numpy()[:3898]
+                if mode == "exact":
+                    assert np.array_equal(bits(got_p), bits(want_p))
+                else:
+                    assert rel_err(got_p, want_p, floor=1e-3) <= REL_TOL
