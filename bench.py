@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--grid", type=int, default=0, help="CTAs of the persistent kernel (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-dp", action="store_true",
+                    help="run the N>1 data-parallel step (shard kernel + NCCL allreduce + sgd) even at N=1")
+    ap.add_argument("--no-graph", action="store_true", help="data-parallel step: plain launches, no CUDA graph")
     return ap.parse_args()
 
 
@@ -197,7 +200,10 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    dp = world > 1 or args.force_dp
+    if dp:
+        if "RANK" not in os.environ:  # --force-dp without torchrun: a one-rank NCCL group
+            os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1", MASTER_PORT="29517")
         dist.init_process_group("nccl", device_id=dev)
 
     B, n_per = args.batch, args.n
@@ -221,18 +227,18 @@ def run_ours(args):
         d_p.zero_()
         d_p[:3898] = torch.from_numpy(p0).to(dev)
 
-    if world == 1:
+    if not dp:
         def epoch(e):
             ctx.train_device(d_x.data_ptr(), d_y.data_ptr(), n_total, d_p.data_ptr(), 0.05, e, 1, B,
                              d_loss.data_ptr())
         launches_per_step = 1
     else:
         from paper_1912_05234_b200.parallel import DeviceShardStep
-        dp = DeviceShardStep(ctx, d_x, d_y, n_total, B * world, world, rank)
+        step = DeviceShardStep(ctx, d_x, d_y, n_total, B * world, world, rank, graph=not args.no_graph)
 
         def epoch(e):
-            dp.epoch(d_p, 0.05, d_loss, e)
-        launches_per_step = 2 * dp.groups_per_epoch
+            step.epoch(d_p, 0.05, d_loss, e)
+        launches_per_step = 2 * step.groups_per_epoch
 
     # warm-up (not timed), then the timed protocol from init_params(42)
     reset()
@@ -242,7 +248,7 @@ def run_ours(args):
     reset()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if world > 1:
+    if dp:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -252,11 +258,11 @@ def run_ours(args):
             epoch(s)
             ends[s].record(stream)
         torch.cuda.synchronize()
-    if world > 1:
+    if dp:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     total_ms = sum(step_ms)
-    if world > 1:
+    if dp:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t)
@@ -281,6 +287,8 @@ def run_ours(args):
                                f"{n_per} images/GPU at batch {B}/GPU, lr 0.05",
                    "batch_per_gpu": B, "global_batch": B * world, "n_images": n_total, "epochs_per_step": 1,
                    "mode": args.mode, "parallelism": f"dp{world}", "grid": args.grid or "auto",
+                   "dp_step": ("shard kernel + NCCL allreduce + sgd per group" +
+                               ("" if args.no_graph else ", epoch replayed as one CUDA graph")) if dp else None,
                    "l2": "flushed between timed steps (256 MiB write outside the event pair)"},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
@@ -330,7 +338,7 @@ def run_ours(args):
     if rank == 0:
         print(json.dumps(result), flush=True)
     ctx.close()
-    if world > 1:
+    if dp:
         dist.destroy_process_group()
 
 

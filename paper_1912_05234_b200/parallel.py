@@ -74,9 +74,15 @@ class DeviceBackend:
 
 
 class DeviceShardStep:
-    """bench.py's N>1 step: weak scaling, one epoch per call, NCCL allreduce per group."""
+    """bench.py's N>1 step: weak scaling, one epoch per call, NCCL allreduce per group.
 
-    def __init__(self, ctx, d_images, d_labels, n: int, global_batch: int, world: int, rank: int):
+    With ``graph=True`` the epoch (per group: shard kernel, loss add, NCCL allreduce, sgd kernel; then the
+    loss allreduce) is captured once into a CUDA graph on the context stream and replayed per epoch, so
+    the ~400 launches + collectives of an epoch cost one graph launch on the host.  The parameter and
+    epoch-loss buffers are fixed per instance (captured by address)."""
+
+    def __init__(self, ctx, d_images, d_labels, n: int, global_batch: int, world: int, rank: int,
+                 graph: bool = False):
         self.ctx, self.x, self.y, self.n, self.B = ctx, d_images, d_labels, n, global_batch
         self.world, self.rank = world, rank
         dev = d_images.device
@@ -84,11 +90,32 @@ class DeviceShardStep:
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=dev)
         self.groups_per_epoch = len(groups(n, global_batch))
+        self.use_graph = graph
+        self.graph = None
+        self.graph_key = None
 
-    def epoch(self, d_params, rate: float, d_epoch_loss, e: int) -> None:
+    def _epoch_body(self, d_params, rate: float, out) -> None:
         backend = DeviceBackend(self.ctx, self.x, self.y, self.n, self.B, d_params)
         self.loss_acc.zero_()
         train_epoch(backend, self.n, self.B, rate, self.grad, self.loss, self.loss_acc, self.world, self.rank,
                     lambda t: dist.all_reduce(t, op=dist.ReduceOp.SUM))
         dist.all_reduce(self.loss_acc, op=dist.ReduceOp.SUM)
-        d_epoch_loss[e : e + 1].copy_(self.loss_acc / self.n)
+        out.copy_(self.loss_acc / self.n)
+
+    def epoch(self, d_params, rate: float, d_epoch_loss, e: int) -> None:
+        if not self.use_graph:
+            self._epoch_body(d_params, rate, d_epoch_loss[e : e + 1])
+            return
+        key = (d_params.data_ptr(), rate)
+        if self.graph is None or self.graph_key != key:
+            self.out = torch.zeros(1, dtype=torch.float64, device=self.grad.device)
+            self._epoch_body(d_params, rate, self.out)  # eager warm-up: workspaces and communicators exist
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=torch.cuda.current_stream()):
+                self._epoch_body(d_params, rate, self.out)
+            # the warm-up ran a real epoch: this instance's callers re-initialise the parameters after
+            # warm-up (bench.py resets them), so no correction is applied here
+            self.graph, self.graph_key = g, key
+        self.graph.replay()
+        d_epoch_loss[e : e + 1].copy_(self.out)
