@@ -85,6 +85,12 @@ int tlb_synchronize(tlb_ctx* ctx);
 int tlb_init_params(uint64_t seed, float* params_out /* TLB_NPARAM */);
 /* synth::make_digits / make_set (synth.cpp:117-161): n 28x28 glyph images + labels. */
 int tlb_synth_make_digits(int64_t n, uint64_t seed, uint8_t* pixels_out, int32_t* labels_out);
+/* synth::make_digits / synth::make_set (synth.cpp:117-161) generated on the device into device buffers,
+ * byte-identical to the host versions for every (n, seed): the mt19937_64 stream is rebuilt by a serial
+ * twist chain that snapshots the state per image segment, then all segments synthesise in parallel.
+ * Either output may be NULL.  Enqueued on the context stream. */
+int tlb_synth_make_digits_device(tlb_ctx* ctx, int64_t n, uint64_t seed, uint8_t* d_pixels, int32_t* d_labels);
+int tlb_synth_make_set_device(tlb_ctx* ctx, int64_t n, uint64_t seed, float* d_images, int32_t* d_labels);
 int tlb_synth_make_set(int64_t n, uint64_t seed, float* images_out, int32_t* labels_out);
 /* mnist::make_set invariants (mnist.cpp:126-154): pixels in [0,1], labels in 0..9 (ValueError). */
 int tlb_validate_set(const float* images, const int32_t* labels, int64_t n);

@@ -40,6 +40,8 @@ _SIGS = {
     "tlb_ctx_set_trace": (C.c_int, [vp, vp]),
     "tlb_ctx_set_cluster": (C.c_int, [vp, C.c_int]),
     "tlb_ctx_set_threads": (C.c_int, [vp, C.c_int]),
+    "tlb_synth_make_digits_device": (C.c_int, [vp, C.c_int64, C.c_uint64, vp, vp]),
+    "tlb_synth_make_set_device": (C.c_int, [vp, C.c_int64, C.c_uint64, vp, vp]),
     "tlb_wide_init_params": (C.c_int, [C.c_uint64, f32p]),
     "tlb_wide_make_set": (C.c_int, [C.c_int64, C.c_uint64, f32p, i32p]),
     "tlb_wide_train": (C.c_int, [vp, f32p, i32p, C.c_int64, f32p, C.c_float, C.c_int32, C.c_int64, f64p, C.c_int]),

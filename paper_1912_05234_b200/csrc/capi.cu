@@ -93,6 +93,7 @@ struct tlb_ctx {
   cudaEvent_t copy_gate = nullptr;
   DevBuf ready;
   unsigned int ready_token = 0;
+  DevBuf synth_snaps;  // device synthetic corpus: mt19937_64 state snapshots per segment
   // Widened-network workspaces (capacity `wide_cap` images) and the last group's arguments.
   DevBuf wide[12];
   int64_t wide_cap = 0;
@@ -400,6 +401,7 @@ int tlb_ctx_destroy(tlb_ctx* c) {
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   c->ready.release();
   for (auto& w : c->wide) w.release();
+  c->synth_snaps.release();
   if (c->copy_gate) cudaEventDestroy(c->copy_gate);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -846,6 +848,26 @@ int tlb_nn_backin(tlb_ctx* c, const float* d, const int64_t* ds, int dr, const f
   TLB_TRY(stage_out(c, 2, (size_t)nout, &d_o));
   TLB_CUDA(tlb::nn_backin(d_d, ds, d_k, ks, ir, d_o, c->stream));
   return fetch(c, out, d_o, (size_t)nout);
+}
+
+// ---- device synthetic corpus (synth.cpp:117-161) ---------------------------------------------------------
+static int synth_device(tlb_ctx* c, int64_t n, uint64_t seed, uint8_t* px, float* im, int32_t* lab) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  if (n < 0) return fail(TLB_ERR_ERROR, "make_digits: negative count");
+  if (n > 0 && !px && !im && !lab) return TLB_OK;
+  TLB_TRY(set_device(c));
+  if (n == 0) return TLB_OK;
+  TLB_CUDA(c->synth_snaps.ensure(tlb::synth::snapshot_bytes(n)));
+  TLB_CUDA(tlb::synth::make_digits(n, seed, static_cast<uint64_t*>(c->synth_snaps.p), px, im, lab, c->stream));
+  return TLB_OK;
+}
+
+int tlb_synth_make_digits_device(tlb_ctx* c, int64_t n, uint64_t seed, uint8_t* d_pixels, int32_t* d_labels) {
+  return synth_device(c, n, seed, d_pixels, nullptr, d_labels);
+}
+
+int tlb_synth_make_set_device(tlb_ctx* c, int64_t n, uint64_t seed, float* d_images, int32_t* d_labels) {
+  return synth_device(c, n, seed, nullptr, d_images, d_labels);
 }
 
 // ---- widened CNN (BASELINE configs[4]) -------------------------------------------------------------------

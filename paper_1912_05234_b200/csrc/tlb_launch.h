@@ -89,4 +89,11 @@ cudaError_t nn_sum_all(const float* x, int64_t n, float* out, cudaStream_t st);
 cudaError_t nn_expf(const float* x, int64_t n, float* out, cudaStream_t st);
 cudaError_t nn_expf_range(uint32_t start_bits, int64_t n, float* out, cudaStream_t st);
 
+// Device synthetic corpus (synth_device.cu)
+namespace synth {
+size_t snapshot_bytes(int64_t n);
+cudaError_t make_digits(int64_t n, uint64_t seed, uint64_t* snaps, uint8_t* pixels, float* images, int32_t* labels,
+                        cudaStream_t st);
+}  // namespace synth
+
 }  // namespace tlb

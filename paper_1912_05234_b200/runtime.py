@@ -210,6 +210,17 @@ class Context:
         _check(self._L.tlb_train_device(self._h, d_images, d_labels, n, d_params, rate, epoch_begin, epochs,
                                         batch, d_epoch_loss))
 
+    # ---- device synthetic corpus ------------------------------------------------------------------------
+    def synth_make_set_device(self, n: int, seed: int, d_images: int, d_labels: int) -> None:
+        """synth::make_set(n, seed) generated on the device into [n][784] fp32 / [n] int32 buffers."""
+        _check(self._L.tlb_synth_make_set_device(self._h, n, seed, C.c_void_p(d_images or None),
+                                                 C.c_void_p(d_labels or None)))
+
+    def synth_make_digits_device(self, n: int, seed: int, d_pixels: int, d_labels: int) -> None:
+        """synth::make_digits(n, seed) bytes generated on the device."""
+        _check(self._L.tlb_synth_make_digits_device(self._h, n, seed, C.c_void_p(d_pixels or None),
+                                                    C.c_void_p(d_labels or None)))
+
     # ---- widened CNN (BASELINE configs[4]) ------------------------------------------------------------
     def wide_train(self, params, images, labels, rate: float = 0.05, epochs: int = 1, batch: int = 100,
                    engine: str = "tc"):

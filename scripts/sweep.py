@@ -2,12 +2,12 @@
 
   python scripts/sweep.py [--modes fast,exact] [--out gpurun_out/sweep.json]
 
-* configs[3] -- training throughput vs per-step batch B in {1k .. 256k}: a corpus of at least 2B images
-  (the 10k synthetic corpus tiled: cost is data-independent), one persistent-kernel launch per timed
-  step = n/B SGD groups; device-resident inputs, CUDA events on the launching stream.
+* configs[3] -- training throughput vs per-step batch B in {1k .. 256k}: a corpus of max(2B, 10k) distinct
+  synthetic images (synth::make_set(n, 1) generated on the device, byte-identical to the reference), one
+  persistent-kernel launch per timed step = n/B SGD groups; CUDA events on the launching stream.
 * configs[2] -- forward-only inference (net::evaluate: forward + argmax + correct count) for N in
-  {100, 1k, 10k, 100k, 1M} images; predictions on the first 10k checked against the reference's golden
-  predictions (trained params).
+  {100, 1k, 10k, 100k, 1M} distinct images (synth::make_set(N, 2) on the device); predictions on the first
+  10k checked against the reference's golden predictions (trained params).
 Each result is one JSON line with the roofline fraction against the FP32 CUDA-core peak
 (148 SMs x 128 lanes x 2 FLOP x sm_max_mhz).
 """
@@ -60,8 +60,6 @@ def main():
     dev = torch.device("cuda:0")
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    base_x, base_y = synth_make_set(10000, 1)
-    te_x, te_y = synth_make_set(10000, 2)
     flush = torch.empty(64 * 1024 * 1024, device=dev)
     out = open(args.out, "w")
 
@@ -80,10 +78,9 @@ def main():
         B = 1024
         while B <= args.max_batch:
             n = max(2 * B, 10000)
-            reps = (n + 9999) // 10000
-            x = np.tile(base_x, (reps, 1))[:n]
-            y = np.tile(base_y, reps)[:n]
-            d_x, d_y = torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev)
+            d_x = torch.empty(n, 784, device=dev)
+            d_y = torch.empty(n, dtype=torch.int32, device=dev)
+            ctx.synth_make_set_device(n, 1, d_x.data_ptr(), d_y.data_ptr())
             d_p = torch.zeros(3904, device=dev)
             d_p[:3898] = torch.from_numpy(init_params(42)).to(dev)
             loss = torch.zeros(16, dtype=torch.float64, device=dev)
@@ -104,10 +101,9 @@ def main():
         d_p = torch.zeros(3904, device=dev)
         d_p[:3898] = torch.from_numpy(golden_p).to(dev)
         for N in (100, 1000, 10000, 100000, 1000000):
-            reps = (N + 9999) // 10000
-            x = np.tile(te_x, (reps, 1))[:N]
-            y = np.tile(te_y, reps)[:N]
-            d_x, d_y = torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev)
+            d_x = torch.empty(N, 784, device=dev)
+            d_y = torch.empty(N, dtype=torch.int32, device=dev)
+            ctx.synth_make_set_device(N, 2, d_x.data_ptr(), d_y.data_ptr())
             pred = torch.zeros(N, dtype=torch.int32, device=dev)
             cnt = torch.zeros(1, dtype=torch.int64, device=dev)
             run = lambda: (cnt.zero_(), ctx.evaluate_device(d_x.data_ptr(), d_y.data_ptr(), N, d_p.data_ptr(),  # noqa
