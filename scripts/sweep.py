@@ -24,7 +24,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_1912_05234_b200 import Context  # noqa: E402
-from paper_1912_05234_b200.runtime import init_params, synth_make_set  # noqa: E402
+from paper_1912_05234_b200.runtime import init_params  # noqa: E402
 
 TRAIN_FLOP, FWD_FLOP = 1_048_320, 407_040
 
