@@ -202,6 +202,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     dp = world > 1 or args.force_dp
     if dp:
+        os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's version banner off stdout (one JSON line)
         if "RANK" not in os.environ:  # --force-dp without torchrun: a one-rank NCCL group
             os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1", MASTER_PORT="29517")
         dist.init_process_group("nccl", device_id=dev)
@@ -292,7 +293,7 @@ def run_ours(args):
                    "l2": "flushed between timed steps (256 MiB write outside the event pair)"},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp32_peak, "traffic": ncu_traffic(args.mode, B, n_per, world),
+                     "frac": achieved / fp32_peak, "traffic": None if dp else ncu_traffic(args.mode, B, n_per, world),
                      "traffic_note": "DRAM bytes/launch from profiles/r1/ncu_train_cluster_keymetrics.csv; "
                                      f"algorithmic input bytes/launch = {n_per * 3136}",
                      "per_launch": f"{n_per} images x {FLOP_PER_TRAIN_IMAGE} algorithmic FLOP",
