@@ -47,7 +47,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-dp", action="store_true",
                     help="run the N>1 data-parallel step (shard kernel + NCCL allreduce + sgd) even at N=1")
-    ap.add_argument("--no-graph", action="store_true", help="data-parallel step: plain launches, no CUDA graph")
+    ap.add_argument("--no-graph", action="store_true", help="NCCL data-parallel step: plain launches, no CUDA graph")
+    ap.add_argument("--dp-mode", choices=["nvlink", "nccl"], default="nvlink",
+                    help="N>1 step: fused clustered kernel over NVLink peer memory (default; falls back to "
+                         "nccl when symmetric memory is unavailable or a peer times out) or NCCL allreduce")
     return ap.parse_args()
 
 
@@ -201,8 +204,13 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dp = world > 1 or args.force_dp
+    real_stdout = None
     if dp:
-        os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's version banner off stdout (one JSON line)
+        # NCCL / torch.distributed print banners on stdout while communicators come up (lazily, at the
+        # first collective): send fd 1 to stderr until the JSON line, so stdout carries exactly one line.
+        sys.stdout.flush()
+        real_stdout = os.dup(1)
+        os.dup2(2, 1)
         if "RANK" not in os.environ:  # --force-dp without torchrun: a one-rank NCCL group
             os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1", MASTER_PORT="29517")
         dist.init_process_group("nccl", device_id=dev)
@@ -228,6 +236,7 @@ def run_ours(args):
         d_p.zero_()
         d_p[:3898] = torch.from_numpy(p0).to(dev)
 
+    dp_used, dp_note = None, None
     if not dp:
         def epoch(e):
             ctx.train_device(d_x.data_ptr(), d_y.data_ptr(), n_total, d_p.data_ptr(), 0.05, e, 1, B,
@@ -235,17 +244,39 @@ def run_ours(args):
         launches_per_step = 1
     else:
         from paper_1912_05234_b200.parallel import DeviceShardStep
-        step = DeviceShardStep(ctx, d_x, d_y, n_total, B * world, world, rank, graph=not args.no_graph)
+        from paper_1912_05234_b200.parallel import FusedDPStep
+        step, dp_used, dp_note = None, "nccl", None
+        if args.dp_mode == "nvlink" and args.mode == "fast":
+            try:
+                step = FusedDPStep(ctx, d_x, d_y, n_total, B * world, world, rank)
+                dp_used = "nvlink"
+            except Exception as exc:  # symmetric memory unavailable: NCCL path
+                dp_note = f"fused NVLink step unavailable ({type(exc).__name__}: {exc}); NCCL fallback"
+                print(dp_note, file=sys.stderr)
+        if step is None:
+            step = DeviceShardStep(ctx, d_x, d_y, n_total, B * world, world, rank, graph=not args.no_graph)
 
         def epoch(e):
             step.epoch(d_p, 0.05, d_loss, e)
-        launches_per_step = 2 * step.groups_per_epoch
+        launches_per_step = 1 if dp_used == "nvlink" else 2 * step.groups_per_epoch
 
     # warm-up (not timed), then the timed protocol from init_params(42)
     reset()
     for w in range(args.warmup):
         epoch(w % max(args.steps, 1))
     torch.cuda.synchronize()
+    if dp and dp_used == "nvlink":
+        try:
+            step.check()
+        except RuntimeError as exc:  # a peer timed out: rerun the warm-up on the NCCL path
+            dp_used, dp_note = "nccl", f"{exc}; NCCL fallback"
+            print(dp_note, file=sys.stderr)
+            step = DeviceShardStep(ctx, d_x, d_y, n_total, B * world, world, rank, graph=not args.no_graph)
+            launches_per_step = 2 * step.groups_per_epoch
+            reset()
+            for w in range(args.warmup):
+                epoch(w % max(args.steps, 1))
+            torch.cuda.synchronize()
     reset()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -263,6 +294,8 @@ def run_ours(args):
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     total_ms = sum(step_ms)
+    if dp and dp_used == "nvlink":
+        step.check()  # a watchdog trip during the timed epochs invalidates the number
     if dp:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -288,8 +321,12 @@ def run_ours(args):
                                f"{n_per} images/GPU at batch {B}/GPU, lr 0.05",
                    "batch_per_gpu": B, "global_batch": B * world, "n_images": n_total, "epochs_per_step": 1,
                    "mode": args.mode, "parallelism": f"dp{world}", "grid": args.grid or "auto",
-                   "dp_step": ("shard kernel + NCCL allreduce + sgd per group" +
-                               ("" if args.no_graph else ", epoch replayed as one CUDA graph")) if dp else None,
+                   "dp_step": None if not dp else (
+                       "fused: one clustered launch per epoch, fixed-point gradient slices added into the owning "
+                       "GPU's accumulator over NVLink peer memory (no collective call)" if dp_used == "nvlink" else
+                       "shard kernel + NCCL allreduce + sgd per group" +
+                       ("" if args.no_graph else ", epoch replayed as one CUDA graph")),
+                   "dp_note": dp_note,
                    "l2": "flushed between timed steps (256 MiB write outside the event pair)"},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
@@ -336,6 +373,9 @@ def run_ours(args):
                                   "sample": f"{meta['epochs']} epoch(s) x {n_per} images at batch {B}, reference "
                                             f"net::train (oracle/_ref) with {meta['cores']} workers, "
                                             f"{meta['seconds']:.1f} s"}
+    if real_stdout is not None:
+        sys.stdout.flush()
+        os.dup2(real_stdout, 1)
     if rank == 0:
         print(json.dumps(result), flush=True)
     ctx.close()

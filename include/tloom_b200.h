@@ -136,6 +136,19 @@ int tlb_train_shard_device(tlb_ctx* ctx, const float* d_images, const int32_t* d
                            int64_t batch, int64_t group, int64_t shard_lo, int64_t shard_hi,
                            const float* d_params, float* d_grad_sum, double* d_loss_sum);
 /* sgd_step on device buffers (post-allreduce): d_params -= rate * (d_grad_sum / m). */
+/* Fused data parallelism over NVLink (one call per rank, no NCCL on the data path): rank `rank` of
+ * `world` (<= 8) trains static_chunk(group, world, rank) of every global group of `batch` examples in ONE
+ * persistent clustered launch; the 2^-40 fixed-point gradient accumulator of slice s (of 8) and its
+ * arrival counter live in rank (s % world)'s workspace and every rank adds into it over peer memory
+ * (system-scope `red`), then applies the identical sgd_step with the global group size.  peer_ws holds
+ * every rank's workspace pointer (tlb_dp_workspace_bytes each, zeroed before the first call, e.g. a
+ * torch symmetric-memory buffer); seq_base = SGD steps run on these workspaces since they were zeroed.
+ * A peer wait longer than timeout_s sets the watchdog word (u32 at byte offset
+ * tlb_dp_workspace_bytes() - 32 of this rank's workspace) and ends the kernel instead of hanging. */
+size_t tlb_dp_workspace_bytes(void);
+int tlb_train_dp_device(tlb_ctx* ctx, const float* d_images, const int32_t* d_labels, int64_t n, float* d_params,
+                        float rate, int32_t epoch_begin, int32_t epochs, int64_t batch, double* d_epoch_loss,
+                        int world, int rank, void* const* peer_ws, uint64_t seq_base, double timeout_s);
 int tlb_apply_sgd_device(tlb_ctx* ctx, float* d_params, const float* d_grad_sum, float rate,
                          int64_t m);
 int tlb_evaluate_device(tlb_ctx* ctx, const float* d_images, const int32_t* d_labels, int64_t n,

@@ -40,6 +40,9 @@ _SIGS = {
     "tlb_ctx_set_trace": (C.c_int, [vp, vp]),
     "tlb_ctx_set_cluster": (C.c_int, [vp, C.c_int]),
     "tlb_ctx_set_threads": (C.c_int, [vp, C.c_int]),
+    "tlb_dp_workspace_bytes": (C.c_size_t, []),
+    "tlb_train_dp_device": (C.c_int, [vp, vp, vp, C.c_int64, vp, C.c_float, C.c_int32, C.c_int32, C.c_int64, vp,
+                                      C.c_int, C.c_int, C.POINTER(vp), C.c_uint64, C.c_double]),
     "tlb_synth_make_digits_device": (C.c_int, [vp, C.c_int64, C.c_uint64, vp, vp]),
     "tlb_synth_make_set_device": (C.c_int, [vp, C.c_int64, C.c_uint64, vp, vp]),
     "tlb_wide_init_params": (C.c_int, [C.c_uint64, f32p]),
@@ -89,7 +92,7 @@ def declared_symbols() -> list[str]:
     """Every function the public header declares."""
     with open(HEADER) as f:
         text = f.read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(tlb_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|size_t)\s+(tlb_\w+)\s*\(", text, re.M)))
 
 
 _LIB = None

@@ -271,6 +271,13 @@ int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t 
   return TLB_OK;
 }
 
+struct DpArgs {
+  int world, rank;
+  void* const* peer_ws;  // world pointers: every rank's symmetric workspace (tlb_dp_workspace_bytes)
+  uint64_t seq_base;
+  long long timeout_cycles;
+};
+
 int check_train_args(int64_t n, int32_t epochs, float rate, int64_t batch) {
   // network.cpp:211-214 then mnist::batches (mnist.cpp:170)
   if (n == 0) return fail(TLB_ERR_ERROR, "train: empty dataset");
@@ -286,13 +293,17 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
                   float rate, int32_t epoch_begin, int32_t epochs, int64_t batch, double* d_epoch_loss,
                   int64_t shard_lo = 0, int64_t shard_hi = 0, int64_t group = -1, float* grad_out = nullptr,
                   double* loss_out = nullptr, const unsigned int* ready = nullptr, unsigned int token = 0,
-                  int64_t chunk = 1) {
+                  int64_t chunk = 1, const DpArgs* dp = nullptr) {
   const int64_t spe = (n + batch - 1) / batch;
   const int64_t m_max = std::min<int64_t>(batch, n);
   const int64_t m_local = grad_out ? std::max<int64_t>(0, std::min(shard_hi, m_max) - shard_lo) : m_max;
   // Clustered fast kernel: one example per CTA per step, every CTA co-resident.
   const int csz = tlb::cluster_size();
-  const int clusters = (int)((std::max<int64_t>(m_local, 1) + csz - 1) / csz);
+  int clusters = (int)((std::max<int64_t>(m_local, 1) + csz - 1) / csz);
+  if (dp) {  // every rank launches the same grid: size it for the largest static_chunk
+    const int64_t block = (m_max + dp->world - 1) / dp->world;
+    clusters = (int)((std::max<int64_t>(block, 1) + csz - 1) / csz);
+  }
   const bool clustered = !exact(c) && c->use_cluster && c->grid_override == 0 && c->max_clusters > 0 &&
                          clusters <= c->max_clusters;
   const int threads = pick_threads(c, m_local);
@@ -331,6 +342,31 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.ready_token = token;
   a.chunk = chunk;
   a.ready_step_end = a.step_begin + spe;  // only the call's first epoch can outrun the copies
+  if (clustered) {
+    if (dp) {  // fused data parallelism: slice s lives on rank s % world (peer memory)
+      a.dp_world = dp->world;
+      a.dp_rank = dp->rank;
+      for (int sl = 0; sl < 8; ++sl) {
+        char* base = static_cast<char*>(dp->peer_ws[sl % dp->world]);
+        a.slice_acc[sl] = reinterpret_cast<unsigned long long*>(base);
+        a.slice_cnt[sl] = reinterpret_cast<unsigned int*>(base + tlb::dp_counter_offset()) + sl;
+      }
+      a.loss_acc = reinterpret_cast<unsigned long long*>(static_cast<char*>(dp->peer_ws[0]) + 3 * TLB_PSTRIDE * 8);
+      a.seq_base = dp->seq_base;
+      a.dp_error = reinterpret_cast<unsigned int*>(static_cast<char*>(dp->peer_ws[dp->rank]) +
+                                                   tlb::dp_counter_offset()) + 8;
+      a.dp_timeout_cycles = dp->timeout_cycles;
+    } else {
+      for (int sl = 0; sl < 8; ++sl) {
+        a.slice_acc[sl] = static_cast<unsigned long long*>(c->work.p);
+        a.slice_cnt[sl] = static_cast<unsigned int*>(c->barrier.p) + sl;
+      }
+      a.loss_acc = static_cast<unsigned long long*>(c->work.p) + 3 * TLB_PSTRIDE;
+    }
+  } else if (dp) {
+    return fail(TLB_ERR_ARG, "fused data parallelism needs fast mode and groups of <= 8 x co-resident clusters "
+                             "per rank");
+  }
   if (a.step_end <= a.step_begin) return TLB_OK;
   if (clustered) TLB_CUDA(tlb::launch_train_cluster(a, clusters, c->stream));
   else TLB_CUDA(tlb::launch_train(exact(c), a, grid, threads, c->stream));
@@ -674,6 +710,24 @@ int tlb_train_shard_device(tlb_ctx* c, const float* d_images, const int32_t* d_l
   TLB_TRY(set_device(c));
   return enqueue_train(c, d_images, d_labels, n, const_cast<float*>(d_params), 1.0f, 0, 1, batch, nullptr, shard_lo,
                        shard_hi, group, d_grad_sum, d_loss_sum);
+}
+
+size_t tlb_dp_workspace_bytes(void) { return tlb::dp_workspace_bytes(); }
+
+int tlb_train_dp_device(tlb_ctx* c, const float* d_images, const int32_t* d_labels, int64_t n, float* d_params,
+                        float rate, int32_t epoch_begin, int32_t epochs, int64_t batch, double* d_epoch_loss, int world,
+                        int rank, void* const* peer_ws, uint64_t seq_base, double timeout_s) {
+  if (!c || !d_params || !d_epoch_loss || !peer_ws) return fail(TLB_ERR_ARG, "tlb_train_dp_device: null argument");
+  TLB_TRY(check_train_args(n, epochs, rate, batch));
+  if (world < 1 || world > 8 || rank < 0 || rank >= world)
+    return fail(TLB_ERR_ARG, "tlb_train_dp_device: world must be 1..8 and 0 <= rank < world");
+  for (int r = 0; r < world; ++r)
+    if (!peer_ws[r]) return fail(TLB_ERR_ARG, "tlb_train_dp_device: null peer workspace");
+  if (exact(c)) return fail(TLB_ERR_ARG, "tlb_train_dp_device: fused data parallelism runs in fast mode");
+  TLB_TRY(set_device(c));
+  const DpArgs dp{world, rank, peer_ws, seq_base, (long long)(timeout_s * 2.0e9)};
+  return enqueue_train(c, d_images, d_labels, n, d_params, rate, epoch_begin, epochs, batch, d_epoch_loss, 0, 0, -1,
+                       nullptr, nullptr, nullptr, 0, 1, &dp);
 }
 
 int tlb_apply_sgd_device(tlb_ctx* c, float* d_params, const float* d_grad_sum, float rate, int64_t m) {

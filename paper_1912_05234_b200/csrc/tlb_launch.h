@@ -36,6 +36,18 @@ struct TrainArgs {
   unsigned int ready_token;
   int64_t chunk;
   int64_t ready_step_end;
+  // Fused data parallelism over NVLink peer memory (clustered kernel, dp_world > 0): rank dp_rank of
+  // dp_world trains static_chunk(group, dp_world, dp_rank) of every global group; slice s of the
+  // fixed-point gradient accumulator and its arrival counter live on rank s % dp_world, the loss
+  // accumulator on rank 0 (symmetric buffers, peer pointers).  seq_base = steps run on these buffers
+  // since they were zeroed (triple-buffer phase and counter targets continue across launches).
+  int dp_world, dp_rank;
+  unsigned long long* slice_acc[8];  // [3][3904] u64 accumulator holding slice s (local or peer)
+  unsigned int* slice_cnt[8];        // arrival counter of slice s
+  unsigned long long* loss_acc;      // [3] u64 loss accumulators
+  uint64_t seq_base;
+  unsigned int* dp_error;            // set when a peer wait times out (the kernel then exits)
+  long long dp_timeout_cycles;
 };
 
 struct CellArgs {
@@ -69,6 +81,8 @@ cudaError_t launch_train(bool exact, const TrainArgs& a, int grid, int threads, 
 cudaError_t cluster_train_capacity(int* max_clusters);
 int cluster_size();
 size_t cluster_work_bytes();
+size_t dp_workspace_bytes();
+size_t dp_counter_offset();
 cudaError_t launch_train_cluster(const TrainArgs& a, int clusters, cudaStream_t st);
 cudaError_t launch_cells(bool exact, const CellArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_eval(bool exact, const EvalArgs& a, int grid, int threads, cudaStream_t st);

@@ -36,14 +36,31 @@ __device__ __forceinline__ int64_t group_size(const TrainArgs& a, int64_t st) {
   return rem < a.batch ? rem : a.batch;
 }
 
-// Examples of group `st` handled by this launch: the whole group, or the DP shard of it.
-__device__ __forceinline__ int64_t local_size(const TrainArgs& a, int64_t st) {
+// Examples of group `st` handled by this launch: the whole group, the DP shard of it given by the
+// caller (grad_out mode), or this rank's static_chunk of it (fused data parallelism).
+__device__ __forceinline__ void local_range(const TrainArgs& a, int64_t st, int64_t& lo, int64_t& hi) {
   const int64_t m = group_size(a, st);
-  if (!a.grad_out) return m;
-  const int64_t hi = a.shard_hi < m ? a.shard_hi : m;
-  return hi > a.shard_lo ? hi - a.shard_lo : 0;
+  if (a.dp_world > 0) {
+    static_chunk(m, a.dp_world, a.dp_rank, lo, hi);
+  } else if (a.grad_out) {
+    lo = a.shard_lo < m ? a.shard_lo : m;
+    hi = a.shard_hi < m ? a.shard_hi : m;
+    if (hi < lo) hi = lo;
+  } else {
+    lo = 0;
+    hi = m;
+  }
 }
-__device__ __forceinline__ int64_t local_offset(const TrainArgs& a) { return a.grad_out ? a.shard_lo : 0; }
+__device__ __forceinline__ int64_t local_size(const TrainArgs& a, int64_t st) {
+  int64_t lo, hi;
+  local_range(a, st, lo, hi);
+  return hi - lo;
+}
+__device__ __forceinline__ int64_t local_offset(const TrainArgs& a, int64_t st) {
+  int64_t lo, hi;
+  local_range(a, st, lo, hi);
+  return lo;
+}
 
 __device__ __forceinline__ bool first_job(const TrainArgs& a, int64_t from, Job& j) {
   for (int64_t st = from; st < a.step_end; ++st) {
@@ -66,7 +83,7 @@ __device__ __forceinline__ bool next_job(const TrainArgs& a, Job& j) {
 }
 
 __device__ __forceinline__ int64_t job_index(const TrainArgs& a, const Job& j) {
-  return (j.step % a.steps_per_epoch) * a.batch + local_offset(a) + j.e;
+  return (j.step % a.steps_per_epoch) * a.batch + local_offset(a, j.step) + j.e;
 }
 
 __device__ __forceinline__ const float* job_image(const TrainArgs& a, const Job& j) {
@@ -207,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
   uint32_t consumed = 0;
 
   for (int64_t st = a.step_begin; st < a.step_end; ++st) {
-    const int64_t ks = st % a.steps_per_epoch, start = ks * a.batch + local_offset(a);
+    const int64_t ks = st % a.steps_per_epoch, start = ks * a.batch + local_offset(a, st);
     const int64_t m = local_size(a, st);
     int64_t lo, hi;
     static_chunk(m, G, blockIdx.x, lo, hi);
@@ -301,8 +318,16 @@ constexpr double kUnfix = 1.0 / kFix;
 // [3] u64 loss accumulators, [kCluster] u32 slice arrival counters (zeroed by the host per launch).
 constexpr int64_t kAccWords = 3 * (int64_t)kPStride + 3;
 
-__device__ __forceinline__ void red_add_u64(unsigned long long* p, long long v) {
-  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// Fixed-point accumulation: device scope on one GPU, system scope when the accumulator may be a peer
+// GPU's memory (fused data parallelism over NVLink).
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, long long v, bool sys) {
+  if (sys) asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a) {
@@ -313,9 +338,15 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
   smem_setup(s);
   const uint32_t rank = cluster_rank(), cid = cluster_id(), ncl = cluster_count();
   const int G = gridDim.x;
-  unsigned long long* const acc = reinterpret_cast<unsigned long long*>(a.work);  // [3][kPStride]
-  unsigned long long* const lacc = acc + 3 * kPStride;                             // [3]
-  unsigned int* const cnt = a.barrier;  // [kCluster] slice arrival counters
+  // This CTA owns gradient slice `rank`: its accumulator and arrival counter (local, or on the peer
+  // GPU rank % dp_world in fused data-parallel mode), and the loss accumulator (rank 0's).
+  const bool dp = a.dp_world > 0;
+  const int world = dp ? a.dp_world : 1;
+  unsigned long long* const acc = a.slice_acc[rank];  // [3][kPStride]
+  unsigned long long* const lacc = a.loss_acc;        // [3]
+  unsigned int* const cnt = a.slice_cnt[rank];
+  const bool owner = !dp || (int)(rank % (uint32_t)world) == a.dp_rank;  // zeroes its slice's next buffer
+  __shared__ int timed_out;
   unsigned long long* const trace = blockIdx.x == 0 ? a.trace : nullptr;
 
   Job pf;
@@ -325,9 +356,10 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
   load_params(s, a.params);  // once: afterwards the parameters live in shared memory
 
   for (int64_t st = a.step_begin; st < a.step_end; ++st) {
-    const int64_t ls = st - a.step_begin;  // local step: accumulator buffer ls % 3
-    const int64_t ks = st % a.steps_per_epoch, start = ks * a.batch + local_offset(a);
-    const int64_t m = local_size(a, st);
+    const int64_t ls = st - a.step_begin;  // local step
+    const uint64_t seq = a.seq_base + (uint64_t)ls;  // steps on these accumulators: buffer seq % 3
+    const int64_t ks = st % a.steps_per_epoch, start = ks * a.batch + local_offset(a, st);
+    const int64_t m = local_size(a, st), m_global = group_size(a, st);
     int64_t lo, hi;
     static_chunk(m, G, blockIdx.x, lo, hi);
     s.tr = trace ? trace + ls * 16 : nullptr;
@@ -364,52 +396,64 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     mark(s, 9);
     cluster_sync_all();  // every pushed slice has landed
     mark(s, 10);
-    const int b = (int)(ls % 3), bn = (int)((ls + 1) % 3);
+    const int b = (int)(seq % 3), bn = (int)((seq + 1) % 3);
     const int j = (int)rank * kSlice + (int)threadIdx.x;  // this thread's parameter (threads < 488)
     if (threadIdx.x < kSlice) {
       float sum = rx[threadIdx.x];
 #pragma unroll
       for (int q = 1; q < kCluster; ++q) sum += rx[q * kSlice + threadIdx.x];
-      red_add_u64(acc + b * kPStride + j, __double2ll_rn((double)sum * kFix));
-      if (cid == 0) acc[bn * kPStride + j] = 0ull;  // next step's accumulator
+      red_add_u64(acc + b * kPStride + j, __double2ll_rn((double)sum * kFix), dp);
+      if (cid == 0 && owner) acc[bn * kPStride + j] = 0ull;  // next step's accumulator
     }
     if (rank == 0 && threadIdx.x == kSlice) {
       double l = 0.0;
       for (int q = 0; q < kCluster; ++q) l = __dadd_rn(l, loss_rx[q]);
-      red_add_u64(lacc + b, __double2ll_rn(l * kFix));
-      if (cid == 0) lacc[bn] = 0ull;
+      red_add_u64(lacc + b, __double2ll_rn(l * kFix), dp);
+      if (cid == 0 && (!dp || a.dp_rank == 0)) lacc[bn] = 0ull;
     }
     __syncthreads();
     mark(s, 14);
-    // ---- 3/4. arrival on slice `rank`, then wait for every cluster's contribution ----
+    // ---- 3/4. arrival on slice `rank`, then wait for every cluster's (and every GPU's) contribution ----
     if (threadIdx.x == 0) {
-      __threadfence();
-      unsigned int* c = cnt + rank;
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(c) : "memory");
-      const unsigned int want = (unsigned int)((ls + 1) * ncl);
+      timed_out = 0;
+      if (dp) {  // release at system scope is cumulative over the CTA's adds (ordered by the barrier)
+        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+      } else {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+      }
+      const unsigned int want = (unsigned int)((seq + 1) * ncl * (uint64_t)world);
       unsigned int v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
-      while ((int)(v - want) < 0) {
+      const long long t0 = clock64();
+      for (;;) {
+        if (dp) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+        else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+        if ((int)(v - want) >= 0) break;
+        if (dp && clock64() - t0 > a.dp_timeout_cycles) {  // a peer never arrived: fail, do not hang
+          atomicExch(a.dp_error, 1u);
+          timed_out = 1;
+          break;
+        }
         __nanosleep(32);
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
       }
     }
     __syncthreads();
+    if (timed_out) return;
     mark(s, 11);
     if (threadIdx.x < kSlice) {
-      const long long t = (long long)__ldcg(acc + b * kPStride + j);
+      const long long t = (long long)(dp ? ld_sys_u64(acc + b * kPStride + j) : __ldcg(acc + b * kPStride + j));
       if (j < kNParam) {
         const float gsum = (float)((double)t * kUnfix);
         if (a.grad_out) {  // data-parallel shard: the shard's gradient sum goes to the allreduce
           if (cid == 0) a.grad_out[j] = gsum;
         } else {
-          s.P[j] = fsub(s.P[j], fmul(a.rate, __fdiv_rn(gsum, (float)m)));
+          s.P[j] = fsub(s.P[j], fmul(a.rate, __fdiv_rn(gsum, (float)m_global)));
           if (cid == 0) __stcg(a.params + j, s.P[j]);
         }
       }
     }
     if (blockIdx.x == 0 && threadIdx.x == kSlice) {
-      const double l = (double)(long long)__ldcg(lacc + b) * kUnfix;
+      const double l = (double)(long long)(dp ? ld_sys_u64(lacc + b) : __ldcg(lacc + b)) * kUnfix;
       if (a.grad_out) {
         a.loss_out[0] = l;
       } else {
@@ -587,12 +631,19 @@ cudaError_t cluster_train_capacity(int* max_clusters) {
 
 int cluster_size() { return kCluster; }
 size_t cluster_work_bytes() { return kAccWords * sizeof(unsigned long long); }
+// Fused-DP symmetric workspace per rank: [3][kPStride] u64 accumulators | [3] u64 loss | pad |
+// [kCluster] u32 slice counters | u32 watchdog flag.
+size_t dp_workspace_bytes() { return kAccWords * sizeof(unsigned long long) + 8 + 64; }
+size_t dp_counter_offset() { return kAccWords * sizeof(unsigned long long) + 8; }
 
 // Grid = clusters * 8 CTAs, all co-resident (clusters <= cluster_train_capacity): the kernel's grid
 // barrier needs co-residency, which the cooperative attribute also asserts where the driver allows it.
 cudaError_t launch_train_cluster(const TrainArgs& a, int clusters, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(a.barrier, 0, kCluster * sizeof(unsigned int), st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(a.work, 0, kAccWords * sizeof(unsigned long long), st);
+  cudaError_t e = cudaSuccess;
+  if (a.dp_world == 0) {  // single GPU: fresh accumulators per launch (fused DP: the caller's seq_base)
+    e = cudaMemsetAsync(a.barrier, 0, kCluster * sizeof(unsigned int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a.work, 0, kAccWords * sizeof(unsigned long long), st);
+  }
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * kCluster);

@@ -119,3 +119,41 @@ class DeviceShardStep:
             self.graph, self.graph_key = g, key
         self.graph.replay()
         d_epoch_loss[e : e + 1].copy_(self.out)
+
+
+class FusedDPStep:
+    """Fused data parallelism over NVLink (tlb_train_dp_device): one persistent clustered launch per
+    epoch per rank and NO collective call on the data path -- each rank's clusters add their fixed-point
+    gradient slices straight into the owning rank's accumulator (slice s on rank s % world) through
+    peer pointers of a torch symmetric-memory workspace, wait on that slice's arrival counter, and apply
+    the identical update.  Falls back (raises) when symmetric memory is unavailable; a peer that never
+    arrives trips the kernel's watchdog (``check()`` raises) instead of hanging."""
+
+    def __init__(self, ctx, d_images, d_labels, n: int, global_batch: int, world: int, rank: int,
+                 timeout_s: float = 2.0):
+        import torch.distributed._symmetric_memory as symm_mem
+        from . import _lib
+        self.ctx, self.x, self.y, self.n, self.B = ctx, d_images, d_labels, n, global_batch
+        self.world, self.rank, self.timeout_s = world, rank, timeout_s
+        nbytes = int(_lib.lib().tlb_dp_workspace_bytes())
+        self.ws = symm_mem.empty(nbytes, dtype=torch.uint8, device=d_images.device)
+        self.ws.zero_()
+        group = dist.group.WORLD
+        self.handle = symm_mem.rendezvous(self.ws, group.group_name if hasattr(group, "group_name") else group)
+        self.peers = [int(p) for p in self.handle.buffer_ptrs]
+        self.err_off = nbytes - 32
+        self.seq = 0
+        self.groups_per_epoch = len(groups(n, global_batch))
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    def epoch(self, d_params, rate: float, d_epoch_loss, e: int) -> None:
+        self.ctx.train_dp_device(self.x.data_ptr(), self.y.data_ptr(), self.n, d_params.data_ptr(), rate, e, 1, self.B,
+                                 d_epoch_loss.data_ptr(), self.world, self.rank, self.peers, self.seq, self.timeout_s)
+        self.seq += self.groups_per_epoch
+
+    def check(self) -> None:
+        """Raise if a peer wait timed out in any launch so far (reads this rank's watchdog word)."""
+        flag = self.ws[self.err_off:self.err_off + 4].view(torch.int32).item()
+        if flag:
+            raise RuntimeError("fused data parallelism: a peer GPU never arrived (watchdog)")

@@ -246,6 +246,14 @@ class Context:
     def wide_gemm_device(self, which: int, engine: str) -> None:
         _check(self._L.tlb_wide_gemm_device(self._h, which, WIDE_ENGINES[engine]))
 
+    def train_dp_device(self, d_images: int, d_labels: int, n: int, d_params: int, rate: float, epoch_begin: int,
+                        epochs: int, batch: int, d_epoch_loss: int, world: int, rank: int, peer_ws: list,
+                        seq_base: int, timeout_s: float = 2.0) -> None:
+        """Fused data parallelism over NVLink peer memory (tlb_train_dp_device)."""
+        arr = (C.c_void_p * len(peer_ws))(*[C.c_void_p(p) for p in peer_ws])
+        _check(self._L.tlb_train_dp_device(self._h, d_images, d_labels, n, d_params, rate, epoch_begin, epochs, batch,
+                                           d_epoch_loss, world, rank, arr, seq_base, timeout_s))
+
     def train_shard_device(self, d_images: int, d_labels: int, n: int, batch: int, group: int, shard_lo: int,
                            shard_hi: int, d_params: int, d_grad_sum: int, d_loss_sum: int) -> None:
         _check(self._L.tlb_train_shard_device(self._h, d_images, d_labels, n, batch, group, shard_lo, shard_hi,
