@@ -364,3 +364,28 @@ def test_dp_shards_sum_to_the_full_group(orc, small):
                     assert np.array_equal(bits(got_p), bits(want_p))
                 else:
                     assert rel_err(got_p, want_p, floor=1e-3) <= REL_TOL
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_overlapped_ingestion_equals_resident_data(orc, zhang_sets, mode):
+    """tlb_train streams the dataset in chunks on a copy stream while the kernel trains (device ready
+    flags): for sizes around the chunk boundary (84 images per 256 KiB rounded up to whole groups) and
+    repeated calls with growing and shrinking sizes, the result equals training on device-resident data."""
+    import torch
+    from paper_1912_05234_b200 import Context
+    (tr_x, tr_y), _ = zhang_sets
+    p0 = orc.init_params(42)
+    dev = torch.device("cuda:0")
+    with Context(0, mode=mode) as c:
+        c.set_stream(torch.cuda.current_stream().cuda_stream)
+        for n, batch in ((1, 100), (83, 7), (200, 100), (5000, 100), (300, 100), (1001, 77)):
+            got_p, got_l = c.train(p0, tr_x[:n], tr_y[:n], epochs=2, batch=batch)
+            d_x = torch.from_numpy(tr_x[:n]).to(dev)
+            d_y = torch.from_numpy(tr_y[:n]).to(dev)
+            d_p = torch.zeros(3904, device=dev)
+            d_p[:3898] = torch.from_numpy(p0).to(dev)
+            d_l = torch.zeros(2, dtype=torch.float64, device=dev)
+            c.train_device(d_x.data_ptr(), d_y.data_ptr(), n, d_p.data_ptr(), 0.05, 0, 2, batch, d_l.data_ptr())
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(got_p), bits(d_p.cpu().numpy()[:3898])), n
+            assert list(got_l) == d_l.cpu().numpy().tolist(), n
