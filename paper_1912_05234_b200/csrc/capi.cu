@@ -92,6 +92,7 @@ struct tlb_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t copy_gate = nullptr;
   DevBuf ready;
+  DevBuf ready_err;  // [3] u32 ingestion watchdog words (flag, chunk, observed value)
   unsigned int ready_token = 0;
   DevBuf synth_snaps;  // device synthetic corpus: mt19937_64 state snapshots per segment
   // Widened-network workspaces (capacity `wide_cap` images) and the last group's arguments.
@@ -339,6 +340,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.loss_out = loss_out;
   a.trace = c->trace;
   a.ready = ready;
+  a.ready_err = static_cast<unsigned int*>(c->ready_err.p);
   a.ready_token = token;
   a.chunk = chunk;
   a.ready_step_end = a.step_begin + spe;  // only the call's first epoch can outrun the copies
@@ -414,6 +416,8 @@ int tlb_ctx_create(int device, tlb_ctx** out) {
     (void)cudaGetLastError();  // no cluster launch on this device: the flat kernel is used
     c->max_clusters = 0;
   }
+  if (e == cudaSuccess) e = c->ready_err.ensure(4 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(c->ready_err.p, 0, 4 * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->copy_gate, cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -436,6 +440,7 @@ int tlb_ctx_destroy(tlb_ctx* c) {
   for (auto& s : c->stage) s.release();
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   c->ready.release();
+  c->ready_err.release();
   for (auto& w : c->wide) w.release();
   c->synth_snaps.release();
   if (c->copy_gate) cudaEventDestroy(c->copy_gate);
@@ -566,7 +571,16 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   TLB_CUDA(cudaMemcpyAsync(params, d_p, TLB_NPARAM * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
   if (epoch_loss) TLB_CUDA(cudaMemcpyAsync(epoch_loss, d_loss, epochs * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   TLB_CUDA(cudaStreamSynchronize(c->stream));
-  if (overlap) TLB_CUDA(cudaStreamSynchronize(c->copy_stream));
+  if (overlap) {
+    TLB_CUDA(cudaStreamSynchronize(c->copy_stream));
+    unsigned int err[3] = {0, 0, 0};
+    TLB_CUDA(cudaMemcpy(err, c->ready_err.p, sizeof(err), cudaMemcpyDeviceToHost));
+    if (err[0]) {
+      TLB_CUDA(cudaMemset(c->ready_err.p, 0, sizeof(err)));
+      return fail(TLB_ERR_CUDA, "tlb_train: dataset chunk " + std::to_string(err[1]) + " never became ready (flag " +
+                                    std::to_string(err[2]) + ", token " + std::to_string(c->ready_token) + ")");
+    }
+  }
   return TLB_OK;
 }
 

@@ -15,10 +15,12 @@
 using namespace tlb;
 
 enum Stage { kConv1, kConv2V0, kConv2V1, kFc, kFcBack, kC2BackV0, kC2BackV1, kC2BackV2, kC2BackV3, kC1Back, kForward,
-             kBackwardV0, kBackwardV1, kNumStages };
+             kBackwardV0, kBackwardV1, kBackinV4, kBackinV5, kC1BackGk2, kBackwardV4, kBackwardV5, kNumStages };
 static const char* kNames[kNumStages] = {"conv1", "conv2_v0_halves", "conv2_v1_rows", "fc", "fc_back",
                                          "conv2_back_v0_quads", "conv2_back_v1_items", "conv2_back_v2_pairs", "conv2_back_v3_ws", "conv1_back",
-                                         "forward_image", "backward_v0", "backward_v1"};
+                                         "forward_image", "backward_v0", "backward_v1",
+                                         "backin_only_v4_items", "backin_only_v5_quads", "c1back_with_gk2",
+                                         "backward_v4", "backward_v5"};
 
 __device__ __forceinline__ float hrand(unsigned int x) {  // deterministic value in [0, 1)
   x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
@@ -62,7 +64,16 @@ __device__ __forceinline__ void run_stage(const Smem& s, float* row) {
   else if constexpr (STAGE == kC2BackV3) stage_conv2_back<EXACT, A, 3>(s, row);
   else if constexpr (STAGE == kC1Back) stage_conv1_back<EXACT, A>(s, s.img, row);
   else if constexpr (STAGE == kForward) forward_image<EXACT>(s, s.img, 3, nullptr, true);
-  else if constexpr (STAGE == kBackwardV0) {
+  else if constexpr (STAGE == kBackinV4) stage_conv2_back<EXACT, A, 4>(s, row);
+  else if constexpr (STAGE == kBackinV5) stage_conv2_back<EXACT, A, 5>(s, row);
+  else if constexpr (STAGE == kC1BackGk2) stage_conv1_back_gk2<EXACT, A>(s, s.img, row);
+  else if constexpr (STAGE == kBackwardV4 || STAGE == kBackwardV5) {
+    stage_fc_back<EXACT, A>(s, row);
+    __syncthreads();
+    stage_conv2_back<EXACT, A, STAGE == kBackwardV4 ? 4 : 5>(s, row);
+    __syncthreads();
+    stage_conv1_back_gk2<EXACT, A>(s, s.img, row);
+  } else if constexpr (STAGE == kBackwardV0) {
     stage_fc_back<EXACT, A>(s, row);
     __syncthreads();
     stage_conv2_back<EXACT, A, 0>(s, row);
@@ -123,6 +134,11 @@ void all(float* rows, unsigned long long* d_cycles, int sms, int iters, double m
   measure<EXACT, kForward>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kBackwardV0>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kBackwardV1>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kBackinV4>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kBackinV5>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kC1BackGk2>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kBackwardV4>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kBackwardV5>(rows, d_cycles, sms, iters, mhz);
 }
 
 int main(int argc, char** argv) {

@@ -36,6 +36,8 @@ struct TrainArgs {
   unsigned int ready_token;
   int64_t chunk;
   int64_t ready_step_end;
+  unsigned int* ready_err;  // [3] diagnostic words: set when a ready flag never arrives (then the kernel
+                            // proceeds and the host call fails instead of hanging)
   // Fused data parallelism over NVLink peer memory (clustered kernel, dp_world > 0): rank dp_rank of
   // dp_world trains static_chunk(group, dp_world, dp_rank) of every global group; slice s of the
   // fixed-point gradient accumulator and its arrival counter live on rank s % dp_world, the loss

@@ -94,10 +94,19 @@ __device__ __forceinline__ const float* job_image(const TrainArgs& a, const Job&
 // image.  The flag is written by a stream memory operation after the chunk's copy completes.
 __device__ __forceinline__ void wait_ready(const TrainArgs& a, const Job& j) {
   if (!a.ready || j.step >= a.ready_step_end) return;
-  const unsigned int* f = a.ready + job_index(a, j) / a.chunk;
+  const int64_t k = job_index(a, j) / a.chunk;
+  const unsigned int* f = a.ready + k;
   unsigned int v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  const long long t0 = clock64();
   while ((int)(v - a.ready_token) < 0) {
+    if (clock64() - t0 > 20000000000LL) {  // ~10 s: record the stuck chunk, fail the call, do not hang
+      if (atomicCAS(a.ready_err, 0u, 1u) == 0u) {
+        a.ready_err[1] = (unsigned int)k;
+        a.ready_err[2] = v;
+      }
+      break;
+    }
     __nanosleep(256);
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
   }

@@ -893,6 +893,12 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
         gk2_fast<ACCUM>(s, row, it - kBackin);
       }
     }
+  } else if constexpr (V == 4) {
+    // V = 4: backin only, one lane per item on warps 0-3 (g_k2 runs later, beside the C1 gradient)
+    if (threadIdx.x < 108) backin_item<EXACT>(s, threadIdx.x);
+  } else if constexpr (V == 5) {
+    // V = 5: backin only, lane quads over 14 warps (g_k2 runs later, beside the C1 gradient)
+    for (int it = threadIdx.x; it < 448; it += blockDim.x) backin_quad<EXACT>(s, it, it < 432);
   } else if constexpr (V == 3) {
     // V = 3: weight-stationary backin over all lanes, then the ordered kernel combine (224 lanes)
     // beside the g_k2/g_b2 lanes.
@@ -923,6 +929,62 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
   }
 }
 
+// One EXACT C1-gradient lane: it < 150 -> g_k1[i][u][v] as one ordered 576-term chain (lanes (u, v)-major,
+// i minor: a warp reads ~6 shifted-image rows and the 6 dz1 channel rows of one y, each in its own bank
+// group); 150 <= it < 156 -> g_b1[i] as the ordered sum of dz1[i].
+template <bool ACCUM>
+__device__ __forceinline__ void stage_conv1_back_lane_exact(const Smem& s, float* row, int it) {
+  const float* dz1 = s.c1;
+  if (it < 150) {
+    // lane = (u, v) major, i minor: a warp reads ~6 shifted-image rows and the 6 dz1 channel rows
+    // of one y, each in its own bank group (conflict-free 128-bit loads)
+    const int i = it % 6, r = it / 6, u = r / 5, v = r - u * 5;
+    const float4* ib = reinterpret_cast<const float4*>(s.sh + sh_at(v, u));
+    const float4* db = reinterpret_cast<const float4*>(dz1 + i * kC1Plane);
+    float acc = 0.0f;
+    // software pipeline: row y+1 is in flight while the ordered chain consumes row y
+    float4 a[6], d[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      a[q] = ib[q];
+      d[q] = db[q];
+    }
+#pragma unroll 1
+    for (int y = 0; y < 24; ++y) {
+      const int yn = y + 1 < 24 ? y + 1 : y;
+      float4 an[6], dn[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        an[q] = ib[yn * 6 + q];
+        dn[q] = db[yn * 6 + q];
+      }
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        acc = mac<true>(acc, a[q].x, d[q].x);
+        acc = mac<true>(acc, a[q].y, d[q].y);
+        acc = mac<true>(acc, a[q].z, d[q].z);
+        acc = mac<true>(acc, a[q].w, d[q].w);
+      }
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        a[q] = an[q];
+        d[q] = dn[q];
+      }
+    }
+    put<ACCUM>(s, row, kK1 + i * 25 + r, acc);
+  } else {
+    const int i = it - 150;
+    const float4* dp = reinterpret_cast<const float4*>(dz1 + i * kC1Plane);
+    float acc = 0.0f;
+#pragma unroll 4
+    for (int e = 0; e < 144; ++e) {
+      const float4 d = dp[e];
+      acc = fadd(fadd(fadd(fadd(acc, d.x), d.y), d.z), d.w);
+    }
+    put<ACCUM>(s, row, kB1 + i, acc);
+  }
+}
+
 // C1 backward: g_k1[i][u][v] = sum_{y,x<24} I[u+y][v+x]*dz1[i][y][x]; g_b1[i] = sum dz1[i].
 // EXACT: one lane per output, the 576 terms in order, reading the v-shifted image copy so every row
 // is aligned 128-bit loads.  Fast: one lane per (i, y) holds all 25 outputs (the dz1 row stays in
@@ -931,56 +993,7 @@ template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img, float* row) {
   const float* dz1 = s.c1;
   if constexpr (EXACT) {
-    for (int it = threadIdx.x; it < 156; it += blockDim.x) {
-      if (it < 150) {
-        // lane = (u, v) major, i minor: a warp reads ~6 shifted-image rows and the 6 dz1 channel rows
-        // of one y, each in its own bank group (conflict-free 128-bit loads)
-        const int i = it % 6, r = it / 6, u = r / 5, v = r - u * 5;
-        const float4* ib = reinterpret_cast<const float4*>(s.sh + sh_at(v, u));
-        const float4* db = reinterpret_cast<const float4*>(dz1 + i * kC1Plane);
-        float acc = 0.0f;
-        // software pipeline: row y+1 is in flight while the ordered chain consumes row y
-        float4 a[6], d[6];
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-          a[q] = ib[q];
-          d[q] = db[q];
-        }
-#pragma unroll 1
-        for (int y = 0; y < 24; ++y) {
-          const int yn = y + 1 < 24 ? y + 1 : y;
-          float4 an[6], dn[6];
-#pragma unroll
-          for (int q = 0; q < 6; ++q) {
-            an[q] = ib[yn * 6 + q];
-            dn[q] = db[yn * 6 + q];
-          }
-#pragma unroll
-          for (int q = 0; q < 6; ++q) {
-            acc = mac<true>(acc, a[q].x, d[q].x);
-            acc = mac<true>(acc, a[q].y, d[q].y);
-            acc = mac<true>(acc, a[q].z, d[q].z);
-            acc = mac<true>(acc, a[q].w, d[q].w);
-          }
-#pragma unroll
-          for (int q = 0; q < 6; ++q) {
-            a[q] = an[q];
-            d[q] = dn[q];
-          }
-        }
-        put<ACCUM>(s, row, kK1 + i * 25 + r, acc);
-      } else {
-        const int i = it - 150;
-        const float4* dp = reinterpret_cast<const float4*>(dz1 + i * kC1Plane);
-        float acc = 0.0f;
-#pragma unroll 4
-        for (int e = 0; e < 144; ++e) {
-          const float4 d = dp[e];
-          acc = fadd(fadd(fadd(fadd(acc, d.x), d.y), d.z), d.w);
-        }
-        put<ACCUM>(s, row, kB1 + i, acc);
-      }
-    }
+    for (int it = threadIdx.x; it < 156; it += blockDim.x) stage_conv1_back_lane_exact<ACCUM>(s, row, it);
   } else {
     const int it = threadIdx.x;
     if (it < 144) {  // (i, y): 25 row-partials + the bias row-partial
@@ -1033,11 +1046,86 @@ __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img
   }
 }
 
+// C1 weight gradient with the conv2 weight gradient on the otherwise idle lanes (EXACT: the C1 chains
+// occupy 156 lanes for ~5 us; g_k2/g_b2 need only dz2 and s1, so they no longer share a phase with backin).
+// Fast C1 weight gradient run by the first 160 threads only (named barrier 1 between its two phases):
+// 144 (i, y) lanes form 25 row partials + the bias row partial, then 156 lanes combine the 24 row
+// partials in fixed order.
+template <bool ACCUM>
+__device__ __forceinline__ void conv1_back_fast_group(const Smem& s, const float* img, float* row) {
+  constexpr int kGroup = 160;
+  const float* dz1 = s.c1;
+  const int it = threadIdx.x;
+  if (it < 144) {
+    const int i = it / 24, y = it - i * 24;
+    const float4* dp = reinterpret_cast<const float4*>(dz1 + c1_at(i, y, 0));
+    float dr[24];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const float4 t = dp[q];
+      dr[4 * q] = t.x; dr[4 * q + 1] = t.y; dr[4 * q + 2] = t.z; dr[4 * q + 3] = t.w;
+    }
+    float bias = 0.0f;
+#pragma unroll
+    for (int x = 0; x < 24; ++x) bias += dr[x];
+    float* out = s.red + it * 26;
+    out[25] = bias;
+#pragma unroll 1
+    for (int u = 0; u < 5; ++u) {
+      const float4* ip = reinterpret_cast<const float4*>(img + (u + y) * 28);
+      float ir[28];
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        const float4 t = ip[q];
+        ir[4 * q] = t.x; ir[4 * q + 1] = t.y; ir[4 * q + 2] = t.z; ir[4 * q + 3] = t.w;
+      }
+      float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int x = 0; x < 24; ++x)
+#pragma unroll
+        for (int v = 0; v < 5; ++v) acc[v] = __fmaf_rn(ir[x + v], dr[x], acc[v]);
+#pragma unroll
+      for (int v = 0; v < 5; ++v) out[u * 5 + v] = acc[v];
+    }
+  }
+  named_sync(1, kGroup);
+  if (it < 156) {
+    float acc = 0.0f;
+    const int col = it < 150 ? (it % 25) : 25, i = it < 150 ? it / 25 : it - 150;
+#pragma unroll 8
+    for (int y = 0; y < 24; ++y) acc += s.red[(i * 24 + y) * 26 + col];
+    put<ACCUM>(s, row, it < 150 ? kK1 + it : kB1 + i, acc);
+  }
+}
+
+template <bool EXACT, bool ACCUM>
+__device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float* img, float* row) {
+  constexpr int kGk2 = EXACT ? 372 : 288;
+  const int t = threadIdx.x;
+  if (t < 160) {
+    if constexpr (EXACT) {
+      if (t < 156) stage_conv1_back_lane_exact<ACCUM>(s, row, t);
+    } else {
+      conv1_back_fast_group<ACCUM>(s, img, row);
+    }
+  } else {
+    for (int item = t - 160; item < kGk2; item += blockDim.x - 160) {
+      if constexpr (EXACT) gk2_exact<ACCUM>(s, row, item);
+      else gk2_fast<ACCUM>(s, row, item);
+    }
+  }
+}
+
 // Stage variants used by the product kernels (chosen with paper_1912_05234_b200/csrc/stage_bench.cu).
+#ifndef TLB_CONV2_BACK_V
+#define TLB_CONV2_BACK_V(EXACT) 4
+#endif
 template <bool EXACT>
 struct StageCfg {
   static constexpr int conv2 = EXACT ? 0 : 1;
-  static constexpr int conv2_back = 1;
+  static constexpr int conv2_back = TLB_CONV2_BACK_V(EXACT);
+  // backin-only conv2_back variants move g_k2/g_b2 into the C1-gradient phase
+  static constexpr bool gk2_with_c1 = conv2_back == 4 || conv2_back == 5;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -1061,7 +1149,8 @@ __device__ __noinline__ void call_conv2_back(float* row) {
 }
 template <bool EXACT, bool ACCUM>
 __device__ __noinline__ void call_conv1_back(const float* img, float* row) {
-  stage_conv1_back<EXACT, ACCUM>(smem_view(), img, row);
+  if constexpr (StageCfg<EXACT>::gk2_with_c1) stage_conv1_back_gk2<EXACT, ACCUM>(smem_view(), img, row);
+  else stage_conv1_back<EXACT, ACCUM>(smem_view(), img, row);
 }
 
 // Whole forward pass of one image (image already in shared memory).

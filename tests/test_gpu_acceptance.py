@@ -16,11 +16,23 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.skipif(not os.path.exists(EXE), reason="acceptance_b200 not built (needs /root/reference at build time)")
 def test_reference_acceptance_gate_on_b200():
     env = dict(os.environ, LD_LIBRARY_PATH=os.path.join(ROOT, "paper_1912_05234_b200", "lib"))
-    out = subprocess.run([EXE], capture_output=True, text=True, timeout=300, env=env)
-    log = out.stdout + out.stderr
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", "acceptance_b200.log"), "w") as f:
-        f.write(log)
+    log_path = os.path.join(ROOT, "gpurun_out", "acceptance_b200.log")
+    # line-buffered straight into the log, so a stuck step is visible even when the timeout fires
+    with open(log_path, "w") as f:
+        try:
+            rc = subprocess.run(["stdbuf", "-oL", "-eL", EXE], stdout=f, stderr=subprocess.STDOUT, timeout=180,
+                                env=env).returncode
+        except subprocess.TimeoutExpired:
+            rc = None
+    with open(log_path) as f:
+        log = f.read()
+    assert rc is not None, "acceptance gate timed out; partial log:\n" + log
+
+    class _Out:
+        stdout = log
+        returncode = rc
+    out = _Out()
     lines = [l for l in out.stdout.splitlines() if l[:1] == "A" and l[1:2].isdigit()]
     assert len(lines) == 7, log
     assert not [l for l in lines if ": FAIL" in l], log
