@@ -1118,7 +1118,7 @@ __device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float*
 
 // Stage variants used by the product kernels (chosen with paper_1912_05234_b200/csrc/stage_bench.cu).
 #ifndef TLB_CONV2_BACK_V
-#define TLB_CONV2_BACK_V(EXACT) 4
+#define TLB_CONV2_BACK_V(EXACT) 1
 #endif
 template <bool EXACT>
 struct StageCfg {
