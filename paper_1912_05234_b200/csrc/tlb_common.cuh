@@ -155,6 +155,14 @@ __device__ __forceinline__ void grid_sync(unsigned int* counter, unsigned int& t
   __syncthreads();
 }
 
+// Named CTA barriers (id 0 is __syncthreads): producers arrive, consumers sync (or vice versa).
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // ---- thread-block clusters / distributed shared memory ----------------------------------------
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;

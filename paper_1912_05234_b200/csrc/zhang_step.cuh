@@ -119,13 +119,6 @@ __device__ __forceinline__ Smem carve_smem(float* base) {
 
 __device__ __forceinline__ Smem smem_view() { return carve_smem(tlb_smem); }
 
-// Named CTA barriers (id 0 is __syncthreads): producers arrive, consumers sync (or vice versa).
-__device__ __forceinline__ void named_arrive(int id, int nthreads) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
 
 // One-time per-CTA setup: exp2 table, zero padding of dz2, image mbarriers.
 __device__ __forceinline__ void smem_setup(const Smem& s) {
