@@ -189,11 +189,14 @@ __global__ void __launch_bounds__(kThreadsTC, 2) tc_gemm_kernel(Op op) {
         }
       }
     };
+    // prefetch distance 2: chunks c+1 and c+2 are in flight while chunk c is stored
+    float na[16], nb[kBElems];
     if (nchunks > 0) gather(0, va, vb);
+    if (nchunks > 1) gather(1, na, nb);
     for (int c = 0; c < nchunks; ++c) {
       const int s = c % kStages;
-      float na[16], nb[kBElems];
-      if (c + 1 < nchunks) gather(c + 1, na, nb);
+      float n2a[16], n2b[kBElems];
+      if (c + 2 < nchunks) gather(c + 2, n2a, n2b);
       if (c >= kStages) mbar_wait(&empty[s], ((c / kStages) - 1) & 1);
       uint8_t* st = base + s * Cfg::kStageBytes;
       uint8_t *ahi = st, *alo = st + Cfg::kABytes, *bhi = st + 2 * Cfg::kABytes, *blo = bhi + Cfg::kBBytes;
@@ -225,9 +228,15 @@ __global__ void __launch_bounds__(kThreadsTC, 2) tc_gemm_kernel(Op op) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
       mbar_arrive(&full[s]);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) va[e] = na[e];
+      for (int e = 0; e < 16; ++e) {
+        va[e] = na[e];
+        na[e] = n2a[e];
+      }
 #pragma unroll
-      for (int e = 0; e < kBElems; ++e) vb[e] = nb[e];
+      for (int e = 0; e < kBElems; ++e) {
+        vb[e] = nb[e];
+        nb[e] = n2b[e];
+      }
     }
   } else if (lane == 0) {
     // ---- MMA issuer (warp 8, one lane) ----
