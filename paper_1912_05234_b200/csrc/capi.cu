@@ -258,8 +258,7 @@ WriteValue32Fn write_value32() {
 // Upload n images on the copy stream in chunks of `chunk` images, raising ready[k] to `token` after
 // chunk k.  The copy stream first waits for all earlier work on the context stream (buffer reuse).
 int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t chunk, unsigned int token) {
-  TLB_CUDA(cudaEventRecord(c->copy_gate, c->stream));
-  TLB_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));
+  TLB_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));  // recorded by the caller
   unsigned int* flags = static_cast<unsigned int*>(c->ready.p);
   for (int64_t k = 0, lo = 0; lo < n; ++k, lo += chunk) {
     const int64_t cnt = std::min(chunk, n - lo);
@@ -270,6 +269,15 @@ int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t 
     if (r != CUDA_SUCCESS) return fail(TLB_ERR_CUDA, "cuStreamWriteValue32 failed: " + std::to_string((int)r));
   }
   return TLB_OK;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
 }
 
 struct DpArgs {
@@ -546,7 +554,9 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
       TLB_CUDA(cudaMemset(c->ready.p, 0, c->ready.cap));
       c->ready_token = 1;
     }
-    TLB_TRY(ingest_images(c, images, d_img, n, chunk, c->ready_token));
+    // The copy stream may only overwrite the staging buffer after all earlier work on the context
+    // stream: gate it on an event recorded now, before this call's kernel (which waits on the copies).
+    TLB_CUDA(cudaEventRecord(c->copy_gate, c->stream));
   } else if (n) {
     TLB_CUDA(cudaMemcpyAsync(d_img, images, (size_t)n * 784 * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   }
@@ -556,13 +566,20 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   TLB_CUDA(cudaMemsetAsync(d_p, 0, TLB_PSTRIDE * sizeof(float), c->stream));
   TLB_CUDA(cudaMemcpyAsync(d_p, params, TLB_NPARAM * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   TLB_TRY(stage_out(c, 3, (size_t)epochs, &d_loss));
+  // Pinned source: launch the kernel first, then enqueue the chunk copies (the host's ~200 enqueue calls
+  // overlap the running kernel, which polls the ready flags).  Pageable source: copies first -- the
+  // driver stages pageable memory synchronously on the host.
+  const bool copies_first = overlap && !is_pinned(images);
+  if (copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, c->ready_token));
   if (!on_epoch) {
     TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, 0, epochs, batch, d_loss, 0, 0, -1, nullptr, nullptr,
                           rdy, c->ready_token, chunk));
+    if (overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, c->ready_token));
   } else {
     for (int32_t e = 0; e < epochs; ++e) {
       TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, e, 1, batch, d_loss, 0, 0, -1, nullptr, nullptr,
                             e == 0 ? rdy : nullptr, c->ready_token, chunk));
+      if (e == 0 && overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, c->ready_token));
       double mean = 0.0;
       TLB_TRY(fetch(c, &mean, d_loss + e, 1));
       on_epoch(e + 1, mean, user);
