@@ -1,5 +1,5 @@
-// zhang_step.cuh -- one 512-thread CTA runs the whole Zhang-CNN training cell of one image out of
-// shared memory.
+// zhang_step.cuh -- one CTA (512 threads, or 256 with two CTAs per SM) runs the whole Zhang-CNN
+// training cell of one image out of shared memory.
 //
 // Reference path (proj/src/network.cpp:81-169, kernels proj/src/nn.cpp:96-217):
 //   c1 = sigmoid(mconv(I,k1,b1)); s1 = avgpool(c1); c2 = sigmoid(mconv(s1,k2,b2)); s2 = avgpool(c2);
@@ -13,8 +13,10 @@
 // outer chain staying on one lane.  With EXACT=false the same stages use FFMA and split long sums
 // across lanes (deterministic fixed trees; within the 1e-4 tolerance).
 //
-// One CTA per SM (16 warps) keeps the latency-bound batch-100 step busy; shared memory per CTA is
-// ~125 KB (layout in carve_smem).
+// Batch 100 runs one 512-thread CTA per SM (16 warps, latency-bound step); launches with more than one
+// image per SM run 256-thread CTAs, two per SM, whose barrier stalls overlap (the stages loop over their
+// lanes).  Shared memory: a common prefix + an aliased fast/EXACT tail (+ the clustered kernel's DSMEM
+// receive buffer), see carve_smem: 104 KB fast, 94 KB EXACT, 146 KB clustered.
 #pragma once
 
 #include "tlb_common.cuh"
