@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
   float* const rx = s.term;   // [8 source ranks][488]: slices pushed to this CTA (it owns slice `rank`)
   __shared__ double loss_rx[kCluster];  // rank 0: the 8 CTAs' fp64 loss sums of the step (pushed)
   smem_setup(s);
+  cluster_sync_all();  // every CTA of the cluster is running before any peer stores into its shared memory
   const uint32_t rank = cluster_rank(), cid = cluster_id(), ncl = cluster_count();
   const int G = gridDim.x;
   // This CTA owns gradient slice `rank`: its accumulator and arrival counter (local, or on the peer
