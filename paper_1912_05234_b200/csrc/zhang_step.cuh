@@ -21,6 +21,11 @@
 
 #include "tlb_common.cuh"
 
+// EXACT C1 weight gradient: register-blocked v-groups (1, default) or one lane per output (0).
+#ifndef TLB_C1BACK_EXACT_BLOCKED
+#define TLB_C1BACK_EXACT_BLOCKED 1
+#endif
+
 namespace tlb {
 
 constexpr int kThreads = 512;
@@ -984,11 +989,70 @@ __device__ __forceinline__ void stage_conv1_back_lane_exact(const Smem& s, float
 // EXACT: one lane per output, the 576 terms in order, reading the v-shifted image copy so every row
 // is aligned 128-bit loads.  Fast: one lane per (i, y) holds all 25 outputs (the dz1 row stays in
 // registers and feeds 5 image rows), then a fixed-order combine over the 24 row partials.
+// EXACT C1 weight gradient, register-blocked: lane (u, i) of a warp owns the chains of outputs
+// (i, u, V0..V0+NV-1) -- the image row u+y (28 floats) and the dz1 row (i, y) are loaded once per y and
+// feed NV ordered 576-term chains (each chain still adds its products in the reference order: y, then x).
+// Two warps cover v = {0,1,2} and {3,4}; a third holds the six g_b1 chains.
+template <bool ACCUM, int V0, int NV>
+__device__ __forceinline__ void c1back_exact_vgroup(const Smem& s, const float* img, float* row, int lane) {
+  if (lane >= 30) return;
+  const int u = lane / 6, i = lane - u * 6;  // i minor: the six dz1 channel rows sit in distinct bank groups
+  const float4* ib = reinterpret_cast<const float4*>(img + u * 28);
+  const float4* db = reinterpret_cast<const float4*>(s.c1 + i * kC1Plane);
+  float acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0f;
+  float4 a[7], d[6];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) a[q] = ib[q];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) d[q] = db[q];
+#pragma unroll 1
+  for (int y = 0; y < 24; ++y) {
+    const int yn = y + 1 < 24 ? y + 1 : y;
+    float4 an[7], dn[6];  // next row in flight while this row's chains run
+#pragma unroll
+    for (int q = 0; q < 7; ++q) an[q] = ib[yn * 7 + q];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) dn[q] = db[yn * 6 + q];
+    const float ir[28] = {a[0].x, a[0].y, a[0].z, a[0].w, a[1].x, a[1].y, a[1].z, a[1].w, a[2].x, a[2].y,
+                          a[2].z, a[2].w, a[3].x, a[3].y, a[3].z, a[3].w, a[4].x, a[4].y, a[4].z, a[4].w,
+                          a[5].x, a[5].y, a[5].z, a[5].w, a[6].x, a[6].y, a[6].z, a[6].w};
+    const float dr[24] = {d[0].x, d[0].y, d[0].z, d[0].w, d[1].x, d[1].y, d[1].z, d[1].w,
+                          d[2].x, d[2].y, d[2].z, d[2].w, d[3].x, d[3].y, d[3].z, d[3].w,
+                          d[4].x, d[4].y, d[4].z, d[4].w, d[5].x, d[5].y, d[5].z, d[5].w};
+#pragma unroll
+    for (int x = 0; x < 24; ++x)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) acc[v] = mac<true>(acc[v], ir[V0 + v + x], dr[x]);
+#pragma unroll
+    for (int q = 0; q < 7; ++q) a[q] = an[q];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) d[q] = dn[q];
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) put<ACCUM>(s, row, kK1 + i * 25 + u * 5 + V0 + v, acc[v]);
+}
+
+template <bool ACCUM>
+__device__ __forceinline__ void stage_conv1_back_exact_blocked(const Smem& s, const float* img, float* row) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (blockDim.x >= 96) {
+    if (warp == 0) c1back_exact_vgroup<ACCUM, 0, 3>(s, img, row, lane);
+    else if (warp == 1) c1back_exact_vgroup<ACCUM, 3, 2>(s, img, row, lane);
+    else if (warp == 2 && lane < 6) stage_conv1_back_lane_exact<ACCUM>(s, row, 150 + lane);
+  }
+}
+
 template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void stage_conv1_back(const Smem& s, const float* img, float* row) {
   const float* dz1 = s.c1;
   if constexpr (EXACT) {
+#if TLB_C1BACK_EXACT_BLOCKED
+    stage_conv1_back_exact_blocked<ACCUM>(s, img, row);
+#else
     for (int it = threadIdx.x; it < 156; it += blockDim.x) stage_conv1_back_lane_exact<ACCUM>(s, row, it);
+#endif
   } else {
     const int it = threadIdx.x;
     if (it < 144) {  // (i, y): 25 row-partials + the bias row-partial
