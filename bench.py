@@ -364,7 +364,9 @@ def run_ours(args):
         result["e2e"] = {"value": args.steps * n_total / sum(times), "unit": "images/s",
                          "h2d_bytes_per_step": images.nbytes + labels.nbytes + 3898 * 4,
                          "d2h_bytes_per_step": 3898 * 4 + 8,
-                         "api": "tlb_train (net::train) on pinned host buffers, wall clock per call"}
+                         "api": "tlb_train (net::train) on pinned host buffers, wall clock per call",
+                         "call_ms": {"median": 1e3 * sorted(times)[len(times) // 2], "min": 1e3 * min(times),
+                                     "max": 1e3 * max(times)}}
         result["gpu_launches"] += args.steps
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -255,20 +255,34 @@ WriteValue32Fn write_value32() {
   return fn;
 }
 
-// Upload n images on the copy stream in chunks of `chunk` images, raising ready[k] to `token` after
-// chunk k.  The copy stream first waits for all earlier work on the context stream (buffer reuse).
-int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t chunk, unsigned int token) {
+// Upload n images on the copy stream, raising ready[k] to `token` after chunk k lands: chunk > 0 =
+// fixed chunks of `chunk` images; chunk == 0 = geometric chunks of SGD groups (group 0, then groups
+// [2^(k-1), 2^k)), see TrainArgs::chunk.  The copy stream first waits for all earlier work on the
+// context stream (buffer reuse).
+int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t chunk, int64_t batch,
+                  unsigned int token) {
   TLB_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));  // recorded by the caller
   unsigned int* flags = static_cast<unsigned int*>(c->ready.p);
-  for (int64_t k = 0, lo = 0; lo < n; ++k, lo += chunk) {
-    const int64_t cnt = std::min(chunk, n - lo);
+  for (int64_t k = 0, lo = 0; lo < n; ++k) {
+    const int64_t hi = chunk > 0 ? lo + chunk : (k == 0 ? 1 : (int64_t)1 << k) * batch;
+    const int64_t cnt = std::min(hi, n) - lo;
     TLB_CUDA(cudaMemcpyAsync(dev + lo * 784, host + lo * 784, (size_t)cnt * 784 * sizeof(float),
                              cudaMemcpyHostToDevice, c->copy_stream));
     const CUresult r = write_value32()(reinterpret_cast<CUstream>(c->copy_stream),
                                        reinterpret_cast<CUdeviceptr>(flags + k), token, CU_STREAM_WRITE_VALUE_DEFAULT);
     if (r != CUDA_SUCCESS) return fail(TLB_ERR_CUDA, "cuStreamWriteValue32 failed: " + std::to_string((int)r));
+    lo += cnt;
   }
   return TLB_OK;
+}
+
+// Number of ingestion chunks for n images (see ingest_images).
+int64_t ingest_chunks(int64_t n, int64_t chunk, int64_t batch) {
+  if (chunk > 0) return (n + chunk - 1) / chunk;
+  const int64_t groups = (n + batch - 1) / batch;
+  int64_t k = 1;
+  while (((int64_t)1 << (k - 1)) < groups) ++k;  // chunk k-1 ends at group 2^(k-1)
+  return groups <= 1 ? 1 : k;
 }
 
 bool is_pinned(const void* p) {
@@ -536,10 +550,14 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   float* d_p;
   double* d_loss;
   // The dataset streams in on the copy stream while the first epoch already trains on the chunks
-  // that have landed (chunk = whole SGD groups, >= 256 KiB); labels/params are tiny and go first.
-  const int64_t per = std::max<int64_t>(1, (256 * 1024 + 784 * 4 - 1) / (784 * 4));
-  const int64_t chunk = ((per + batch - 1) / batch) * batch;
-  const int64_t nchunks = (n + chunk - 1) / chunk;
+  // that have landed; labels/params are tiny and go first.
+  // Default: geometric chunks (8 copies for 100 groups); TLB_INGEST_CHUNK=<images> = fixed chunks.
+  static const int64_t fixed_chunk = [] {
+    const char* e = std::getenv("TLB_INGEST_CHUNK");
+    return e ? std::max<int64_t>(0, std::atoll(e)) : (int64_t)0;
+  }();
+  const int64_t chunk = fixed_chunk;
+  const int64_t nchunks = ingest_chunks(n, chunk, batch);
   const bool overlap = write_value32() != nullptr;
   TLB_TRY(stage_out(c, 0, (size_t)n * 784, &d_img));
   if (overlap) {
@@ -570,16 +588,16 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   // overlap the running kernel, which polls the ready flags).  Pageable source: copies first -- the
   // driver stages pageable memory synchronously on the host.
   const bool copies_first = overlap && !is_pinned(images);
-  if (copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, c->ready_token));
+  if (copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token));
   if (!on_epoch) {
     TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, 0, epochs, batch, d_loss, 0, 0, -1, nullptr, nullptr,
                           rdy, c->ready_token, chunk));
-    if (overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, c->ready_token));
+    if (overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token));
   } else {
     for (int32_t e = 0; e < epochs; ++e) {
       TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, e, 1, batch, d_loss, 0, 0, -1, nullptr, nullptr,
                             e == 0 ? rdy : nullptr, c->ready_token, chunk));
-      if (e == 0 && overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, c->ready_token));
+      if (e == 0 && overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token));
       double mean = 0.0;
       TLB_TRY(fetch(c, &mean, d_loss + e, 1));
       on_epoch(e + 1, mean, user);

@@ -29,9 +29,11 @@ struct TrainArgs {
   float* grad_out;
   double* loss_out;
   unsigned long long* trace;  // optional [steps][16] clock64 stamps of CTA 0 (tlb_ctx_set_trace)
-  // Overlapped ingestion (tlb_train on host buffers): images arrive in chunks of `chunk` images on a
-  // copy stream; ready[k] >= ready_token once chunk k is resident.  Steps < ready_step_end poll the
-  // flag before the image's TMA load; nullptr = every image already resident.
+  // Overlapped ingestion (tlb_train on host buffers): images arrive in chunks on a copy stream;
+  // ready[k] >= ready_token once chunk k is resident.  chunk > 0: chunk k = images [k*chunk, (k+1)*chunk);
+  // chunk == 0: geometric chunks of whole SGD groups -- chunk 0 = group 0, chunk k >= 1 = groups
+  // [2^(k-1), 2^k) -- so a 100-group epoch needs 8 copies, each landing well before it is consumed.
+  // Steps < ready_step_end poll the flag before the image's TMA load; nullptr = every image resident.
   const unsigned int* ready;
   unsigned int ready_token;
   int64_t chunk;

@@ -94,7 +94,13 @@ __device__ __forceinline__ const float* job_image(const TrainArgs& a, const Job&
 // image.  The flag is written by a stream memory operation after the chunk's copy completes.
 __device__ __forceinline__ void wait_ready(const TrainArgs& a, const Job& j) {
   if (!a.ready || j.step >= a.ready_step_end) return;
-  const int64_t k = job_index(a, j) / a.chunk;
+  int64_t k;
+  if (a.chunk > 0) {
+    k = job_index(a, j) / a.chunk;
+  } else {  // geometric: group g lives in chunk floor(log2 g) + 1 (group 0 in chunk 0)
+    const int64_t g = j.step % a.steps_per_epoch;
+    k = g == 0 ? 0 : 64 - __clzll((long long)g);
+  }
   const unsigned int* f = a.ready + k;
   unsigned int v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");

@@ -368,9 +368,10 @@ def test_dp_shards_sum_to_the_full_group(orc, small):
 
 @pytest.mark.parametrize("mode", ["exact", "fast"])
 def test_overlapped_ingestion_equals_resident_data(orc, zhang_sets, mode):
-    """tlb_train streams the dataset in chunks on a copy stream while the kernel trains (device ready
-    flags): for sizes around the chunk boundary (84 images per 256 KiB rounded up to whole groups) and
-    repeated calls with growing and shrinking sizes, the result equals training on device-resident data."""
+    """tlb_train streams the dataset in geometric chunks of SGD groups (group 0, then [2^(k-1), 2^k)) on
+    a copy stream while the kernel trains (device ready flags): for group counts on and around the chunk
+    boundaries, pageable and pinned sources, and repeated calls with growing and shrinking sizes, the
+    result equals training on device-resident data."""
     import torch
     from paper_1912_05234_b200 import Context
     (tr_x, tr_y), _ = zhang_sets
@@ -378,8 +379,14 @@ def test_overlapped_ingestion_equals_resident_data(orc, zhang_sets, mode):
     dev = torch.device("cuda:0")
     with Context(0, mode=mode) as c:
         c.set_stream(torch.cuda.current_stream().cuda_stream)
-        for n, batch in ((1, 100), (83, 7), (200, 100), (5000, 100), (300, 100), (1001, 77)):
-            got_p, got_l = c.train(p0, tr_x[:n], tr_y[:n], epochs=2, batch=batch)
+        cases = ((1, 100), (83, 7), (200, 100), (5000, 100), (300, 100), (1001, 77), (2, 1), (3, 1), (4, 1),
+                 (5, 1), (129, 1), (800, 100), (801, 100), (10000, 100))
+        for i, (n, batch) in enumerate(cases):
+            xs, ys = tr_x[:n], tr_y[:n]
+            if i % 2:  # pinned source: the kernel is enqueued before the chunk copies
+                xs = torch.from_numpy(np.ascontiguousarray(xs)).pin_memory().numpy()
+                ys = torch.from_numpy(np.ascontiguousarray(ys)).pin_memory().numpy()
+            got_p, got_l = c.train(p0, xs, ys, epochs=2, batch=batch)
             d_x = torch.from_numpy(tr_x[:n]).to(dev)
             d_y = torch.from_numpy(tr_y[:n]).to(dev)
             d_p = torch.zeros(3904, device=dev)
