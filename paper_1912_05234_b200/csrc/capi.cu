@@ -255,16 +255,24 @@ WriteValue32Fn write_value32() {
   return fn;
 }
 
+// First SGD group of geometric ingestion chunk k (TrainArgs::chunk == 0; the kernel's wait_ready
+// inverts it): 0, 1, 2, 3, 4, 6, 8, 12, 16, 24, ...
+int64_t geo_chunk_start(int64_t k) {
+  if (k < 2) return k;
+  const int64_t e = k / 2;
+  return ((int64_t)1 << e) + (k % 2) * ((int64_t)1 << (e - 1));
+}
+
 // Upload n images on the copy stream, raising ready[k] to `token` after chunk k lands: chunk > 0 =
-// fixed chunks of `chunk` images; chunk == 0 = geometric chunks of SGD groups (group 0, then groups
-// [2^(k-1), 2^k)), see TrainArgs::chunk.  The copy stream first waits for all earlier work on the
+// fixed chunks of `chunk` images; chunk == 0 = geometric chunks of SGD groups (groups 0 and 1, then
+// the halves of each [2^e, 2^(e+1))), see TrainArgs::chunk.  The copy stream first waits for all earlier work on the
 // context stream (buffer reuse).
 int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t chunk, int64_t batch,
                   unsigned int token) {
   TLB_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));  // recorded by the caller
   unsigned int* flags = static_cast<unsigned int*>(c->ready.p);
   for (int64_t k = 0, lo = 0; lo < n; ++k) {
-    const int64_t hi = chunk > 0 ? lo + chunk : (k == 0 ? 1 : (int64_t)1 << k) * batch;
+    const int64_t hi = chunk > 0 ? lo + chunk : geo_chunk_start(k + 1) * batch;
     const int64_t cnt = std::min(hi, n) - lo;
     TLB_CUDA(cudaMemcpyAsync(dev + lo * 784, host + lo * 784, (size_t)cnt * 784 * sizeof(float),
                              cudaMemcpyHostToDevice, c->copy_stream));
@@ -280,9 +288,9 @@ int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t 
 int64_t ingest_chunks(int64_t n, int64_t chunk, int64_t batch) {
   if (chunk > 0) return (n + chunk - 1) / chunk;
   const int64_t groups = (n + batch - 1) / batch;
-  int64_t k = 1;
-  while (((int64_t)1 << (k - 1)) < groups) ++k;  // chunk k-1 ends at group 2^(k-1)
-  return groups <= 1 ? 1 : k;
+  int64_t k = 0;
+  while (geo_chunk_start(k + 1) < groups) ++k;
+  return k + 1;
 }
 
 bool is_pinned(const void* p) {
@@ -551,7 +559,7 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   double* d_loss;
   // The dataset streams in on the copy stream while the first epoch already trains on the chunks
   // that have landed; labels/params are tiny and go first.
-  // Default: geometric chunks (8 copies for 100 groups); TLB_INGEST_CHUNK=<images> = fixed chunks.
+  // Default: geometric chunks (14 copies for 100 groups); TLB_INGEST_CHUNK=<images> = fixed chunks.
   static const int64_t fixed_chunk = [] {
     const char* e = std::getenv("TLB_INGEST_CHUNK");
     return e ? std::max<int64_t>(0, std::atoll(e)) : (int64_t)0;

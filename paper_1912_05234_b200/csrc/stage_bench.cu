@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <vector>
 
@@ -15,12 +16,17 @@
 using namespace tlb;
 
 enum Stage { kConv1, kConv2V0, kConv2V1, kFc, kFcBack, kC2BackV0, kC2BackV1, kC2BackV2, kC2BackV3, kC1Back, kForward,
-             kBackwardV0, kBackwardV1, kBackinV4, kBackinV5, kC1BackGk2, kBackwardV4, kBackwardV5, kNumStages };
+             kBackwardV0, kBackwardV1, kBackinV4, kBackinV5, kC1BackGk2, kBackwardV4, kBackwardV5, kC2BackV6, kC2BackV7, kBackwardV6, kBackwardV7, kC2BackV8, kBackwardV8,
+             kBackinV9, kBackwardV9, kC2BackV10, kBackwardV10, kBackwardV11, kBackwardV12, kBackwardV13, kNumStages };
 static const char* kNames[kNumStages] = {"conv1", "conv2_v0_halves", "conv2_v1_rows", "fc", "fc_back",
                                          "conv2_back_v0_quads", "conv2_back_v1_items", "conv2_back_v2_pairs", "conv2_back_v3_ws", "conv1_back",
                                          "forward_image", "backward_v0", "backward_v1",
                                          "backin_only_v4_items", "backin_only_v5_quads", "c1back_with_gk2",
-                                         "backward_v4", "backward_v5"};
+                                         "backward_v4", "backward_v5", "conv2_back_v6_rows2", "conv2_back_v7_rows4",
+                                         "backward_v6", "backward_v7", "conv2_back_v8_rows4p", "backward_v8",
+                                         "backin_only_v9_rows4p", "backward_v9", "conv2_back_v10_split_gk2",
+                                         "backward_v10", "backward_v11_gk160", "backward_v12_gk192",
+                                         "backward_v13_gk128"};
 
 __device__ __forceinline__ float hrand(unsigned int x) {  // deterministic value in [0, 1)
   x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
@@ -67,6 +73,34 @@ __device__ __forceinline__ void run_stage(const Smem& s, float* row) {
   else if constexpr (STAGE == kBackinV4) stage_conv2_back<EXACT, A, 4>(s, row);
   else if constexpr (STAGE == kBackinV5) stage_conv2_back<EXACT, A, 5>(s, row);
   else if constexpr (STAGE == kC1BackGk2) stage_conv1_back_gk2<EXACT, A>(s, s.img, row);
+  else if constexpr (STAGE == kC2BackV6 || STAGE == kC2BackV7) {
+    if constexpr (!EXACT) stage_conv2_back<false, A, STAGE == kC2BackV6 ? 6 : 7>(s, row);
+  } else if constexpr (STAGE == kBackwardV6 || STAGE == kBackwardV7 || STAGE == kBackwardV8) {
+    if constexpr (!EXACT) {
+      stage_fc_back<EXACT, A>(s, row);
+      __syncthreads();
+      stage_conv2_back<false, A, STAGE == kBackwardV6 ? 6 : STAGE == kBackwardV7 ? 7 : 8>(s, row);
+      __syncthreads();
+      stage_conv1_back<EXACT, A>(s, s.img, row);
+    }
+  } else if constexpr (STAGE == kC2BackV8) {
+    if constexpr (!EXACT) stage_conv2_back<false, A, 8>(s, row);
+  } else if constexpr (STAGE == kBackinV9) {
+    if constexpr (!EXACT) stage_conv2_back<false, A, 9>(s, row);
+  } else if constexpr (STAGE == kC2BackV10) {
+    if constexpr (!EXACT) stage_conv2_back<false, A, 10>(s, row);
+  } else if constexpr (STAGE == kBackwardV9 || STAGE == kBackwardV10 || STAGE == kBackwardV11 ||
+                       STAGE == kBackwardV12 || STAGE == kBackwardV13) {
+    if constexpr (!EXACT) {
+      constexpr int V = STAGE == kBackwardV9 ? 9 : STAGE == kBackwardV10 ? 10 : STAGE == kBackwardV11 ? 11
+                      : STAGE == kBackwardV12 ? 12 : 13;
+      stage_fc_back<EXACT, A>(s, row);
+      __syncthreads();
+      stage_conv2_back<false, A, V>(s, row);
+      __syncthreads();
+      stage_conv1_back_gk2<false, A, gk2_split_lanes(V)>(s, s.img, row);
+    }
+  }
   else if constexpr (STAGE == kBackwardV4 || STAGE == kBackwardV5) {
     stage_fc_back<EXACT, A>(s, row);
     __syncthreads();
@@ -105,6 +139,41 @@ __global__ void __launch_bounds__(kThreads, 1) stage_kernel(float* rows, unsigne
   if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
 }
 
+// One fresh fast run of STAGE (accumulating into G): dump c1 (dz1 after backin) and G.
+template <int STAGE>
+__global__ void __launch_bounds__(kThreads, 1) verify_kernel(float* out) {
+  const Smem s = carve_smem(tlb_smem);
+  smem_setup(s);
+  fill(s);
+  run_stage<false, STAGE>(s, nullptr);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kC1Floats; i += blockDim.x) out[i] = s.c1[i];
+  for (int i = threadIdx.x; i < kPStride; i += blockDim.x) out[kC1Floats + i] = s.G[i];
+}
+
+template <int STAGE>
+std::vector<float> run_verify(float* d_out) {
+  auto k = verify_kernel<STAGE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  k<<<1, kThreads, kSmemBytes>>>(d_out);
+  cudaDeviceSynchronize();
+  std::vector<float> got(kC1Floats + kPStride);
+  cudaMemcpy(got.data(), d_out, got.size() * sizeof(float), cudaMemcpyDeviceToHost);
+  return got;
+}
+
+template <int STAGE, int REF>
+void verify(float* d_out) {
+  const std::vector<float> want = run_verify<REF>(d_out), got = run_verify<STAGE>(d_out);
+  double md = 0, mv = 0;
+  for (size_t i = 0; i < got.size(); ++i) {
+    md = std::max(md, (double)std::fabs(got[i] - want[i]));
+    mv = std::max(mv, (double)std::fabs(want[i]));
+  }
+  printf("{\"verify\": \"%s vs %s\", \"max_abs_diff\": %.3e, \"max_abs\": %.3e, \"err\": \"%s\"}\n", kNames[STAGE],
+         kNames[REF], md, mv, cudaGetErrorString(cudaGetLastError()));
+}
+
 template <bool EXACT, int STAGE>
 void measure(float* rows, unsigned long long* d_cycles, int sms, int iters, double mhz) {
   auto k = stage_kernel<EXACT, STAGE>;
@@ -139,6 +208,21 @@ void all(float* rows, unsigned long long* d_cycles, int sms, int iters, double m
   measure<EXACT, kC1BackGk2>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kBackwardV4>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kBackwardV5>(rows, d_cycles, sms, iters, mhz);
+  if constexpr (!EXACT) {
+    measure<EXACT, kC2BackV6>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kC2BackV7>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kBackwardV6>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kBackwardV7>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kC2BackV8>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kBackwardV8>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kBackinV9>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kBackwardV9>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kC2BackV10>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kBackwardV10>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kBackwardV11>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kBackwardV12>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kBackwardV13>(rows, d_cycles, sms, iters, mhz);
+  }
 }
 
 int main(int argc, char** argv) {
@@ -150,6 +234,18 @@ int main(int argc, char** argv) {
   cudaMalloc(&rows, (size_t)sms * kPStride * sizeof(float));
   cudaMalloc(&d_cycles, sms * sizeof(unsigned long long));
   const double mhz = 1965.0;
+  {  // numerics of the fast variants against V1 (same inputs)
+    float* d_out;
+    cudaMalloc(&d_out, (kC1Floats + kPStride) * sizeof(float));
+    verify<kC2BackV6, kC2BackV1>(d_out);
+    verify<kC2BackV7, kC2BackV1>(d_out);
+    verify<kC2BackV8, kC2BackV1>(d_out);
+    verify<kBackwardV9, kBackwardV1>(d_out);
+    verify<kBackwardV10, kBackwardV1>(d_out);
+    verify<kBackwardV11, kBackwardV1>(d_out);
+    verify<kBackwardV13, kBackwardV1>(d_out);
+    cudaFree(d_out);
+  }
   all<false>(rows, d_cycles, sms, iters, mhz);
   all<true>(rows, d_cycles, sms, iters, mhz);
   return 0;

@@ -31,8 +31,9 @@ struct TrainArgs {
   unsigned long long* trace;  // optional [steps][16] clock64 stamps of CTA 0 (tlb_ctx_set_trace)
   // Overlapped ingestion (tlb_train on host buffers): images arrive in chunks on a copy stream;
   // ready[k] >= ready_token once chunk k is resident.  chunk > 0: chunk k = images [k*chunk, (k+1)*chunk);
-  // chunk == 0: geometric chunks of whole SGD groups -- chunk 0 = group 0, chunk k >= 1 = groups
-  // [2^(k-1), 2^k) -- so a 100-group epoch needs 8 copies, each landing well before it is consumed.
+  // chunk == 0: geometric chunks of whole SGD groups -- groups 0 and 1, then each [2^e, 2^(e+1)) in two
+  // halves (chunk 2e, 2e + 1) -- 14 copies for a 100-group epoch; chunk k lands before group 1.5x its
+  // start is reached whenever H2D >= 1.5 x (group bytes / group time), ~29 GB/s at batch 100.
   // Steps < ready_step_end poll the flag before the image's TMA load; nullptr = every image resident.
   const unsigned int* ready;
   unsigned int ready_token;

@@ -97,9 +97,14 @@ __device__ __forceinline__ void wait_ready(const TrainArgs& a, const Job& j) {
   int64_t k;
   if (a.chunk > 0) {
     k = job_index(a, j) / a.chunk;
-  } else {  // geometric: group g lives in chunk floor(log2 g) + 1 (group 0 in chunk 0)
+  } else {  // geometric (see TrainArgs::chunk): groups 0, 1, then [2^e, 2^e + 2^(e-1)), [.., 2^(e+1))
     const int64_t g = j.step % a.steps_per_epoch;
-    k = g == 0 ? 0 : 64 - __clzll((long long)g);
+    if (g < 2) {
+      k = g;
+    } else {
+      const int e = 63 - __clzll((long long)g);
+      k = 2 * e + (int)((g - (1ll << e)) >= (1ll << (e - 1)));
+    }
   }
   const unsigned int* f = a.ready + k;
   unsigned int v;

@@ -866,6 +866,97 @@ __device__ __forceinline__ void backin_combine(const Smem& s, int it) {
   }
 }
 
+// Fast backin in scatter form, no padded taps.  Lane = (channel c, d_s1 row p, kernel split s): for
+// each of its 12/SPLITS kernels i it holds the 25 weights of k2[i][c] and, for every valid tap row u1
+// (dz2 row y = p - u1 in 0..7), scatters the 8 dz2 values of row y into the 12 row accumulators:
+// acc[x + u2] += k2[i][c][u1][u2] * dz2[i][y][x] -- exactly the 115,200 valid multiply-adds of the
+// reference's clipped sums (nn.cpp:169-189), against 259,200 for the padded 2x4 tiles.  Rows are
+// ordered by their valid-tap count (p = 4..7 first, 0/11 last) so the lanes of a warp take the same
+// trip count.  The SPLITS lanes of a (c, p) combine by xor shuffles; each then finishes 12/SPLITS
+// columns (backavgpool + backsigmoid through c1, nn.cpp:148-158 / 131-133).
+__device__ __forceinline__ int backin_row_of(int k) {  // k-th row by descending valid-tap count
+  constexpr unsigned long long kOrder = 0xB0A192837654ULL;  // nibbles, low first: 4,5,6,7,3,8,2,9,1,10,0,11
+  return (int)((kOrder >> (4 * k)) & 0xF);
+}
+
+// WP: weights read as scalars from the unpadded P (stride 25 per (i, c): distinct banks across the
+// warp's (i, c) pairs) instead of float4s from the padded Kp (stride 40: 8-way bank groups).
+template <int SPLITS, bool WP = false>
+__device__ __forceinline__ void backin_rows(const Smem& s, int t) {
+  constexpr int KPL = 12 / SPLITS;
+  const bool valid = t < 72 * SPLITS;  // padding lanes compute combo 0 for the warp-wide shuffles
+  const int combo = valid ? t / SPLITS : 0, part = t % SPLITS;
+  const int p = backin_row_of(combo / 6), c = combo - (combo / 6) * 6;
+  float acc[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) acc[q] = 0.0f;
+#pragma unroll 1
+  for (int k = 0; k < KPL; ++k) {
+    const int i = part * KPL + k;
+    float w[5][5];
+    if constexpr (WP) {
+      const float* wp = s.P + kK2 + (i * 6 + c) * 25;
+#pragma unroll
+      for (int u1 = 0; u1 < 5; ++u1)
+#pragma unroll
+        for (int u2 = 0; u2 < 5; ++u2) w[u1][u2] = wp[u1 * 5 + u2];
+    } else {
+#pragma unroll
+      for (int u1 = 0; u1 < 5; ++u1) {
+        const float4* wp = reinterpret_cast<const float4*>(s.Kp + ((i * 6 + c) * 5 + u1) * 8);
+        const float4 w0 = wp[0], w1 = wp[1];
+        w[u1][0] = w0.x; w[u1][1] = w0.y; w[u1][2] = w0.z; w[u1][3] = w0.w; w[u1][4] = w1.x;
+      }
+    }
+#pragma unroll
+    for (int u1 = 0; u1 < 5; ++u1) {
+      const int y = p - u1;
+      if (y < 0 || y > 7) continue;
+      const float4* dp = reinterpret_cast<const float4*>(s.dzp + dzp_at(i, y + 4, 4));
+      const float4 d0 = dp[0], d1 = dp[1];
+      const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+#pragma unroll
+        for (int u2 = 0; u2 < 5; ++u2) acc[x + u2] = __fmaf_rn(w[u1][u2], d[x], acc[x + u2]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 12; ++q) {
+#pragma unroll
+    for (int m = 1; m < SPLITS; m <<= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], m);
+  }
+  constexpr int QN = 12 / SPLITS;  // d_s1 columns this lane finishes: q0 .. q0 + QN - 1
+  const int q0 = part * QN;
+  float mine[QN];
+#pragma unroll
+  for (int k = 0; k < QN; ++k) {  // select acc[q0 + k] without dynamic register indexing
+    float v = acc[k];
+#pragma unroll
+    for (int pp = 1; pp < SPLITS; ++pp)
+      if (part == pp) v = acc[pp * QN + k];
+    mine[k] = v;
+  }
+  if (!valid) return;
+#pragma unroll
+  for (int dy = 0; dy < 2; ++dy) {
+    float* cp = s.c1 + c1_at(c, 2 * p + dy, 2 * q0);
+#pragma unroll
+    for (int k = 0; k < QN; ++k) {
+      const float dc = fmul(mine[k], 0.25f);
+      float2 v = *reinterpret_cast<float2*>(cp + 2 * k);
+      v.x = fmul(fmul(dc, v.x), fsub(1.0f, v.x));
+      v.y = fmul(fmul(dc, v.y), fsub(1.0f, v.y));
+      *reinterpret_cast<float2*>(cp + 2 * k) = v;
+    }
+  }
+}
+
+// g_k2 quad lanes done beside the scatter-form backin in conv2_back variants 10..13 (whole warps).
+__host__ __device__ constexpr int gk2_split_lanes(int V) {
+  return V == 10 ? 224 : V == 11 ? 160 : V == 12 ? 192 : V == 13 ? 128 : 0;
+}
+
 // C2 backward stage.  V = 0: backin lane quads on warps 0-13 (432 lanes), then the g_k2/g_b2 lanes;
 // V = 1: one backin lane per item on warps 0-3, concurrent with the g_k2/g_b2 lanes on warps 4+.
 template <bool EXACT, bool ACCUM, int V>
@@ -892,6 +983,32 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
       } else {
         gk2_fast<ACCUM>(s, row, it - kBackin);
       }
+    }
+  } else if constexpr (V == 6 || V == 7 || V == 8) {
+    // V = 6/7/8 (fast only): scatter-form backin rows with 2 / 4 / 4 kernel splits per (c, p) beside
+    // the g_k2/g_b2 lane quads (8: weights from P)
+    static_assert(!EXACT, "scatter-form backin reorders the reference's sums");
+    constexpr int kSplits = V == 6 ? 2 : 4;
+    constexpr int kBackin = (72 * kSplits + 31) / 32 * 32;
+    for (int it = threadIdx.x; it < kBackin + kGk2; it += blockDim.x) {
+      if (it < kBackin) {
+        backin_rows<kSplits, V == 8>(s, it);
+      } else {
+        gk2_fast<ACCUM>(s, row, it - kBackin);
+      }
+    }
+  } else if constexpr (V == 9) {
+    // V = 9 (fast only): scatter-form backin rows (4 splits, weights from P) alone on warps 0-8;
+    // g_k2/g_b2 runs beside the C1 gradient
+    static_assert(!EXACT, "scatter-form backin reorders the reference's sums");
+    for (int it = threadIdx.x; it < 288; it += blockDim.x) backin_rows<4, true>(s, it);
+  } else if constexpr (V >= 10 && V <= 13) {
+    // V = 10..13 (fast only): backin rows on warps 0-8 beside the first gk2_split_lanes(V) g_k2 quad
+    // lanes on warps 9-15; the remaining quads run beside the C1 gradient
+    static_assert(!EXACT, "scatter-form backin reorders the reference's sums");
+    for (int it = threadIdx.x; it < 288 + gk2_split_lanes(V); it += blockDim.x) {  // whole warps per round
+      if (it < 288) backin_rows<4, true>(s, it);
+      else gk2_fast<ACCUM>(s, row, it - 288);
     }
   } else if constexpr (V == 4) {
     // V = 4: backin only, one lane per item on warps 0-3 (g_k2 runs later, beside the C1 gradient)
@@ -1157,7 +1274,7 @@ __device__ __forceinline__ void conv1_back_fast_group(const Smem& s, const float
   }
 }
 
-template <bool EXACT, bool ACCUM>
+template <bool EXACT, bool ACCUM, int GLO = 0>
 __device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float* img, float* row) {
   constexpr int kGk2 = EXACT ? 372 : 288;
   const int t = threadIdx.x;
@@ -1168,7 +1285,7 @@ __device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float*
       conv1_back_fast_group<ACCUM>(s, img, row);
     }
   } else {
-    for (int item = t - 160; item < kGk2; item += blockDim.x - 160) {
+    for (int item = GLO + t - 160; item < kGk2; item += blockDim.x - 160) {
       if constexpr (EXACT) gk2_exact<ACCUM>(s, row, item);
       else gk2_fast<ACCUM>(s, row, item);
     }
@@ -1177,14 +1294,15 @@ __device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float*
 
 // Stage variants used by the product kernels (chosen with paper_1912_05234_b200/csrc/stage_bench.cu).
 #ifndef TLB_CONV2_BACK_V
-#define TLB_CONV2_BACK_V(EXACT) 1
+#define TLB_CONV2_BACK_V(EXACT) ((EXACT) ? 1 : 12)
 #endif
 template <bool EXACT>
 struct StageCfg {
   static constexpr int conv2 = EXACT ? 0 : 1;
   static constexpr int conv2_back = TLB_CONV2_BACK_V(EXACT);
   // backin-only conv2_back variants move g_k2/g_b2 into the C1-gradient phase
-  static constexpr bool gk2_with_c1 = conv2_back == 4 || conv2_back == 5;
+  static constexpr bool gk2_with_c1 = conv2_back == 4 || conv2_back == 5 || conv2_back >= 9;
+  static constexpr int gk2_lo = gk2_split_lanes(conv2_back);  // g_k2 lanes already done in conv2_back
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -1208,7 +1326,8 @@ __device__ __noinline__ void call_conv2_back(float* row) {
 }
 template <bool EXACT, bool ACCUM>
 __device__ __noinline__ void call_conv1_back(const float* img, float* row) {
-  if constexpr (StageCfg<EXACT>::gk2_with_c1) stage_conv1_back_gk2<EXACT, ACCUM>(smem_view(), img, row);
+  if constexpr (StageCfg<EXACT>::gk2_with_c1)
+    stage_conv1_back_gk2<EXACT, ACCUM, StageCfg<EXACT>::gk2_lo>(smem_view(), img, row);
   else stage_conv1_back<EXACT, ACCUM>(smem_view(), img, row);
 }
 
