@@ -124,8 +124,13 @@ __device__ __forceinline__ void wait_ready(const TrainArgs& a, const Job& j) {
   asm volatile("fence.proxy.async.global;" ::: "memory");  // the TMA read below follows the flag
 }
 
+// Thread 0: start the job's image TMA into buffer `buf` and an async copy of its label into s.lab[buf]
+// -- the label's L2 latency overlaps the previous image's stages instead of preceding the forward pass.
+// Thread 0 completes the copy (cp_async_wait_all) when the job starts, before issuing the next one;
+// the forward pass reads s.lab[buf] only after its first CTA barrier (forward_image's `lab`).
 __device__ __forceinline__ void issue_job(const Smem& s, const TrainArgs& a, int buf, const Job& j) {
   wait_ready(a, j);
+  cp_async4(s.lab + buf, a.labels + job_index(a, j));
   issue_image(s, buf, job_image(a, j));
 }
 
@@ -261,6 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
     for (int64_t e = lo; e < hi; ++e) {
       const int buf = consumed & 1;
       mbar_wait(&s.bar[buf], (consumed >> 1) & 1);
+      if (threadIdx.x == 0) cp_async_wait_all();  // this job's label (published by conv1's barrier)
       mark(s, 2);
       if (pf_valid) {
         Job nx = pf;
@@ -271,10 +277,9 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
           pf_valid = false;
         }
       }
-      const int label = __ldg(a.labels + start + e);
-      forward_image<EXACT>(s, s.img + buf * kImg, label, nullptr, true);
+      forward_image<EXACT>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf);
       if (threadIdx.x == 0) {
-        const float l = example_loss(s, label, nullptr);
+        const float l = example_loss(s, s.lab[buf], nullptr);
         if constexpr (EXACT) a.losses[e] = l;
         else cta_loss = __dadd_rn(cta_loss, (double)l);
       }
@@ -392,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     for (int64_t e = lo; e < hi; ++e) {
       const int buf = consumed & 1;
       mbar_wait(&s.bar[buf], (consumed >> 1) & 1);
+      if (threadIdx.x == 0) cp_async_wait_all();  // this job's label (published by conv1's barrier)
       mark(s, 2);
       if (pf_valid) {
         Job nx = pf;
@@ -402,9 +408,8 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
           pf_valid = false;
         }
       }
-      const int label = __ldg(a.labels + start + e);
-      forward_image<false>(s, s.img + buf * kImg, label, nullptr, true);
-      if (threadIdx.x == 0) cta_loss = __dadd_rn(cta_loss, (double)example_loss(s, label, nullptr));
+      forward_image<false>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf);
+      if (threadIdx.x == 0) cta_loss = __dadd_rn(cta_loss, (double)example_loss(s, s.lab[buf], nullptr));
       backward_image<false, true>(s, s.img + buf * kImg, nullptr);
       ++consumed;
     }

@@ -46,6 +46,7 @@ struct Smem {
   float* red;  // fast C1 weight-gradient row partials [144][26]
   float* G;    // fast per-CTA gradient accumulator [3904]
   float* term; // backin per-kernel terms b_i(c, p, q): [12][6][12][12]
+  int* lab;    // labels of the two image buffers (train kernels; aliases out[12..13], unused by the FC)
   uint64_t* tab;
   uint64_t* bar;
   unsigned long long* tr;  // optional per-stage clock64 trace (CTA 0 only), nullptr otherwise
@@ -109,7 +110,9 @@ __device__ __forceinline__ Smem carve_smem(float* base) {
   s.s1 = p; p += 864;
   s.c2 = p; p += 768;
   s.s2 = p; p += 192;
-  s.out = p; p += 16;
+  s.out = p;
+  s.lab = reinterpret_cast<int*>(p + 12);
+  p += 16;
   s.dz = p; p += 16;
   s.dzp = p; p += kDzp;
   s.tab = reinterpret_cast<uint64_t*>(p);
@@ -1331,12 +1334,15 @@ __device__ __noinline__ void call_conv1_back(const float* img, float* row) {
   else stage_conv1_back<EXACT, ACCUM>(smem_view(), img, row);
 }
 
-// Whole forward pass of one image (image already in shared memory).
+// Whole forward pass of one image (image already in shared memory).  `lab` (train kernels): the label
+// sits in shared memory, written by an async copy that thread 0 completed before conv1; it is read only
+// after conv1's barrier.
 template <bool EXACT>
 __device__ __forceinline__ void forward_image(const Smem& s, const float* img, int label, const float* y,
-                                              bool want_dz) {
+                                              bool want_dz, const int* lab = nullptr) {
   call_conv1<EXACT>(img);
   __syncthreads();
+  if (lab) label = *lab;
   mark(s, 3);
   call_conv2<EXACT>();  // includes avgpool
   __syncthreads();

@@ -1,0 +1,51 @@
+"""Overlapped-ingestion check shared by tests/test_gpu_parity.py (in process, default chunk policy) and
+run as ``python tests/_ingest_check.py`` under other TLB_INGEST_CHUNK policies: tlb_train on host
+buffers (pageable and pinned) must equal tlb_train_device on resident data, bit for bit."""
+import numpy as np
+
+CASES = ((1, 100), (83, 7), (200, 100), (5000, 100), (300, 100), (1001, 77), (2, 1), (3, 1), (4, 1), (5, 1),
+         (129, 1), (800, 100), (801, 100), (10000, 100))
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def check(orc, tr_x, tr_y, mode):
+    import torch
+    from paper_1912_05234_b200 import Context
+    p0 = orc.init_params(42)
+    dev = torch.device("cuda:0")
+    with Context(0, mode=mode) as c:
+        c.set_stream(torch.cuda.current_stream().cuda_stream)
+        for i, (n, batch) in enumerate(CASES):
+            xs, ys = tr_x[:n], tr_y[:n]
+            if i % 2:  # pinned source: the kernel is enqueued before the chunk copies
+                xs = torch.from_numpy(np.ascontiguousarray(xs)).pin_memory().numpy()
+                ys = torch.from_numpy(np.ascontiguousarray(ys)).pin_memory().numpy()
+            got_p, got_l = c.train(p0, xs, ys, epochs=2, batch=batch)
+            d_x = torch.from_numpy(tr_x[:n]).to(dev)
+            d_y = torch.from_numpy(tr_y[:n]).to(dev)
+            d_p = torch.zeros(3904, device=dev)
+            d_p[:3898] = torch.from_numpy(p0).to(dev)
+            d_l = torch.zeros(2, dtype=torch.float64, device=dev)
+            c.train_device(d_x.data_ptr(), d_y.data_ptr(), n, d_p.data_ptr(), 0.05, 0, 2, batch, d_l.data_ptr())
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(got_p), bits(d_p.cpu().numpy()[:3898])), (mode, n, batch)
+            assert list(got_l) == d_l.cpu().numpy().tolist(), (mode, n, batch)
+
+
+def main():
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import Oracle
+    orc = Oracle()
+    tr_x, tr_y = orc.make_set(10000, 1)
+    for mode in ("exact", "fast"):
+        check(orc, tr_x, tr_y, mode)
+    print("ingestion ok")
+
+
+if __name__ == "__main__":
+    main()

@@ -368,31 +368,24 @@ def test_dp_shards_sum_to_the_full_group(orc, small):
 
 @pytest.mark.parametrize("mode", ["exact", "fast"])
 def test_overlapped_ingestion_equals_resident_data(orc, zhang_sets, mode):
-    """tlb_train streams the dataset in geometric chunks of SGD groups (group 0, then [2^(k-1), 2^k)) on
-    a copy stream while the kernel trains (device ready flags): for group counts on and around the chunk
-    boundaries, pageable and pinned sources, and repeated calls with growing and shrinking sizes, the
-    result equals training on device-resident data."""
-    import torch
-    from paper_1912_05234_b200 import Context
+    """tlb_train streams the dataset in chunks of whole SGD groups (>= 512 KiB) on a copy stream while the
+    kernel trains (device ready flags): for group counts on and around the chunk boundaries, pageable and
+    pinned sources, and repeated calls with growing and shrinking sizes, the result equals training on
+    device-resident data (tests/_ingest_check.py)."""
+    from _ingest_check import check  # tests/ is on sys.path (pytest rootdir insertion)
     (tr_x, tr_y), _ = zhang_sets
-    p0 = orc.init_params(42)
-    dev = torch.device("cuda:0")
-    with Context(0, mode=mode) as c:
-        c.set_stream(torch.cuda.current_stream().cuda_stream)
-        cases = ((1, 100), (83, 7), (200, 100), (5000, 100), (300, 100), (1001, 77), (2, 1), (3, 1), (4, 1),
-                 (5, 1), (129, 1), (800, 100), (801, 100), (10000, 100))
-        for i, (n, batch) in enumerate(cases):
-            xs, ys = tr_x[:n], tr_y[:n]
-            if i % 2:  # pinned source: the kernel is enqueued before the chunk copies
-                xs = torch.from_numpy(np.ascontiguousarray(xs)).pin_memory().numpy()
-                ys = torch.from_numpy(np.ascontiguousarray(ys)).pin_memory().numpy()
-            got_p, got_l = c.train(p0, xs, ys, epochs=2, batch=batch)
-            d_x = torch.from_numpy(tr_x[:n]).to(dev)
-            d_y = torch.from_numpy(tr_y[:n]).to(dev)
-            d_p = torch.zeros(3904, device=dev)
-            d_p[:3898] = torch.from_numpy(p0).to(dev)
-            d_l = torch.zeros(2, dtype=torch.float64, device=dev)
-            c.train_device(d_x.data_ptr(), d_y.data_ptr(), n, d_p.data_ptr(), 0.05, 0, 2, batch, d_l.data_ptr())
-            torch.cuda.synchronize()
-            assert np.array_equal(bits(got_p), bits(d_p.cpu().numpy()[:3898])), n
-            assert list(got_l) == d_l.cpu().numpy().tolist(), n
+    check(orc, tr_x, tr_y, mode)
+
+
+@pytest.mark.parametrize("policy", ["0", "37", "100"])
+def test_overlapped_ingestion_chunk_policies(policy):
+    """The same check under the other chunk policies (TLB_INGEST_CHUNK: 0 = geometric group chunks,
+    N = fixed chunks of N images, not group-aligned), both modes, in a fresh process."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TLB_INGEST_CHUNK=policy)
+    out = subprocess.run([sys.executable, os.path.join(root, "tests", "_ingest_check.py")], cwd=root, env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "ingestion ok" in out.stdout
