@@ -85,10 +85,21 @@ __constant__ uint64_t kExpTab[32] = {
 };
 __device__ __forceinline__ uint64_t exp_tab_entry(int i) { return kExpTab[i]; }
 
+// ---- non-negative 64-bit quotient / remainder with a 32-bit fast path ------------------------------
+// The persistent kernels recompute step/example indices per job on every thread; the 64-bit integer
+// division is a ~100-instruction software routine, the 32-bit one a few instructions.
+__host__ __device__ __forceinline__ int64_t udiv(int64_t a, int64_t b) {
+#ifdef __CUDA_ARCH__
+  if ((((uint64_t)a | (uint64_t)b) >> 32) == 0) return (int64_t)((uint32_t)a / (uint32_t)b);
+#endif
+  return a / b;
+}
+__host__ __device__ __forceinline__ int64_t umod(int64_t a, int64_t b) { return a - udiv(a, b) * b; }
+
 // ---- static_chunk (runtime.cpp:138-145): ceil-block split of [0,n) over `workers` -------------
 __host__ __device__ __forceinline__ void static_chunk(int64_t n, int workers, int w, int64_t& lo,
                                                       int64_t& hi) {
-  const int64_t block = (n + workers - 1) / workers;
+  const int64_t block = udiv(n + workers - 1, workers);
   lo = (int64_t)w * block;
   if (lo > n) lo = n;
   hi = lo + block;

@@ -31,7 +31,7 @@ struct Job {
 };
 
 __device__ __forceinline__ int64_t group_size(const TrainArgs& a, int64_t st) {
-  const int64_t start = (st % a.steps_per_epoch) * a.batch;
+  const int64_t start = umod(st, a.steps_per_epoch) * a.batch;
   const int64_t rem = a.n - start;
   return rem < a.batch ? rem : a.batch;
 }
@@ -83,7 +83,7 @@ __device__ __forceinline__ bool next_job(const TrainArgs& a, Job& j) {
 }
 
 __device__ __forceinline__ int64_t job_index(const TrainArgs& a, const Job& j) {
-  return (j.step % a.steps_per_epoch) * a.batch + local_offset(a, j.step) + j.e;
+  return umod(j.step, a.steps_per_epoch) * a.batch + local_offset(a, j.step) + j.e;
 }
 
 __device__ __forceinline__ const float* job_image(const TrainArgs& a, const Job& j) {
@@ -96,9 +96,9 @@ __device__ __forceinline__ void wait_ready(const TrainArgs& a, const Job& j) {
   if (!a.ready || j.step >= a.ready_step_end) return;
   int64_t k;
   if (a.chunk > 0) {
-    k = job_index(a, j) / a.chunk;
+    k = udiv(job_index(a, j), a.chunk);
   } else {  // geometric (see TrainArgs::chunk): groups 0, 1, then [2^e, 2^e + 2^(e-1)), [.., 2^(e+1))
-    const int64_t g = j.step % a.steps_per_epoch;
+    const int64_t g = umod(j.step, a.steps_per_epoch);
     if (g < 2) {
       k = g;
     } else {
@@ -124,9 +124,9 @@ __device__ __forceinline__ void wait_ready(const TrainArgs& a, const Job& j) {
   asm volatile("fence.proxy.async.global;" ::: "memory");  // the TMA read below follows the flag
 }
 
-// Thread 0: start the job's image TMA into buffer `buf` and an async copy of its label into s.lab[buf]
+// Issuer thread: start the job's image TMA into buffer `buf` and an async copy of its label into s.lab[buf]
 // -- the label's L2 latency overlaps the previous image's stages instead of preceding the forward pass.
-// Thread 0 completes the copy (cp_async_wait_all) when the job starts, before issuing the next one;
+// The issuer completes the copy (cp_async_wait_all) when the job starts, before issuing the next one;
 // the forward pass reads s.lab[buf] only after its first CTA barrier (forward_image's `lab`).
 __device__ __forceinline__ void issue_job(const Smem& s, const TrainArgs& a, int buf, const Job& j) {
   wait_ready(a, j);
@@ -245,11 +245,14 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
 
   Job pf;
   bool pf_valid = first_job(a, a.step_begin, pf);
-  if (threadIdx.x == 0 && pf_valid) issue_job(s, a, 0, pf);
+  // The prefetch issuer is lane 0 of the last warp: conv1 leaves that warp idle (448 item lanes), so
+  // the next job's index math, label copy and TMA issue stay off the first stage's critical path.
+  const bool issuer = threadIdx.x == blockDim.x - 32;
+  if (issuer && pf_valid) issue_job(s, a, 0, pf);
   uint32_t consumed = 0;
 
   for (int64_t st = a.step_begin; st < a.step_end; ++st) {
-    const int64_t ks = st % a.steps_per_epoch, start = ks * a.batch + local_offset(a, st);
+    const int64_t ks = umod(st, a.steps_per_epoch), start = ks * a.batch + local_offset(a, st);
     const int64_t m = local_size(a, st);
     int64_t lo, hi;
     static_chunk(m, G, blockIdx.x, lo, hi);
@@ -266,15 +269,17 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
     for (int64_t e = lo; e < hi; ++e) {
       const int buf = consumed & 1;
       mbar_wait(&s.bar[buf], (consumed >> 1) & 1);
-      if (threadIdx.x == 0) cp_async_wait_all();  // this job's label (published by conv1's barrier)
       mark(s, 2);
-      if (pf_valid) {
-        Job nx = pf;
-        if (next_job(a, nx)) {
-          if (threadIdx.x == 0) issue_job(s, a, buf ^ 1, nx);
-          pf = nx;
-        } else {
-          pf_valid = false;
+      if (issuer) {
+        cp_async_wait_all();  // this job's label (published by conv1's barrier)
+        if (pf_valid) {
+          Job nx = pf;
+          if (next_job(a, nx)) {
+            issue_job(s, a, buf ^ 1, nx);
+            pf = nx;
+          } else {
+            pf_valid = false;
+          }
         }
       }
       forward_image<EXACT>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf);
@@ -303,11 +308,11 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
     // (the activation buffers are free now) so the ordered sums run out of SMEM, not L2.
     int64_t nrows = m;  // EXACT: one row per example (reference order); fast: CTA partials in CTA order
     if constexpr (!EXACT) {
-      const int64_t block = (m + G - 1) / G;
-      nrows = m > 0 ? (m + block - 1) / block : 0;
+      const int64_t block = udiv(m + G - 1, G);
+      nrows = m > 0 ? udiv(m + block - 1, block) : 0;
     }
     reduce_slice<EXACT>(s, a, nrows, m);
-    if (blockIdx.x == G - 1) reduce_loss<EXACT>(s, a, m, nrows, ks, st / a.steps_per_epoch);
+    if (blockIdx.x == G - 1) reduce_loss<EXACT>(s, a, m, nrows, ks, udiv(st, a.steps_per_epoch));
     __syncthreads();
     mark(s, 12);
     grid_sync(a.barrier, target);
@@ -377,14 +382,17 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
 
   Job pf;
   bool pf_valid = first_job(a, a.step_begin, pf);
-  if (threadIdx.x == 0 && pf_valid) issue_job(s, a, 0, pf);
+  // The prefetch issuer is lane 0 of the last warp: conv1 leaves that warp idle (448 item lanes), so
+  // the next job's index math, label copy and TMA issue stay off the first stage's critical path.
+  const bool issuer = threadIdx.x == blockDim.x - 32;
+  if (issuer && pf_valid) issue_job(s, a, 0, pf);
   uint32_t consumed = 0;
   load_params(s, a.params);  // once: afterwards the parameters live in shared memory
 
   for (int64_t st = a.step_begin; st < a.step_end; ++st) {
     const int64_t ls = st - a.step_begin;  // local step
     const uint64_t seq = a.seq_base + (uint64_t)ls;  // steps on these accumulators: buffer seq % 3
-    const int64_t ks = st % a.steps_per_epoch, start = ks * a.batch + local_offset(a, st);
+    const int64_t ks = umod(st, a.steps_per_epoch), start = ks * a.batch + local_offset(a, st);
     const int64_t m = local_size(a, st), m_global = group_size(a, st);
     int64_t lo, hi;
     static_chunk(m, G, blockIdx.x, lo, hi);
@@ -397,15 +405,17 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     for (int64_t e = lo; e < hi; ++e) {
       const int buf = consumed & 1;
       mbar_wait(&s.bar[buf], (consumed >> 1) & 1);
-      if (threadIdx.x == 0) cp_async_wait_all();  // this job's label (published by conv1's barrier)
       mark(s, 2);
-      if (pf_valid) {
-        Job nx = pf;
-        if (next_job(a, nx)) {
-          if (threadIdx.x == 0) issue_job(s, a, buf ^ 1, nx);
-          pf = nx;
-        } else {
-          pf_valid = false;
+      if (issuer) {
+        cp_async_wait_all();  // this job's label (published by conv1's barrier)
+        if (pf_valid) {
+          Job nx = pf;
+          if (next_job(a, nx)) {
+            issue_job(s, a, buf ^ 1, nx);
+            pf = nx;
+          } else {
+            pf_valid = false;
+          }
         }
       }
       forward_image<false>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf);
@@ -483,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       if (a.grad_out) {
         a.loss_out[0] = l;
       } else {
-        const int64_t ep = st / a.steps_per_epoch;
+        const int64_t ep = udiv(st, a.steps_per_epoch);
         const double run = (ks != 0 ? a.epoch_loss[ep] : 0.0) + l;
         a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(run, (double)a.n) : run;
       }
