@@ -17,7 +17,7 @@ using namespace tlb;
 
 enum Stage { kConv1, kConv2V0, kConv2V1, kFc, kFcBack, kC2BackV0, kC2BackV1, kC2BackV2, kC2BackV3, kC1Back, kForward,
              kBackwardV0, kBackwardV1, kBackinV4, kBackinV5, kC1BackGk2, kBackwardV4, kBackwardV5, kC2BackV6, kC2BackV7, kBackwardV6, kBackwardV7, kC2BackV8, kBackwardV8,
-             kBackinV9, kBackwardV9, kC2BackV10, kBackwardV10, kBackwardV11, kBackwardV12, kBackwardV13, kNumStages };
+             kBackinV9, kBackwardV9, kC2BackV10, kBackwardV10, kBackwardV11, kBackwardV12, kBackwardV13, kConv2V2, kNumStages };
 static const char* kNames[kNumStages] = {"conv1", "conv2_v0_halves", "conv2_v1_rows", "fc", "fc_back",
                                          "conv2_back_v0_quads", "conv2_back_v1_items", "conv2_back_v2_pairs", "conv2_back_v3_ws", "conv1_back",
                                          "forward_image", "backward_v0", "backward_v1",
@@ -26,7 +26,7 @@ static const char* kNames[kNumStages] = {"conv1", "conv2_v0_halves", "conv2_v1_r
                                          "backward_v6", "backward_v7", "conv2_back_v8_rows4p", "backward_v8",
                                          "backin_only_v9_rows4p", "backward_v9", "conv2_back_v10_split_gk2",
                                          "backward_v10", "backward_v11_gk160", "backward_v12_gk192",
-                                         "backward_v13_gk128"};
+                                         "backward_v13_gk128", "conv2_v2_rows_p"};
 
 __device__ __forceinline__ float hrand(unsigned int x) {  // deterministic value in [0, 1)
   x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
@@ -62,6 +62,7 @@ __device__ __forceinline__ void run_stage(const Smem& s, float* row) {
   if constexpr (STAGE == kConv1) stage_conv1<EXACT>(s, s.img);
   else if constexpr (STAGE == kConv2V0) stage_conv2<EXACT, 0>(s);
   else if constexpr (STAGE == kConv2V1) stage_conv2<EXACT, 1>(s);
+  else if constexpr (STAGE == kConv2V2) stage_conv2<EXACT, 2>(s);
   else if constexpr (STAGE == kFc) stage_fc<EXACT>(s, 3, nullptr, true);
   else if constexpr (STAGE == kFcBack) stage_fc_back<EXACT, A>(s, row);
   else if constexpr (STAGE == kC2BackV0) stage_conv2_back<EXACT, A, 0>(s, row);
@@ -193,6 +194,7 @@ void all(float* rows, unsigned long long* d_cycles, int sms, int iters, double m
   measure<EXACT, kConv1>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kConv2V0>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kConv2V1>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kConv2V2>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kFc>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kFcBack>(rows, d_cycles, sms, iters, mhz);
   measure<EXACT, kC2BackV0>(rows, d_cycles, sms, iters, mhz);

@@ -65,11 +65,18 @@ __device__ __forceinline__ float sigmoid_ref(float x, const uint64_t* tab) {
   return __frcp_rn(__fadd_rn(1.0f, glibc_expf(-x, tab)));
 }
 
-// Mode-dependent logistic: EXACT = the reference's bits; fast = ex2.approx-based exp (a few ulp).
+// Mode-dependent logistic: EXACT = the reference's bits; fast = ex2.approx-based exp and the MUFU
+// reciprocal (rcp.approx, ~1 ulp; 1 + e^-x >= 1, so no subnormal input, and inputs above 2^126 flush
+// the result to +0 as the logistic should) -- two MUFU ops instead of the IEEE reciprocal sequence.
+__device__ __forceinline__ float rcp_approx(float y) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(y));
+  return r;
+}
 template <bool EXACT>
 __device__ __forceinline__ float sigmoid_m(float x, const uint64_t* tab) {
   if constexpr (EXACT) return sigmoid_ref(x, tab);
-  else return __frcp_rn(1.0f + __expf(-x));
+  else return rcp_approx(1.0f + __expf(-x));
 }
 
 // glibc's __exp2f_data.tab (N = 32): asuint64(2^(i/32)) - (i << 47); copied to shared memory.

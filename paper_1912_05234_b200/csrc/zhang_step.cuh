@@ -254,7 +254,8 @@ __device__ __forceinline__ void stage_conv1(const Smem& s, const float* img) {
 // Per output the 150 taps run (c, ky, kx) row-major (nn.cpp:14-33).  Fast mode splits the channel
 // sum over a lane pair (c < 3, c >= 3) and combines with a shuffle; EXACT keeps one ordered chain.
 // The two rows of each pooling window are neighbouring lane groups and meet through a shuffle.
-template <bool EXACT>
+// WP: weights read as scalars from P instead of the padded Kp copy (the clustered kernel keeps no Kp).
+template <bool EXACT, bool WP = false>
 __device__ __forceinline__ void stage_conv2_rows(const Smem& s) {
   constexpr int kSplit = EXACT ? 1 : 2;
   const int it = threadIdx.x;
@@ -272,9 +273,16 @@ __device__ __forceinline__ void stage_conv2_rows(const Smem& s) {
       const float4* src = reinterpret_cast<const float4*>(s.s1 + (c * 12 + y + ky) * 12);
       const float4 v0 = src[0], v1 = src[1], v2 = src[2];
       const float in[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
-      const float4* wp = reinterpret_cast<const float4*>(s.Kp + ((i * 6 + c) * 5 + ky) * 8);
-      const float4 w0 = wp[0], w1 = wp[1];
-      const float w[5] = {w0.x, w0.y, w0.z, w0.w, w1.x};
+      float w[5];
+      if constexpr (WP) {
+        const float* wp = s.P + kK2 + ((i * 6 + c) * 5 + ky) * 5;
+#pragma unroll
+        for (int kx = 0; kx < 5; ++kx) w[kx] = wp[kx];
+      } else {
+        const float4* wp = reinterpret_cast<const float4*>(s.Kp + ((i * 6 + c) * 5 + ky) * 8);
+        const float4 w0 = wp[0], w1 = wp[1];
+        w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w; w[4] = w1.x;
+      }
 #pragma unroll
       for (int kx = 0; kx < 5; ++kx)
 #pragma unroll
@@ -353,6 +361,7 @@ __device__ __forceinline__ void stage_conv2_halves(const Smem& s) {
 template <bool EXACT, int V>
 __device__ __forceinline__ void stage_conv2(const Smem& s) {
   if constexpr (V == 0) stage_conv2_halves<EXACT>(s);
+  else if constexpr (V == 2) stage_conv2_rows<EXACT, true>(s);
   else stage_conv2_rows<EXACT>(s);
 }
 
