@@ -324,15 +324,16 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
 // train_cluster_kernel: the fast-mode persistent train kernel for groups that fit one image per CTA
 // (batch <= grid).  CTAs form clusters of 8 (distributed shared memory); per step:
 //   1. each CTA runs forward+backward of its image, accumulating the gradient in its shared G;
-//   2. CTA q pushes slice r (488 floats) of its G into the receive buffer of owner CTA r (DSMEM
-//      stores); cluster barrier; owner r sums the 8 received slices in rank order;
+//   2. CTA q pushes slice r (488 floats) of its G into the receive buffer of owner CTA r (st.async
+//      DSMEM stores completing on r's mbarrier); owner r waits for them and sums the 8 slices in rank order;
 //   3. owner r adds its cluster partial into ONE global accumulator as 2^-40 fixed point
 //      (red.global.add.u64: integer addition is associative, so the sum is the same whatever order
 //      the clusters arrive in -- deterministic run to run), then bumps the slice-r arrival counter;
 //   4. owner r of every cluster waits until all clusters have arrived on slice r (no grid-wide
 //      barrier: only the 8-way slice counter), reads the slice total and applies sgd_step
 //      (network.cpp:171-180) to its copy of slice r;
-//   5. owner r pushes its updated slice into every CTA of its cluster (DSMEM); cluster barrier.
+//   5. owner r pushes its updated slice into every CTA of its cluster (st.async on their mbarriers);
+//      each CTA waits for the 7 foreign slices.
 // The parameters never round-trip through L2 between steps.  Accumulators are triple-buffered by
 // step; buffer (s+1) % 3 is zeroed by cluster 0 during step s before it signals step s (every CTA
 // that adds into it in step s+1 has observed that signal).  Not the reference's example-order chain:
@@ -364,9 +365,19 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
   static_assert(StageCfg<false>::conv2_back != 3, "the DSMEM receive buffer reuses the backin term buffer");
   Smem s = carve_smem(tlb_smem);
   float* const rx = s.term;   // [8 source ranks][488]: slices pushed to this CTA (it owns slice `rank`)
-  __shared__ double loss_rx[kCluster];  // rank 0: the 8 CTAs' fp64 loss sums of the step (pushed)
+  __shared__ double loss_rx[kCluster + 1];  // rank 0: the 8 CTAs' fp64 loss sums of the step (pushed);
+                                             // [kCluster]: this CTA's DP-timeout flag
+  // xbar[0]: the step's gradient slices (and, on rank 0, losses) have landed in rx / loss_rx;
+  // xbar[1]: the other owners' updated parameter slices have landed in P.  Peers write with st.async
+  // (complete_tx on these barriers), so no cluster-wide release/acquire barrier sits in the step.
+  __shared__ __align__(8) uint64_t xbar[2];
   smem_setup(s);
-  cluster_sync_all();  // every CTA of the cluster is running before any peer stores into its shared memory
+  if (threadIdx.x == 0) {
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+    fence_barrier_init();
+  }
+  cluster_sync_all();  // every CTA of the cluster is running (barriers initialised) before peers store into it
   const uint32_t rank = cluster_rank(), cid = cluster_id(), ncl = cluster_count();
   const int G = gridDim.x;
   // This CTA owns gradient slice `rank`: its accumulator and arrival counter (local, or on the peer
@@ -377,7 +388,6 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
   unsigned long long* const lacc = a.loss_acc;        // [3]
   unsigned int* const cnt = a.slice_cnt[rank];
   const bool owner = !dp || (int)(rank % (uint32_t)world) == a.dp_rank;  // zeroes its slice's next buffer
-  __shared__ int timed_out;
   unsigned long long* const trace = blockIdx.x == 0 ? a.trace : nullptr;
 
   Job pf;
@@ -424,13 +434,22 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       ++consumed;
     }
     // ---- 2. push slice q of G to its owner q; owner sums the 8 received slices (rank order) ----
-    if (threadIdx.x == 0) dsmem_st_f64(dsmem_map(&loss_rx[rank], 0), cta_loss);
+    const uint32_t parity = (uint32_t)(ls & 1);
+    if (threadIdx.x == 0) st_async_f64(dsmem_map(&loss_rx[rank], 0), cta_loss, dsmem_map(&xbar[0], 0));
     for (int i = threadIdx.x; i < kCluster * kSlice4; i += blockDim.x) {
       const int q = i / kSlice4, o = 4 * (i - q * kSlice4);
-      dsmem_st4(dsmem_map(rx + (int)rank * kSlice + o, q), *reinterpret_cast<const float4*>(s.G + q * kSlice + o));
+      st_async_v4(dsmem_map(rx + (int)rank * kSlice + o, q), *reinterpret_cast<const float4*>(s.G + q * kSlice + o),
+                  dsmem_map(&xbar[0], q));
     }
     mark(s, 9);
-    cluster_sync_all();  // every pushed slice has landed
+    if (threadIdx.x == 0)
+      mbar_arrive_expect_tx(&xbar[0], kCluster * kSlice * sizeof(float) + (rank == 0 ? kCluster * sizeof(double) : 0));
+    if (!dp) {
+      mbar_wait_cluster(&xbar[0], parity);  // every slice pushed to this owner has landed
+    } else if (__syncthreads_or(!mbar_wait_cluster_for(&xbar[0], parity, a.dp_timeout_cycles))) {
+      if (threadIdx.x == 0) atomicExch(a.dp_error, 1u);  // a cluster peer gave up (dead peer GPU)
+      return;
+    }
     mark(s, 10);
     const int b = (int)(seq % 3), bn = (int)((seq + 1) % 3);
     const int j = (int)rank * kSlice + (int)threadIdx.x;  // this thread's parameter (threads < 488)
@@ -450,14 +469,12 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     __syncthreads();
     mark(s, 14);
     // ---- 3/4. arrival on slice `rank`, then wait for every cluster's (and every GPU's) contribution ----
+    // Thread 0 arrives and polls (per-thread polling floods the counters' L2 lines: +0.6 us).  Release
+    // at gpu/sys scope is cumulative over the CTA's adds, which the barrier above orders before it.
     if (threadIdx.x == 0) {
-      timed_out = 0;
-      if (dp) {  // release at system scope is cumulative over the CTA's adds (ordered by the barrier)
-        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
-      } else {
-        __threadfence();
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
-      }
+      int t_out = 0;
+      if (dp) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+      else asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
       const unsigned int want = (unsigned int)((seq + 1) * ncl * (uint64_t)world);
       unsigned int v;
       const long long t0 = clock64();
@@ -467,14 +484,16 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
         if ((int)(v - want) >= 0) break;
         if (dp && clock64() - t0 > a.dp_timeout_cycles) {  // a peer never arrived: fail, do not hang
           atomicExch(a.dp_error, 1u);
-          timed_out = 1;
+          t_out = 1;
           break;
         }
         __nanosleep(32);
       }
+      loss_rx[kCluster] = t_out;  // (slot past the losses) broadcast through the barrier below
     }
     __syncthreads();
-    if (timed_out) return;
+    const int to = (int)loss_rx[kCluster];
+    if (to) return;
     mark(s, 11);
     if (threadIdx.x < kSlice) {
       const long long t = (long long)(dp ? ld_sys_u64(acc + b * kPStride + j) : __ldcg(acc + b * kPStride + j));
@@ -504,9 +523,15 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     for (int i = threadIdx.x; i < (kCluster - 1) * kSlice4; i += blockDim.x) {
       const int qi = i / kSlice4, q = qi < (int)rank ? qi : qi + 1;
       const int o = (int)rank * kSlice + 4 * (i - qi * kSlice4);
-      dsmem_st4(dsmem_map(s.P + o, q), *reinterpret_cast<const float4*>(s.P + o));
+      st_async_v4(dsmem_map(s.P + o, q), *reinterpret_cast<const float4*>(s.P + o), dsmem_map(&xbar[1], q));
     }
-    cluster_sync_all();  // every owner's slice has landed everywhere
+    if (threadIdx.x == 0) mbar_arrive_expect_tx(&xbar[1], (kCluster - 1) * kSlice * sizeof(float));
+    if (!dp) {
+      mbar_wait_cluster(&xbar[1], parity);  // every other owner's slice has landed here
+    } else if (__syncthreads_or(!mbar_wait_cluster_for(&xbar[1], parity, a.dp_timeout_cycles))) {
+      if (threadIdx.x == 0) atomicExch(a.dp_error, 1u);
+      return;
+    }
     mark(s, 15);
     for (int idx = threadIdx.x; idx < kKp; idx += blockDim.x) {
       const int row = idx >> 3, k = idx & 7;
@@ -515,6 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     __syncthreads();
     mark(s, 13);
   }
+  if (!dp) cluster_sync_all();  // no CTA leaves while a peer's DSMEM traffic may still target it
 }
 
 // ------------------------------------------------------------------------------------------------
