@@ -10,7 +10,8 @@ import os
 import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libtloom_b200.so")
+# TLB_LIB: developer A/B builds (paper_1912_05234_b200.build.build_variant); default = the in-tree library
+LIB_PATH = os.environ.get("TLB_LIB") or os.path.join(PKG, "lib", "libtloom_b200.so")
 HEADER = os.path.join(os.path.dirname(PKG), "include", "tloom_b200.h")
 
 TLB_OK = 0

@@ -88,6 +88,28 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(tag: str, defines: list[str]) -> str:
+    """Developer A/B builds: the library with zhang_kernels.cu compiled under extra -D flags, written to
+    lib/variants/libtloom_b200_<tag>.so (select at run time with TLB_LIB=<path>)."""
+    lib = build()
+    vdir = os.path.join(OBJ, "variant_" + tag)
+    os.makedirs(vdir, exist_ok=True)
+    obj = os.path.join(vdir, "zhang_kernels.o")
+    cmd = [NVCC] + CU_FLAGS + ["-D" + d for d in defines] + ["-c", os.path.join(CSRC, "zhang_kernels.cu"), "-o", obj]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError(f"variant build failed:\n{out.stderr}")
+    objs = [obj] + [os.path.join(OBJ, os.path.splitext(src)[0].replace("/", "_") + ".o")
+                    for src in SOURCES + HOST_SOURCES if src != "zhang_kernels.cu"]
+    os.makedirs(os.path.join(LIBDIR, "variants"), exist_ok=True)
+    vlib = os.path.join(LIBDIR, "variants", f"libtloom_b200_{tag}.so")
+    out = subprocess.run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", vlib] + objs, capture_output=True,
+                         text=True)
+    if out.returncode != 0:
+        raise RuntimeError(f"variant link failed:\n{out.stderr}")
+    return vlib
+
+
 TOOLS = {"tensorloom": "tools/tensorloom_cli.cpp", "tensorloom-datagen": "tools/datagen.cpp"}
 BINDIR = os.path.join(PKG, "bin")
 

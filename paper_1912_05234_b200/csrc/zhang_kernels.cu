@@ -363,6 +363,8 @@ __device__ __forceinline__ unsigned long long ld_sys_u64(const unsigned long lon
 
 __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a) {
   static_assert(StageCfg<false>::conv2_back != 3, "the DSMEM receive buffer reuses the backin term buffer");
+  static_assert(TLB_CLUSTER_KP || (StageCfg<false>::conv2 == 2 && StageCfg<false>::conv2_back >= 9),
+                "the clustered kernel keeps no padded k2 copy (Kp): its stages must read k2 from P");
   Smem s = carve_smem(tlb_smem);
   float* const rx = s.term;   // [8 source ranks][488]: slices pushed to this CTA (it owns slice `rank`)
   __shared__ double loss_rx[kCluster + 1];  // rank 0: the 8 CTAs' fp64 loss sums of the step (pushed);
@@ -533,11 +535,13 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       return;
     }
     mark(s, 15);
+#if TLB_CLUSTER_KP  // A/B switch: keep the padded k2 copy (conv2 reading Kp)
     for (int idx = threadIdx.x; idx < kKp; idx += blockDim.x) {
       const int row = idx >> 3, k = idx & 7;
       s.Kp[idx] = k < 5 ? s.P[kK2 + row * 5 + k] : 0.0f;
     }
     __syncthreads();
+#endif  // otherwise no padded k2 copy to rebuild: the fast stages read k2 from P
     mark(s, 13);
   }
   if (!dp) cluster_sync_all();  // no CTA leaves while a peer's DSMEM traffic may still target it

@@ -1305,12 +1305,18 @@ __device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float*
 }
 
 // Stage variants used by the product kernels (chosen with paper_1912_05234_b200/csrc/stage_bench.cu).
+#ifndef TLB_FAST_CONV2_V
+#define TLB_FAST_CONV2_V 2
+#endif
+#ifndef TLB_CLUSTER_KP
+#define TLB_CLUSTER_KP 0
+#endif
 #ifndef TLB_CONV2_BACK_V
 #define TLB_CONV2_BACK_V(EXACT) ((EXACT) ? 1 : 12)
 #endif
 template <bool EXACT>
 struct StageCfg {
-  static constexpr int conv2 = EXACT ? 0 : 1;
+  static constexpr int conv2 = EXACT ? 0 : TLB_FAST_CONV2_V;
   static constexpr int conv2_back = TLB_CONV2_BACK_V(EXACT);
   // backin-only conv2_back variants move g_k2/g_b2 into the C1-gradient phase
   static constexpr bool gk2_with_c1 = conv2_back == 4 || conv2_back == 5 || conv2_back >= 9;
