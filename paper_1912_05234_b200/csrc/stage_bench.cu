@@ -17,7 +17,7 @@ using namespace tlb;
 
 enum Stage { kConv1, kConv2V0, kConv2V1, kFc, kFcBack, kC2BackV0, kC2BackV1, kC2BackV2, kC2BackV3, kC1Back, kForward,
              kBackwardV0, kBackwardV1, kBackinV4, kBackinV5, kC1BackGk2, kBackwardV4, kBackwardV5, kC2BackV6, kC2BackV7, kBackwardV6, kBackwardV7, kC2BackV8, kBackwardV8,
-             kBackinV9, kBackwardV9, kC2BackV10, kBackwardV10, kBackwardV11, kBackwardV12, kBackwardV13, kConv2V2, kNumStages };
+             kBackinV9, kBackwardV9, kC2BackV10, kBackwardV10, kBackwardV11, kBackwardV12, kBackwardV13, kConv2V2, kBackwardV14, kNumStages };
 static const char* kNames[kNumStages] = {"conv1", "conv2_v0_halves", "conv2_v1_rows", "fc", "fc_back",
                                          "conv2_back_v0_quads", "conv2_back_v1_items", "conv2_back_v2_pairs", "conv2_back_v3_ws", "conv1_back",
                                          "forward_image", "backward_v0", "backward_v1",
@@ -26,7 +26,7 @@ static const char* kNames[kNumStages] = {"conv1", "conv2_v0_halves", "conv2_v1_r
                                          "backward_v6", "backward_v7", "conv2_back_v8_rows4p", "backward_v8",
                                          "backin_only_v9_rows4p", "backward_v9", "conv2_back_v10_split_gk2",
                                          "backward_v10", "backward_v11_gk160", "backward_v12_gk192",
-                                         "backward_v13_gk128", "conv2_v2_rows_p"};
+                                         "backward_v13_gk128", "conv2_v2_rows_p", "backward_v14_gk2rows"};
 
 __device__ __forceinline__ float hrand(unsigned int x) {  // deterministic value in [0, 1)
   x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
@@ -91,15 +91,15 @@ __device__ __forceinline__ void run_stage(const Smem& s, float* row) {
   } else if constexpr (STAGE == kC2BackV10) {
     if constexpr (!EXACT) stage_conv2_back<false, A, 10>(s, row);
   } else if constexpr (STAGE == kBackwardV9 || STAGE == kBackwardV10 || STAGE == kBackwardV11 ||
-                       STAGE == kBackwardV12 || STAGE == kBackwardV13) {
+                       STAGE == kBackwardV12 || STAGE == kBackwardV13 || STAGE == kBackwardV14) {
     if constexpr (!EXACT) {
       constexpr int V = STAGE == kBackwardV9 ? 9 : STAGE == kBackwardV10 ? 10 : STAGE == kBackwardV11 ? 11
-                      : STAGE == kBackwardV12 ? 12 : 13;
+                      : STAGE == kBackwardV12 ? 12 : STAGE == kBackwardV13 ? 13 : 14;
       stage_fc_back<EXACT, A>(s, row);
       __syncthreads();
       stage_conv2_back<false, A, V>(s, row);
       __syncthreads();
-      stage_conv1_back_gk2<false, A, gk2_split_lanes(V)>(s, s.img, row);
+      stage_conv1_back_gk2<false, A, gk2_split_lanes(V), V == 14>(s, s.img, row);
     }
   }
   else if constexpr (STAGE == kBackwardV4 || STAGE == kBackwardV5) {
@@ -224,6 +224,7 @@ void all(float* rows, unsigned long long* d_cycles, int sms, int iters, double m
     measure<EXACT, kBackwardV11>(rows, d_cycles, sms, iters, mhz);
     measure<EXACT, kBackwardV12>(rows, d_cycles, sms, iters, mhz);
     measure<EXACT, kBackwardV13>(rows, d_cycles, sms, iters, mhz);
+    measure<EXACT, kBackwardV14>(rows, d_cycles, sms, iters, mhz);
   }
 }
 
@@ -246,6 +247,7 @@ int main(int argc, char** argv) {
     verify<kBackwardV10, kBackwardV1>(d_out);
     verify<kBackwardV11, kBackwardV1>(d_out);
     verify<kBackwardV13, kBackwardV1>(d_out);
+    verify<kBackwardV14, kBackwardV1>(d_out);
     cudaFree(d_out);
   }
   all<false>(rows, d_cycles, sms, iters, mhz);

@@ -22,6 +22,9 @@
 #include "tlb_common.cuh"
 
 // EXACT C1 weight gradient: register-blocked v-groups (1, default) or one lane per output (0).
+#ifndef TLB_C1BACK_GROUP2
+#define TLB_C1BACK_GROUP2 1
+#endif
 #ifndef TLB_C1BACK_EXACT_BLOCKED
 #define TLB_C1BACK_EXACT_BLOCKED 1
 #endif
@@ -788,6 +791,33 @@ __device__ __forceinline__ void gk2_fast(const Smem& s, float* row, int t) {
   if (c == 0 && q4 == 0) put<ACCUM>(s, row, kB2 + i, bsum);
 }
 
+// Fast g_k2/g_b2 in row form: lane t < 360 -> (c, u) = t / 12, kernel i = t % 12 (the twelve kernels of a
+// (c, u) share the s1 rows: broadcast loads), five outputs v over the 64 taps in (y, x) order with FFMA,
+// no cross-lane reduction; the (c, u) = (0, 0) lanes also form g_b2[i] (row sums, then over y).
+template <bool ACCUM>
+__device__ __forceinline__ void gk2_rows(const Smem& s, float* row, int t) {
+  const int cu = t / 12, i = t - cu * 12, c = cu / 5, u = cu - c * 5;
+  float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+  float bsum = 0.0f;
+#pragma unroll 2
+  for (int y = 0; y < 8; ++y) {
+    const float4* sp = reinterpret_cast<const float4*>(s.s1 + (c * 12 + u + y) * 12);
+    const float4 a = sp[0], b = sp[1], cc = sp[2];
+    const float sr[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, cc.x, cc.y, cc.z, cc.w};
+    const float4* dp = reinterpret_cast<const float4*>(s.dzp + dzp_at(i, y + 4, 4));
+    const float4 d0 = dp[0], d1 = dp[1];
+    const float dr[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+    for (int x = 0; x < 8; ++x)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) acc[v] = __fmaf_rn(sr[v + x], dr[x], acc[v]);
+    if (cu == 0) bsum += ((dr[0] + dr[1]) + (dr[2] + dr[3])) + ((dr[4] + dr[5]) + (dr[6] + dr[7]));
+  }
+#pragma unroll
+  for (int v = 0; v < 5; ++v) put<ACCUM>(s, row, kK2 + ((i * 6 + c) * 5 + u) * 5 + v, acc[v]);
+  if (cu == 0) put<ACCUM>(s, row, kB2 + i, bsum);
+}
+
 // Weight-stationary backin.  Lane t < 504 -> kernel i = t / 42, channel c = t % 6 and tile group
 // tg = (t % 42) / 6; it keeps the 25 weights of k2[i][c] in registers and walks tiles tg, tg+7, tg+14
 // (2 rows x 4 columns of d_s1[c]), streaming six padded dz2[i] rows per tile.  The six lanes of a
@@ -966,7 +996,7 @@ __device__ __forceinline__ void backin_rows(const Smem& s, int t) {
 
 // g_k2 quad lanes done beside the scatter-form backin in conv2_back variants 10..13 (whole warps).
 __host__ __device__ constexpr int gk2_split_lanes(int V) {
-  return V == 10 ? 224 : V == 11 ? 160 : V == 12 ? 192 : V == 13 ? 128 : 0;
+  return V == 10 ? 224 : V == 11 ? 160 : V == 12 ? 192 : V == 13 ? 128 : V == 14 ? 224 : 0;
 }
 
 // C2 backward stage.  V = 0: backin lane quads on warps 0-13 (432 lanes), then the g_k2/g_b2 lanes;
@@ -1014,6 +1044,14 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
     // g_k2/g_b2 runs beside the C1 gradient
     static_assert(!EXACT, "scatter-form backin reorders the reference's sums");
     for (int it = threadIdx.x; it < 288; it += blockDim.x) backin_rows<4, true>(s, it);
+  } else if constexpr (V == 14) {
+    // V = 14 (fast only): backin rows on warps 0-8 beside g_k2 row lanes 0-223 on warps 9-15; row
+    // lanes 224-359 run beside the C1 gradient
+    static_assert(!EXACT, "scatter-form backin reorders the reference's sums");
+    for (int it = threadIdx.x; it < 288 + 224; it += blockDim.x) {
+      if (it < 288) backin_rows<4, true>(s, it);
+      else gk2_rows<ACCUM>(s, row, it - 288);
+    }
   } else if constexpr (V >= 10 && V <= 13) {
     // V = 10..13 (fast only): backin rows on warps 0-8 beside the first gk2_split_lanes(V) g_k2 quad
     // lanes on warps 9-15; the remaining quads run beside the C1 gradient
@@ -1286,10 +1324,77 @@ __device__ __forceinline__ void conv1_back_fast_group(const Smem& s, const float
   }
 }
 
-template <bool EXACT, bool ACCUM, int GLO = 0>
+// Fast C1 weight gradient on 288 lanes (512-thread CTAs): lane pair (i, y) splits the five tap rows
+// u = 0..2 | 3..4 (+ the bias row-partial), so phase 1 takes ~390 instead of ~635 issue slots per lane;
+// the fixed-order combine over y is unchanged (named barrier 1 over the 288 lanes).
+template <bool ACCUM>
+__device__ __forceinline__ void conv1_back_fast_group2(const Smem& s, const float* img, float* row) {
+  constexpr int kGroup = 288;
+  const float* dz1 = s.c1;
+  const int it = threadIdx.x;  // < kGroup
+  const int pr = it >> 1, h = it & 1;
+  const int i = pr / 24, y = pr - i * 24;
+  const float4* dp = reinterpret_cast<const float4*>(dz1 + c1_at(i, y, 0));
+  float dr[24];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const float4 t = dp[q];
+    dr[4 * q] = t.x; dr[4 * q + 1] = t.y; dr[4 * q + 2] = t.z; dr[4 * q + 3] = t.w;
+  }
+  float* out = s.red + pr * 26;
+  if (h) {
+    float bias = 0.0f;
+#pragma unroll
+    for (int x = 0; x < 24; ++x) bias += dr[x];
+    out[25] = bias;
+  }
+  const int u0 = h ? 3 : 0, un = h ? 2 : 3;
+#pragma unroll 1
+  for (int k = 0; k < un; ++k) {
+    const int u = u0 + k;
+    const float4* ip = reinterpret_cast<const float4*>(img + (u + y) * 28);
+    float ir[28];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      const float4 t = ip[q];
+      ir[4 * q] = t.x; ir[4 * q + 1] = t.y; ir[4 * q + 2] = t.z; ir[4 * q + 3] = t.w;
+    }
+    float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int x = 0; x < 24; ++x)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) acc[v] = __fmaf_rn(ir[x + v], dr[x], acc[v]);
+#pragma unroll
+    for (int v = 0; v < 5; ++v) out[u * 5 + v] = acc[v];
+  }
+  named_sync(1, kGroup);
+  if (it < 156) {
+    float acc = 0.0f;
+    const int col = it < 150 ? (it % 25) : 25, ii = it < 150 ? it / 25 : it - 150;
+#pragma unroll 8
+    for (int yy = 0; yy < 24; ++yy) acc += s.red[(ii * 24 + yy) * 26 + col];
+    put<ACCUM>(s, row, it < 150 ? kK1 + it : kB1 + ii, acc);
+  }
+}
+
+template <bool EXACT, bool ACCUM, int GLO = 0, bool ROWS = false>
 __device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float* img, float* row) {
-  constexpr int kGk2 = EXACT ? 372 : 288;
+  constexpr int kGk2 = EXACT ? 372 : ROWS ? 360 : 288;
   const int t = threadIdx.x;
+  if constexpr (!EXACT && TLB_C1BACK_GROUP2) {
+    if (blockDim.x >= 512) {  // C1 gradient on warps 0-8, the remaining g_k2 lanes on warps 9+
+      if (t < 288) {
+        conv1_back_fast_group2<ACCUM>(s, img, row);
+      } else {
+        for (int item = GLO + t - 288; item < kGk2; item += blockDim.x - 288) {
+          if constexpr (ROWS) gk2_rows<ACCUM>(s, row, item);
+          else gk2_fast<ACCUM>(s, row, item);
+        }
+      }
+      return;
+    }
+  }
+  static_assert(!ROWS || !EXACT, "row-form g_k2 is a fast-mode stage");
   if (t < 160) {
     if constexpr (EXACT) {
       if (t < 156) stage_conv1_back_lane_exact<ACCUM>(s, row, t);
@@ -1299,6 +1404,7 @@ __device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float*
   } else {
     for (int item = GLO + t - 160; item < kGk2; item += blockDim.x - 160) {
       if constexpr (EXACT) gk2_exact<ACCUM>(s, row, item);
+      else if constexpr (ROWS) gk2_rows<ACCUM>(s, row, item);
       else gk2_fast<ACCUM>(s, row, item);
     }
   }
@@ -1312,7 +1418,7 @@ __device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float*
 #define TLB_CLUSTER_KP 0
 #endif
 #ifndef TLB_CONV2_BACK_V
-#define TLB_CONV2_BACK_V(EXACT) ((EXACT) ? 1 : 12)
+#define TLB_CONV2_BACK_V(EXACT) ((EXACT) ? 1 : 14)
 #endif
 template <bool EXACT>
 struct StageCfg {
@@ -1321,6 +1427,7 @@ struct StageCfg {
   // backin-only conv2_back variants move g_k2/g_b2 into the C1-gradient phase
   static constexpr bool gk2_with_c1 = conv2_back == 4 || conv2_back == 5 || conv2_back >= 9;
   static constexpr int gk2_lo = gk2_split_lanes(conv2_back);  // g_k2 lanes already done in conv2_back
+  static constexpr bool gk2_rows = conv2_back == 14;            // row-form g_k2 lanes (gk2_rows)
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -1345,7 +1452,7 @@ __device__ __noinline__ void call_conv2_back(float* row) {
 template <bool EXACT, bool ACCUM>
 __device__ __noinline__ void call_conv1_back(const float* img, float* row) {
   if constexpr (StageCfg<EXACT>::gk2_with_c1)
-    stage_conv1_back_gk2<EXACT, ACCUM, StageCfg<EXACT>::gk2_lo>(smem_view(), img, row);
+    stage_conv1_back_gk2<EXACT, ACCUM, StageCfg<EXACT>::gk2_lo, StageCfg<EXACT>::gk2_rows>(smem_view(), img, row);
   else stage_conv1_back<EXACT, ACCUM>(smem_view(), img, row);
 }
 
