@@ -106,6 +106,11 @@ __host__ __device__ __forceinline__ int64_t umod(int64_t a, int64_t b) { return 
 // ---- static_chunk (runtime.cpp:138-145): ceil-block split of [0,n) over `workers` -------------
 __host__ __device__ __forceinline__ void static_chunk(int64_t n, int workers, int w, int64_t& lo,
                                                       int64_t& hi) {
+  if (n <= workers) {  // block of 1 (or 0): no division
+    lo = w < n ? w : n;
+    hi = w + 1 < n ? w + 1 : n;
+    return;
+  }
   const int64_t block = udiv(n + workers - 1, workers);
   lo = (int64_t)w * block;
   if (lo > n) lo = n;

@@ -30,16 +30,19 @@ struct Job {
   int64_t step, e, hi;
 };
 
-__device__ __forceinline__ int64_t group_size(const TrainArgs& a, int64_t st) {
-  const int64_t start = umod(st, a.steps_per_epoch) * a.batch;
-  const int64_t rem = a.n - start;
+// Size of SGD group ks (0 <= ks < steps_per_epoch) of the epoch.
+__device__ __forceinline__ int64_t group_size_k(const TrainArgs& a, int64_t ks) {
+  const int64_t rem = a.n - ks * a.batch;
   return rem < a.batch ? rem : a.batch;
 }
+__device__ __forceinline__ int64_t group_size(const TrainArgs& a, int64_t st) {
+  return group_size_k(a, umod(st, a.steps_per_epoch));
+}
 
-// Examples of group `st` handled by this launch: the whole group, the DP shard of it given by the
+// Examples of group ks handled by this launch: the whole group, the DP shard of it given by the
 // caller (grad_out mode), or this rank's static_chunk of it (fused data parallelism).
-__device__ __forceinline__ void local_range(const TrainArgs& a, int64_t st, int64_t& lo, int64_t& hi) {
-  const int64_t m = group_size(a, st);
+__device__ __forceinline__ void local_range_k(const TrainArgs& a, int64_t ks, int64_t& lo, int64_t& hi) {
+  const int64_t m = group_size_k(a, ks);
   if (a.dp_world > 0) {
     static_chunk(m, a.dp_world, a.dp_rank, lo, hi);
   } else if (a.grad_out) {
@@ -53,12 +56,12 @@ __device__ __forceinline__ void local_range(const TrainArgs& a, int64_t st, int6
 }
 __device__ __forceinline__ int64_t local_size(const TrainArgs& a, int64_t st) {
   int64_t lo, hi;
-  local_range(a, st, lo, hi);
+  local_range_k(a, umod(st, a.steps_per_epoch), lo, hi);
   return hi - lo;
 }
 __device__ __forceinline__ int64_t local_offset(const TrainArgs& a, int64_t st) {
   int64_t lo, hi;
-  local_range(a, st, lo, hi);
+  local_range_k(a, umod(st, a.steps_per_epoch), lo, hi);
   return lo;
 }
 
@@ -251,9 +254,12 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
   if (issuer && pf_valid) issue_job(s, a, 0, pf);
   uint32_t consumed = 0;
 
-  for (int64_t st = a.step_begin; st < a.step_end; ++st) {
-    const int64_t ks = umod(st, a.steps_per_epoch), start = ks * a.batch + local_offset(a, st);
-    const int64_t m = local_size(a, st);
+  // group index within the epoch and epoch of step st, advanced incrementally (no per-step division)
+  int64_t ks = umod(a.step_begin, a.steps_per_epoch), ep = udiv(a.step_begin, a.steps_per_epoch);
+  for (int64_t st = a.step_begin; st < a.step_end; ++st, ks = ks + 1 == a.steps_per_epoch ? (++ep, 0) : ks + 1) {
+    int64_t l_lo, l_hi;
+    local_range_k(a, ks, l_lo, l_hi);
+    const int64_t m = l_hi - l_lo;
     int64_t lo, hi;
     static_chunk(m, G, blockIdx.x, lo, hi);
     s.tr = trace ? trace + (st - a.step_begin) * 16 : nullptr;
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
       nrows = m > 0 ? udiv(m + block - 1, block) : 0;
     }
     reduce_slice<EXACT>(s, a, nrows, m);
-    if (blockIdx.x == G - 1) reduce_loss<EXACT>(s, a, m, nrows, ks, udiv(st, a.steps_per_epoch));
+    if (blockIdx.x == G - 1) reduce_loss<EXACT>(s, a, m, nrows, ks, ep);
     __syncthreads();
     mark(s, 12);
     grid_sync(a.barrier, target);
@@ -401,11 +407,14 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
   uint32_t consumed = 0;
   load_params(s, a.params);  // once: afterwards the parameters live in shared memory
 
-  for (int64_t st = a.step_begin; st < a.step_end; ++st) {
+  // group index within the epoch and epoch of step st, advanced incrementally (no per-step division)
+  int64_t ks = umod(a.step_begin, a.steps_per_epoch), ep = udiv(a.step_begin, a.steps_per_epoch);
+  for (int64_t st = a.step_begin; st < a.step_end; ++st, ks = ks + 1 == a.steps_per_epoch ? (++ep, 0) : ks + 1) {
     const int64_t ls = st - a.step_begin;  // local step
     const uint64_t seq = a.seq_base + (uint64_t)ls;  // steps on these accumulators: buffer seq % 3
-    const int64_t ks = umod(st, a.steps_per_epoch), start = ks * a.batch + local_offset(a, st);
-    const int64_t m = local_size(a, st), m_global = group_size(a, st);
+    int64_t l_lo, l_hi;
+    local_range_k(a, ks, l_lo, l_hi);
+    const int64_t m = l_hi - l_lo, m_global = group_size_k(a, ks);
     int64_t lo, hi;
     static_chunk(m, G, blockIdx.x, lo, hi);
     s.tr = trace ? trace + ls * 16 : nullptr;
@@ -514,7 +523,6 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       if (a.grad_out) {
         a.loss_out[0] = l;
       } else {
-        const int64_t ep = udiv(st, a.steps_per_epoch);
         const double run = (ks != 0 ? a.epoch_loss[ep] : 0.0) + l;
         a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(run, (double)a.n) : run;
       }

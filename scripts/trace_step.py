@@ -52,6 +52,8 @@ ctx.train_device(d_x.data_ptr(), d_y.data_ptr(), args.n, d_p.data_ptr(), 0.05, 1
 e1.record(s)
 torch.cuda.synchronize()
 t = tr.view(steps, 16).cpu().numpy().astype(np.int64)
+if os.environ.get("TRACE_DUMP"):
+    np.save(os.environ["TRACE_DUMP"], t)
 d = np.diff(t[:, :14], axis=1)  # stage durations (cycles)
 med = np.median(d[1:], axis=0)
 mhz = 1965.0
