@@ -443,8 +443,52 @@ __device__ __forceinline__ void put(const Smem& s, float* row, int idx, float v)
 // FC backward: g_fc[i][j] = 0 + s2[j]*dz[i]; g_b = 0 + dz; d_s2[j] = sum_i fc[i][j]*dz[i]
 // (backin with singleton error, nn.cpp:193-217, summed over i as network.cpp:135-138), then
 // backavgpool (nn.cpp:148-158) and backsigmoid through c2 -> dz2 (into the padded buffer).
+// d_s2[j] = sum_i fc[i][j]*dz[i] (FFMA), then backavgpool + backsigmoid through c2 -> dz2 (fast mode).
+__device__ __forceinline__ void fc_back_dz2(const Smem& s, int j) {
+  float ds = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 10; ++i) ds = mac<false>(ds, s.P[kFC + i * 192 + j], s.dz[i]);
+  const float dc = fmul(ds, 0.25f);
+  const int c = j >> 4, py = (j >> 2) & 3, px = j & 3;
+#pragma unroll
+  for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+    for (int dx = 0; dx < 2; ++dx) {
+      const int yy = 2 * py + dy, xx = 2 * px + dx;
+      const float o = s.c2[(c * 8 + yy) * 8 + xx];
+      s.dzp[dzp_at(c, yy + 4, xx + 4)] = fmul(fmul(dc, o), fsub(1.0f, o));
+    }
+}
+
 template <bool EXACT, bool ACCUM>
 __device__ __forceinline__ void stage_fc_back(const Smem& s, float* row) {
+  if constexpr (!EXACT && ACCUM) {
+    // Fast accumulating kernels: lanes 0-191 run the d_s2 -> dz2 chain while lanes 192+ add the FC
+    // gradient into G four columns at a time (480 float4 entries + 10 biases, FFMA).
+    for (int t = threadIdx.x; t < 192 + 320; t += blockDim.x) {
+      if (t < 192) {
+        fc_back_dz2(s, t);
+      } else {
+        for (int q = t - 192; q < 490; q += 320) {
+          if (q < 480) {
+            const int i = q / 48, j4 = q - i * 48;
+            const float4 sv = *reinterpret_cast<const float4*>(s.s2 + 4 * j4);
+            const float d = s.dz[i];
+            float4* g = reinterpret_cast<float4*>(s.G + kFC + 4 * q);
+            float4 gv = *g;
+            gv.x = __fmaf_rn(sv.x, d, gv.x);
+            gv.y = __fmaf_rn(sv.y, d, gv.y);
+            gv.z = __fmaf_rn(sv.z, d, gv.z);
+            gv.w = __fmaf_rn(sv.w, d, gv.w);
+            *g = gv;
+          } else {
+            s.G[kB + q - 480] += s.dz[q - 480];
+          }
+        }
+      }
+    }
+    return;
+  }
   for (int idx = threadIdx.x; idx < 1930; idx += blockDim.x) {
     if (idx < 1920) {
       const int i = idx / 192, j = idx - i * 192;
