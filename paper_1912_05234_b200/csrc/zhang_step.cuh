@@ -32,6 +32,19 @@
 namespace tlb {
 
 constexpr int kThreads = 512;
+// backin_rows kernel-loop unroll (A/B: 3 = the three kernels' loads can overlap, +0.7% vs 1)
+#ifndef TLB_BACKIN_KUNROLL
+#define TLB_BACKIN_KUNROLL 3
+#endif
+constexpr int kBackinKUnroll = TLB_BACKIN_KUNROLL;
+#ifndef TLB_GK2R_YUNROLL
+#define TLB_GK2R_YUNROLL 2
+#endif
+constexpr int kGk2rYUnroll = TLB_GK2R_YUNROLL;  // gk2_rows tap-row loop unroll (A/B switch)
+#ifndef TLB_C1G2_UNROLL
+#define TLB_C1G2_UNROLL 1
+#endif
+constexpr int kC1g2Unroll = TLB_C1G2_UNROLL;  // conv1_back_fast_group2 tap-row loop unroll (A/B switch)
 
 struct Smem {
   float* P;    // parameters [3904]
@@ -843,7 +856,7 @@ __device__ __forceinline__ void gk2_rows(const Smem& s, float* row, int t) {
   const int cu = t / 12, i = t - cu * 12, c = cu / 5, u = cu - c * 5;
   float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
   float bsum = 0.0f;
-#pragma unroll 2
+#pragma unroll kGk2rYUnroll
   for (int y = 0; y < 8; ++y) {
     const float4* sp = reinterpret_cast<const float4*>(s.s1 + (c * 12 + u + y) * 12);
     const float4 a = sp[0], b = sp[1], cc = sp[2];
@@ -976,7 +989,7 @@ __device__ __forceinline__ void backin_rows(const Smem& s, int t) {
   float acc[12];
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = 0.0f;
-#pragma unroll 1
+#pragma unroll kBackinKUnroll
   for (int k = 0; k < KPL; ++k) {
     const int i = part * KPL + k;
     float w[5][5];
@@ -1393,7 +1406,7 @@ __device__ __forceinline__ void conv1_back_fast_group2(const Smem& s, const floa
     out[25] = bias;
   }
   const int u0 = h ? 3 : 0, un = h ? 2 : 3;
-#pragma unroll 1
+#pragma unroll kC1g2Unroll
   for (int k = 0; k < un; ++k) {
     const int u = u0 + k;
     const float4* ip = reinterpret_cast<const float4*>(img + (u + y) * 28);
