@@ -130,17 +130,29 @@ class FusedDPStep:
     arrives trips the kernel's watchdog (``check()`` raises) instead of hanging."""
 
     def __init__(self, ctx, d_images, d_labels, n: int, global_batch: int, world: int, rank: int,
-                 timeout_s: float = 2.0):
-        import torch.distributed._symmetric_memory as symm_mem
+                 timeout_s: float = 2.0, ipc: bool = False):
         from . import _lib
         self.ctx, self.x, self.y, self.n, self.B = ctx, d_images, d_labels, n, global_batch
         self.world, self.rank, self.timeout_s = world, rank, timeout_s
         nbytes = int(_lib.lib().tlb_dp_workspace_bytes())
-        self.ws = symm_mem.empty(nbytes, dtype=torch.uint8, device=d_images.device)
-        self.ws.zero_()
-        group = dist.group.WORLD
-        self.handle = symm_mem.rendezvous(self.ws, group.group_name if hasattr(group, "group_name") else group)
-        self.peers = [int(p) for p in self.handle.buffer_ptrs]
+        if not ipc:
+            import torch.distributed._symmetric_memory as symm_mem
+            self.ws = symm_mem.empty(nbytes, dtype=torch.uint8, device=d_images.device)
+            self.ws.zero_()
+            group = dist.group.WORLD
+            self.handle = symm_mem.rendezvous(self.ws, group.group_name if hasattr(group, "group_name") else group)
+            self.peers = [int(p) for p in self.handle.buffer_ptrs]
+        else:
+            # Plain CUDA IPC handles exchanged over the process group (any backend): the ranks may share
+            # one device, which torch symmetric memory refuses -- used to run the cross-process protocol
+            # on a single GPU.
+            from torch.multiprocessing.reductions import reduce_tensor
+            self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=d_images.device)
+            torch.cuda.synchronize()
+            handles = [None] * world
+            dist.all_gather_object(handles, reduce_tensor(self.ws))
+            self._peer_tensors = [self.ws if r == rank else fn(*args) for r, (fn, args) in enumerate(handles)]
+            self.peers = [int(t.data_ptr()) for t in self._peer_tensors]
         self.err_off = nbytes - 32
         self.seq = 0
         self.groups_per_epoch = len(groups(n, global_batch))
