@@ -200,7 +200,11 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TLB_BENCH_SAME_GPU=1 (developer check of the N>1 plumbing on a one-GPU box): every rank on cuda:0,
+    # a gloo process group and CUDA-IPC-mapped DP workspaces; use a small --batch so all ranks' kernels
+    # are co-resident.  Not a throughput number.
+    same_gpu = os.environ.get("TLB_BENCH_SAME_GPU") == "1"
+    local = 0 if same_gpu else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dp = world > 1 or args.force_dp
@@ -213,7 +217,10 @@ def run_ours(args):
         os.dup2(2, 1)
         if "RANK" not in os.environ:  # --force-dp without torchrun: a one-rank NCCL group
             os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1", MASTER_PORT="29517")
-        dist.init_process_group("nccl", device_id=dev)
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     B, n_per = args.batch, args.n
     n_total = n_per * world
@@ -248,7 +255,7 @@ def run_ours(args):
         step, dp_used, dp_note = None, "nccl", None
         if args.dp_mode == "nvlink" and args.mode == "fast":
             try:
-                step = FusedDPStep(ctx, d_x, d_y, n_total, B * world, world, rank)
+                step = FusedDPStep(ctx, d_x, d_y, n_total, B * world, world, rank, ipc=same_gpu)
                 dp_used = "nvlink"
             except Exception as exc:  # symmetric memory unavailable: NCCL path
                 dp_note = f"fused NVLink step unavailable ({type(exc).__name__}: {exc}); NCCL fallback"
@@ -260,46 +267,55 @@ def run_ours(args):
             step.epoch(d_p, 0.05, d_loss, e)
         launches_per_step = 1 if dp_used == "nvlink" else 2 * step.groups_per_epoch
 
-    # warm-up (not timed), then the timed protocol from init_params(42)
-    reset()
-    for w in range(args.warmup):
-        epoch(w % max(args.steps, 1))
-    torch.cuda.synchronize()
-    if dp and dp_used == "nvlink":
+    def all_max(v: float) -> float:  # max over ranks (a CPU tensor for gloo, device for NCCL)
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if same_gpu else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t)
+
+    def fused_tripped() -> bool:  # did ANY rank's fused kernel hit its peer-wait watchdog?  (all agree)
         try:
             step.check()
-        except RuntimeError as exc:  # a peer timed out: rerun the warm-up on the NCCL path
-            dp_used, dp_note = "nccl", f"{exc}; NCCL fallback"
-            print(dp_note, file=sys.stderr)
-            step = DeviceShardStep(ctx, d_x, d_y, n_total, B * world, world, rank, graph=not args.no_graph)
-            launches_per_step = 2 * step.groups_per_epoch
-            reset()
-            for w in range(args.warmup):
-                epoch(w % max(args.steps, 1))
-            torch.cuda.synchronize()
-    reset()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if dp:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for s in range(args.steps):
-            flush.fill_(float(s))  # L2 flush between timed steps, outside the event pair
-            starts[s].record(stream)
-            epoch(s)
-            ends[s].record(stream)
+            mine = 0.0
+        except RuntimeError:
+            mine = 1.0
+        return all_max(mine) > 0
+
+    def run_protocol():
+        # warm-up (not timed), then the timed protocol from init_params(42)
+        reset()
+        for w in range(args.warmup):
+            epoch(w % max(args.steps, 1))
         torch.cuda.synchronize()
+        if dp and dp_used == "nvlink" and fused_tripped():
+            return None, None
+        reset()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        if dp:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            for s in range(args.steps):
+                flush.fill_(float(s))  # L2 flush between timed steps, outside the event pair
+                starts[s].record(stream)
+                epoch(s)
+                ends[s].record(stream)
+            torch.cuda.synchronize()
+        if dp:
+            dist.barrier()
+        if dp and dp_used == "nvlink" and fused_tripped():  # a trip during the timed epochs: re-measure
+            return None, None
+        return sum(a.elapsed_time(b) for a, b in zip(starts, ends)), clk
+
+    total_ms, clk = run_protocol()
+    if total_ms is None:  # the fused path tripped on some rank: every rank moves to NCCL together
+        dp_used, dp_note = "nccl", "fused NVLink step: a peer-wait watchdog tripped; NCCL fallback"
+        print(dp_note, file=sys.stderr)
+        step = DeviceShardStep(ctx, d_x, d_y, n_total, B * world, world, rank, graph=not args.no_graph)
+        launches_per_step = 2 * step.groups_per_epoch
+        total_ms, clk = run_protocol()
     if dp:
-        dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
-    total_ms = sum(step_ms)
-    if dp and dp_used == "nvlink":
-        step.check()  # a watchdog trip during the timed epochs invalidates the number
-    if dp:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t)
+        total_ms = all_max(total_ms)
     losses = d_loss[: args.steps].cpu().numpy().tolist()
     value = args.steps * n_total / (total_ms / 1e3)
 

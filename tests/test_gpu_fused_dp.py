@@ -1,6 +1,6 @@
 """Fused data parallelism over NVLink peer memory (tlb_train_dp_device via parallel.FusedDPStep).
 
-Only one GPU is available to this build, so the multi-GPU protocol is exercised at world size 1 through
+Only one GPU is available to this build: the protocol runs at world size 1 through
 a real torch symmetric-memory workspace and process group: the slice owners, the system-scope fixed-point
 adds, the per-slice arrival counters continuing across launches (seq_base) and the watchdog word all run
 the code path a multi-GPU job runs.  The result must be bitwise identical to the single-GPU clustered
