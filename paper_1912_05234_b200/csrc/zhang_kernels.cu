@@ -409,6 +409,8 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
 
   // group index within the epoch and epoch of step st, advanced incrementally (no per-step division)
   int64_t ks = umod(a.step_begin, a.steps_per_epoch), ep = udiv(a.step_begin, a.steps_per_epoch);
+  // CTA 0's loss thread: the epoch's running loss sum (a launch may start mid-epoch: resume it)
+  double loss_run = (blockIdx.x == 0 && threadIdx.x == kSlice && !a.grad_out && ks != 0) ? a.epoch_loss[ep] : 0.0;
   for (int64_t st = a.step_begin; st < a.step_end; ++st, ks = ks + 1 == a.steps_per_epoch ? (++ep, 0) : ks + 1) {
     const int64_t ls = st - a.step_begin;  // local step
     const uint64_t seq = a.seq_base + (uint64_t)ls;  // steps on these accumulators: buffer seq % 3
@@ -522,9 +524,9 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       const double l = (double)(long long)(dp ? ld_sys_u64(lacc + b) : __ldcg(lacc + b)) * kUnfix;
       if (a.grad_out) {
         a.loss_out[0] = l;
-      } else {
-        const double run = (ks != 0 ? a.epoch_loss[ep] : 0.0) + l;
-        a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(run, (double)a.n) : run;
+      } else {  // running epoch sum kept in a register: no dependent L2 read on CTA 0's critical path
+        loss_run = (ks != 0 ? loss_run : 0.0) + l;
+        a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(loss_run, (double)a.n) : loss_run;
       }
     }
     __syncthreads();
