@@ -33,6 +33,9 @@ namespace tlb {
 
 constexpr int kThreads = 512;
 // backin_rows kernel-loop unroll (A/B: 3 = the three kernels' loads can overlap, +0.7% vs 1)
+#ifndef TLB_GK2R_SPLIT
+#define TLB_GK2R_SPLIT 96  // row-form g_k2 lanes beside backin, the rest beside the C1 gradient (A/B: 64-160 best)
+#endif
 #ifndef TLB_BACKIN_KUNROLL
 #define TLB_BACKIN_KUNROLL 3
 #endif
@@ -1053,7 +1056,7 @@ __device__ __forceinline__ void backin_rows(const Smem& s, int t) {
 
 // g_k2 quad lanes done beside the scatter-form backin in conv2_back variants 10..13 (whole warps).
 __host__ __device__ constexpr int gk2_split_lanes(int V) {
-  return V == 10 ? 224 : V == 11 ? 160 : V == 12 ? 192 : V == 13 ? 128 : V == 14 ? 224 : 0;
+  return V == 10 ? 224 : V == 11 ? 160 : V == 12 ? 192 : V == 13 ? 128 : V == 14 ? TLB_GK2R_SPLIT : 0;
 }
 
 // C2 backward stage.  V = 0: backin lane quads on warps 0-13 (432 lanes), then the g_k2/g_b2 lanes;
@@ -1105,7 +1108,7 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
     // V = 14 (fast only): backin rows on warps 0-8 beside g_k2 row lanes 0-223 on warps 9-15; row
     // lanes 224-359 run beside the C1 gradient
     static_assert(!EXACT, "scatter-form backin reorders the reference's sums");
-    for (int it = threadIdx.x; it < 288 + 224; it += blockDim.x) {
+    for (int it = threadIdx.x; it < 288 + gk2_split_lanes(14); it += blockDim.x) {
       if (it < 288) backin_rows<4, true>(s, it);
       else gk2_rows<ACCUM>(s, row, it - 288);
     }
