@@ -33,6 +33,9 @@ namespace tlb {
 
 constexpr int kThreads = 512;
 // backin_rows kernel-loop unroll (A/B: 3 = the three kernels' loads can overlap, +0.7% vs 1)
+#ifndef TLB_CONV1_ROWS2
+#define TLB_CONV1_ROWS2 1  // fast conv1: 1 = two rows x 8 columns per lane, 2 = two rows x 4, 0 = row strips
+#endif
 #ifndef TLB_GK2R_SPLIT
 #define TLB_GK2R_SPLIT 96  // row-form g_k2 lanes beside backin, the rest beside the C1 gradient (A/B: 64-160 best)
 #endif
@@ -213,8 +216,69 @@ __device__ __forceinline__ void build_shifted(const Smem& s, const float* img, i
 // two rows of a pooling window sit on adjacent lanes and meet through a shuffle.  Per output: taps
 // (ky,kx) row-major (nn.cpp:28-33), then + b1[i] (nn.cpp:123); pool ((p00+p01)+p10)+p11, *0.25f.
 // Warps 13.5..15 meanwhile build the v-shifted image copies used by the C1 weight gradient.
+// Fast conv1 variant (TLB_CONV1_ROWS2): lane = (channel i, pooled row py, 8-column strip xs) computes
+// both conv rows 2py, 2py+1 (16 outputs): the six image rows it loads and the 25 weights serve both
+// rows, and the 2x2 pooling windows are lane-local (no shuffle).  216 lanes.
+template <int W>  // output columns per lane: 8 (216 lanes) or 4 (432 lanes)
+__device__ __forceinline__ void stage_conv1_rows2(const Smem& s, const float* img) {
+  constexpr int kStrips = 24 / W, kItems = 6 * 12 * kStrips;
+  for (int it = threadIdx.x; it < (kItems + 31) / 32 * 32; it += blockDim.x) {
+    if (it >= kItems) continue;
+    const int i = it / (12 * kStrips), rem = it - i * 12 * kStrips, py = rem / kStrips, xs = rem - py * kStrips;
+    const int y0 = 2 * py, x0 = W * xs;
+    const float* k = s.P + kK1 + i * 25;
+    float a[2][W];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int o = 0; o < W; ++o) a[r][o] = 0.0f;
+#pragma unroll
+    for (int rr = 0; rr < 6; ++rr) {  // image row y0 + rr feeds conv row r with ky = rr - r
+      const float4* src = reinterpret_cast<const float4*>(img + (y0 + rr) * 28 + x0);
+      float in[W + 4];
+#pragma unroll
+      for (int q = 0; q < (W + 4) / 4; ++q) {
+        const float4 v = src[q];
+        in[4 * q] = v.x; in[4 * q + 1] = v.y; in[4 * q + 2] = v.z; in[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int ky = rr - r;
+        if (ky < 0 || ky > 4) continue;
+#pragma unroll
+        for (int kx = 0; kx < 5; ++kx) {
+          const float w = k[ky * 5 + kx];
+#pragma unroll
+          for (int o = 0; o < W; ++o) a[r][o] = __fmaf_rn(in[o + kx], w, a[r][o]);
+        }
+      }
+    }
+    const float b = s.P[kB1 + i];
+    float t[2][W];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+#pragma unroll
+      for (int o = 0; o < W; ++o) t[r][o] = sigmoid_m<false>(fadd(a[r][o], b), s.tab);
+      float4* d = reinterpret_cast<float4*>(s.c1 + c1_at(i, y0 + r, x0));
+#pragma unroll
+      for (int q = 0; q < W / 4; ++q) d[q] = make_float4(t[r][4 * q], t[r][4 * q + 1], t[r][4 * q + 2], t[r][4 * q + 3]);
+    }
+    float pv[W / 2];
+#pragma unroll
+    for (int px = 0; px < W / 2; ++px)  // avgpool (nn.cpp:144): ((p00 + p01) + p10) + p11, then * 0.25f
+      pv[px] = fmul(fadd(fadd(fadd(t[0][2 * px], t[0][2 * px + 1]), t[1][2 * px]), t[1][2 * px + 1]), 0.25f);
+    float* sp = s.s1 + (i * 12 + py) * 12 + (W / 2) * xs;
+    if constexpr (W == 8) *reinterpret_cast<float4*>(sp) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+    else *reinterpret_cast<float2*>(sp) = make_float2(pv[0], pv[1]);
+  }
+}
+
 template <bool EXACT>
 __device__ __forceinline__ void stage_conv1(const Smem& s, const float* img) {
+  if constexpr (!EXACT && TLB_CONV1_ROWS2) {
+    stage_conv1_rows2<TLB_CONV1_ROWS2 == 2 ? 4 : 8>(s, img);
+    return;
+  }
   // 448 item lanes (14 full warps; items >= 432 are padding lanes, valid = false); with fewer threads
   // than items the lanes loop (whole warps per round, so the pool shuffle stays warp-uniform).
   for (int it = threadIdx.x; it < 448; it += blockDim.x) {
