@@ -332,24 +332,38 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
 //   1. each CTA runs forward+backward of its image, accumulating the gradient in its shared G;
 //   2. CTA q pushes slice r (488 floats) of its G into the receive buffer of owner CTA r (st.async
 //      DSMEM stores completing on r's mbarrier); owner r waits for them and sums the 8 slices in rank order;
-//   3. owner r adds its cluster partial into ONE global accumulator as 2^-40 fixed point
+//   3. owner r adds its cluster partial into ONE global accumulator as 2^-32 fixed point
 //      (red.global.add.u64: integer addition is associative, so the sum is the same whatever order
-//      the clusters arrive in -- deterministic run to run), then bumps the slice-r arrival counter;
-//   4. owner r of every cluster waits until all clusters have arrived on slice r (no grid-wide
-//      barrier: only the 8-way slice counter), reads the slice total and applies sgd_step
-//      (network.cpp:171-180) to its copy of slice r;
+//      the clusters arrive in -- deterministic run to run).  Single GPU: each word also counts its
+//      contributions (packed words, kPackBias); fused DP: the owner bumps the slice-r arrival counter;
+//   4. owner r of every cluster waits until all clusters have contributed to slice r (no grid-wide
+//      barrier: per-word counts, or the 8-way slice counter), reads the slice total and applies
+//      sgd_step (network.cpp:171-180) to its copy of slice r;
 //   5. owner r pushes its updated slice into every CTA of its cluster (st.async on their mbarriers);
 //      each CTA waits for the 7 foreign slices.
 // The parameters never round-trip through L2 between steps.  Accumulators are triple-buffered by
-// step; buffer (s+1) % 3 is zeroed by cluster 0 during step s before it signals step s (every CTA
-// that adds into it in step s+1 has observed that signal).  Not the reference's example-order chain:
+// step; with counters, buffer (s+1) % 3 is zeroed by cluster 0 during step s before it signals step s
+// (every CTA that adds into it in step s+1 has observed that signal); packed words are never zeroed.  Not the reference's example-order chain:
 // EXACT mode keeps train_kernel<true>.
 // ------------------------------------------------------------------------------------------------
 constexpr int kCluster = 8;
 constexpr int kSlice = kPStride / kCluster;  // 488 floats per owner CTA
 constexpr int kSlice4 = kSlice / 4;
 static_assert(kSlice % 4 == 0, "slice must be float4-aligned");
-constexpr double kFix = 1099511627776.0;  // 2^40: gradient sums |g| < 2^23 (sigmoid-bounded terms)
+constexpr double kFix = 4294967296.0;  // 2^32 (both schemes: the fused-DP counters and the packed words
+                                       // give bitwise the same sums)
+// Packed accumulator word (single GPU): each cluster adds llrint(sum * 2^32) + 2^51, so a word that has
+// received K contributions since it was last read differs from that read by K * 2^51 + S with
+// |S| < 2^50 (|sums| < 2^18): K = (diff + 2^50) >> 51, S = diff - K * 2^51, all modulo 2^64 -- the
+// count needs no separate counter and the words never need zeroing.  A word of buffer s % 3 gets its
+// next contributions only in step s + 3, after every cluster completed step s + 2, i.e. after every
+// reader of step s.  2^-32 resolution: ~1e-10 absolute on gradient sums (fast mode).
+#ifndef TLB_PACKED_ACC
+#define TLB_PACKED_ACC 1
+#endif
+constexpr double kPackFix = kFix;
+constexpr double kPackUnfix = 1.0 / kPackFix;
+constexpr long long kPackBias = 1ll << 51;
 constexpr double kUnfix = 1.0 / kFix;
 // Cluster-kernel global workspace (in TrainArgs::work): [3][kPStride] u64 gradient accumulators,
 // [3] u64 loss accumulators, [kCluster] u32 slice arrival counters (zeroed by the host per launch).
@@ -409,6 +423,11 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
 
   // group index within the epoch and epoch of step st, advanced incrementally (no per-step division)
   int64_t ks = umod(a.step_begin, a.steps_per_epoch), ep = udiv(a.step_begin, a.steps_per_epoch);
+  // Single-GPU launches use packed accumulators (count + fixed-point sum in one word, see kPackBias);
+  // fused data parallelism keeps the per-slice arrival counters.  packed_prevK: this thread's word of
+  // buffer K as last read (the words are never zeroed: each step reads the difference).
+  const bool packed = TLB_PACKED_ACC && !dp && a.grad_out == nullptr;
+  unsigned long long packed_prev0 = 0ull, packed_prev1 = 0ull, packed_prev2 = 0ull;
   // CTA 0's loss thread: the epoch's running loss sum (a launch may start mid-epoch: resume it)
   double loss_run = (blockIdx.x == 0 && threadIdx.x == kSlice && !a.grad_out && ks != 0) ? a.epoch_loss[ep] : 0.0;
   for (int64_t st = a.step_begin; st < a.step_end; ++st, ks = ks + 1 == a.steps_per_epoch ? (++ep, 0) : ks + 1) {
@@ -470,63 +489,116 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       float sum = rx[threadIdx.x];
 #pragma unroll
       for (int q = 1; q < kCluster; ++q) sum += rx[q * kSlice + threadIdx.x];
-      red_add_u64(acc + b * kPStride + j, __double2ll_rn((double)sum * kFix), dp);
-      if (cid == 0 && owner) acc[bn * kPStride + j] = 0ull;  // next step's accumulator
+      if (packed) {
+        red_add_u64(acc + b * kPStride + j, __double2ll_rn((double)sum * kPackFix) + kPackBias, false);
+      } else {
+        red_add_u64(acc + b * kPStride + j, __double2ll_rn((double)sum * kFix), dp);
+        if (cid == 0 && owner) acc[bn * kPStride + j] = 0ull;  // next step's accumulator
+      }
     }
     if (rank == 0 && threadIdx.x == kSlice) {
       double l = 0.0;
       for (int q = 0; q < kCluster; ++q) l = __dadd_rn(l, loss_rx[q]);
-      red_add_u64(lacc + b, __double2ll_rn(l * kFix), dp);
-      if (cid == 0 && (!dp || a.dp_rank == 0)) lacc[bn] = 0ull;
-    }
-    __syncthreads();
-    mark(s, 14);
-    // ---- 3/4. arrival on slice `rank`, then wait for every cluster's (and every GPU's) contribution ----
-    // Thread 0 arrives and polls (per-thread polling floods the counters' L2 lines: +0.6 us).  Release
-    // at gpu/sys scope is cumulative over the CTA's adds, which the barrier above orders before it.
-    if (threadIdx.x == 0) {
-      int t_out = 0;
-      if (dp) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
-      else asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
-      const unsigned int want = (unsigned int)((seq + 1) * ncl * (uint64_t)world);
-      unsigned int v;
-      const long long t0 = clock64();
-      for (;;) {
-        if (dp) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-        else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-        if ((int)(v - want) >= 0) break;
-        if (dp && clock64() - t0 > a.dp_timeout_cycles) {  // a peer never arrived: fail, do not hang
-          atomicExch(a.dp_error, 1u);
-          t_out = 1;
-          break;
-        }
-        __nanosleep(32);
-      }
-      loss_rx[kCluster] = t_out;  // (slot past the losses) broadcast through the barrier below
-    }
-    __syncthreads();
-    const int to = (int)loss_rx[kCluster];
-    if (to) return;
-    mark(s, 11);
-    if (threadIdx.x < kSlice) {
-      const long long t = (long long)(dp ? ld_sys_u64(acc + b * kPStride + j) : __ldcg(acc + b * kPStride + j));
-      if (j < kNParam) {
-        const float gsum = (float)((double)t * kUnfix);
-        if (a.grad_out) {  // data-parallel shard: the shard's gradient sum goes to the allreduce
-          if (cid == 0) a.grad_out[j] = gsum;
-        } else {
-          s.P[j] = fsub(s.P[j], fmul(a.rate, __fdiv_rn(gsum, (float)m_global)));
-          if (cid == 0) __stcg(a.params + j, s.P[j]);
-        }
+      if (packed) {
+        red_add_u64(lacc + b, __double2ll_rn(l * kPackFix) + kPackBias, false);
+      } else {
+        red_add_u64(lacc + b, __double2ll_rn(l * kFix), dp);
+        if (cid == 0 && (!dp || a.dp_rank == 0)) lacc[bn] = 0ull;
       }
     }
-    if (blockIdx.x == 0 && threadIdx.x == kSlice) {
-      const double l = (double)(long long)(dp ? ld_sys_u64(lacc + b) : __ldcg(lacc + b)) * kUnfix;
-      if (a.grad_out) {
-        a.loss_out[0] = l;
-      } else {  // running epoch sum kept in a register: no dependent L2 read on CTA 0's critical path
+    if (packed) {
+      // ---- 3/4 (single GPU). Each accumulator word counts its own contributions (see kPackBias): the
+      // owner threads wait for their words' ncl-th contribution and read the sum in the same L2 round
+      // trip -- no arrival counter, no barrier between the adds and the SGD.  Lane 0 of a warp polls
+      // first (its word completes with the others of the burst), then each lane confirms its own.
+      mark(s, 14);
+      int64_t dsum = 0;
+      if (threadIdx.x < kSlice || (blockIdx.x == 0 && threadIdx.x == kSlice)) {
+        const unsigned long long* w = threadIdx.x < kSlice ? acc + b * kPStride + j : lacc + b;
+        unsigned long long prev = b == 0 ? packed_prev0 : b == 1 ? packed_prev1 : packed_prev2;
+        const unsigned long long want = (unsigned long long)ncl;
+        auto count_of = [&](unsigned long long v) { return (v - prev + (1ull << 50)) >> 51; };
+        unsigned long long v;
+        if ((threadIdx.x & 31) == 0) {
+          for (;;) {
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(w) : "memory");
+            if (count_of(v) >= want) break;
+            __nanosleep(32);
+          }
+        }
+        __syncwarp(__activemask());
+        for (;;) {
+          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(w) : "memory");
+          if (count_of(v) >= want) break;
+          __nanosleep(32);
+        }
+        dsum = (int64_t)(v - prev - want * (unsigned long long)kPackBias);
+        if (b == 0) packed_prev0 = v;
+        else if (b == 1) packed_prev1 = v;
+        else packed_prev2 = v;
+      }
+      mark(s, 11);
+      if (threadIdx.x < kSlice && j < kNParam) {
+        const float gsum = (float)((double)dsum * kPackUnfix);
+        s.P[j] = fsub(s.P[j], fmul(a.rate, __fdiv_rn(gsum, (float)m_global)));
+        if (cid == 0) __stcg(a.params + j, s.P[j]);
+      }
+      if (blockIdx.x == 0 && threadIdx.x == kSlice) {
+        const double l = (double)dsum * kPackUnfix;
         loss_run = (ks != 0 ? loss_run : 0.0) + l;
         a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(loss_run, (double)a.n) : loss_run;
+      }
+    }
+    if (!packed) {
+      __syncthreads();
+      mark(s, 14);
+      // ---- 3/4. arrival on slice `rank`, then wait for every cluster's (and every GPU's) contribution ----
+      // Thread 0 arrives and polls (per-thread polling floods the counters' L2 lines: +0.6 us).  Release
+      // at gpu/sys scope is cumulative over the CTA's adds, which the barrier above orders before it.
+      if (threadIdx.x == 0) {
+        int t_out = 0;
+        if (dp) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+        else asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+        const unsigned int want = (unsigned int)((seq + 1) * ncl * (uint64_t)world);
+        unsigned int v;
+        const long long t0 = clock64();
+        for (;;) {
+          if (dp) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+          else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+          if ((int)(v - want) >= 0) break;
+          if (dp && clock64() - t0 > a.dp_timeout_cycles) {  // a peer never arrived: fail, do not hang
+            atomicExch(a.dp_error, 1u);
+            t_out = 1;
+            break;
+          }
+          __nanosleep(32);
+        }
+        loss_rx[kCluster] = t_out;  // (slot past the losses) broadcast through the barrier below
+      }
+      __syncthreads();
+      const int to = (int)loss_rx[kCluster];
+      if (to) return;
+      mark(s, 11);
+      if (threadIdx.x < kSlice) {
+        const long long t = (long long)(dp ? ld_sys_u64(acc + b * kPStride + j) : __ldcg(acc + b * kPStride + j));
+        if (j < kNParam) {
+          const float gsum = (float)((double)t * kUnfix);
+          if (a.grad_out) {  // data-parallel shard: the shard's gradient sum goes to the allreduce
+            if (cid == 0) a.grad_out[j] = gsum;
+          } else {
+            s.P[j] = fsub(s.P[j], fmul(a.rate, __fdiv_rn(gsum, (float)m_global)));
+            if (cid == 0) __stcg(a.params + j, s.P[j]);
+          }
+        }
+      }
+      if (blockIdx.x == 0 && threadIdx.x == kSlice) {
+        const double l = (double)(long long)(dp ? ld_sys_u64(lacc + b) : __ldcg(lacc + b)) * kUnfix;
+        if (a.grad_out) {
+          a.loss_out[0] = l;
+        } else {  // running epoch sum kept in a register: no dependent L2 read on CTA 0's critical path
+          loss_run = (ks != 0 ? loss_run : 0.0) + l;
+          a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(loss_run, (double)a.n) : loss_run;
+        }
       }
     }
     __syncthreads();
