@@ -383,20 +383,23 @@ __device__ __forceinline__ unsigned long long ld_sys_u64(const unsigned long lon
 
 __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a) {
   static_assert(StageCfg<false>::conv2_back != 3, "the DSMEM receive buffer reuses the backin term buffer");
-  static_assert(TLB_CLUSTER_KP || (StageCfg<false>::conv2 == 2 && StageCfg<false>::conv2_back >= 9),
+  static_assert(StageCfg<false>::conv2 == 2 && StageCfg<false>::conv2_back >= 9,
                 "the clustered kernel keeps no padded k2 copy (Kp): its stages must read k2 from P");
   Smem s = carve_smem(tlb_smem);
   float* const rx = s.term;   // [8 source ranks][488]: slices pushed to this CTA (it owns slice `rank`)
   __shared__ double loss_rx[kCluster + 1];  // rank 0: the 8 CTAs' fp64 loss sums of the step (pushed);
                                              // [kCluster]: this CTA's DP-timeout flag
   // xbar[0]: the step's gradient slices (and, on rank 0, losses) have landed in rx / loss_rx;
-  // xbar[1]: the other owners' updated parameter slices have landed in P.  Peers write with st.async
+  // xbar[1]: parameter slice 0 (k1, b1: all conv1 reads) has landed in P; xbar[2]: the other foreign
+  // slices have.  On one GPU a step waits for xbar[1] only and the next step's conv1 runs while slices
+  // 1-7 arrive; it waits for xbar[2] after conv1.  Peers write with st.async
   // (complete_tx on these barriers), so no cluster-wide release/acquire barrier sits in the step.
-  __shared__ __align__(8) uint64_t xbar[2];
+  __shared__ __align__(8) uint64_t xbar[3];
   smem_setup(s);
   if (threadIdx.x == 0) {
     mbar_init(&xbar[0], 1);
     mbar_init(&xbar[1], 1);
+    mbar_init(&xbar[2], 1);
     fence_barrier_init();
   }
   cluster_sync_all();  // every CTA of the cluster is running (barriers initialised) before peers store into it
@@ -460,7 +463,10 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
           }
         }
       }
-      forward_image<false>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf);
+      // (single GPU: parameter slices 1-7 of the previous step's update land during conv1)
+      const bool pending = !dp && ls > 0;
+      forward_image<false>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf, pending ? &xbar[2] : nullptr,
+                           (uint32_t)((ls - 1) & 1));
       if (threadIdx.x == 0) cta_loss = __dadd_rn(cta_loss, (double)example_loss(s, s.lab[buf], nullptr));
       backward_image<false, true>(s, s.img + buf * kImg, nullptr);
       ++consumed;
@@ -604,29 +610,31 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     __syncthreads();
     mark(s, 12);
     // ---- 5. push the updated slice into the other CTAs of the cluster ----
+    // slice 0 goes to the peers' xbar[1], slices 1-7 to their xbar[2]
+    uint64_t* const pbar = rank == 0 ? &xbar[1] : &xbar[2];
     for (int i = threadIdx.x; i < (kCluster - 1) * kSlice4; i += blockDim.x) {
       const int qi = i / kSlice4, q = qi < (int)rank ? qi : qi + 1;
       const int o = (int)rank * kSlice + 4 * (i - qi * kSlice4);
-      st_async_v4(dsmem_map(s.P + o, q), *reinterpret_cast<const float4*>(s.P + o), dsmem_map(&xbar[1], q));
+      st_async_v4(dsmem_map(s.P + o, q), *reinterpret_cast<const float4*>(s.P + o), dsmem_map(pbar, q));
     }
-    if (threadIdx.x == 0) mbar_arrive_expect_tx(&xbar[1], (kCluster - 1) * kSlice * sizeof(float));
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&xbar[1], rank == 0 ? 0u : (uint32_t)(kSlice * sizeof(float)));
+      mbar_arrive_expect_tx(&xbar[2], (uint32_t)((rank == 0 ? kCluster - 1 : kCluster - 2) * kSlice * sizeof(float)));
+    }
     if (!dp) {
-      mbar_wait_cluster(&xbar[1], parity);  // every other owner's slice has landed here
-    } else if (__syncthreads_or(!mbar_wait_cluster_for(&xbar[1], parity, a.dp_timeout_cycles))) {
+      mbar_wait_cluster(&xbar[1], parity);  // slice 0 has landed (slices 1-7: after the next conv1)
+    } else if (__syncthreads_or(!mbar_wait_cluster_for(&xbar[1], parity, a.dp_timeout_cycles) ||
+                                !mbar_wait_cluster_for(&xbar[2], parity, a.dp_timeout_cycles))) {
       if (threadIdx.x == 0) atomicExch(a.dp_error, 1u);
       return;
     }
     mark(s, 15);
-#if TLB_CLUSTER_KP  // A/B switch: keep the padded k2 copy (conv2 reading Kp)
-    for (int idx = threadIdx.x; idx < kKp; idx += blockDim.x) {
-      const int row = idx >> 3, k = idx & 7;
-      s.Kp[idx] = k < 5 ? s.P[kK2 + row * 5 + k] : 0.0f;
-    }
-    __syncthreads();
-#endif  // otherwise no padded k2 copy to rebuild: the fast stages read k2 from P
     mark(s, 13);
   }
-  if (!dp) cluster_sync_all();  // no CTA leaves while a peer's DSMEM traffic may still target it
+  if (!dp) {
+    if (a.step_end > a.step_begin) mbar_wait_cluster(&xbar[2], (uint32_t)((a.step_end - a.step_begin - 1) & 1));
+    cluster_sync_all();  // no CTA leaves while a peer's DSMEM traffic may still target it
+  }
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -1538,9 +1538,6 @@ __device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float*
 #ifndef TLB_FAST_CONV2_V
 #define TLB_FAST_CONV2_V 2
 #endif
-#ifndef TLB_CLUSTER_KP
-#define TLB_CLUSTER_KP 0
-#endif
 #ifndef TLB_CONV2_BACK_V
 #define TLB_CONV2_BACK_V(EXACT) ((EXACT) ? 1 : 14)
 #endif
@@ -1585,10 +1582,13 @@ __device__ __noinline__ void call_conv1_back(const float* img, float* row) {
 // after conv1's barrier.
 template <bool EXACT>
 __device__ __forceinline__ void forward_image(const Smem& s, const float* img, int label, const float* y,
-                                              bool want_dz, const int* lab = nullptr) {
+                                              bool want_dz, const int* lab = nullptr, uint64_t* post_conv1 = nullptr,
+                                              uint32_t post_conv1_parity = 0) {
   call_conv1<EXACT>(img);
   __syncthreads();
   if (lab) label = *lab;
+  // clustered kernel: the parameters conv2 and later stages read may still be arriving during conv1
+  if (post_conv1) mbar_wait_cluster(post_conv1, post_conv1_parity);
   mark(s, 3);
   call_conv2<EXACT>();  // includes avgpool
   __syncthreads();
