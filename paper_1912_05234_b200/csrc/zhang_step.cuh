@@ -36,6 +36,12 @@ constexpr int kThreads = 512;
 #ifndef TLB_CONV1_ROWS2
 #define TLB_CONV1_ROWS2 1  // fast conv1: 1 = two rows x 8 columns per lane, 2 = two rows x 4, 0 = row strips
 #endif
+#ifndef TLB_V15_C1_LANES
+#define TLB_V15_C1_LANES 0
+#endif
+#ifndef TLB_EXACT_GK2_SPLIT
+#define TLB_EXACT_GK2_SPLIT 224  // EXACT V15: ordered g_k2 chains beside backin (the rest beside C1)
+#endif
 #ifndef TLB_GK2R_SPLIT
 #define TLB_GK2R_SPLIT 96  // row-form g_k2 lanes beside backin, the rest beside the C1 gradient (A/B: 64-160 best)
 #endif
@@ -1118,9 +1124,76 @@ __device__ __forceinline__ void backin_rows(const Smem& s, int t) {
   }
 }
 
+// EXACT backin in scatter form, bit-identical to the reference's clipped nested sums (nn.cpp:169-189,
+// network.cpp:135-138).  Lane = (channel c, d_s1 row p, kernel split of 3) as in backin_rows.  Per
+// kernel i and per valid tap row ky (ascending, = off1 + u1; dz2 row y = p - ky), the twelve row sums
+// rs[q] start at +0 and take k2[i][c][ky][kx] * dz2[i][y][q - kx] over the valid kx in ascending order
+// (kx outer, x inner: each output sees its kx in order), each product rounded then added (no FMA);
+// then b_i[q] = b_i[q] + rs[q] (the outer sum, from +0).  Only valid terms are formed -- the clipped
+// sums add exactly these, in this order.  Finally d_s1[q] = ((0 + b_0[q]) + b_1[q]) + ... + b_11[q]:
+// the four split lanes pass their per-kernel terms to part 0 by shuffle in kernel order.
+__device__ __forceinline__ void backin_rows_exact(const Smem& s, int t) {
+  constexpr int SPLITS = 4, KPL = 3;
+  const bool valid = t < 72 * SPLITS;
+  const int combo = valid ? t / SPLITS : 0, part = t % SPLITS;
+  const int p = backin_row_of(combo / 6), c = combo - (combo / 6) * 6;
+  float b[KPL][12];
+#pragma unroll
+  for (int k = 0; k < KPL; ++k) {
+    const int i = part * KPL + k;
+    const float* wp = s.P + kK2 + (i * 6 + c) * 25;
+#pragma unroll
+    for (int q = 0; q < 12; ++q) b[k][q] = 0.0f;
+#pragma unroll
+    for (int ky = 0; ky < 5; ++ky) {
+      const int y = p - ky;
+      if (y < 0 || y > 7) continue;
+      const float4* dp = reinterpret_cast<const float4*>(s.dzp + dzp_at(i, y + 4, 4));
+      const float4 d0 = dp[0], d1 = dp[1];
+      const float d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+      float w[5];
+#pragma unroll
+      for (int kx = 0; kx < 5; ++kx) w[kx] = wp[ky * 5 + kx];
+      float rs[12];
+#pragma unroll
+      for (int q = 0; q < 12; ++q) rs[q] = 0.0f;
+#pragma unroll
+      for (int kx = 0; kx < 5; ++kx)
+#pragma unroll
+        for (int x = 0; x < 8; ++x) rs[x + kx] = fadd(rs[x + kx], fmul(w[kx], d[x]));
+#pragma unroll
+      for (int q = 0; q < 12; ++q) b[k][q] = fadd(b[k][q], rs[q]);
+    }
+  }
+  const int base = (threadIdx.x & 31) & ~(SPLITS - 1);
+  float acc[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) acc[q] = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 12; ++i)
+#pragma unroll
+    for (int q = 0; q < 12; ++q) acc[q] = fadd(acc[q], __shfl_sync(0xffffffffu, b[i % KPL][q], base + i / KPL));
+  if (!valid || part != 0) return;
+#pragma unroll
+  for (int dy = 0; dy < 2; ++dy) {  // backavgpool (x0.25) + backsigmoid through c1 -> dz1, 24 columns
+    float* cp = s.c1 + c1_at(c, 2 * p + dy, 0);
+#pragma unroll
+    for (int q4 = 0; q4 < 6; ++q4) {
+      float4 v = reinterpret_cast<float4*>(cp)[q4];
+      const float dc0 = fmul(acc[2 * q4], 0.25f), dc1 = fmul(acc[2 * q4 + 1], 0.25f);
+      v.x = fmul(fmul(dc0, v.x), fsub(1.0f, v.x));
+      v.y = fmul(fmul(dc0, v.y), fsub(1.0f, v.y));
+      v.z = fmul(fmul(dc1, v.z), fsub(1.0f, v.z));
+      v.w = fmul(fmul(dc1, v.w), fsub(1.0f, v.w));
+      reinterpret_cast<float4*>(cp)[q4] = v;
+    }
+  }
+}
+
 // g_k2 quad lanes done beside the scatter-form backin in conv2_back variants 10..13 (whole warps).
 __host__ __device__ constexpr int gk2_split_lanes(int V) {
-  return V == 10 ? 224 : V == 11 ? 160 : V == 12 ? 192 : V == 13 ? 128 : V == 14 ? TLB_GK2R_SPLIT : 0;
+  return V == 10 ? 224 : V == 11 ? 160 : V == 12 ? 192 : V == 13 ? 128 : V == 14 ? TLB_GK2R_SPLIT
+       : V == 15 ? TLB_EXACT_GK2_SPLIT : 0;
 }
 
 // C2 backward stage.  V = 0: backin lane quads on warps 0-13 (432 lanes), then the g_k2/g_b2 lanes;
@@ -1168,6 +1241,14 @@ __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
     // g_k2/g_b2 runs beside the C1 gradient
     static_assert(!EXACT, "scatter-form backin reorders the reference's sums");
     for (int it = threadIdx.x; it < 288; it += blockDim.x) backin_rows<4, true>(s, it);
+  } else if constexpr (V == 15) {
+    // V = 15 (EXACT): scatter-form exact backin on warps 0-8 beside ordered g_k2 chains 0-223 on warps
+    // 9-15; chains 224-371 run beside the C1 gradient
+    static_assert(EXACT, "V15 is the EXACT schedule");
+    for (int it = threadIdx.x; it < 288 + gk2_split_lanes(15); it += blockDim.x) {
+      if (it < 288) backin_rows_exact(s, it);
+      else gk2_exact<ACCUM>(s, row, it - 288);
+    }
   } else if constexpr (V == 14) {
     // V = 14 (fast only): backin rows on warps 0-8 beside g_k2 row lanes 0-223 on warps 9-15; row
     // lanes 224-359 run beside the C1 gradient
@@ -1519,6 +1600,19 @@ __device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float*
     }
   }
   static_assert(!ROWS || !EXACT, "row-form g_k2 is a fast-mode stage");
+  if constexpr (EXACT && GLO > 0) {  // V15: ordered C1 chains on the first warps, g_k2 chains after them
+    constexpr int kC1 = TLB_V15_C1_LANES ? 160 : 96;  // one chain per lane (5 warps) | blocked (3 warps)
+    if (t < kC1) {
+      if constexpr (TLB_V15_C1_LANES) {
+        if (t < 156) stage_conv1_back_lane_exact<ACCUM>(s, row, t);
+      } else {
+        stage_conv1_back_exact_blocked<ACCUM>(s, img, row);
+      }
+    } else {
+      for (int item = GLO + t - kC1; item < kGk2; item += blockDim.x - kC1) gk2_exact<ACCUM>(s, row, item);
+    }
+    return;
+  }
   if (t < 160) {
     if constexpr (EXACT) {
       if (t < 156) stage_conv1_back_lane_exact<ACCUM>(s, row, t);
@@ -1538,8 +1632,11 @@ __device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float*
 #ifndef TLB_FAST_CONV2_V
 #define TLB_FAST_CONV2_V 2
 #endif
+#ifndef TLB_EXACT_CONV2_BACK_V
+#define TLB_EXACT_CONV2_BACK_V 15
+#endif
 #ifndef TLB_CONV2_BACK_V
-#define TLB_CONV2_BACK_V(EXACT) ((EXACT) ? 1 : 14)
+#define TLB_CONV2_BACK_V(EXACT) ((EXACT) ? TLB_EXACT_CONV2_BACK_V : 14)
 #endif
 template <bool EXACT>
 struct StageCfg {
