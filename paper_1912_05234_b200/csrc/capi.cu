@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -67,6 +69,26 @@ struct DevBuf {
   }
 };
 
+struct HostBuf {  // pinned host memory (async H2D/D2H staging of small per-call blocks)
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(bytes, 4096);
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
 struct tlb_ctx {
   int device = 0;
   int sm_count = 0;
@@ -93,6 +115,7 @@ struct tlb_ctx {
   cudaEvent_t copy_gate = nullptr;
   DevBuf ready;
   DevBuf ready_err;  // [3] u32 ingestion watchdog words (flag, chunk, observed value)
+  HostBuf pin;       // tlb_train: pinned params / losses / watchdog words
   unsigned int ready_token = 0;
   DevBuf synth_snaps;  // device synthetic corpus: mt19937_64 state snapshots per segment
   // Widened-network workspaces (capacity `wide_cap` images) and the last group's arguments.
@@ -268,11 +291,11 @@ int64_t geo_chunk_start(int64_t k) {
 // the halves of each [2^e, 2^(e+1))), see TrainArgs::chunk.  The copy stream first waits for all earlier work on the
 // context stream (buffer reuse).
 int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t chunk, int64_t batch,
-                  unsigned int token) {
+                  unsigned int token, int64_t head = 0) {
   TLB_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));  // recorded by the caller
   unsigned int* flags = static_cast<unsigned int*>(c->ready.p);
   for (int64_t k = 0, lo = 0; lo < n; ++k) {
-    const int64_t hi = chunk > 0 ? lo + chunk : geo_chunk_start(k + 1) * batch;
+    const int64_t hi = chunk > 0 ? lo + (k == 0 && head > 0 ? head : chunk) : geo_chunk_start(k + 1) * batch;
     const int64_t cnt = std::min(hi, n) - lo;
     TLB_CUDA(cudaMemcpyAsync(dev + lo * 784, host + lo * 784, (size_t)cnt * 784 * sizeof(float),
                              cudaMemcpyHostToDevice, c->copy_stream));
@@ -285,7 +308,8 @@ int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t 
 }
 
 // Number of ingestion chunks for n images (see ingest_images).
-int64_t ingest_chunks(int64_t n, int64_t chunk, int64_t batch) {
+int64_t ingest_chunks(int64_t n, int64_t chunk, int64_t batch, int64_t head = 0) {
+  if (chunk > 0 && head > 0) return n <= head ? 1 : 1 + (n - head + chunk - 1) / chunk;
   if (chunk > 0) return (n + chunk - 1) / chunk;
   const int64_t groups = (n + batch - 1) / batch;
   int64_t k = 0;
@@ -324,7 +348,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
                   float rate, int32_t epoch_begin, int32_t epochs, int64_t batch, double* d_epoch_loss,
                   int64_t shard_lo = 0, int64_t shard_hi = 0, int64_t group = -1, float* grad_out = nullptr,
                   double* loss_out = nullptr, const unsigned int* ready = nullptr, unsigned int token = 0,
-                  int64_t chunk = 1, const DpArgs* dp = nullptr) {
+                  int64_t chunk = 1, const DpArgs* dp = nullptr, int64_t chunk_head = 0) {
   const int64_t spe = (n + batch - 1) / batch;
   const int64_t m_max = std::min<int64_t>(batch, n);
   const int64_t m_local = grad_out ? std::max<int64_t>(0, std::min(shard_hi, m_max) - shard_lo) : m_max;
@@ -373,6 +397,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.ready_err = static_cast<unsigned int*>(c->ready_err.p);
   a.ready_token = token;
   a.chunk = chunk;
+  a.chunk_head = chunk_head;
   a.ready_step_end = a.step_begin + spe;  // only the call's first epoch can outrun the copies
   if (clustered) {
     if (dp) {  // fused data parallelism: slice s lives on rank s % world (peer memory)
@@ -471,6 +496,7 @@ int tlb_ctx_destroy(tlb_ctx* c) {
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   c->ready.release();
   c->ready_err.release();
+  c->pin.release();
   for (auto& w : c->wide) w.release();
   c->synth_snaps.release();
   if (c->copy_gate) cudaEventDestroy(c->copy_gate);
@@ -543,8 +569,25 @@ int tlb_synchronize(tlb_ctx* c) {
 }
 
 // ---- network, host buffers ------------------------------------------------------------------
+// TLB_HOST_TRACE=1: per-call host timeline of tlb_train on stderr (developer diagnostics of the e2e path).
+struct HostTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  std::string log;
+  HostTrace() : on(std::getenv("TLB_HOST_TRACE") != nullptr), t0(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    log += std::string(" ") + what + "=" + std::to_string((int)us);
+  }
+  ~HostTrace() {
+    if (on) fprintf(stderr, "tlb_train host us:%s\n", log.c_str());
+  }
+};
+
 int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n, float* params, float rate,
               int32_t epochs, int64_t batch, double* epoch_loss, tlb_epoch_cb on_epoch, void* user) {
+  HostTrace ht;
   if (!c || !params) return fail(TLB_ERR_ARG, "tlb_train: null argument");
   TLB_TRY(check_train_args(n, epochs, rate, batch));
   if (!images || !labels) return fail(TLB_ERR_ARG, "tlb_train: null dataset");
@@ -552,6 +595,7 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
     if (labels[i] < 0 || labels[i] > 9)
       return fail(TLB_ERR_VALUE, "one_hot: label " + std::to_string(labels[i]) + " out of range 0..9");
   TLB_TRY(set_device(c));
+  ht.mark("checked");
   if (epochs == 0) return TLB_OK;
   float* d_img;
   int32_t* d_lab;
@@ -570,7 +614,9 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   const int64_t group_bytes = batch * 784 * (int64_t)sizeof(float);
   const int64_t chunk = chunk_env >= 0 ? chunk_env
                                        : batch * std::max<int64_t>(1, (512 * 1024 + group_bytes - 1) / group_bytes);
-  const int64_t nchunks = ingest_chunks(n, chunk, batch);
+  // the first chunk is the first SGD group alone: the first step can start once it is resident
+  const int64_t head = (chunk_env < 0 && chunk > batch) ? batch : 0;
+  const int64_t nchunks = ingest_chunks(n, chunk, batch, head);
   const bool overlap = write_value32() != nullptr;
   TLB_TRY(stage_out(c, 0, (size_t)n * 784, &d_img));
   if (overlap) {
@@ -595,40 +641,55 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   TLB_TRY(stage_in(c, 1, labels, (size_t)n, &d_lab));
   TLB_TRY(stage_out(c, 2, TLB_PSTRIDE, &d_p));
   TLB_CUDA(cudaMemsetAsync(d_p, 0, TLB_PSTRIDE * sizeof(float), c->stream));
-  TLB_CUDA(cudaMemcpyAsync(d_p, params, TLB_NPARAM * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  // params / losses / watchdog words travel through a pinned host block (async copies, one sync)
+  const size_t pin_bytes = TLB_PSTRIDE * sizeof(float) + (size_t)epochs * sizeof(double) + 4 * sizeof(unsigned int);
+  TLB_CUDA(c->pin.ensure(pin_bytes));
+  float* h_p = static_cast<float*>(c->pin.p);
+  double* h_loss = reinterpret_cast<double*>(h_p + TLB_PSTRIDE);
+  unsigned int* h_err = reinterpret_cast<unsigned int*>(h_loss + epochs);
+  std::memcpy(h_p, params, TLB_NPARAM * sizeof(float));
+  TLB_CUDA(cudaMemcpyAsync(d_p, h_p, TLB_NPARAM * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   TLB_TRY(stage_out(c, 3, (size_t)epochs, &d_loss));
   // Pinned source: launch the kernel first, then enqueue the chunk copies (the host's ~200 enqueue calls
   // overlap the running kernel, which polls the ready flags).  Pageable source: copies first -- the
   // driver stages pageable memory synchronously on the host.
+  ht.mark("staged");
   const bool copies_first = overlap && !is_pinned(images);
-  if (copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token));
+  if (copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token, head));
   if (!on_epoch) {
     TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, 0, epochs, batch, d_loss, 0, 0, -1, nullptr, nullptr,
-                          rdy, c->ready_token, chunk));
-    if (overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token));
+                          rdy, c->ready_token, chunk, nullptr, head));
+    ht.mark("launched");
+    if (overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token, head));
+    ht.mark("ingest_enqueued");
   } else {
     for (int32_t e = 0; e < epochs; ++e) {
       TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, e, 1, batch, d_loss, 0, 0, -1, nullptr, nullptr,
-                            e == 0 ? rdy : nullptr, c->ready_token, chunk));
-      if (e == 0 && overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token));
+                            e == 0 ? rdy : nullptr, c->ready_token, chunk, nullptr, head));
+      if (e == 0 && overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token, head));
       double mean = 0.0;
       TLB_TRY(fetch(c, &mean, d_loss + e, 1));
       on_epoch(e + 1, mean, user);
     }
   }
-  TLB_CUDA(cudaMemcpyAsync(params, d_p, TLB_NPARAM * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-  if (epoch_loss) TLB_CUDA(cudaMemcpyAsync(epoch_loss, d_loss, epochs * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  TLB_CUDA(cudaMemcpyAsync(h_p, d_p, TLB_NPARAM * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  if (epoch_loss) TLB_CUDA(cudaMemcpyAsync(h_loss, d_loss, epochs * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (overlap) TLB_CUDA(cudaMemcpyAsync(h_err, c->ready_err.p, 3 * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+  ht.mark("d2h_enqueued");
   TLB_CUDA(cudaStreamSynchronize(c->stream));
+  ht.mark("stream_synced");
+  std::memcpy(params, h_p, TLB_NPARAM * sizeof(float));
+  if (epoch_loss) std::memcpy(epoch_loss, h_loss, epochs * sizeof(double));
   if (overlap) {
-    TLB_CUDA(cudaStreamSynchronize(c->copy_stream));
-    unsigned int err[3] = {0, 0, 0};
-    TLB_CUDA(cudaMemcpy(err, c->ready_err.p, sizeof(err), cudaMemcpyDeviceToHost));
+    TLB_CUDA(cudaStreamSynchronize(c->copy_stream));  // (the kernel consumed every chunk: already done)
+    const unsigned int err[3] = {h_err[0], h_err[1], h_err[2]};
     if (err[0]) {
       TLB_CUDA(cudaMemset(c->ready_err.p, 0, sizeof(err)));
       return fail(TLB_ERR_CUDA, "tlb_train: dataset chunk " + std::to_string(err[1]) + " never became ready (flag " +
                                     std::to_string(err[2]) + ", token " + std::to_string(c->ready_token) + ")");
     }
   }
+  ht.mark("done");
   return TLB_OK;
 }
 

@@ -38,6 +38,7 @@ struct TrainArgs {
   const unsigned int* ready;
   unsigned int ready_token;
   int64_t chunk;
+  int64_t chunk_head;  // chunk > 0: the first chunk holds chunk_head images (0 = chunk), the rest chunk each
   int64_t ready_step_end;
   unsigned int* ready_err;  // [3] diagnostic words: set when a ready flag never arrives (then the kernel
                             // proceeds and the host call fails instead of hanging)

@@ -99,7 +99,9 @@ __device__ __forceinline__ void wait_ready(const TrainArgs& a, const Job& j) {
   if (!a.ready || j.step >= a.ready_step_end) return;
   int64_t k;
   if (a.chunk > 0) {
-    k = udiv(job_index(a, j), a.chunk);
+    const int64_t idx = job_index(a, j);
+    if (a.chunk_head > 0) k = idx < a.chunk_head ? 0 : 1 + udiv(idx - a.chunk_head, a.chunk);
+    else k = udiv(idx, a.chunk);
   } else {  // geometric (see TrainArgs::chunk): groups 0, 1, then [2^e, 2^e + 2^(e-1)), [.., 2^(e+1))
     const int64_t g = umod(j.step, a.steps_per_epoch);
     if (g < 2) {
