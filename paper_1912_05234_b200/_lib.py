@@ -59,7 +59,8 @@ _SIGS = {
     "tlb_synth_make_digits": (C.c_int, [C.c_int64, C.c_uint64, u8p, i32p]),
     "tlb_synth_make_set": (C.c_int, [C.c_int64, C.c_uint64, f32p, i32p]),
     "tlb_validate_set": (C.c_int, [f32p, i32p, C.c_int64]),
-    "tlb_train": (C.c_int, [vp, f32p, i32p, C.c_int64, f32p, C.c_float, C.c_int32, C.c_int64, f64p, EPOCH_CB, vp]),
+    # raw addresses (c_void_p) on the e2e path: ~4 us per ctypes pointer conversion avoided per call
+    "tlb_train": (C.c_int, [vp, vp, vp, C.c_int64, vp, C.c_float, C.c_int32, C.c_int64, vp, EPOCH_CB, vp]),
     "tlb_forward": (C.c_int, [vp, f32p, C.c_int64, f32p, f32p, f32p]),
     "tlb_forward_backward": (C.c_int, [vp, f32p, i32p, f32p, C.c_int64, f32p, f32p, f32p]),
     "tlb_backward": (C.c_int, [vp, f32p, f32p, f32p, C.c_int64, f32p, f32p]),

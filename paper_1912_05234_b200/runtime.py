@@ -31,6 +31,9 @@ def _ip(a: Optional[np.ndarray]):
     return a.ctypes.data_as(i32p) if a is not None else None
 
 
+_NO_EPOCH_CB = _lib.EPOCH_CB()  # null callback
+
+
 def _shape(s) -> np.ndarray:
     return np.ascontiguousarray(list(s), dtype=np.int64)
 
@@ -162,9 +165,9 @@ class Context:
         p = np.array(params, np.float32, copy=True)
         images, labels = _f32(images), np.ascontiguousarray(labels, np.int32)
         losses = np.zeros(max(epochs, 1), np.float64)
-        cb = _lib.EPOCH_CB(lambda e, l, _u: on_epoch(e, l)) if on_epoch else _lib.EPOCH_CB()
-        _check(self._L.tlb_train(self._h, _fp(images), _ip(labels), len(labels), _fp(p), rate, epochs, batch,
-                                 losses.ctypes.data_as(_lib.f64p), cb, None))
+        cb = _lib.EPOCH_CB(lambda e, l, _u: on_epoch(e, l)) if on_epoch else _NO_EPOCH_CB
+        _check(self._L.tlb_train(self._h, images.ctypes.data, labels.ctypes.data, len(labels), p.ctypes.data, rate,
+                                 epochs, batch, losses.ctypes.data, cb, None))
         return p, losses[: max(epochs, 0)]
 
     def forward(self, images, params, acts: bool = False):
