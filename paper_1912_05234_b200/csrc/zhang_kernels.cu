@@ -8,6 +8,9 @@
 //                         reference's parallel_build cell) or one per-CTA partial (fast); grid barrier;
 //                         fixed-order reduction + sgd_step over the 3,898 parameters and the fp64
 //                         epoch-loss sum (network.cpp:236-248); grid barrier.
+//  * train_cluster_kernel the fast persistent kernel for groups that fit one image per CTA: 8-CTA
+//                         clusters, DSMEM (st.async + mbarrier) exchange, packed fixed-point
+//                         accumulators in L2, parameters resident in shared memory (see below).
 //  * cells_kernel<EXACT>  per-example forward(+backward) rows / activations (net::forward/backward).
 //  * eval_kernel<EXACT>   forward + argmax + correct count (net::predict / net::evaluate).
 //  * sgd_kernel           net::sgd_step on a reduced gradient (also the post-allreduce step of DP).

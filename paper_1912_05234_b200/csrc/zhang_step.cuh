@@ -8,10 +8,14 @@
 // Every stage maps the reference's per-output computation onto CTA threads.  With EXACT=true each
 // output is produced in exactly the reference's summation order with separately rounded products (no
 // FMA), the glibc expf restatement and IEEE reciprocal, so results are bitwise identical to the
-// reference (SURVEY.md §8(a) numerics contract).  Where an output's order is a nested sum (backin), the
-// independent inner sums are computed by two lanes and handed over with warp shuffles, the ordered
-// outer chain staying on one lane.  With EXACT=false the same stages use FFMA and split long sums
-// across lanes (deterministic fixed trees; within the 1e-4 tolerance).
+// reference (SURVEY.md §8(a) numerics contract).  Where an output's order is a chain over kernels
+// (backin's acc = acc + b_i), the per-kernel terms are formed by separate lanes and handed to one lane by
+// warp shuffles, which adds them in kernel order; backin forms only the valid (unclipped) taps, in the
+// reference's order (backin_rows_exact).  With EXACT=false the stages use FFMA, split long sums across
+// lanes (deterministic fixed trees; within the 1e-4 tolerance) and the MUFU sigmoid; the schedule of
+// the fast backward (scatter-form backin, row-form g_k2 split across the C2/C1 phases) and of every
+// variant kept for the stage bench (csrc/stage_bench.cu) is chosen by the TLB_* switches below, each
+// settled by a same-box A/B (profiles/README.md).
 //
 // Batch 100 runs one 512-thread CTA per SM (16 warps, latency-bound step); launches with more than one
 // image per SM run 256-thread CTAs, two per SM, whose barrier stalls overlap (the stages loop over their
