@@ -344,12 +344,13 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
 //   4. owner r of every cluster waits until all clusters have contributed to slice r (no grid-wide
 //      barrier: per-word counts, or the 8-way slice counter), reads the slice total and applies
 //      sgd_step (network.cpp:171-180) to its copy of slice r;
-//   5. owner r pushes its updated slice into every CTA of its cluster (st.async on their mbarriers);
-//      each CTA waits for the 7 foreign slices.
+//   5. owner r pushes its updated slice into every CTA of its cluster (st.async on their mbarriers:
+//      slice 0 -- everything conv1 reads -- on its own barrier); a CTA waits for slice 0 before the
+//      next conv1 and for the other six foreign slices after it (single GPU; fused DP waits for all).
 // The parameters never round-trip through L2 between steps.  Accumulators are triple-buffered by
 // step; with counters, buffer (s+1) % 3 is zeroed by cluster 0 during step s before it signals step s
-// (every CTA that adds into it in step s+1 has observed that signal); packed words are never zeroed.  Not the reference's example-order chain:
-// EXACT mode keeps train_kernel<true>.
+// (every CTA that adds into it in step s+1 has observed that signal); packed words are never zeroed.
+// Not the reference's example-order chain: EXACT mode keeps train_kernel<true>.
 // ------------------------------------------------------------------------------------------------
 constexpr int kCluster = 8;
 constexpr int kSlice = kPStride / kCluster;  // 488 floats per owner CTA
