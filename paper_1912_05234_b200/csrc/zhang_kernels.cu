@@ -477,6 +477,9 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       backward_image<false, true>(s, s.img + buf * kImg, nullptr);
       ++consumed;
     }
+    // A CTA without an image this step still completes the previous step's slice 1-7 phase before it
+    // re-arms that barrier below (an arrival on an incomplete phase would corrupt its count).
+    if (!dp && ls > 0 && lo >= hi) mbar_wait_cluster(&xbar[2], (uint32_t)((ls - 1) & 1));
     // ---- 2. push slice q of G to its owner q; owner sums the 8 received slices (rank order) ----
     const uint32_t parity = (uint32_t)(ls & 1);
     if (threadIdx.x == 0) st_async_f64(dsmem_map(&loss_rx[rank], 0), cta_loss, dsmem_map(&xbar[0], 0));

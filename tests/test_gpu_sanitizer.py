@@ -1,4 +1,5 @@
-"""compute-sanitizer regression guard: racecheck (shared memory incl. DSMEM) and memcheck over the
+"""compute-sanitizer regression guard: racecheck (shared memory incl. DSMEM), memcheck and synccheck
+(barrier / mbarrier phase use) over the
 persistent train kernels (clustered fast, flat fast, EXACT) on a few images -- 0 hazards, 0 errors."""
 import os
 import shutil
@@ -13,7 +14,7 @@ SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitize
 
 
 @pytest.mark.skipif(not os.path.exists(SAN), reason="compute-sanitizer not installed")
-@pytest.mark.parametrize("tool", ["racecheck", "memcheck"])
+@pytest.mark.parametrize("tool", ["racecheck", "memcheck", "synccheck"])
 def test_train_kernels_clean_under_sanitizer(tool):
     out = subprocess.run([SAN, "--tool", tool, "--error-exitcode", "9", sys.executable,
                           os.path.join(ROOT, "scripts", "sanitize.py"), "--only",
