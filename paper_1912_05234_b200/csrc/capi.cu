@@ -278,6 +278,15 @@ WriteValue32Fn write_value32() {
   return fn;
 }
 
+// First SGD group of ramp chunk k (TrainArgs::chunk = -C): 0, 1, 2, 4, ..., C, 2C, 3C, ...
+int64_t ramp_chunk_start(int64_t k, int64_t C) {
+  if (k == 0) return 0;
+  int64_t lg = 0;
+  while (((int64_t)1 << lg) < C) ++lg;  // C is a power of two
+  if (k <= lg) return (int64_t)1 << (k - 1);
+  return C * (k - lg);
+}
+
 // First SGD group of geometric ingestion chunk k (TrainArgs::chunk == 0; the kernel's wait_ready
 // inverts it): 0, 1, 2, 3, 4, 6, 8, 12, 16, 24, ...
 int64_t geo_chunk_start(int64_t k) {
@@ -291,11 +300,12 @@ int64_t geo_chunk_start(int64_t k) {
 // the halves of each [2^e, 2^(e+1))), see TrainArgs::chunk.  The copy stream first waits for all earlier work on the
 // context stream (buffer reuse).
 int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t chunk, int64_t batch,
-                  unsigned int token, int64_t head = 0) {
+                  unsigned int token) {
   TLB_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));  // recorded by the caller
   unsigned int* flags = static_cast<unsigned int*>(c->ready.p);
   for (int64_t k = 0, lo = 0; lo < n; ++k) {
-    const int64_t hi = chunk > 0 ? lo + (k == 0 && head > 0 ? head : chunk) : geo_chunk_start(k + 1) * batch;
+    const int64_t hi = chunk > 0 ? lo + chunk
+                       : chunk < 0 ? ramp_chunk_start(k + 1, -chunk) * batch : geo_chunk_start(k + 1) * batch;
     const int64_t cnt = std::min(hi, n) - lo;
     TLB_CUDA(cudaMemcpyAsync(dev + lo * 784, host + lo * 784, (size_t)cnt * 784 * sizeof(float),
                              cudaMemcpyHostToDevice, c->copy_stream));
@@ -308,12 +318,11 @@ int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t 
 }
 
 // Number of ingestion chunks for n images (see ingest_images).
-int64_t ingest_chunks(int64_t n, int64_t chunk, int64_t batch, int64_t head = 0) {
-  if (chunk > 0 && head > 0) return n <= head ? 1 : 1 + (n - head + chunk - 1) / chunk;
+int64_t ingest_chunks(int64_t n, int64_t chunk, int64_t batch) {
   if (chunk > 0) return (n + chunk - 1) / chunk;
   const int64_t groups = (n + batch - 1) / batch;
   int64_t k = 0;
-  while (geo_chunk_start(k + 1) < groups) ++k;
+  while ((chunk < 0 ? ramp_chunk_start(k + 1, -chunk) : geo_chunk_start(k + 1)) < groups) ++k;
   return k + 1;
 }
 
@@ -348,7 +357,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
                   float rate, int32_t epoch_begin, int32_t epochs, int64_t batch, double* d_epoch_loss,
                   int64_t shard_lo = 0, int64_t shard_hi = 0, int64_t group = -1, float* grad_out = nullptr,
                   double* loss_out = nullptr, const unsigned int* ready = nullptr, unsigned int token = 0,
-                  int64_t chunk = 1, const DpArgs* dp = nullptr, int64_t chunk_head = 0) {
+                  int64_t chunk = 1, const DpArgs* dp = nullptr) {
   const int64_t spe = (n + batch - 1) / batch;
   const int64_t m_max = std::min<int64_t>(batch, n);
   const int64_t m_local = grad_out ? std::max<int64_t>(0, std::min(shard_hi, m_max) - shard_lo) : m_max;
@@ -397,7 +406,6 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.ready_err = static_cast<unsigned int*>(c->ready_err.p);
   a.ready_token = token;
   a.chunk = chunk;
-  a.chunk_head = chunk_head;
   a.ready_step_end = a.step_begin + spe;  // only the call's first epoch can outrun the copies
   if (clustered) {
     if (dp) {  // fused data parallelism: slice s lives on rank s % world (peer memory)
@@ -603,20 +611,20 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   double* d_loss;
   // The dataset streams in on the copy stream while the first epoch already trains on the chunks
   // that have landed; labels/params are tiny and go first.
-  // Default: fixed chunks of whole SGD groups, >= 512 KiB (2 groups at batch 100).  Each chunk costs
-  // ~3 us of copy-engine/driver overhead; small fixed chunks keep the copy ahead of the kernel down to
-  // ~21 GB/s of host->device bandwidth (the VMs' pinned H2D measured 18-47 GB/s), where geometric
-  // chunks need ~1.5x the consumption rate.  TLB_INGEST_CHUNK=<images> overrides (0 = geometric).
+  // Default: a ramp of whole SGD groups -- 1 | 1 | 2 | 4 ... up to C groups of >= 1 MiB (4 at batch
+  // 100), then C groups per chunk: the first step waits for one group only, the next chunks double
+  // while the copy gets ahead, and the ~3 us per-chunk copy-engine/driver overhead stays <= 5% on the
+  // slowest VM links (pinned H2D measured 18-55 GB/s).  TLB_INGEST_CHUNK=<images> = fixed chunks,
+  // 0 = unbounded geometric growth.
   static const int64_t chunk_env = [] {
     const char* e = std::getenv("TLB_INGEST_CHUNK");
     return e ? std::max<int64_t>(0, std::atoll(e)) : (int64_t)-1;
   }();
   const int64_t group_bytes = batch * 784 * (int64_t)sizeof(float);
-  const int64_t chunk = chunk_env >= 0 ? chunk_env
-                                       : batch * std::max<int64_t>(1, (512 * 1024 + group_bytes - 1) / group_bytes);
-  // the first chunk is the first SGD group alone: the first step can start once it is resident
-  const int64_t head = (chunk_env < 0 && chunk > batch) ? batch : 0;
-  const int64_t nchunks = ingest_chunks(n, chunk, batch, head);
+  int64_t cap = 1;  // ramp cap C: groups per steady chunk, a power of two
+  while (cap * group_bytes < (int64_t)(1 << 20)) cap *= 2;
+  const int64_t chunk = chunk_env >= 0 ? chunk_env : -cap;
+  const int64_t nchunks = ingest_chunks(n, chunk, batch);
   const bool overlap = write_value32() != nullptr;
   TLB_TRY(stage_out(c, 0, (size_t)n * 784, &d_img));
   if (overlap) {
@@ -655,18 +663,18 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   // driver stages pageable memory synchronously on the host.
   ht.mark("staged");
   const bool copies_first = overlap && !is_pinned(images);
-  if (copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token, head));
+  if (copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token));
   if (!on_epoch) {
     TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, 0, epochs, batch, d_loss, 0, 0, -1, nullptr, nullptr,
-                          rdy, c->ready_token, chunk, nullptr, head));
+                          rdy, c->ready_token, chunk));
     ht.mark("launched");
-    if (overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token, head));
+    if (overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token));
     ht.mark("ingest_enqueued");
   } else {
     for (int32_t e = 0; e < epochs; ++e) {
       TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, e, 1, batch, d_loss, 0, 0, -1, nullptr, nullptr,
-                            e == 0 ? rdy : nullptr, c->ready_token, chunk, nullptr, head));
-      if (e == 0 && overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token, head));
+                            e == 0 ? rdy : nullptr, c->ready_token, chunk));
+      if (e == 0 && overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token));
       double mean = 0.0;
       TLB_TRY(fetch(c, &mean, d_loss + e, 1));
       on_epoch(e + 1, mean, user);

@@ -37,8 +37,8 @@ struct TrainArgs {
   // Steps < ready_step_end poll the flag before the image's TMA load; nullptr = every image resident.
   const unsigned int* ready;
   unsigned int ready_token;
-  int64_t chunk;
-  int64_t chunk_head;  // chunk > 0: the first chunk holds chunk_head images (0 = chunk), the rest chunk each
+  int64_t chunk;  // (chunk < 0: ramp of -chunk = C groups, a power of two: chunks of groups 0 | 1 | 2-3 |
+                  //  4-7 | ... up to C, then C groups each -- the first step waits for one group only)
   int64_t ready_step_end;
   unsigned int* ready_err;  // [3] diagnostic words: set when a ready flag never arrives (then the kernel
                             // proceeds and the host call fails instead of hanging)

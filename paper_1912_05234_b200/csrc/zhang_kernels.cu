@@ -102,9 +102,11 @@ __device__ __forceinline__ void wait_ready(const TrainArgs& a, const Job& j) {
   if (!a.ready || j.step >= a.ready_step_end) return;
   int64_t k;
   if (a.chunk > 0) {
-    const int64_t idx = job_index(a, j);
-    if (a.chunk_head > 0) k = idx < a.chunk_head ? 0 : 1 + udiv(idx - a.chunk_head, a.chunk);
-    else k = udiv(idx, a.chunk);
+    k = udiv(job_index(a, j), a.chunk);
+  } else if (a.chunk < 0) {  // ramp (see TrainArgs::chunk): groups 0 | 1 | 2-3 | ... | C/2..C-1, then C each
+    const int64_t C = -a.chunk, g = umod(j.step, a.steps_per_epoch);
+    if (g < C) k = g == 0 ? 0 : 64 - __clzll((long long)g);
+    else k = (63 - __clzll((long long)C)) + 1 + udiv(g - C, C);
   } else {  // geometric (see TrainArgs::chunk): groups 0, 1, then [2^e, 2^e + 2^(e-1)), [.., 2^(e+1))
     const int64_t g = umod(j.step, a.steps_per_epoch);
     if (g < 2) {

@@ -368,7 +368,7 @@ def test_dp_shards_sum_to_the_full_group(orc, small):
 
 @pytest.mark.parametrize("mode", ["exact", "fast"])
 def test_overlapped_ingestion_equals_resident_data(orc, zhang_sets, mode):
-    """tlb_train streams the dataset in chunks of whole SGD groups (>= 512 KiB) on a copy stream while the
+    """tlb_train streams the dataset in a ramp of whole-group chunks (1, 1, 2, 4, then 4 groups) on a copy stream while the
     kernel trains (device ready flags): for group counts on and around the chunk boundaries, pageable and
     pinned sources, and repeated calls with growing and shrinking sizes, the result equals training on
     device-resident data (tests/_ingest_check.py)."""
@@ -377,10 +377,11 @@ def test_overlapped_ingestion_equals_resident_data(orc, zhang_sets, mode):
     check(orc, tr_x, tr_y, mode)
 
 
-@pytest.mark.parametrize("policy", ["0", "37", "100"])
+@pytest.mark.parametrize("policy", ["0", "37", "200"])
 def test_overlapped_ingestion_chunk_policies(policy):
     """The same check under the other chunk policies (TLB_INGEST_CHUNK: 0 = geometric group chunks,
-    N = fixed chunks of N images, not group-aligned), both modes, in a fresh process."""
+    N = fixed chunks of N images, not group-aligned; 200 = the former 2-group default), both modes, in a
+    fresh process."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
