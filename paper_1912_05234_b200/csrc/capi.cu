@@ -112,6 +112,7 @@ struct tlb_ctx {
   // the train kernel runs; a stream memory operation raises ready[k] to the call's token after
   // chunk k lands (the kernel polls it before the image's TMA load).
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t copy_stream2 = nullptr;  // second copy stream (TLB_INGEST_STREAMS=2): odd chunks from chunk 3
   cudaEvent_t copy_gate = nullptr;
   DevBuf ready;
   DevBuf ready_err;  // [3] u32 ingestion watchdog words (flag, chunk, observed value)
@@ -302,14 +303,21 @@ int64_t geo_chunk_start(int64_t k) {
 int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t chunk, int64_t batch,
                   unsigned int token) {
   TLB_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));  // recorded by the caller
+  static const bool two = [] {
+    const char* e = std::getenv("TLB_INGEST_STREAMS");
+    return e && std::atoi(e) == 2;
+  }();
+  if (two) TLB_CUDA(cudaStreamWaitEvent(c->copy_stream2, c->copy_gate, 0));
   unsigned int* flags = static_cast<unsigned int*>(c->ready.p);
   for (int64_t k = 0, lo = 0; lo < n; ++k) {
     const int64_t hi = chunk > 0 ? lo + chunk
                        : chunk < 0 ? ramp_chunk_start(k + 1, -chunk) * batch : geo_chunk_start(k + 1) * batch;
     const int64_t cnt = std::min(hi, n) - lo;
+    // (two streams: the first chunks stay on one stream so the first step's data is not slowed)
+    cudaStream_t cs = (two && k >= 3 && (k & 1)) ? c->copy_stream2 : c->copy_stream;
     TLB_CUDA(cudaMemcpyAsync(dev + lo * 784, host + lo * 784, (size_t)cnt * 784 * sizeof(float),
-                             cudaMemcpyHostToDevice, c->copy_stream));
-    const CUresult r = write_value32()(reinterpret_cast<CUstream>(c->copy_stream),
+                             cudaMemcpyHostToDevice, cs));
+    const CUresult r = write_value32()(reinterpret_cast<CUstream>(cs),
                                        reinterpret_cast<CUdeviceptr>(flags + k), token, CU_STREAM_WRITE_VALUE_DEFAULT);
     if (r != CUDA_SUCCESS) return fail(TLB_ERR_CUDA, "cuStreamWriteValue32 failed: " + std::to_string((int)r));
     lo += cnt;
@@ -482,6 +490,7 @@ int tlb_ctx_create(int device, tlb_ctx** out) {
   if (e == cudaSuccess) e = c->ready_err.ensure(4 * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(c->ready_err.p, 0, 4 * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream2, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->copy_gate, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete c;
@@ -502,6 +511,7 @@ int tlb_ctx_destroy(tlb_ctx* c) {
   c->barrier.release();
   for (auto& s : c->stage) s.release();
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  if (c->copy_stream2) cudaStreamSynchronize(c->copy_stream2);
   c->ready.release();
   c->ready_err.release();
   c->pin.release();
@@ -509,6 +519,7 @@ int tlb_ctx_destroy(tlb_ctx* c) {
   c->synth_snaps.release();
   if (c->copy_gate) cudaEventDestroy(c->copy_gate);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->copy_stream2) cudaStreamDestroy(c->copy_stream2);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return TLB_OK;
@@ -630,12 +641,14 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   if (overlap) {
     if ((size_t)nchunks * sizeof(unsigned int) > c->ready.cap) {
       TLB_CUDA(cudaStreamSynchronize(c->copy_stream));
+      TLB_CUDA(cudaStreamSynchronize(c->copy_stream2));
       TLB_CUDA(c->ready.ensure((size_t)nchunks * sizeof(unsigned int)));
       TLB_CUDA(cudaMemset(c->ready.p, 0, c->ready.cap));
       c->ready_token = 0;
     }
     if (++c->ready_token == 0) {  // wrapped: restart the token sequence from clean flags
       TLB_CUDA(cudaStreamSynchronize(c->copy_stream));
+      TLB_CUDA(cudaStreamSynchronize(c->copy_stream2));
       TLB_CUDA(cudaMemset(c->ready.p, 0, c->ready.cap));
       c->ready_token = 1;
     }
@@ -690,6 +703,7 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   if (epoch_loss) std::memcpy(epoch_loss, h_loss, epochs * sizeof(double));
   if (overlap) {
     TLB_CUDA(cudaStreamSynchronize(c->copy_stream));  // (the kernel consumed every chunk: already done)
+    TLB_CUDA(cudaStreamSynchronize(c->copy_stream2));
     const unsigned int err[3] = {h_err[0], h_err[1], h_err[2]};
     if (err[0]) {
       TLB_CUDA(cudaMemset(c->ready_err.p, 0, sizeof(err)));
