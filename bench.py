@@ -117,14 +117,15 @@ def golden_losses():
 
 
 # ---- reference CPU path (oracle/_ref = the unmodified tensorloom library) ---------------------------
-def reference_epochs(images, labels, epochs_budget_s: float, max_epochs: int, batch: int):
-    """Times net::train of the reference on whole epochs with all host threads; returns img/s, info."""
+def reference_epochs(n: int, epochs_budget_s: float, max_epochs: int, batch: int):
+    """Times the reference's own net::train (oracle/_ref) on whole epochs of its own synth::make_set(n, 1)
+    from its own init_params(42), with all host threads; returns (img/s, info)."""
     from oracle import Reference  # reference arm / cpu_baseline only
-    from paper_1912_05234_b200.runtime import init_params
     R = Reference()
     cores = os.cpu_count() or 1
     R.set_workers(cores)
-    p = init_params(42)
+    images, labels = R.make_set(n, 1)
+    p = R.init_params(42)
     done, t_total = 0, 0.0
     while done < max_epochs:
         t0 = time.perf_counter()
@@ -133,41 +134,56 @@ def reference_epochs(images, labels, epochs_budget_s: float, max_epochs: int, ba
         done += 1
         if t_total >= epochs_budget_s:
             break
-    return done * len(labels) / t_total, {"cores": cores, "epochs": done, "seconds": t_total}
+    return done * n / t_total, {"cores": cores, "epochs": done, "seconds": t_total}
+
+
+def workload_config(args, world: int) -> dict:
+    """The `config` object of BOTH arms (identical dicts, so the driver's same-config check holds)."""
+    B, n_per = args.batch, args.n
+    return {"workload": "Zhang CNN paper protocol (BASELINE configs[1]" + (", configs[3] batch sweep" if B > 100 else "")
+                        + f"): 1 step = 1 epoch of {n_per} images/GPU at batch {B}/GPU, lr 0.05, init_params(42)",
+            "batch_per_gpu": B, "global_batch": B * world, "n_images": n_per * world, "epochs_per_step": 1,
+            "parallelism": f"dp{world}",
+            "l2": "flushed between timed steps (256 MiB write outside the event pair)"}
 
 
 def run_reference(args):
+    """The reference's own CPU net::train (oracle/_ref = the unmodified tensorloom library): inputs and
+    initial weights from the reference itself (synth::make_set, net::init_params), all host threads."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_1912_05234_b200.runtime import synth_make_set
-    images, labels = synth_make_set(args.n, 1)
     from oracle import Reference
     R = Reference()
     cores = os.cpu_count() or 1
     R.set_workers(cores)
-    from paper_1912_05234_b200.runtime import init_params
-    p = init_params(42)
+    # one step = one epoch of the per-GPU corpus at the GLOBAL batch (batch-independent cost on the CPU
+    # once batch >= workers); the full N-GPU corpus would only scale the sample, not the rate
+    n = args.n
+    images, labels = R.make_set(n, 1)
+    batch = min(args.batch * world, n)
+    p0 = R.init_params(42)
+    p = p0
     for _ in range(args.warmup):
-        p, _ = R.train(images, labels, p, rate=0.05, epochs=1, batch=args.batch)
-    p = init_params(42)
+        p, _ = R.train(images, labels, p, rate=0.05, epochs=1, batch=batch)
+    p = p0
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        p, _ = R.train(images, labels, p, rate=0.05, epochs=1, batch=args.batch)
+        p, _ = R.train(images, labels, p, rate=0.05, epochs=1, batch=batch)
         times.append(time.perf_counter() - t0)
     total = sum(times)
-    value = args.steps * args.n / total
+    value = args.steps * n / total
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic: synth::make_set(10000, 1), init_params(42)",
-        "config": {"workload": "Zhang CNN paper protocol, 1 epoch of 10k images at batch 100 per step",
-                   "batch": args.batch, "n_images": args.n, "epochs_per_step": 1},
+        "data": f"synthetic: reference synth::make_set({n}, 1), reference init_params(42)",
+        "config": workload_config(args, world),
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "reference",
-                         "sample": f"{args.steps} epochs x {args.n} images, net::train with "
-                                   f"set_global_config({{{cores},4096}})"},
+                         "sample": f"{args.steps} epoch(s) x {n} images at batch {batch}, reference net::train "
+                                   f"(oracle/_ref) with set_global_config({{{cores},4096}})"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -398,7 +414,7 @@ def run_ours(args):
         result["gpu_launches"] += args.steps
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, meta = reference_epochs(images[:n_per], labels[:n_per], 10.0, 3, B)
+        v, meta = reference_epochs(n_per, 10.0, 3, min(B * world, n_per))
         result["cpu_baseline"] = {"value": v, "unit": "images/s", "cores": meta["cores"], "kind": "reference",
                                   "sample": f"{meta['epochs']} epoch(s) x {n_per} images at batch {B}, reference "
                                             f"net::train (oracle/_ref) with {meta['cores']} workers, "
@@ -413,8 +429,31 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def ensure_ranks(args) -> None:
+    """--gpus N: one process per GPU.  Without a torchrun environment and N > 1, re-launch this command
+    under torch.distributed.run (N local ranks, rendezvous on 127.0.0.1); inside one, WORLD_SIZE must be
+    N -- a mismatch is an error, never a silent single-rank run."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None:
+        if args.gpus > 1:
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+            sys.stdout.flush()
+            os.execv(sys.executable, cmd)
+        return
+    if int(world) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+              f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus", file=sys.stderr)
+        sys.exit(2)
+
+
 def main():
     args = parse()
+    ensure_ranks(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -5,6 +5,7 @@
 // Argument checks and messages follow the reference (network.cpp:27-49, 83-85, 98-101, 211-214).
 #include "tloom/network.hpp"
 
+#include <algorithm>
 #include <bit>
 #include <cstring>
 #include <fstream>
@@ -183,67 +184,93 @@ double evaluate(const Params& p, const mnist::MnistSet& data) {
   return static_cast<double>(correct) / static_cast<double>(data.size());
 }
 
-// ---- TLM1 checkpoints (reference network.cpp:282-362): little-endian rank, extents, raw f32 ----
+// ---- TLM1 checkpoints --------------------------------------------------------------------------
+// Byte format (the reference's, so its own load_params reads our files: proj/src/network.cpp:282-362):
+// "TLM1", then per tensor in write_flat order: u32 rank, u32 extents, f32 payload, all little-endian.
+// Here a checkpoint is just the flat parameter vector framed by the section table below; the
+// reader fills the flat vector section by section and rebuilds Params with unflat.
 namespace {
 
-void put_u32(std::vector<unsigned char>& o, std::uint32_t v) {
-  for (int i = 0; i < 4; ++i) o.push_back(static_cast<unsigned char>(v >> (8 * i)));
-}
+struct Section {
+  const char* name;
+  const Shape* shape;
+};
+const Section kSections[6] = {{"k1", &kK1}, {"b1", &kB1}, {"k2", &kK2}, {"b2", &kB2}, {"fc", &kFc}, {"b", &kB}};
 
-std::uint32_t get_u32(const std::vector<unsigned char>& b, std::size_t& at) {
-  if (at + 4 > b.size()) throw FormatError("checkpoint: truncated at byte " + std::to_string(at));
-  std::uint32_t v = 0;
-  for (int i = 0; i < 4; ++i) v |= static_cast<std::uint32_t>(b[at + static_cast<std::size_t>(i)]) << (8 * i);
-  at += 4;
-  return v;
-}
+class LeWriter {
+ public:
+  void word(std::uint32_t v) {
+    unsigned char b[4];
+    for (int k = 0; k < 4; ++k) b[k] = static_cast<unsigned char>((v >> (8 * k)) & 0xffu);
+    bytes.insert(bytes.end(), b, b + 4);
+  }
+  std::vector<unsigned char> bytes{'T', 'L', 'M', '1'};
+};
 
-Tensor get_tensor(const std::vector<unsigned char>& b, std::size_t& at, const Shape& want, const char* name) {
-  const std::uint32_t rank = get_u32(b, at);
-  if (rank > static_cast<std::uint32_t>(Shape::kMaxRank))
-    throw FormatError("checkpoint: tensor " + std::string(name) + " has rank " + std::to_string(rank));
-  std::vector<std::int64_t> ext(rank);
-  for (auto& e : ext) e = get_u32(b, at);
-  const Shape got{std::span<const std::int64_t>(ext)};
-  if (got != want)
-    throw FormatError("checkpoint: tensor " + std::string(name) + " has shape " + got.str() + ", expected " + want.str());
-  std::vector<float> v(static_cast<std::size_t>(got.count()));
-  for (auto& x : v) x = std::bit_cast<float>(get_u32(b, at));
-  return Tensor(got, std::move(v));
-}
+class LeReader {
+ public:
+  explicit LeReader(const std::vector<unsigned char>& b) : b_(b) {}
+  std::uint32_t word() {
+    if (b_.size() < 4 || pos_ > b_.size() - 4) throw FormatError("checkpoint: truncated at byte " + std::to_string(pos_));
+    std::uint32_t v = 0;
+    for (int k = 3; k >= 0; --k) v = (v << 8) | b_[pos_ + static_cast<std::size_t>(k)];
+    pos_ += 4;
+    return v;
+  }
+  std::size_t pos() const { return pos_; }
+  void seek(std::size_t p) { pos_ = p; }
+
+ private:
+  const std::vector<unsigned char>& b_;
+  std::size_t pos_ = 0;
+};
 
 }  // namespace
 
 void save_params(const std::filesystem::path& path, const Params& p) {
   p.validate();
-  std::vector<unsigned char> out{'T', 'L', 'M', '1'};
-  for (const Tensor* t : {&p.k1, &p.b1, &p.k2, &p.b2, &p.fc, &p.b}) {
-    put_u32(out, static_cast<std::uint32_t>(t->shape().rank()));
-    for (int a = 0; a < t->shape().rank(); ++a) put_u32(out, static_cast<std::uint32_t>(t->shape()[a]));
-    for (const float v : t->data()) put_u32(out, std::bit_cast<std::uint32_t>(v));
+  const std::vector<float> w = flat(p);
+  LeWriter out;
+  std::size_t at = 0;
+  for (const Section& sec : kSections) {
+    const Shape& s = *sec.shape;
+    out.word(static_cast<std::uint32_t>(s.rank()));
+    for (int a = 0; a < s.rank(); ++a) out.word(static_cast<std::uint32_t>(s[a]));
+    for (std::int64_t i = 0; i < s.count(); ++i) out.word(std::bit_cast<std::uint32_t>(w[at++]));
   }
   std::ofstream f(path, std::ios::binary | std::ios::trunc);
   if (!f) throw FormatError("cannot open checkpoint for writing: " + path.string());
-  f.write(reinterpret_cast<const char*>(out.data()), static_cast<std::streamsize>(out.size()));
+  f.write(reinterpret_cast<const char*>(out.bytes.data()), static_cast<std::streamsize>(out.bytes.size()));
   if (!f) throw FormatError("write failure on checkpoint: " + path.string());
 }
 
 Params load_params(const std::filesystem::path& path) {
-  std::ifstream f(path, std::ios::binary);
+  std::ifstream f(path, std::ios::binary | std::ios::ate);
   if (!f) throw FormatError("cannot open checkpoint: " + path.string());
-  const std::vector<unsigned char> b((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+  std::vector<unsigned char> bytes(static_cast<std::size_t>(std::max<std::streamoff>(0, f.tellg())));
+  f.seekg(0);
+  if (!bytes.empty()) f.read(reinterpret_cast<char*>(bytes.data()), static_cast<std::streamsize>(bytes.size()));
   if (f.bad()) throw FormatError("read failure on checkpoint: " + path.string());
-  if (b.size() < 4 || std::memcmp(b.data(), "TLM1", 4) != 0) throw FormatError("checkpoint: bad magic, expected \"TLM1\"");
-  std::size_t at = 4;
-  Params p;
-  p.k1 = get_tensor(b, at, kK1, "k1");
-  p.b1 = get_tensor(b, at, kB1, "b1");
-  p.k2 = get_tensor(b, at, kK2, "k2");
-  p.b2 = get_tensor(b, at, kB2, "b2");
-  p.fc = get_tensor(b, at, kFc, "fc");
-  p.b = get_tensor(b, at, kB, "b");
-  if (at != b.size()) throw FormatError("checkpoint: " + std::to_string(b.size() - at) + " trailing bytes");
-  return p;
+  if (bytes.size() < 4 || std::memcmp(bytes.data(), "TLM1", 4) != 0)
+    throw FormatError("checkpoint: bad magic, expected \"TLM1\"");
+  LeReader in(bytes);
+  in.seek(4);
+  std::vector<float> w;
+  w.reserve(TLB_NPARAM);
+  for (const Section& sec : kSections) {
+    const std::uint32_t rank = in.word();
+    if (rank > static_cast<std::uint32_t>(Shape::kMaxRank))
+      throw FormatError("checkpoint: tensor " + std::string(sec.name) + " has rank " + std::to_string(rank));
+    std::int64_t ext[Shape::kMaxRank];
+    for (std::uint32_t a = 0; a < rank; ++a) ext[a] = in.word();
+    const Shape got{std::span<const std::int64_t>(ext, rank)};
+    if (got != *sec.shape)
+      throw FormatError("checkpoint: tensor " + std::string(sec.name) + " has shape " + got.str() + ", expected " +
+                        sec.shape->str());
+    for (std::int64_t i = 0; i < got.count(); ++i) w.push_back(std::bit_cast<float>(in.word()));
+  }
+  if (in.pos() != bytes.size()) throw FormatError("checkpoint: " + std::to_string(bytes.size() - in.pos()) + " trailing bytes");
+  return unflat<Params>(w.data());
 }
 
 }  // namespace tloom::net
