@@ -889,6 +889,10 @@ int tlb_evaluate_device(tlb_ctx* c, const float* d_images, const int32_t* d_labe
   if (n <= 0) return TLB_OK;
   TLB_TRY(set_device(c));
   tlb::EvalArgs a{d_images, d_labels, n, d_params, d_pred, nullptr, d_correct};
+  if (!exact(c) && c->grid_override == 0 && c->threads_override == 0) {  // batched forward-only kernel
+    TLB_CUDA(tlb::launch_infer(a, c->sm_count, c->stream));
+    return TLB_OK;
+  }
   const int threads = pick_threads(c, n);
   TLB_CUDA(tlb::launch_eval(exact(c), a, plain_grid(c, n, threads), threads, c->stream));
   return TLB_OK;

@@ -1,0 +1,294 @@
+// infer_kernels.cu -- forward-only inference in fast mode: net::predict / net::evaluate over many images
+// (proj/src/network.cpp:253-280; BASELINE configs[2], 100 .. 1M images).
+//
+// The training kernels keep one image per CTA in flight with every activation resident for the backward
+// pass (104 KB of shared memory, two CTAs per SM).  Inference needs none of that: conv1 pools in registers
+// and conv2 pools through a shuffle, so an image costs only its input (3,136 B), s1 (3,456 B) and s2
+// (768 B) of shared memory.  A CTA therefore runs NI images per round -- every stage's lanes span the NI
+// images, so one CTA barrier is amortised over NI images -- and several CTAs share an SM, whose warps
+// fill each other's barrier stalls.  The NI images of a round are contiguous in HBM and arrive with ONE
+// TMA bulk copy into a double-buffered ring (the next round's copy is in flight during this round).
+//
+// Arithmetic is the fast mode's (FFMA, ex2/rcp MUFU sigmoid; conv2 sums its 150 taps in the reference's
+// (c, ky, kx) order as one FFMA chain); argmax is net::predict's (strict >, lowest index wins ties).  Per round, per CTA:
+//   conv1 : lane = (image, pooled row py, 12-column half, channel i) -> 2x12 conv outputs (600 FFMA),
+//           sigmoid, 2x2 pool in registers -> s1                                    144 lanes / image
+//   conv2 : lane = (image, pooled row py, kernel i) -> 2x8 outputs x 150 taps (2,400 FFMA), sigmoid,
+//           2x2 pool in registers -> s2                                              48 lanes / image
+// Lane maps put the lanes that share an input row side by side (shared-memory broadcast) and spread
+// the weight loads over distinct banks: the round-1 maps cost ~2x the FFMA cycles in smem wavefronts.
+// Default 8 images x 384 threads: conv1 = 1,152 lanes (exactly 3 rounds), conv2 = 384 lanes (exactly
+// one), two CTAs per SM.
+//   fc    : 8 lanes per (image, class) -> 24-term partials + a 3-level shuffle tree, sigmoid -> out
+//   argmax: one lane per image -> pred, correct count (one atomic per CTA thread at the end)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+
+#include "tlb_common.cuh"
+#include "tlb_launch.h"
+
+namespace tlb {
+namespace infer {
+
+// Padded weight copies (built once per CTA from P): conv1 [6][5][8] with channel stride 44 and conv2
+// [12][6][5][8] with kernel stride 244 -- every 5-tap weight row is two aligned 128-bit loads, and the
+// distinct channels / kernels a warp touches fall in distinct bank groups (44/4 = 11 and 244/4 = 61 are
+// odd mod 8).
+constexpr int kW1Stride = 44, kW1Floats = 6 * kW1Stride;
+constexpr int kW2Stride = 244, kW2Floats = 12 * kW2Stride;
+
+template <int NI>
+struct Layout {
+  static constexpr int kW1F = kPStride;                 // padded conv1 weights
+  static constexpr int kW2F = kW1F + kW1Floats;         // padded conv2 weights
+  static constexpr int kImgF = kW2F + kW2Floats;        // [2][NI][784] TMA ring
+  static constexpr int kS1F = kImgF + 2 * NI * kImg;    // [NI][6][12][12]
+  static constexpr int kS2F = kS1F + NI * 864;          // [NI][192]
+  static constexpr int kOutF = kS2F + NI * 192;         // [NI][16]
+  static constexpr int kFloats = kOutF + NI * 16;
+  static constexpr size_t kBytes = (size_t)kFloats * sizeof(float) + 2 * sizeof(uint64_t);
+  static_assert(kImgF % 4 == 0 && kS1F % 4 == 0 && kS2F % 4 == 0, "16-byte aligned regions");
+};
+
+extern __shared__ __align__(128) float infer_smem[];
+
+// Fast logistic of (acc + b) with nb = -b * log2(e) precomputed: one FFMA, ex2.approx.ftz, the add and
+// rcp.approx.ftz (the non-ftz ex2 adds a subnormal-range fix-up of two more instructions).
+__device__ __forceinline__ float logistic(float acc, float nb) {
+  constexpr float kNegLog2e = -1.4426950408889634f;
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmaf_rn(acc, kNegLog2e, nb)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+  return r;
+}
+__device__ __forceinline__ float neg_log2e_times(float b) { return b * -1.4426950408889634f; }
+
+__device__ __forceinline__ void load5(const float* wrow, float (&w)[5]) {
+  const float4 a = *reinterpret_cast<const float4*>(wrow);
+  w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+  w[4] = wrow[4];
+}
+
+// conv1 + sigmoid + avgpool of lane item `it` (< cnt * 144).  Lane = (image k, pooled row py, 12-column
+// half xs, channel i), channel fastest: 2 conv rows x 12 columns (600 FFMA over ky, kx), sigmoid,
+// 2x2 pool in registers -> 6 s1 values.  The six channel lanes of a (py, xs) read the same image rows
+// (broadcast), so every 128-bit image load is one wavefront.
+__device__ __forceinline__ void conv1_item(const float* P, const float* W1, const float* imgs, float* s1s, int it) {
+  const int k = it / 144, r = it - k * 144;
+  const int pos = r / 6, i = r - pos * 6, py = pos >> 1, xs = pos & 1;
+  const int y0 = 2 * py, x0 = 12 * xs;
+  const float* img = imgs + k * kImg;
+  const float* w = W1 + i * kW1Stride;
+  float a[2][12];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int o = 0; o < 12; ++o) a[q][o] = 0.0f;
+#pragma unroll
+  for (int rr = 0; rr < 6; ++rr) {  // image row y0 + rr feeds conv row q with ky = rr - q
+    const float4* src = reinterpret_cast<const float4*>(img + (y0 + rr) * 28 + x0);
+    const float4 v0 = src[0], v1 = src[1], v2 = src[2], v3 = src[3];
+    const float in[16] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w,
+                          v2.x, v2.y, v2.z, v2.w, v3.x, v3.y, v3.z, v3.w};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int ky = rr - q;
+      if (ky < 0 || ky > 4) continue;
+      float wv[5];
+      load5(w + ky * 8, wv);
+#pragma unroll
+      for (int kx = 0; kx < 5; ++kx)
+#pragma unroll
+        for (int o = 0; o < 12; ++o) a[q][o] = __fmaf_rn(in[o + kx], wv[kx], a[q][o]);
+    }
+  }
+  const float nb = neg_log2e_times(P[kB1 + i]);
+  float* dst = s1s + k * 864 + (i * 12 + py) * 12 + 6 * xs;
+#pragma unroll
+  for (int px = 0; px < 6; px += 2) {  // avgpool (nn.cpp:144): ((p00 + p01) + p10) + p11, then * 0.25f
+    float pv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = 2 * (px + h);
+      pv[h] = (((logistic(a[0][c], nb) + logistic(a[0][c + 1], nb)) + logistic(a[1][c], nb)) +
+               logistic(a[1][c + 1], nb)) * 0.25f;
+    }
+    *reinterpret_cast<float2*>(dst + px) = make_float2(pv[0], pv[1]);
+  }
+}
+
+// conv2 + sigmoid + avgpool of lane `it` (< cnt * 48): lane (image k, pooled row py, kernel i), kernel
+// fastest, computes conv rows 2py, 2py+1 (16 outputs, the 150 taps in (c, ky, kx) order as one FFMA
+// chain each) and pools them in registers.  The twelve lanes of a (k, py) stream the same six s1 rows
+// per channel (broadcast), their padded weight rows fall in distinct bank groups, and each loaded s1 row
+// segment feeds up to 2 x 40 FFMA.
+__device__ __forceinline__ void conv2_item(const float* P, const float* W2, const float* s1s, float* s2s, int it) {
+  const int k = it / 48, r = it - k * 48;
+  const int py = r / 12, i = r - py * 12;
+  const float* s1 = s1s + k * 864;
+  float acc[2][8];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int o = 0; o < 8; ++o) acc[q][o] = 0.0f;
+#pragma unroll 1
+  for (int c = 0; c < 6; ++c) {
+    const float* wc = W2 + i * kW2Stride + c * 40;
+#pragma unroll
+    for (int rr = 0; rr < 6; ++rr) {  // s1 row 2py + rr feeds conv row q with ky = rr - q
+      const float4* src = reinterpret_cast<const float4*>(s1 + (c * 12 + 2 * py + rr) * 12);
+      const float4 v0 = src[0], v1 = src[1], v2 = src[2];
+      const float in[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int ky = rr - q;
+        if (ky < 0 || ky > 4) continue;
+        float wv[5];
+        load5(wc + ky * 8, wv);
+#pragma unroll
+        for (int kx = 0; kx < 5; ++kx)
+#pragma unroll
+          for (int o = 0; o < 8; ++o) acc[q][o] = __fmaf_rn(in[o + kx], wv[kx], acc[q][o]);
+      }
+    }
+  }
+  const float nb = neg_log2e_times(P[kB2 + i]);
+  float pv[4];
+#pragma unroll
+  for (int px = 0; px < 4; ++px)  // avgpool (nn.cpp:144)
+    pv[px] = (((logistic(acc[0][2 * px], nb) + logistic(acc[0][2 * px + 1], nb)) + logistic(acc[1][2 * px], nb)) +
+              logistic(acc[1][2 * px + 1], nb)) * 0.25f;
+  *reinterpret_cast<float4*>(s2s + k * 192 + (i * 4 + py) * 4) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+}
+
+// FC + sigmoid: eight lanes per (image, class), each a 24-term FFMA partial from 128-bit loads, joined
+// by a 3-level xor tree.  The caller's loop runs whole warps (the bound is rounded up to 32 lanes: with an
+// odd image count cnt * 80 ends mid-warp); lanes past the last task recompute task 0 and store nothing.
+__device__ __forceinline__ void fc_item(const float* P, const float* s2s, float* outs, int it, bool valid) {
+  const int task = valid ? it >> 3 : 0, part = it & 7, k = task / 10, i = task - k * 10;
+  const float4* s2 = reinterpret_cast<const float4*>(s2s + k * 192 + 24 * part);
+  const float4* w = reinterpret_cast<const float4*>(P + kFC + i * 192 + 24 * part);
+  float acc = 0.0f;
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const float4 x = s2[q], y = w[q];
+    acc = __fmaf_rn(x.x, y.x, acc);
+    acc = __fmaf_rn(x.y, y.y, acc);
+    acc = __fmaf_rn(x.z, y.z, acc);
+    acc = __fmaf_rn(x.w, y.w, acc);
+  }
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  if (valid && part == 0) outs[k * 16 + i] = logistic(acc, neg_log2e_times(P[kB + i]));
+}
+
+template <int NI, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) infer_kernel(EvalArgs a) {
+  using L = Layout<NI>;
+  float* const P = infer_smem;
+  float* const W1 = infer_smem + L::kW1F;
+  float* const W2 = infer_smem + L::kW2F;
+  float* const ring = infer_smem + L::kImgF;
+  float* const s1s = infer_smem + L::kS1F;
+  float* const s2s = infer_smem + L::kS2F;
+  float* const outs = infer_smem + L::kOutF;
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(infer_smem + L::kFloats);
+  const int t = threadIdx.x;
+
+  int64_t lo, hi;
+  static_chunk(a.n, gridDim.x, blockIdx.x, lo, hi);
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  {  // parameters -> shared (read once per CTA), then the padded conv weight copies
+    const float4* src = reinterpret_cast<const float4*>(a.params);
+    float4* dst = reinterpret_cast<float4*>(P);
+    for (int q = t; q < kPStride / 4; q += THREADS) dst[q] = __ldg(src + q);
+  }
+  __syncthreads();
+  for (int q = t; q < kW1Floats + kW2Floats; q += THREADS) {
+    if (q < kW1Floats) {
+      const int i = q / kW1Stride, r = q - i * kW1Stride, ky = r >> 3, kx = r & 7;
+      W1[q] = (ky < 5 && kx < 5) ? P[kK1 + i * 25 + ky * 5 + kx] : 0.0f;
+    } else {
+      const int q2 = q - kW1Floats, i = q2 / kW2Stride, r = q2 - i * kW2Stride, c = r / 40, r2 = r - c * 40;
+      const int ky = r2 >> 3, kx = r2 & 7;
+      W2[q2] = (c < 6 && kx < 5) ? P[kK2 + (i * 6 + c) * 25 + ky * 5 + kx] : 0.0f;
+    }
+  }
+  __syncthreads();
+  auto issue = [&](int buf, int64_t first) {  // thread 0: one bulk copy for the round's images
+    const int cnt = (int)min((int64_t)NI, hi - first);
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bar[buf], (uint32_t)(cnt * kImg * sizeof(float)));
+    tma_load_1d(ring + buf * NI * kImg, a.images + first * kImg, (uint32_t)(cnt * kImg * sizeof(float)), &bar[buf]);
+  };
+  if (t == 0 && lo < hi) issue(0, lo);
+  unsigned long long correct = 0;
+  uint32_t round = 0;
+  for (int64_t first = lo; first < hi; first += NI, ++round) {
+    const int buf = round & 1;
+    const int cnt = (int)min((int64_t)NI, hi - first);
+    mbar_wait(&bar[buf], (round >> 1) & 1);
+    if (t == 0 && first + NI < hi) issue(buf ^ 1, first + NI);  // buffer buf^1 was last read before this round
+    const float* imgs = ring + buf * NI * kImg;
+    for (int it = t; it < cnt * 144; it += THREADS) conv1_item(P, W1, imgs, s1s, it);
+    __syncthreads();
+    for (int it = t; it < cnt * 48; it += THREADS) conv2_item(P, W2, s1s, s2s, it);
+    __syncthreads();
+    for (int it = t; it < (cnt * 80 + 31) / 32 * 32; it += THREADS) fc_item(P, s2s, outs, it, it < cnt * 80);
+    __syncthreads();
+    if (a.yhat)
+      for (int q = t; q < cnt * 10; q += THREADS) a.yhat[(first + q / 10) * 10 + q % 10] = outs[(q / 10) * 16 + q % 10];
+    if (t < cnt) {
+      const float* o = outs + t * 16;
+      int best = 0;  // net::predict (network.cpp:253-261): strict >, lowest index wins ties
+#pragma unroll
+      for (int i = 1; i < 10; ++i)
+        if (o[i] > o[best]) best = i;
+      if (a.pred) a.pred[first + t] = best;
+      if (a.labels) correct += (best == __ldg(a.labels + first + t));
+    }
+    // the next round's fc writes outs only after two more barriers; conv1 rewrites s1 after conv2 read it
+  }
+  if (a.correct && correct) atomicAdd(a.correct, correct);
+}
+
+template <int NI, int THREADS, int MINB>
+cudaError_t launch_cfg(const EvalArgs& a, int sm_count, cudaStream_t st) {
+  constexpr size_t smem = Layout<NI>::kBytes;
+  auto kern = infer_kernel<NI, THREADS, MINB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t rounds = (a.n + NI - 1) / NI;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(rounds, (int64_t)std::max(occ, 1) * sm_count));
+  kern<<<grid, THREADS, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace infer
+
+// TLB_INFER_CFG = "NIxTHREADSxMINB" picks a measured alternative (A/B); default below.
+cudaError_t launch_infer(const EvalArgs& a, int sm_count, cudaStream_t st) {
+  using namespace infer;
+  static const char* cfg = std::getenv("TLB_INFER_CFG");
+  const auto is = [](const char* want) { return cfg && !std::strcmp(cfg, want); };
+  if (is("8x512x2")) return launch_cfg<8, 512, 2>(a, sm_count, st);
+  if (is("4x256x3")) return launch_cfg<4, 256, 3>(a, sm_count, st);
+  if (is("4x192x4")) return launch_cfg<4, 192, 4>(a, sm_count, st);
+  if (is("8x384x1")) return launch_cfg<8, 384, 1>(a, sm_count, st);
+  if (is("16x384x1")) return launch_cfg<16, 384, 1>(a, sm_count, st);
+  return launch_cfg<8, 384, 2>(a, sm_count, st);
+}
+
+}  // namespace tlb

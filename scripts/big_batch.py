@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--mode", default="fast")
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--check", action="store_true", help="eval: trained golden params, predictions of the first "
+                                                         "10k images vs the reference's golden predictions")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     st = torch.cuda.Stream()
@@ -41,6 +43,10 @@ def main():
     ctx.synth_make_set_device(n, 1 if args.what == "train" else 2, x.data_ptr(), y.data_ptr())
     p = torch.zeros(3904, device=dev)
     p[:3898] = torch.from_numpy(init_params(42)).to(dev)
+    if args.check:
+        import numpy as np
+        gp = np.fromfile(os.path.join(ROOT, "tests", "golden", "final_params.f32"), np.float32)
+        p[:3898] = torch.from_numpy(gp).to(dev)
     loss = torch.zeros(4, dtype=torch.float64, device=dev)
     pred = torch.zeros(n, dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -62,7 +68,15 @@ def main():
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     ms = sorted(ts)[len(ts) // 2]
-    print(json.dumps({"what": args.what, "batch": args.batch, "n": n, "mode": args.mode, "ms": ms,
+    extra = {}
+    if args.check and args.what == "eval":
+        import numpy as np
+        gpred = np.fromfile(os.path.join(ROOT, "tests", "golden", "test_pred.u8"), np.uint8).astype(np.int32)
+        m = min(n, 10000)
+        got = pred[:m].cpu().numpy()
+        extra = {"pred_equal_reference_first_10k": bool(np.array_equal(got, gpred[:m])),
+                 "mismatches": int((got != gpred[:m]).sum()), "correct": int(cnt.item())}
+    print(json.dumps({**extra, "what": args.what, "batch": args.batch, "n": n, "mode": args.mode, "ms": ms,
                       "images_per_s": n / ms * 1e3, "tflops": n * flop / ms / 1e9}))
 
 
