@@ -78,6 +78,9 @@ int tlb_ctx_set_cluster(tlb_ctx* ctx, int enable);
 int tlb_ctx_set_threads(tlb_ctx* ctx, int threads);
 int tlb_ctx_info(const tlb_ctx* ctx, int* sm_count, int* train_ctas_per_sm, int* eval_ctas_per_sm,
                  int64_t* smem_bytes_per_cta);
+/* Waits for the context stream and reports device-side failures of earlier device-API launches (a bounded
+ * cross-CTA wait that gave up: TLB_ERR_CUDA; a fast-mode fixed-point gradient overflow: TLB_ERR_VALUE),
+ * clearing them.  tlb_train performs the same check before it returns. */
 int tlb_synchronize(tlb_ctx* ctx);
 
 /* ---- host-side helpers of the reference API --------------------------------------------------- */

@@ -116,6 +116,9 @@ struct tlb_ctx {
   cudaEvent_t copy_gate = nullptr;
   DevBuf ready;
   DevBuf ready_err;  // [3] u32 ingestion watchdog words (flag, chunk, observed value)
+  // [4] u32 device failure words of the train kernels: [0] a bounded cross-CTA wait gave up (abort word),
+  // [1] a fixed-point gradient sum was out of range.  Read and cleared by tlb_train / tlb_synchronize.
+  DevBuf dev_err;
   HostBuf pin;       // tlb_train: pinned params / losses / watchdog words
   unsigned int ready_token = 0;
   DevBuf synth_snaps;  // device synthetic corpus: mt19937_64 state snapshots per segment
@@ -343,6 +346,21 @@ bool is_pinned(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
+constexpr double kWaitLimitSeconds = 2.0;  // bound of the single-GPU cross-CTA waits
+
+// Device failure words (tlb_ctx::dev_err) -> status; clears them.  `words` = the host copy.
+int device_status(tlb_ctx* c, const unsigned int* words) {
+  if (!words[0] && !words[1]) return TLB_OK;
+  cudaMemsetAsync(c->dev_err.p, 0, 4 * sizeof(unsigned int), c->stream);
+  cudaStreamSynchronize(c->stream);
+  if (words[1])
+    return fail(TLB_ERR_VALUE, "train (fast mode): a gradient sum left the fixed-point range of the clustered "
+                               "exchange (|sum| >= 2^18 / clusters; unnormalised inputs or a diverging run) -- the "
+                               "result is invalid; use exact mode or normalised data");
+  return fail(TLB_ERR_CUDA, "train: a cross-CTA wait of the clustered kernel timed out (" +
+                                std::to_string(kWaitLimitSeconds) + " s: SMs held by another process?)");
+}
+
 struct DpArgs {
   int world, rank;
   void* const* peer_ws;  // world pointers: every rank's symmetric workspace (tlb_dp_workspace_bytes)
@@ -415,6 +433,9 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.ready_token = token;
   a.chunk = chunk;
   a.ready_step_end = a.step_begin + spe;  // only the call's first epoch can outrun the copies
+  a.dp_error = static_cast<unsigned int*>(c->dev_err.p);        // single GPU: abort word of the bounded waits
+  a.fix_err = static_cast<unsigned int*>(c->dev_err.p) + 1;
+  a.dp_timeout_cycles = (long long)(kWaitLimitSeconds * 2.0e9);  // ~2 GHz SM clock
   if (clustered) {
     if (dp) {  // fused data parallelism: slice s lives on rank s % world (peer memory)
       a.dp_world = dp->world;
@@ -488,6 +509,8 @@ int tlb_ctx_create(int device, tlb_ctx** out) {
     c->max_clusters = 0;
   }
   if (e == cudaSuccess) e = c->ready_err.ensure(4 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = c->dev_err.ensure(4 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(c->dev_err.p, 0, 4 * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(c->ready_err.p, 0, 4 * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream2, cudaStreamNonBlocking);
@@ -514,6 +537,7 @@ int tlb_ctx_destroy(tlb_ctx* c) {
   if (c->copy_stream2) cudaStreamSynchronize(c->copy_stream2);
   c->ready.release();
   c->ready_err.release();
+  c->dev_err.release();
   c->pin.release();
   for (auto& w : c->wide) w.release();
   c->synth_snaps.release();
@@ -583,8 +607,11 @@ int tlb_ctx_info(const tlb_ctx* c, int* sm, int* occ_train, int* occ_eval, int64
 
 int tlb_synchronize(tlb_ctx* c) {
   if (!c) return fail(TLB_ERR_ARG, "null context");
+  TLB_CUDA(cudaSetDevice(c->device));
   TLB_CUDA(cudaStreamSynchronize(c->stream));
-  return TLB_OK;
+  unsigned int words[4] = {0, 0, 0, 0};  // failures of earlier device-API train launches
+  TLB_CUDA(cudaMemcpy(words, c->dev_err.p, sizeof(words), cudaMemcpyDeviceToHost));
+  return device_status(c, words);
 }
 
 // ---- network, host buffers ------------------------------------------------------------------
@@ -663,7 +690,7 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   TLB_TRY(stage_out(c, 2, TLB_PSTRIDE, &d_p));
   TLB_CUDA(cudaMemsetAsync(d_p, 0, TLB_PSTRIDE * sizeof(float), c->stream));
   // params / losses / watchdog words travel through a pinned host block (async copies, one sync)
-  const size_t pin_bytes = TLB_PSTRIDE * sizeof(float) + (size_t)epochs * sizeof(double) + 4 * sizeof(unsigned int);
+  const size_t pin_bytes = TLB_PSTRIDE * sizeof(float) + (size_t)epochs * sizeof(double) + 8 * sizeof(unsigned int);
   TLB_CUDA(c->pin.ensure(pin_bytes));
   float* h_p = static_cast<float*>(c->pin.p);
   double* h_loss = reinterpret_cast<double*>(h_p + TLB_PSTRIDE);
@@ -696,9 +723,14 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   TLB_CUDA(cudaMemcpyAsync(h_p, d_p, TLB_NPARAM * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
   if (epoch_loss) TLB_CUDA(cudaMemcpyAsync(h_loss, d_loss, epochs * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   if (overlap) TLB_CUDA(cudaMemcpyAsync(h_err, c->ready_err.p, 3 * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+  TLB_CUDA(cudaMemcpyAsync(h_err + 4, c->dev_err.p, 4 * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
   ht.mark("d2h_enqueued");
   TLB_CUDA(cudaStreamSynchronize(c->stream));
   ht.mark("stream_synced");
+  {
+    const unsigned int dev_words[4] = {h_err[4], h_err[5], h_err[6], h_err[7]};
+    TLB_TRY(device_status(c, dev_words));  // params stay untouched on a device failure
+  }
   std::memcpy(params, h_p, TLB_NPARAM * sizeof(float));
   if (epoch_loss) std::memcpy(epoch_loss, h_loss, epochs * sizeof(double));
   if (overlap) {

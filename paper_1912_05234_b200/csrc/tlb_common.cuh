@@ -273,6 +273,35 @@ __device__ __forceinline__ bool mbar_wait_cluster_for(uint64_t* bar, uint32_t pa
     if (clock64() - t0 > limit) return false;
   }
 }
+// Guarded wait of the single-GPU clustered kernel: returns when the phase completes, or -- so that a
+// co-tenant that starves a cluster, or any other protocol failure, fails the call instead of hanging the
+// device -- after `limit` cycles, raising *abort; once *abort is raised every guarded wait of the launch
+// falls through at once (the host then reports the failure).  The abort word is polled only every 256
+// tries, so the common wait (a few hundred cycles) pays no global-memory round trip.
+__device__ __forceinline__ void mbar_wait_cluster_guarded(uint64_t* bar, uint32_t parity, long long limit,
+                                                          unsigned int* abort) {
+  long long t0 = 0;
+  for (unsigned int n = 0;; ++n) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (n == 0) t0 = clock64();
+    if ((n & 255u) == 255u) {
+      if (*reinterpret_cast<volatile unsigned int*>(abort)) return;
+      if (clock64() - t0 > limit) {
+        atomicExch(abort, 1u);
+        return;
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void dsmem_st(uint32_t addr, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }

@@ -52,8 +52,10 @@ struct TrainArgs {
   unsigned int* slice_cnt[8];        // arrival counter of slice s
   unsigned long long* loss_acc;      // [3] u64 loss accumulators
   uint64_t seq_base;
-  unsigned int* dp_error;            // set when a peer wait times out (the kernel then exits)
-  long long dp_timeout_cycles;
+  unsigned int* dp_error;            // set when a peer wait times out (the kernel then exits); single GPU:
+                                     // the abort word of the guarded cluster waits (mbar_wait_cluster_guarded)
+  long long dp_timeout_cycles;       // bound of every cross-CTA / cross-GPU wait
+  unsigned int* fix_err;             // set when a cluster's gradient sum left the fixed-point range (clamped)
 };
 
 struct CellArgs {

@@ -383,6 +383,17 @@ __device__ __forceinline__ void red_add_u64(unsigned long long* p, long long v, 
   if (sys) asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
   else asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Range guard of one cluster's fixed-point contribution: the packed words decode their contribution count
+// only while the step's total stays inside (-2^50, 2^50), so each of the `contributors` words is kept
+// below 2^50 / contributors (|gradient sum| < 2^18 / contributors); an out-of-range or non-finite sum is
+// clamped -- the count stays exact, so no wait can hang -- and flagged, and the host call fails.
+__device__ __forceinline__ double fix_guard(double v, uint32_t contributors, unsigned int* err) {
+  const double lim = 1125899906842624.0 / (double)contributors;  // 2^50 / contributors
+  if (fabs(v) < lim) return v;
+  if (err) atomicExch(err, 1u);
+  return v > 0.0 ? lim - 1.0 : -(lim - 1.0);  // NaN -> the negative bound
+}
+
 __device__ __forceinline__ unsigned long long ld_sys_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -474,14 +485,14 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       // (single GPU: parameter slices 1-7 of the previous step's update land during conv1)
       const bool pending = !dp && ls > 0;
       forward_image<false>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf, pending ? &xbar[2] : nullptr,
-                           (uint32_t)((ls - 1) & 1));
+                           (uint32_t)((ls - 1) & 1), a.dp_timeout_cycles, a.dp_error);
       if (threadIdx.x == 0) cta_loss = __dadd_rn(cta_loss, (double)example_loss(s, s.lab[buf], nullptr));
       backward_image<false, true>(s, s.img + buf * kImg, nullptr);
       ++consumed;
     }
     // A CTA without an image this step still completes the previous step's slice 1-7 phase before it
     // re-arms that barrier below (an arrival on an incomplete phase would corrupt its count).
-    if (!dp && ls > 0 && lo >= hi) mbar_wait_cluster(&xbar[2], (uint32_t)((ls - 1) & 1));
+    if (!dp && ls > 0 && lo >= hi) mbar_wait_cluster_guarded(&xbar[2], (uint32_t)((ls - 1) & 1), a.dp_timeout_cycles, a.dp_error);
     // ---- 2. push slice q of G to its owner q; owner sums the 8 received slices (rank order) ----
     const uint32_t parity = (uint32_t)(ls & 1);
     if (threadIdx.x == 0) st_async_f64(dsmem_map(&loss_rx[rank], 0), cta_loss, dsmem_map(&xbar[0], 0));
@@ -494,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     if (threadIdx.x == 0)
       mbar_arrive_expect_tx(&xbar[0], kCluster * kSlice * sizeof(float) + (rank == 0 ? kCluster * sizeof(double) : 0));
     if (!dp) {
-      mbar_wait_cluster(&xbar[0], parity);  // every slice pushed to this owner has landed
+      mbar_wait_cluster_guarded(&xbar[0], parity, a.dp_timeout_cycles, a.dp_error);  // every slice pushed to this owner
     } else if (__syncthreads_or(!mbar_wait_cluster_for(&xbar[0], parity, a.dp_timeout_cycles))) {
       if (threadIdx.x == 0) atomicExch(a.dp_error, 1u);  // a cluster peer gave up (dead peer GPU)
       return;
@@ -506,20 +517,22 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       float sum = rx[threadIdx.x];
 #pragma unroll
       for (int q = 1; q < kCluster; ++q) sum += rx[q * kSlice + threadIdx.x];
+      const double fx = fix_guard((double)sum * kFix, ncl * (uint32_t)world, a.fix_err);
       if (packed) {
-        red_add_u64(acc + b * kPStride + j, __double2ll_rn((double)sum * kPackFix) + kPackBias, false);
+        red_add_u64(acc + b * kPStride + j, __double2ll_rn(fx) + kPackBias, false);
       } else {
-        red_add_u64(acc + b * kPStride + j, __double2ll_rn((double)sum * kFix), dp);
+        red_add_u64(acc + b * kPStride + j, __double2ll_rn(fx), dp);
         if (cid == 0 && owner) acc[bn * kPStride + j] = 0ull;  // next step's accumulator
       }
     }
     if (rank == 0 && threadIdx.x == kSlice) {
       double l = 0.0;
       for (int q = 0; q < kCluster; ++q) l = __dadd_rn(l, loss_rx[q]);
+      const double fx = fix_guard(l * kFix, ncl * (uint32_t)world, a.fix_err);
       if (packed) {
-        red_add_u64(lacc + b, __double2ll_rn(l * kPackFix) + kPackBias, false);
+        red_add_u64(lacc + b, __double2ll_rn(fx) + kPackBias, false);
       } else {
-        red_add_u64(lacc + b, __double2ll_rn(l * kFix), dp);
+        red_add_u64(lacc + b, __double2ll_rn(fx), dp);
         if (cid == 0 && (!dp || a.dp_rank == 0)) lacc[bn] = 0ull;
       }
     }
@@ -536,19 +549,23 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
         const unsigned long long want = (unsigned long long)ncl;
         auto count_of = [&](unsigned long long v) { return (v - prev + (1ull << 50)) >> 51; };
         unsigned long long v;
-        if ((threadIdx.x & 31) == 0) {
-          for (;;) {
+        // bounded: a word that never completes (a starved cluster) raises the abort word instead of hanging
+        const long long t0 = clock64();
+        auto poll = [&]() {
+          for (unsigned int n = 0;; ++n) {
             asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(w) : "memory");
-            if (count_of(v) >= want) break;
+            if (count_of(v) >= want) return;
+            if ((n & 63u) == 63u &&
+                (*reinterpret_cast<volatile unsigned int*>(a.dp_error) || clock64() - t0 > a.dp_timeout_cycles)) {
+              atomicExch(a.dp_error, 1u);
+              return;
+            }
             __nanosleep(32);
           }
-        }
+        };
+        if ((threadIdx.x & 31) == 0) poll();
         __syncwarp(__activemask());
-        for (;;) {
-          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(w) : "memory");
-          if (count_of(v) >= want) break;
-          __nanosleep(32);
-        }
+        poll();
         dsum = (int64_t)(v - prev - want * (unsigned long long)kPackBias);
         if (b == 0) packed_prev0 = v;
         else if (b == 1) packed_prev1 = v;
@@ -633,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       mbar_arrive_expect_tx(&xbar[2], (uint32_t)((rank == 0 ? kCluster - 1 : kCluster - 2) * kSlice * sizeof(float)));
     }
     if (!dp) {
-      mbar_wait_cluster(&xbar[1], parity);  // slice 0 has landed (slices 1-7: after the next conv1)
+      mbar_wait_cluster_guarded(&xbar[1], parity, a.dp_timeout_cycles, a.dp_error);  // slice 0 (1-7: after conv1)
     } else if (__syncthreads_or(!mbar_wait_cluster_for(&xbar[1], parity, a.dp_timeout_cycles) ||
                                 !mbar_wait_cluster_for(&xbar[2], parity, a.dp_timeout_cycles))) {
       if (threadIdx.x == 0) atomicExch(a.dp_error, 1u);
@@ -643,7 +660,8 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     mark(s, 13);
   }
   if (!dp) {
-    if (a.step_end > a.step_begin) mbar_wait_cluster(&xbar[2], (uint32_t)((a.step_end - a.step_begin - 1) & 1));
+    if (a.step_end > a.step_begin)
+      mbar_wait_cluster_guarded(&xbar[2], (uint32_t)((a.step_end - a.step_begin - 1) & 1), a.dp_timeout_cycles, a.dp_error);
     cluster_sync_all();  // no CTA leaves while a peer's DSMEM traffic may still target it
   }
 }
@@ -826,11 +844,25 @@ cudaError_t launch_train_cluster(const TrainArgs& a, int clusters, cudaStream_t 
   attr[1].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  // TLB_CLUSTER_COOP=1 adds the cooperative attribute (co-residency asserted by the driver); the
-  // default plain cluster launch relies on clusters <= cudaOccupancyMaxActiveClusters on an idle
-  // device, which also keeps the kernel profilable by ncu.
-  static const bool coop = getenv("TLB_CLUSTER_COOP") != nullptr;
-  cfg.numAttrs = coop ? 2 : 1;
+  // Default: the cooperative attribute, so the driver asserts that every cluster is co-resident (the
+  // kernel's cross-cluster waits need it; a co-tenant holding SMs fails the launch instead of starving a
+  // cluster).  TLB_CLUSTER_COOP=0 launches plainly (profilers that cannot replay cooperative launches);
+  // a driver that rejects the attribute combination falls back to the plain launch once.  Either way
+  // every cross-CTA wait is bounded (mbar_wait_cluster_guarded / the packed-word polls).
+  static const bool want_coop = [] {
+    const char* e = getenv("TLB_CLUSTER_COOP");
+    return !(e && e[0] == '0');
+  }();
+  static bool coop_ok = true;
+  if (want_coop && coop_ok) {
+    cfg.numAttrs = 2;
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, train_cluster_kernel, a);
+    if (le != cudaErrorInvalidValue && le != cudaErrorNotSupported && le != cudaErrorInvalidConfiguration)
+      return le;
+    (void)cudaGetLastError();
+    coop_ok = false;
+  }
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, train_cluster_kernel, a);
 }
 

@@ -1684,12 +1684,13 @@ __device__ __noinline__ void call_conv1_back(const float* img, float* row) {
 template <bool EXACT>
 __device__ __forceinline__ void forward_image(const Smem& s, const float* img, int label, const float* y,
                                               bool want_dz, const int* lab = nullptr, uint64_t* post_conv1 = nullptr,
-                                              uint32_t post_conv1_parity = 0) {
+                                              uint32_t post_conv1_parity = 0, long long wait_limit = 0,
+                                              unsigned int* abort = nullptr) {
   call_conv1<EXACT>(img);
   __syncthreads();
   if (lab) label = *lab;
   // clustered kernel: the parameters conv2 and later stages read may still be arriving during conv1
-  if (post_conv1) mbar_wait_cluster(post_conv1, post_conv1_parity);
+  if (post_conv1) mbar_wait_cluster_guarded(post_conv1, post_conv1_parity, wait_limit, abort);
   mark(s, 3);
   call_conv2<EXACT>();  // includes avgpool
   __syncthreads();

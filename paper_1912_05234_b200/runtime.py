@@ -43,6 +43,26 @@ def _check(rc: int) -> None:
         raise_for(rc, _lib.lib().tlb_last_error().decode())
 
 
+# ---- argument checks: the C ABI takes raw pointers, so sizes are verified here (the reference's typed
+# tensors and Params::validate, network.cpp:42-49, make the same mistakes impossible in C++) ----------
+def _check_params(p, who: str) -> None:
+    if np.asarray(p).size != NPARAM:
+        raise_for(2, f"{who}: params hold {np.asarray(p).size} floats, expected {NPARAM} "
+                     "(k1,b1,k2,b2,fc,b in write_flat order)")
+
+
+def _check_images(images: np.ndarray, n: int, who: str) -> None:
+    if images.size != n * 784:
+        raise_for(2, f"{who}: images hold {images.size} floats, expected {n} x 784 for {n} labels")
+
+
+def _images_2d(images, who: str) -> np.ndarray:
+    a = _f32(images)
+    if a.size % 784:
+        raise_for(2, f"{who}: {a.size} image floats is not a whole number of 28x28 images")
+    return a.reshape(-1, 784)
+
+
 # ---- host helpers that need no device ------------------------------------------------------------
 def init_params(seed: int) -> np.ndarray:
     """net::init_params (network.cpp:56-79)."""
@@ -162,8 +182,10 @@ class Context:
     def train(self, params, images, labels, rate: float = 0.05, epochs: int = 10, batch: int = 100,
               on_epoch: Optional[Callable[[int, float], None]] = None):
         """net::train -> (trained params [3898], epoch mean losses [epochs])."""
-        p = np.array(params, np.float32, copy=True)
-        images, labels = _f32(images), np.ascontiguousarray(labels, np.int32)
+        p = np.array(params, np.float32, copy=True).reshape(-1)
+        images, labels = _f32(images), np.ascontiguousarray(labels, np.int32).reshape(-1)
+        _check_params(p, "train")
+        _check_images(images, len(labels), "train")
         losses = np.zeros(max(epochs, 1), np.float64)
         cb = _lib.EPOCH_CB(lambda e, l, _u: on_epoch(e, l)) if on_epoch else _NO_EPOCH_CB
         _check(self._L.tlb_train(self._h, images.ctypes.data, labels.ctypes.data, len(labels), p.ctypes.data, rate,
@@ -172,7 +194,8 @@ class Context:
 
     def forward(self, images, params, acts: bool = False):
         """net::forward for n images -> yhat [n,10] (and activations [n,5290])."""
-        images = _f32(images).reshape(-1, 784)
+        images = _images_2d(images, "forward")
+        _check_params(params, "forward")
         n = images.shape[0]
         yhat = np.zeros((max(n, 1), 10), np.float32)
         a = np.zeros((max(n, 1), NACT), np.float32) if acts else None
@@ -181,8 +204,13 @@ class Context:
 
     def forward_backward(self, images, params, labels=None, targets=None, acts: bool = False):
         """forward + net::backward + net::loss -> cells [n,3899] (3898 grads + loss)."""
-        images = _f32(images).reshape(-1, 784)
+        images = _images_2d(images, "forward_backward")
+        _check_params(params, "forward_backward")
         n = images.shape[0]
+        if labels is not None and np.asarray(labels).size != n:
+            raise_for(2, f"forward_backward: {np.asarray(labels).size} labels for {n} images")
+        if targets is not None and np.asarray(targets).size != 10 * n:
+            raise_for(2, f"forward_backward: targets hold {np.asarray(targets).size} floats, expected {10 * n}")
         cells = np.zeros((max(n, 1), CELL), np.float32)
         a = np.zeros((max(n, 1), NACT), np.float32) if acts else None
         lab = np.ascontiguousarray(labels, np.int32) if labels is not None else None
@@ -193,8 +221,10 @@ class Context:
 
     def evaluate(self, params, images, labels, return_pred: bool = False):
         """net::evaluate -> accuracy (fraction correct); optionally the predictions."""
-        images, labels = _f32(images).reshape(-1, 784), np.ascontiguousarray(labels, np.int32)
+        images, labels = _images_2d(images, "evaluate"), np.ascontiguousarray(labels, np.int32).reshape(-1)
+        _check_params(params, "evaluate")
         n = len(labels)
+        _check_images(images, n, "evaluate")
         pred = np.zeros(max(n, 1), np.int32)
         correct = C.c_int64()
         _check(self._L.tlb_evaluate(self._h, _fp(images), _ip(labels), n, _fp(_f32(params)), _ip(pred),
@@ -203,6 +233,8 @@ class Context:
         return (acc, pred[:n]) if return_pred else acc
 
     def sgd_step(self, params, grads, rate: float, batch: int) -> np.ndarray:
+        _check_params(params, "sgd_step")
+        _check_params(grads, "sgd_step")
         out = np.zeros(NPARAM, np.float32)
         _check(self._L.tlb_sgd_step(self._h, _fp(_f32(params)), _fp(_f32(grads)), rate, batch, _fp(out)))
         return out

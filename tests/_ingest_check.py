@@ -1,6 +1,10 @@
 """Overlapped-ingestion check shared by tests/test_gpu_parity.py (in process, default chunk policy) and
 run as ``python tests/_ingest_check.py`` under other TLB_INGEST_CHUNK policies: tlb_train on host
-buffers (pageable and pinned) must equal tlb_train_device on resident data, bit for bit."""
+buffers (pageable and pinned) must equal tlb_train_device on resident data, bit for bit.
+
+Every case trains on its own window of the corpus (a per-case offset, and labels rotated by the case
+index), so the staging buffer never already holds the expected images from an earlier call: a missing
+or mis-indexed ready-flag wait would read the previous case's bytes and change the result."""
 import numpy as np
 
 CASES = ((1, 100), (83, 7), (200, 100), (5000, 100), (300, 100), (1001, 77), (2, 1), (3, 1), (4, 1), (5, 1),
@@ -19,13 +23,16 @@ def check(orc, tr_x, tr_y, mode):
     with Context(0, mode=mode) as c:
         c.set_stream(torch.cuda.current_stream().cuda_stream)
         for i, (n, batch) in enumerate(CASES):
-            xs, ys = tr_x[:n], tr_y[:n]
+            off = (i * 733) % (len(tr_y) - n + 1)
+            win_x = np.ascontiguousarray(tr_x[off:off + n])
+            win_y = np.ascontiguousarray((tr_y[off:off + n] + i) % 10, np.int32)
+            xs, ys = win_x, win_y
             if i % 2:  # pinned source: the kernel is enqueued before the chunk copies
                 xs = torch.from_numpy(np.ascontiguousarray(xs)).pin_memory().numpy()
                 ys = torch.from_numpy(np.ascontiguousarray(ys)).pin_memory().numpy()
             got_p, got_l = c.train(p0, xs, ys, epochs=2, batch=batch)
-            d_x = torch.from_numpy(tr_x[:n]).to(dev)
-            d_y = torch.from_numpy(tr_y[:n]).to(dev)
+            d_x = torch.from_numpy(win_x).to(dev)
+            d_y = torch.from_numpy(win_y).to(dev)
             d_p = torch.zeros(3904, device=dev)
             d_p[:3898] = torch.from_numpy(p0).to(dev)
             d_l = torch.zeros(2, dtype=torch.float64, device=dev)
