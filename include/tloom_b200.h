@@ -72,6 +72,10 @@ int tlb_ctx_set_trace(tlb_ctx* ctx, void* d_trace);
 /* Fast mode, groups of <= 8 x (co-resident clusters) examples: 1 (default) runs the clustered train
  * kernel (DSMEM gradient pre-reduction, one grid barrier per step); 0 forces the flat kernel. */
 int tlb_ctx_set_cluster(tlb_ctx* ctx, int enable);
+/* Fast mode, groups the clustered kernel does not take: -1 (default) runs the batched train kernel (NI
+ * images per CTA round, batch_train.cu) from 4 x SM-count examples per group (env TLB_BATCHED=0/1
+ * overrides), 0 the one-image-per-CTA flat kernel, 1 the batched kernel for every such group. */
+int tlb_ctx_set_batched(tlb_ctx* ctx, int mode);
 /* CTA size of the flat train / forward kernels: 0 = automatic (default: 256 = two independent CTAs per SM
  * whose barrier stalls overlap once a launch has more than one item per SM, else 512), or forced 256 / 512.
  * Env TLB_FAST_THREADS. */

@@ -26,7 +26,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + os.pat
           "-I" + CSRC]
 CU_FLAGS = ARCH + COMMON + ["-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
-SOURCES = ["zhang_kernels.cu", "infer_kernels.cu", "nn_ops.cu", "wide_kernels.cu", "wide_tc.cu", "synth_device.cu", "capi.cu",
+SOURCES = ["zhang_kernels.cu", "batch_train.cu", "infer_kernels.cu", "nn_ops.cu", "wide_kernels.cu", "wide_tc.cu", "synth_device.cu", "capi.cu",
            "host_data.cpp"]
 # C++ mirror of the reference headers (include/tloom/*.hpp): plain host code, g++ -std=gnu++20
 HOST_SOURCES = ["host/tensor.cpp", "host/runtime.cpp", "host/nn.cpp", "host/network.cpp", "host/mnist.cpp",
@@ -34,7 +34,7 @@ HOST_SOURCES = ["host/tensor.cpp", "host/runtime.cpp", "host/nn.cpp", "host/netw
 CXX = os.environ.get("CXX", "g++")
 CXX_FLAGS = ["-std=gnu++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
              "-I" + os.path.join(CSRC, "host")]
-HEADERS = ["tlb_common.cuh", "zhang_step.cuh", "tlb_launch.h", "tlb_capi_internal.h", "wide_kernels.cuh"]
+HEADERS = ["tlb_common.cuh", "train_common.cuh", "zhang_step.cuh", "tlb_launch.h", "tlb_capi_internal.h", "wide_kernels.cuh"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

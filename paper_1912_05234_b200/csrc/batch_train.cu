@@ -1,0 +1,711 @@
+// batch_train.cu -- fast-mode persistent train kernel for large SGD groups (BASELINE configs[3]: batch
+// 1k .. 256k per GPU; net::train, proj/src/network.cpp:209-251).
+//
+// The one-image-per-CTA kernels (zhang_kernels.cu) keep one image's activations resident and run every
+// stage on that image: at batch >= 1k each stage's barrier is paid per image and every weight-gradient
+// output is read-modified-written in shared memory per image.  Here a CTA trains NI images per ROUND:
+//   * every stage's lanes span the NI images (one barrier per stage per round, not per image);
+//   * the weight-gradient lanes own their outputs and loop over the round's images in registers, so the
+//     CTA's gradient accumulator G (shared memory) is updated once per round per output;
+//   * the NI images of a round are contiguous in HBM and arrive with ONE TMA bulk copy into a
+//     double-buffered ring (the next round -- possibly the next step's first -- is in flight meanwhile).
+// Per step (one SGD group): each CTA trains static_chunk(m, grid, cta) of the group's examples, writes
+// its partial gradient row, grid barrier, CTA b reduces parameters static_chunk(3898, grid, b) over the
+// partial rows in CTA order (fixed tree: deterministic run to run) and applies sgd_step
+// (network.cpp:171-180) or, in DP shard mode, writes the shard's gradient sum; grid barrier.
+//
+// Stages of a round (cnt <= NI images; lane counts per image):
+//   S1 conv1+sigmoid+pool, and g1 = c1(1-c1)                         144 lanes x 600 FFMA
+//   S2 conv2+sigmoid+pool, and g2 = c2(1-c2) into padded dz2 rows     192 lanes x 600 FFMA (row x channel half)
+//   S3 FC+sigmoid, dz = ((o-y)o)(1-o)                                  80 lanes (8 per class)
+//   S4 d_s2 = fc^T dz, dz2 = (d_s2/4) g2                               192 lanes
+//   S5 backin (36 row pairs x 4 kernel-group lanes, valid taps only: 720-840 FFMA each), whose epilogue
+//      writes dz1 = (d_s1/4) g1 in place of g1; g_k2 + g_b2 (720 + 24 lanes over the round's images,
+//      320 FFMA per image); g_fc + g_b (1,930 output lanes)
+//   S6 g_k1 (30 outputs x 8 row-chunk lanes over the round's images), g_b1
+// Arithmetic is the fast mode's (FFMA, ex2/rcp MUFU logistic; fixed summation trees), within the
+// north-star 1e-4 tolerance; EXACT mode never runs here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+
+#include "tlb_common.cuh"
+#include "tlb_launch.h"
+#include "train_common.cuh"
+
+namespace tlb {
+namespace bt {
+
+// Padded weight copies (built per step from P): conv1 rows [6][5][8] in 44-float channel slots, conv2 rows
+// [12][6][5][8] in 244-float kernel slots: every 5-tap row is an aligned float4 + a scalar, and the
+// distinct channels / kernels a warp touches fall in distinct bank groups (11 and 61 float4s, odd mod 8).
+constexpr int kW1Stride = 44, kW1Floats = 6 * kW1Stride;
+constexpr int kW2Stride = 244, kW2Floats = 12 * kW2Stride;
+// Per-image region: g1 (c1(1-c1), then dz1 in place) [6][24][24] in 580-float planes | s1 [6][12][12] |
+// dz2 zero-padded by 4 rows top and bottom [12][16][8] in 132-float kernel slots (g2 = c2(1-c2) first) |
+// s2 [192] | out [10] at 0, dz [10] at 16.
+constexpr int kG1Plane = 580, kG1Floats = 6 * kG1Plane;
+constexpr int kD2K = 132, kD2Floats = 12 * kD2K;
+constexpr int kOffS1 = kG1Floats, kOffD2 = kOffS1 + 864, kOffS2 = kOffD2 + kD2Floats, kOffOd = kOffS2 + 192;
+constexpr int kImgRegion = kOffOd + 32;
+static_assert(kOffS1 % 4 == 0 && kOffD2 % 4 == 0 && kOffS2 % 4 == 0 && kImgRegion % 4 == 0, "float4 regions");
+
+template <int NI>
+struct Layout {
+  static constexpr int kP = 0;
+  static constexpr int kW1 = kP + kPStride;
+  static constexpr int kW2 = kW1 + kW1Floats;
+  static constexpr int kG = kW2 + kW2Floats;
+  static constexpr int kRing = kG + kPStride;          // [2][NI][784] TMA ring
+  static constexpr int kLab = kRing + 2 * NI * kImg;   // [2][NI] labels (ints)
+  static constexpr int kImgs = kLab + 16;
+  static constexpr int kFloats = kImgs + NI * kImgRegion;
+  static constexpr size_t kBytes = (size_t)kFloats * sizeof(float) + 2 * sizeof(uint64_t);
+  static_assert(kRing % 4 == 0 && kImgs % 4 == 0, "16-byte aligned regions");
+  static_assert(2 * NI <= 16, "label slots");
+};
+
+extern __shared__ __align__(128) float bt_smem[];
+
+// logistic(acc + b) with nb = -b log2(e): one FFMA, ex2.approx.ftz, add, rcp.approx.ftz (fast mode).
+__device__ __forceinline__ float logistic(float acc, float nb) {
+  constexpr float kNegLog2e = -1.4426950408889634f;
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmaf_rn(acc, kNegLog2e, nb)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+  return r;
+}
+__device__ __forceinline__ float neg_log2e_times(float b) { return b * -1.4426950408889634f; }
+
+__device__ __forceinline__ void load5(const float* wrow, float (&w)[5]) {
+  const float4 a = *reinterpret_cast<const float4*>(wrow);
+  w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+  w[4] = wrow[4];
+}
+template <int N>
+__device__ __forceinline__ void load_row(const float* src, float (&v)[N]) {
+  static_assert(N % 4 == 0, "float4 rows");
+#pragma unroll
+  for (int q = 0; q < N / 4; ++q) {
+    const float4 x = reinterpret_cast<const float4*>(src)[q];
+    v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+  }
+}
+
+// S1: lane (image k, pooled row py, 12-column half xs, channel i), channel fastest: conv rows 2py, 2py+1
+// x 12 columns over the 25 taps (nn.cpp:28-33 order per output), sigmoid, g1 = c1(1-c1), 2x2 pool.
+__device__ __forceinline__ void conv1_item(const float* P, const float* W1, const float* imgs, float* regs, int it) {
+  const int k = it / 144, r = it - k * 144;
+  const int pos = r / 6, i = r - pos * 6, py = pos >> 1, xs = pos & 1;
+  const int y0 = 2 * py, x0 = 12 * xs;
+  const float* img = imgs + k * kImg;
+  const float* w = W1 + i * kW1Stride;
+  float a[2][12];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int o = 0; o < 12; ++o) a[q][o] = 0.0f;
+#pragma unroll
+  for (int rr = 0; rr < 6; ++rr) {  // image row y0 + rr feeds conv row q with ky = rr - q
+    float in[16];
+    load_row<16>(img + (y0 + rr) * 28 + x0, in);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int ky = rr - q;
+      if (ky < 0 || ky > 4) continue;
+      float wv[5];
+      load5(w + ky * 8, wv);
+#pragma unroll
+      for (int kx = 0; kx < 5; ++kx)
+#pragma unroll
+        for (int o = 0; o < 12; ++o) a[q][o] = __fmaf_rn(in[o + kx], wv[kx], a[q][o]);
+    }
+  }
+  const float nb = neg_log2e_times(P[kB1 + i]);
+  float* reg = regs + k * kImgRegion;
+  float* g1 = reg + i * kG1Plane + y0 * 24 + x0;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+#pragma unroll
+    for (int o = 0; o < 12; ++o) a[q][o] = logistic(a[q][o], nb);
+#pragma unroll
+    for (int o4 = 0; o4 < 3; ++o4) {
+      float4 g;
+      g.x = a[q][4 * o4] * (1.0f - a[q][4 * o4]);
+      g.y = a[q][4 * o4 + 1] * (1.0f - a[q][4 * o4 + 1]);
+      g.z = a[q][4 * o4 + 2] * (1.0f - a[q][4 * o4 + 2]);
+      g.w = a[q][4 * o4 + 3] * (1.0f - a[q][4 * o4 + 3]);
+      *reinterpret_cast<float4*>(g1 + q * 24 + 4 * o4) = g;
+    }
+  }
+  float* s1 = reg + kOffS1 + (i * 12 + py) * 12 + 6 * xs;
+#pragma unroll
+  for (int px = 0; px < 6; px += 2) {  // avgpool (nn.cpp:144): ((p00 + p01) + p10) + p11, then * 0.25f
+    float pv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = 2 * (px + h);
+      pv[h] = (((a[0][c] + a[0][c + 1]) + a[1][c]) + a[1][c + 1]) * 0.25f;
+    }
+    *reinterpret_cast<float2*>(s1 + px) = make_float2(pv[0], pv[1]);
+  }
+}
+
+// S2: lane (image k, pooled row py, kernel i, conv row r of the pooling window, channel half ch), ch fastest:
+// the partial sum of conv row y = 2py + r (8 columns) over channels 3ch..3ch+2 (the 150 taps in
+// (c, ky, kx) order within each half), joined by a shuffle; lane ch then owns columns 4ch..4ch+3: sigmoid,
+// g2 into the padded dz2 row, and -- with the partner row from lane ^ 2 -- the 2x2 pool.
+__device__ __forceinline__ void conv2_item(const float* P, const float* W2, float* regs, int it) {
+  const int ch = it & 1, r = (it >> 1) & 1, rest = it >> 2;
+  const int i = rest % 12, kp = rest / 12, py = kp & 3, k = kp >> 2;
+  const int y = 2 * py + r;
+  float* reg = regs + k * kImgRegion;
+  const float* s1 = reg + kOffS1;
+  float acc[8];
+#pragma unroll
+  for (int o = 0; o < 8; ++o) acc[o] = 0.0f;
+#pragma unroll 1
+  for (int c = 3 * ch; c < 3 * ch + 3; ++c) {
+    const float* wc = W2 + i * kW2Stride + c * 40;
+    const float* srow = s1 + (c * 12 + y) * 12;
+#pragma unroll
+    for (int ky = 0; ky < 5; ++ky) {
+      float in[12], wv[5];
+      load_row<12>(srow + ky * 12, in);
+      load5(wc + ky * 8, wv);
+#pragma unroll
+      for (int kx = 0; kx < 5; ++kx)
+#pragma unroll
+        for (int o = 0; o < 8; ++o) acc[o] = __fmaf_rn(in[o + kx], wv[kx], acc[o]);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < 8; ++o) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], 1);
+  const float nb = neg_log2e_times(P[kB2 + i]);
+  float t[4], u[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) t[j] = logistic(ch ? acc[4 + j] : acc[j], nb);
+  *reinterpret_cast<float4*>(reg + kOffD2 + i * kD2K + (4 + y) * 8 + 4 * ch) =
+      make_float4(t[0] * (1.0f - t[0]), t[1] * (1.0f - t[1]), t[2] * (1.0f - t[2]), t[3] * (1.0f - t[3]));
+#pragma unroll
+  for (int j = 0; j < 4; ++j) u[j] = __shfl_xor_sync(0xffffffffu, t[j], 2);  // conv row y ^ 1
+  if (r == 0)  // avgpool (nn.cpp:144): ((p00 + p01) + p10) + p11, then * 0.25f
+    *reinterpret_cast<float2*>(reg + kOffS2 + (i * 4 + py) * 4 + 2 * ch) =
+        make_float2((((t[0] + t[1]) + u[0]) + u[1]) * 0.25f, (((t[2] + t[3]) + u[2]) + u[3]) * 0.25f);
+}
+
+// S3: eight lanes per (image, class): 24-term partials of the 192-tap FC dot, a 3-level xor tree, sigmoid;
+// dz = ((o - y) o)(1 - o) with y = one_hot(label) (network.cpp:146-152).  Whole warps (see fc_item in
+// infer_kernels.cu); lanes past the last task recompute task 0 and store nothing.
+__device__ __forceinline__ void fc_item(const float* P, float* regs, const int* lab, int it, bool valid) {
+  const int task = valid ? it >> 3 : 0, part = it & 7, k = task / 10, i = task - k * 10;
+  float* reg = regs + k * kImgRegion;
+  const float4* s2 = reinterpret_cast<const float4*>(reg + kOffS2 + 24 * part);
+  const float4* w = reinterpret_cast<const float4*>(P + kFC + i * 192 + 24 * part);
+  float acc = 0.0f;
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const float4 x = s2[q], y = w[q];
+    acc = __fmaf_rn(x.x, y.x, acc);
+    acc = __fmaf_rn(x.y, y.y, acc);
+    acc = __fmaf_rn(x.z, y.z, acc);
+    acc = __fmaf_rn(x.w, y.w, acc);
+  }
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  if (valid && part == 0) {
+    const float o = logistic(acc, neg_log2e_times(P[kB + i]));
+    const float y = i == lab[k] ? 1.0f : 0.0f;
+    reg[kOffOd + i] = o;
+    reg[kOffOd + 16 + i] = ((o - y) * o) * (1.0f - o);
+  }
+}
+
+// S5 backin lane (4 lanes per task, kernels 3ig..3ig+2 each, joined by shuffles): the d_s1 rows pA = pp and
+// pB = pp + 6 of channel c (pp < 6) -- 12 columns each -- over exactly the valid kernel rows of the reference's
+// BackinBox (nn.cpp:169-189): u <= pA for row pA, u >= pB - 7 for row pB (6-7 rows per lane for every pp;
+// the column bounds are compile-time).  Tasks run pp-major, so a warp holds at most two pp values.  Epilogue:
+// dz1 = (d_s1 * 0.25) g1 for conv1 rows 2p, 2p+1 of both rows, columns 6ig..6ig+5 (in place of g1).
+__device__ __forceinline__ void backin_acc(const float* d2i, const float* wrow, int p, int u0, int u1, float (&acc)[12]) {
+#pragma unroll 1
+  for (int u = u0; u <= u1; ++u) {
+    float d[8], w[5];
+    load_row<8>(d2i + (4 + p - u) * 8, d);
+    load5(wrow + u * 8, w);
+#pragma unroll
+    for (int q = 0; q < 12; ++q)
+#pragma unroll
+      for (int v = 0; v < 5; ++v)
+        if (q - v >= 0 && q - v < 8) acc[q] = __fmaf_rn(w[v], d[q - v], acc[q]);
+  }
+}
+
+__device__ __forceinline__ void backin_dz1(float* g1c, int p, int ig, const float (&acc)[12]) {
+  float ds[3];
+#pragma unroll
+  for (int h = 0; h < 3; ++h)
+    ds[h] = 0.25f * (ig == 0 ? acc[h] : ig == 1 ? acc[3 + h] : ig == 2 ? acc[6 + h] : acc[9 + h]);
+  float* g1 = g1c + (2 * p) * 24 + 6 * ig;
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      float2* q2 = reinterpret_cast<float2*>(g1 + a * 24 + 2 * h);
+      const float2 g = *q2;
+      *q2 = make_float2(ds[h] * g.x, ds[h] * g.y);
+    }
+  }
+}
+
+__device__ __forceinline__ void backin_item(const float* W2, float* regs, int bi, int cnt, bool valid) {
+  const int ig = bi & 3, task = valid ? bi >> 2 : 0;
+  const int c = task % 6, kp = task / 6, k = kp % cnt, pp = kp / cnt;
+  float* reg = regs + k * kImgRegion;
+  float accA[12], accB[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) accA[q] = accB[q] = 0.0f;
+  const int pA = pp, pB = pp + 6;
+#pragma unroll 1
+  for (int ii = 0; ii < 3; ++ii) {
+    const int i = 3 * ig + ii;
+    const float* wrow = W2 + i * kW2Stride + c * 40;
+    const float* d2i = reg + kOffD2 + i * kD2K;
+    backin_acc(d2i, wrow, pA, 0, min(4, pA), accA);
+    backin_acc(d2i, wrow, pB, max(0, pB - 7), 4, accB);
+  }
+#pragma unroll
+  for (int q = 0; q < 12; ++q) {
+    accA[q] += __shfl_xor_sync(0xffffffffu, accA[q], 1);
+    accB[q] += __shfl_xor_sync(0xffffffffu, accB[q], 1);
+    accA[q] += __shfl_xor_sync(0xffffffffu, accA[q], 2);
+    accB[q] += __shfl_xor_sync(0xffffffffu, accB[q], 2);
+  }
+  if (!valid) return;
+  float* g1c = reg + c * kG1Plane;
+  backin_dz1(g1c, pA, ig, accA);
+  backin_dz1(g1c, pB, ig, accB);
+}
+
+// S5 weight-gradient lane of conv2 (or of its bias): G[k2(i,c,u,0..4)] += sum over the round's images, rows
+// y in half yh (4 rows), x < 8 of s1[c][u+y][v+x] * dz2[i][y][x] (nn.cpp:96-108 via backweights); the two
+// row halves join by a shuffle.  Items 720..743: g_b2 (kernel i, half yh).  Kernel i varies fastest after yh:
+// the lanes of a (c, u) read the same s1 rows (broadcast).
+__device__ __forceinline__ void gk2_item(float* G, const float* regs, int it, int cnt) {
+  const int yh = it & 1, task = it >> 1;
+  float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+  if (task < 360) {
+    const int i = task % 12, cu = task / 12, c = cu / 5, u = cu - c * 5;
+#pragma unroll 1
+    for (int k = 0; k < cnt; ++k) {
+      const float* reg = regs + k * kImgRegion;
+      const float* s1 = reg + kOffS1 + (c * 12 + u + 4 * yh) * 12;
+      const float* d2 = reg + kOffD2 + i * kD2K + (4 + 4 * yh) * 8;
+#pragma unroll 2
+      for (int y = 0; y < 4; ++y) {
+        float in[12], d[8];
+        load_row<12>(s1 + y * 12, in);
+        load_row<8>(d2 + y * 8, d);
+#pragma unroll
+        for (int v = 0; v < 5; ++v)
+#pragma unroll
+          for (int x = 0; x < 8; ++x) acc[v] = __fmaf_rn(in[v + x], d[x], acc[v]);
+      }
+    }
+  } else if (task < 372) {
+    const int i = task - 360;
+    for (int k = 0; k < cnt; ++k) {
+      const float4* d = reinterpret_cast<const float4*>(regs + k * kImgRegion + kOffD2 + i * kD2K + (4 + 4 * yh) * 8);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 v = d[q];
+        acc[0] += (v.x + v.y) + (v.z + v.w);
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < 5; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], 1);
+  if (yh == 0) {
+    if (task < 360) {
+      const int i = task % 12, cu = task / 12, c = cu / 5, u = cu - c * 5;
+      float* g = G + kK2 + ((i * 6 + c) * 5 + u) * 5;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) g[v] += acc[v];
+    } else if (task < 372) {
+      G[kB2 + task - 360] += acc[0];
+    }
+  }
+}
+
+// S6: g_k1 lane (kernel i, row u, row chunk yc of 3 rows), yc fastest: 5 partials over the round's images;
+// or a g_b1 lane (kernel i, row chunk yc).  The 8 row-chunk lanes join by a 3-level xor tree.
+__device__ __forceinline__ void gk1_item(float* G, const float* imgs, const float* regs, int it, int cnt) {
+  const int yc = it & 7;
+  float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+  const bool bias = it >= 240;
+  const int task = bias ? (it - 240) >> 3 : it >> 3;
+  const int i = bias ? task : task / 5, u = bias ? 0 : task - (task / 5) * 5;
+  if (!bias) {
+#pragma unroll 1
+    for (int k = 0; k < cnt; ++k) {
+      const float* img = imgs + k * kImg + u * 28;
+      const float* dz1 = regs + k * kImgRegion + i * kG1Plane;
+#pragma unroll 1
+      for (int yy = 0; yy < 3; ++yy) {
+        const int y = 3 * yc + yy;
+        float in[28], d[24];
+        load_row<28>(img + y * 28, in);
+        load_row<24>(dz1 + y * 24, d);
+#pragma unroll
+        for (int v = 0; v < 5; ++v)
+#pragma unroll
+          for (int x = 0; x < 24; ++x) acc[v] = __fmaf_rn(in[v + x], d[x], acc[v]);
+      }
+    }
+  } else {
+    for (int k = 0; k < cnt; ++k) {
+      const float4* dz1 = reinterpret_cast<const float4*>(regs + k * kImgRegion + i * kG1Plane + 3 * yc * 24);
+#pragma unroll
+      for (int q = 0; q < 18; ++q) {
+        const float4 v = dz1[q];
+        acc[0] += (v.x + v.y) + (v.z + v.w);
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], 4);
+    acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], 2);
+    acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], 1);
+  }
+  if (yc == 0) {
+    if (bias) {
+      G[kB1 + i] += acc[0];
+    } else {
+      float* g = G + kK1 + i * 25 + u * 5;
+#pragma unroll
+      for (int v = 0; v < 5; ++v) g[v] += acc[v];
+    }
+  }
+}
+
+// Rounds of one CTA: (step, first local example, end of the CTA's chunk).
+struct Round {
+  int64_t step, e, hi;
+};
+
+template <int NI>
+__device__ __forceinline__ bool first_round(const TrainArgs& a, int64_t from, Round& r) {
+  for (int64_t st = from; st < a.step_end; ++st) {
+    int64_t lo, hi;
+    static_chunk(local_size(a, st), gridDim.x, blockIdx.x, lo, hi);
+    if (lo < hi) {
+      r = Round{st, lo, hi};
+      return true;
+    }
+  }
+  return false;
+}
+template <int NI>
+__device__ __forceinline__ bool next_round(const TrainArgs& a, Round& r) {
+  if (r.e + NI < r.hi) {
+    r.e += NI;
+    return true;
+  }
+  return first_round<NI>(a, r.step + 1, r);
+}
+
+// Issuer: the round's labels (cp.async, completed at the round's start) and ONE bulk copy of its images.
+template <int NI>
+__device__ __forceinline__ void issue_round(const TrainArgs& a, float* ring, int* lab, uint64_t* bar, int buf,
+                                            const Round& r) {
+  const int cnt = (int)min((int64_t)NI, r.hi - r.e);
+  const int64_t first = umod(r.step, a.steps_per_epoch) * a.batch + local_offset(a, r.step) + r.e;
+  for (int q = 0; q < cnt; ++q) wait_ready_at(a, r.step, first + q);
+  for (int q = 0; q < cnt; ++q) cp_async4(lab + buf * NI + q, a.labels + first + q);
+  fence_proxy_async_smem();
+  mbar_arrive_expect_tx(&bar[buf], (uint32_t)(cnt * kImg * sizeof(float)));
+  tma_load_1d(ring + buf * NI * kImg, a.images + first * kImg, (uint32_t)(cnt * kImg * sizeof(float)), &bar[buf]);
+}
+
+template <int NI, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
+  static_assert(T % 32 == 0, "stage loops run whole warps");
+  using L = Layout<NI>;
+  float* const P = bt_smem + L::kP;
+  float* const W1 = bt_smem + L::kW1;
+  float* const W2 = bt_smem + L::kW2;
+  float* const G = bt_smem + L::kG;
+  float* const ring = bt_smem + L::kRing;
+  int* const lab = reinterpret_cast<int*>(bt_smem + L::kLab);
+  float* const regs = bt_smem + L::kImgs;
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(bt_smem + L::kFloats);
+  const int t = threadIdx.x, nb = gridDim.x;
+  unsigned int target = 0;
+
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  for (int q = t; q < NI * kImgRegion; q += T) regs[q] = 0.0f;  // dz2 pad rows stay zero
+  __syncthreads();
+  const bool issuer = t == T - 32;  // lane 0 of the last warp (idle in S2/S6 of a full round)
+  Round pf;
+  bool pf_valid = first_round<NI>(a, a.step_begin, pf);
+  if (issuer && pf_valid) issue_round<NI>(a, ring, lab, bar, 0, pf);
+  uint32_t consumed = 0;
+
+  int64_t ks = umod(a.step_begin, a.steps_per_epoch), ep = udiv(a.step_begin, a.steps_per_epoch);
+  for (int64_t st = a.step_begin; st < a.step_end; ++st, ks = ks + 1 == a.steps_per_epoch ? (++ep, 0) : ks + 1) {
+    int64_t l_lo, l_hi;
+    local_range_k(a, ks, l_lo, l_hi);
+    const int64_t m = l_hi - l_lo;
+    int64_t lo, hi;
+    static_chunk(m, nb, blockIdx.x, lo, hi);
+
+    // ---- the step's weights -> shared (+ padded conv copies), zero the CTA gradient ----
+    {
+      const float4* src = reinterpret_cast<const float4*>(a.params);
+      float4* dst = reinterpret_cast<float4*>(P);
+      for (int q = t; q < kPStride / 4; q += T) dst[q] = __ldcg(src + q);
+      for (int q = t; q < kPStride; q += T) G[q] = 0.0f;
+    }
+    __syncthreads();
+    for (int q = t; q < kW1Floats + kW2Floats; q += T) {
+      if (q < kW1Floats) {
+        const int i = q / kW1Stride, rr = q - i * kW1Stride, ky = rr >> 3, kx = rr & 7;
+        W1[q] = (ky < 5 && kx < 5) ? P[kK1 + i * 25 + ky * 5 + kx] : 0.0f;
+      } else {
+        const int q2 = q - kW1Floats, i = q2 / kW2Stride, rr = q2 - i * kW2Stride, c = rr / 40, r2 = rr - c * 40;
+        const int ky = r2 >> 3, kx = r2 & 7;
+        W2[q2] = (c < 6 && kx < 5) ? P[kK2 + (i * 6 + c) * 25 + ky * 5 + kx] : 0.0f;
+      }
+    }
+    __syncthreads();
+
+    double cta_loss = 0.0;  // thread 0: this CTA's example losses in example order (fp64)
+    for (int64_t e = lo; e < hi; e += NI) {
+      const int cnt = (int)min((int64_t)NI, hi - e);
+      const int buf = consumed & 1;
+      mbar_wait(&bar[buf], (consumed >> 1) & 1);
+      if (issuer) {
+        cp_async_wait_all();  // this round's labels (published by S1's barrier)
+        if (pf_valid) {
+          Round nx = pf;
+          if (next_round<NI>(a, nx)) {
+            issue_round<NI>(a, ring, lab, bar, buf ^ 1, nx);  // buf^1 was last read by the previous round's S6
+            pf = nx;
+          } else {
+            pf_valid = false;
+          }
+        }
+      }
+      const float* imgs = ring + buf * NI * kImg;
+      const int* rl = lab + buf * NI;
+      // S1
+      for (int it = t; it < cnt * 144; it += T) conv1_item(P, W1, imgs, regs, it);
+      __syncthreads();
+      // S2 (cnt * 192 lanes: whole warps)
+      for (int it = t; it < cnt * 192; it += T) conv2_item(P, W2, regs, it);
+      __syncthreads();
+      // S3
+      for (int it = t; it < (cnt * 80 + 31) / 32 * 32; it += T) fc_item(P, regs, rl, it, it < cnt * 80);
+      __syncthreads();
+      // S4: d_s2 = fc^T dz -> dz2 = (d_s2 / 4) g2 in place; thread 0 adds the round's losses
+      if (t == 0) {
+        for (int k = 0; k < cnt; ++k) {  // net::loss (network.cpp:97-109)
+          const float* od = regs + k * kImgRegion + kOffOd;
+          float l = 0.0f;
+#pragma unroll
+          for (int i = 0; i < 10; ++i) {
+            const float d = (i == rl[k] ? 1.0f : 0.0f) - od[i];
+            l = __fmaf_rn(d, d, l);
+          }
+          cta_loss += (double)(0.5f * l);
+        }
+      }
+      for (int it = t; it < cnt * 192; it += T) {
+        const int k = it / 192, j = it - k * 192;
+        float* reg = regs + k * kImgRegion;
+        const float* dz = reg + kOffOd + 16;
+        float ds = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 10; ++i) ds = __fmaf_rn(P[kFC + i * 192 + j], dz[i], ds);
+        ds *= 0.25f;  // backavgpool (nn.cpp:148-158)
+        const int i2 = j >> 4, py = (j >> 2) & 3, px = j & 3;
+        float* d2 = reg + kOffD2 + i2 * kD2K + (4 + 2 * py) * 8 + 2 * px;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          float2* q2 = reinterpret_cast<float2*>(d2 + rr * 8);
+          const float2 g = *q2;
+          *q2 = make_float2(ds * g.x, ds * g.y);
+        }
+      }
+      __syncthreads();
+      // S5: backin (heaviest items first; 4-lane groups, whole warps) | g_k2 + g_b2 (lane pairs, whole
+      // warps) | g_fc + g_b (one lane per output, light items that fill the tail)
+      {
+        const int nbi = (cnt * 144 + 31) / 32 * 32, n2 = nbi + 768, nfc = n2 + 1930;
+        for (int it = t; it < nfc; it += T) {
+          if (it < nbi) {
+            backin_item(W2, regs, it, cnt, it < cnt * 144);
+          } else if (it < n2) {
+            gk2_item(G, regs, it - nbi, cnt);
+          } else if (it < n2 + 1920) {
+            const int o = it - n2, i = o / 192, j = o - i * 192;
+            float g = 0.0f;
+            for (int k = 0; k < cnt; ++k) {
+              const float* reg = regs + k * kImgRegion;
+              g = __fmaf_rn(reg[kOffS2 + j], reg[kOffOd + 16 + i], g);
+            }
+            G[kFC + o] += g;
+          } else {
+            const int i = it - n2 - 1920;
+            float g = 0.0f;
+            for (int k = 0; k < cnt; ++k) g += regs[k * kImgRegion + kOffOd + 16 + i];
+            G[kB + i] += g;
+          }
+        }
+      }
+      __syncthreads();
+      // S6: g_k1 (240 lanes) + g_b1 (48 lanes)
+      for (int it = t; it < 288; it += T) gk1_item(G, imgs, regs, it, cnt);
+      __syncthreads();
+      ++consumed;
+    }
+
+    // ---- CTA partial -> work row; grid barrier; ordered reduction + sgd_step; grid barrier ----
+    if (lo < hi) {
+      float4* dst = reinterpret_cast<float4*>(a.work + (int64_t)blockIdx.x * kPStride);
+      const float4* src = reinterpret_cast<const float4*>(G);
+      for (int q = t; q < kPStride / 4; q += T) __stcg(dst + q, src[q]);
+      if (t == 0) a.loss_part[blockIdx.x] = cta_loss;
+    }
+    grid_sync(a.barrier, target);
+    const int64_t block = m > 0 ? udiv(m + nb - 1, nb) : 1;
+    const int64_t nrows = m > 0 ? udiv(m + block - 1, block) : 0;  // CTAs that had examples
+    {
+      int64_t j0, j1;
+      static_chunk(kNParam, nb, blockIdx.x, j0, j1);
+      float* red = G;  // the CTA gradient is in its work row; G is zeroed again at the next step
+      for (int64_t jb = j0; jb < j1; jb += T) {
+        const int W = (int)min((int64_t)T, j1 - jb);
+        const int rstep = T / W, c = t % W, r0 = t / W;
+        float acc = 0.0f;
+        if (r0 < rstep) {
+          int64_t r = r0;
+          for (; r + 3 * rstep < nrows; r += 4 * rstep) {  // four loads in flight, fixed order
+            const float v0 = __ldcg(a.work + r * kPStride + jb + c);
+            const float v1 = __ldcg(a.work + (r + rstep) * kPStride + jb + c);
+            const float v2 = __ldcg(a.work + (r + 2 * rstep) * kPStride + jb + c);
+            const float v3 = __ldcg(a.work + (r + 3 * rstep) * kPStride + jb + c);
+            acc = ((acc + v0) + v1) + (v2 + v3);
+          }
+          for (; r < nrows; r += rstep) acc += __ldcg(a.work + r * kPStride + jb + c);
+        }
+        red[t] = acc;
+        __syncthreads();
+        if (t < W) {
+          float s = 0.0f;
+          for (int q = 0; q < rstep; ++q) s += red[t + q * W];
+          const int j = (int)jb + t;
+          if (a.grad_out) a.grad_out[j] = s;
+          else __stcg(a.params + j, fsub(P[j], fmul(a.rate, __fdiv_rn(s, (float)m))));
+        }
+        __syncthreads();
+      }
+    }
+    if (blockIdx.x == nb - 1) {  // fp64 loss of the group (network.cpp:239-242): CTA partials in CTA order
+      double* dl = reinterpret_cast<double*>(G);  // G is free until the next step zeroes it
+      double l = (!a.grad_out && ks != 0) ? a.epoch_loss[ep] : 0.0;
+      for (int64_t r0 = 0; r0 < nrows; r0 += 1024) {
+        const int n = (int)min((int64_t)1024, nrows - r0);
+        for (int q = t; q < n; q += T) dl[q] = __ldcg(a.loss_part + r0 + q);
+        __syncthreads();
+        if (t == 0)
+          for (int q = 0; q < n; ++q) l = __dadd_rn(l, dl[q]);
+        __syncthreads();
+      }
+      if (t == 0) {
+        if (a.grad_out) a.loss_out[0] = l;
+        else a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(l, (double)a.n) : l;
+      }
+    }
+    grid_sync(a.barrier, target);
+  }
+}
+
+template <int NI, int T, int MINB>
+cudaError_t prep(int* occ) {
+  auto kern = train_batch_kernel<NI, T, MINB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Layout<NI>::kBytes);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, T, Layout<NI>::kBytes);
+}
+
+template <int NI, int T, int MINB>
+cudaError_t launch_cfg(const TrainArgs& a, int sm_count, int64_t m_max, cudaStream_t st, int* grid_out) {
+  int occ = 0;
+  cudaError_t e = prep<NI, T, MINB>(&occ);
+  if (e != cudaSuccess) return e;
+  const int64_t cap = (int64_t)std::max(occ, 1) * sm_count;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cap, (m_max + NI - 1) / NI));
+  if (grid_out) {  // sizing query only
+    *grid_out = grid;
+    return cudaSuccess;
+  }
+  e = cudaMemsetAsync(a.barrier, 0, sizeof(unsigned int), st);
+  if (e != cudaSuccess) return e;
+  void* args[] = {const_cast<TrainArgs*>(&a)};
+  return cudaLaunchCooperativeKernel((const void*)train_batch_kernel<NI, T, MINB>, dim3(grid), dim3(T), args,
+                                     Layout<NI>::kBytes, st);
+}
+
+// TLB_BATCH_CFG = "NIxTHREADSxMINB" picks a measured alternative (A/B); default below.
+template <typename F>
+cudaError_t dispatch(F&& f) {
+  static const char* cfg = std::getenv("TLB_BATCH_CFG");
+  const auto is = [](const char* want) { return cfg && !std::strcmp(cfg, want); };
+  if (is("2x512x1")) return f.template operator()<2, 512, 1>();
+  if (is("3x384x1")) return f.template operator()<3, 384, 1>();
+  if (is("4x512x1")) return f.template operator()<4, 512, 1>();
+  if (is("4x768x1")) return f.template operator()<4, 768, 1>();
+  return f.template operator()<2, 384, 2>();
+}
+
+struct GridQuery {
+  int sm;
+  int64_t m;
+  int* g;
+  template <int NI, int T, int MINB>
+  cudaError_t operator()() { return launch_cfg<NI, T, MINB>(TrainArgs{}, sm, m, nullptr, g); }
+};
+struct Launcher {
+  const TrainArgs& a;
+  int sm;
+  int64_t m;
+  cudaStream_t st;
+  template <int NI, int T, int MINB>
+  cudaError_t operator()() { return launch_cfg<NI, T, MINB>(a, sm, m, st, nullptr); }
+};
+
+}  // namespace bt
+
+// Grid of the batched train kernel for groups of up to m_max local examples (the work-row count).
+int batch_train_grid(int sm_count, int64_t m_max) {
+  int grid = 0;
+  bt::GridQuery q{sm_count, m_max, &grid};
+  if (bt::dispatch(q) != cudaSuccess) return 0;
+  return grid;
+}
+
+cudaError_t launch_train_batch(const TrainArgs& a, int sm_count, int64_t m_max, cudaStream_t st) {
+  bt::Launcher l{a, sm_count, m_max, st};
+  return bt::dispatch(l);
+}
+
+}  // namespace tlb

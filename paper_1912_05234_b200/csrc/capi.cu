@@ -106,6 +106,7 @@ struct tlb_ctx {
   int threads_override = 0;
   int max_clusters = 0;    // co-resident 8-CTA clusters of train_cluster_kernel (0 = unavailable)
   bool use_cluster = true;
+  int batched = -1;  // batched fast train kernel: -1 auto (TLB_BATCHED or the group-size rule), 0 off, 1 on
   DevBuf work, losses, loss_part, barrier;  // persistent-train workspaces
   DevBuf stage[8];                 // host-API staging buffers
   // Overlapped ingestion for tlb_train: the dataset is copied chunk by chunk on `copy_stream` while
@@ -254,6 +255,18 @@ int pick_threads(const tlb_ctx* c, int64_t items) {
   return items > c->sm_count ? 256 : 512;
 }
 
+// Batched fast kernel from this many local examples per group (TLB_BATCHED=0 never, =1 always).
+bool use_batched(const tlb_ctx* c, int64_t m_local) {
+  static const int mode = [] {
+    const char* e = getenv("TLB_BATCHED");
+    return e ? atoi(e) : -1;
+  }();
+  const int want = c->batched >= 0 ? c->batched : mode;
+  if (want == 0) return false;
+  if (want == 1) return true;
+  return m_local >= 4 * (int64_t)c->sm_count;
+}
+
 int train_grid(tlb_ctx* c, int64_t m_max, int threads) {
   const int occ = c->occ_train[exact(c) ? 1 : 0][threads == 256 ? 0 : 1];
   const int coop = std::max(1, occ * c->sm_count);
@@ -396,8 +409,13 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   }
   const bool clustered = !exact(c) && c->use_cluster && c->grid_override == 0 && c->max_clusters > 0 &&
                          clusters <= c->max_clusters;
+  // Large groups (configs[3]): the batched fast kernel (NI images per CTA round, batch_train.cu).
+  const bool batched = !exact(c) && !clustered && !dp && c->grid_override == 0 && use_batched(c, m_local);
   const int threads = pick_threads(c, m_local);
-  const int grid = clustered ? clusters * csz : train_grid(c, std::max<int64_t>(m_local, 1), threads);
+  const int grid = clustered ? clusters * csz
+                   : batched ? tlb::batch_train_grid(c->sm_count, std::max<int64_t>(m_local, 1))
+                             : train_grid(c, std::max<int64_t>(m_local, 1), threads);
+  if (grid <= 0) return fail(TLB_ERR_CUDA, "train: batched kernel configuration failed");
   const int64_t rows = exact(c) ? std::max<int64_t>(m_local, 1) : grid;
   TLB_CUDA(c->work.ensure(clustered ? tlb::cluster_work_bytes() : (size_t)rows * TLB_PSTRIDE * sizeof(float)));
   TLB_CUDA(c->losses.ensure((size_t)std::max<int64_t>(m_local, 1) * sizeof(float)));
@@ -463,6 +481,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   }
   if (a.step_end <= a.step_begin) return TLB_OK;
   if (clustered) TLB_CUDA(tlb::launch_train_cluster(a, clusters, c->stream));
+  else if (batched) TLB_CUDA(tlb::launch_train_batch(a, c->sm_count, std::max<int64_t>(m_local, 1), c->stream));
   else TLB_CUDA(tlb::launch_train(exact(c), a, grid, threads, c->stream));
   return TLB_OK;
 }
@@ -580,6 +599,13 @@ int tlb_ctx_set_threads(tlb_ctx* c, int threads) {
   if (threads != 0 && threads != 256 && threads != 512)
     return fail(TLB_ERR_ARG, "tlb_ctx_set_threads: 0 (automatic), 256 or 512");
   c->threads_override = threads;
+  return TLB_OK;
+}
+
+int tlb_ctx_set_batched(tlb_ctx* c, int mode) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  if (mode < -1 || mode > 1) return fail(TLB_ERR_ARG, "tlb_ctx_set_batched: -1 (automatic), 0 or 1");
+  c->batched = mode;
   return TLB_OK;
 }
 

@@ -94,6 +94,9 @@ size_t dp_counter_offset();
 cudaError_t launch_train_cluster(const TrainArgs& a, int clusters, cudaStream_t st);
 cudaError_t launch_cells(bool exact, const CellArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_eval(bool exact, const EvalArgs& a, int grid, int threads, cudaStream_t st);
+// Fast-mode batched train kernel for large groups (batch_train.cu): NI images per CTA round.
+int batch_train_grid(int sm_count, int64_t m_max);
+cudaError_t launch_train_batch(const TrainArgs& a, int sm_count, int64_t m_max, cudaStream_t st);
 // Fast-mode batched inference (infer_kernels.cu): forward + argmax + correct count over n images.
 cudaError_t launch_infer(const EvalArgs& a, int sm_count, cudaStream_t st);
 cudaError_t launch_sgd(const float* params, const float* grad, float rate, int64_t m, float* out, int n,

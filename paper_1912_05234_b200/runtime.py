@@ -165,6 +165,11 @@ class Context:
         """Fast mode: clustered train kernel (DSMEM pre-reduction) when the group fits (default on)."""
         _check(self._L.tlb_ctx_set_cluster(self._h, 1 if enable else 0))
 
+    def set_batched(self, mode: int) -> None:
+        """Fast mode, large groups: -1 automatic (batched kernel from 4 x SM-count examples per group), 0 the
+        one-image-per-CTA flat kernel, 1 the batched kernel (NI images per CTA round) for every such group."""
+        _check(self._L.tlb_ctx_set_batched(self._h, int(mode)))
+
     def set_trace(self, d_trace_ptr: int) -> None:
         """Per-stage clock64 stamps of CTA 0 into a device buffer of [steps][16] uint64 (0 disables)."""
         _check(self._L.tlb_ctx_set_trace(self._h, C.c_void_p(d_trace_ptr or None)))
