@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--force-dp", action="store_true",
                     help="run the N>1 data-parallel step (shard kernel + NCCL allreduce + sgd) even at N=1")
     ap.add_argument("--no-graph", action="store_true", help="NCCL data-parallel step: plain launches, no CUDA graph")
+    ap.add_argument("--plan", action="store_true",
+                    help="print this rank's launch plan (rank, world, device) as JSON and exit (no GPU work)")
     ap.add_argument("--dp-mode", choices=["nvlink", "nccl"], default="nvlink",
                     help="N>1 step: fused clustered kernel over NVLink peer memory (default; falls back to "
                          "nccl when symmetric memory is unavailable or a peer times out) or NCCL allreduce")
@@ -207,6 +209,18 @@ def ncu_traffic(mode: str, batch: int, n: int, world: int):
 
 
 # ---- our arm ----------------------------------------------------------------------------------------
+def shard_rows(n_total: int, global_batch: int, world: int, rank: int) -> np.ndarray:
+    """Dataset rows of this rank's shards, group by group: static_chunk(m_g, world, rank) of every SGD group
+    (runtime.cpp:138-145, network.cpp:228-234) -- the rank's local corpus in the shard layout
+    (tlb_ctx_set_shard_layout), shard of group g at local row g * ceil(global_batch / world)."""
+    from paper_1912_05234_b200.parallel import groups, static_chunk
+    rows = []
+    for g, (start, m) in enumerate(groups(n_total, global_batch)):
+        lo, hi = static_chunk(m, world, rank)
+        rows.append(np.arange(start + lo, start + hi))
+    return np.concatenate(rows) if rows else np.zeros(0, np.int64)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -240,13 +254,19 @@ def run_ours(args):
 
     B, n_per = args.batch, args.n
     n_total = n_per * world
+    Bg = B * world
     images, labels = synth_make_set(n_total, 1)
+    if dp:  # weak scaling: each rank keeps only its shards (1/world of the corpus) in HBM
+        rows = shard_rows(n_total, Bg, world, rank)
+        images, labels = np.ascontiguousarray(images[rows]), np.ascontiguousarray(labels[rows])
     stream = torch.cuda.Stream(device=dev)  # a real stream: torch's default stream handle is 0
     torch.cuda.set_stream(stream)
     ctx = Context(local, mode=args.mode)
     ctx.set_stream(stream.cuda_stream)
     if args.grid:
         ctx.set_grid(args.grid)
+    if dp:
+        ctx.set_shard_layout(B)
 
     d_x = torch.from_numpy(images).to(dev)
     d_y = torch.from_numpy(labels).to(dev)
@@ -271,13 +291,13 @@ def run_ours(args):
         step, dp_used, dp_note = None, "nccl", None
         if args.dp_mode == "nvlink" and args.mode == "fast":
             try:
-                step = FusedDPStep(ctx, d_x, d_y, n_total, B * world, world, rank, ipc=same_gpu)
+                step = FusedDPStep(ctx, d_x, d_y, n_total, Bg, world, rank, ipc=same_gpu)
                 dp_used = "nvlink"
             except Exception as exc:  # symmetric memory unavailable: NCCL path
                 dp_note = f"fused NVLink step unavailable ({type(exc).__name__}: {exc}); NCCL fallback"
                 print(dp_note, file=sys.stderr)
         if step is None:
-            step = DeviceShardStep(ctx, d_x, d_y, n_total, B * world, world, rank, graph=not args.no_graph)
+            step = DeviceShardStep(ctx, d_x, d_y, n_total, Bg, world, rank, graph=not (args.no_graph or same_gpu))
 
         def epoch(e):
             step.epoch(d_p, 0.05, d_loss, e)
@@ -288,21 +308,29 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t)
 
-    def fused_tripped() -> bool:  # did ANY rank's fused kernel hit its peer-wait watchdog?  (all agree)
+    def fused_failed(ok: bool) -> bool:
+        """Did ANY rank's fused step fail -- an argument error (e.g. a shard beyond the clustered kernel's
+        co-resident capacity) or a peer-wait watchdog trip?  Every rank takes part, so all agree."""
         try:
             step.check()
-            mine = 0.0
         except RuntimeError:
-            mine = 1.0
-        return all_max(mine) > 0
+            ok = False
+        return all_max(0.0 if ok else 1.0) > 0
 
     def run_protocol():
         # warm-up (not timed), then the timed protocol from init_params(42)
         reset()
-        for w in range(args.warmup):
-            epoch(w % max(args.steps, 1))
-        torch.cuda.synchronize()
-        if dp and dp_used == "nvlink" and fused_tripped():
+        ok = True
+        try:
+            for w in range(args.warmup):
+                epoch(w % max(args.steps, 1))
+            torch.cuda.synchronize()
+        except Exception as exc:  # noqa: BLE001 -- only the fused step can fail here (NCCL path: re-raised)
+            if not (dp and dp_used == "nvlink"):
+                raise
+            print(f"fused NVLink step failed in warm-up: {type(exc).__name__}: {exc}", file=sys.stderr)
+            ok = False
+        if dp and dp_used == "nvlink" and fused_failed(ok):
             return None, None
         reset()
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -319,15 +347,16 @@ def run_ours(args):
             torch.cuda.synchronize()
         if dp:
             dist.barrier()
-        if dp and dp_used == "nvlink" and fused_tripped():  # a trip during the timed epochs: re-measure
+        if dp and dp_used == "nvlink" and fused_failed(True):  # a trip during the timed epochs: re-measure
             return None, None
         return sum(a.elapsed_time(b) for a, b in zip(starts, ends)), clk
 
     total_ms, clk = run_protocol()
-    if total_ms is None:  # the fused path tripped on some rank: every rank moves to NCCL together
-        dp_used, dp_note = "nccl", "fused NVLink step: a peer-wait watchdog tripped; NCCL fallback"
+    if total_ms is None:  # the fused path failed on some rank: every rank moves to NCCL together
+        dp_used = "nccl"
+        dp_note = "fused NVLink step failed (argument error or peer-wait watchdog); NCCL fallback"
         print(dp_note, file=sys.stderr)
-        step = DeviceShardStep(ctx, d_x, d_y, n_total, B * world, world, rank, graph=not args.no_graph)
+        step = DeviceShardStep(ctx, d_x, d_y, n_total, Bg, world, rank, graph=not (args.no_graph or same_gpu))
         launches_per_step = 2 * step.groups_per_epoch
         total_ms, clk = run_protocol()
     if dp:
@@ -339,7 +368,9 @@ def run_ours(args):
     info = ctx.info()
     peaks = measured_peaks()
     max_mhz = peaks.get("sm_max_mhz", 1965.0)
-    fp32_peak = info["sm_count"] * FP32_LANES_PER_SM * 2 * max_mhz * 1e6 / 1e12
+    fp32_nominal = info["sm_count"] * FP32_LANES_PER_SM * 2 * max_mhz * 1e6 / 1e12
+    ffma = measured_ffma_peak()
+    fp32_peak = ffma["tflops"] if ffma else fp32_nominal
     flop_per_launch = n_per * FLOP_PER_TRAIN_IMAGE
     achieved = flop_per_launch / (total_ms / args.steps / 1e3) / 1e12
     clocks = clk.summary()
@@ -348,26 +379,28 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": f"synthetic: synth::make_set({n_total}, 1) (reference generator restated in C++), init_params(42)",
-        "config": {"workload": "Zhang CNN paper protocol (BASELINE configs[1]): 1 step = 1 epoch of "
-                               f"{n_per} images/GPU at batch {B}/GPU, lr 0.05",
-                   "batch_per_gpu": B, "global_batch": B * world, "n_images": n_total, "epochs_per_step": 1,
-                   "mode": args.mode, "parallelism": f"dp{world}", "grid": args.grid or "auto",
-                   "dp_step": None if not dp else (
-                       "fused: one clustered launch per epoch, fixed-point gradient slices added into the owning "
-                       "GPU's accumulator over NVLink peer memory (no collective call)" if dp_used == "nvlink" else
-                       "shard kernel + NCCL allreduce + sgd per group" +
-                       ("" if args.no_graph else ", epoch replayed as one CUDA graph")),
-                   "dp_note": dp_note,
-                   "l2": "flushed between timed steps (256 MiB write outside the event pair)"},
+        "data": f"synthetic: synth::make_set({n_total}, 1) (reference generator restated in C++), init_params(42)"
+                + ("; each rank holds its static_chunk shards of every group" if dp else ""),
+        "config": workload_config(args, world),
+        "impl_config": dict(mode=args.mode, grid=args.grid or "auto",
+                       dp_step=None if not dp else (
+                           "fused: one clustered launch per epoch, fixed-point gradient slices added into the owning "
+                           "GPU's accumulator over NVLink peer memory (no collective call)" if dp_used == "nvlink" else
+                           "shard kernel + NCCL allreduce + sgd per group" +
+                           ("" if args.no_graph else ", epoch replayed as one CUDA graph")),
+                       dp_note=dp_note),
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp32_peak, "traffic": None if dp else ncu_traffic(args.mode, B, n_per, world),
                      "traffic_note": "DRAM bytes/launch from profiles/r1/ncu_train_cluster_keymetrics.csv; "
                                      f"algorithmic input bytes/launch = {n_per * 3136}",
                      "per_launch": f"{n_per} images x {FLOP_PER_TRAIN_IMAGE} algorithmic FLOP",
-                     "peak_source": f"{info['sm_count']} SMs x 128 FP32 lanes x 2 x sm_max_mhz {max_mhz} "
-                                    "(MEASURED_PEAKS.json clocks); FFMA-bound path (no HBM/tensor bound)"},
+                     "peak_source": (f"measured FFMA peak {ffma['tflops']:.2f} TFLOP/s ({ffma['source']}); nominal "
+                                     f"{fp32_nominal:.2f} = {info['sm_count']} SMs x 128 lanes x 2 x {max_mhz} MHz"
+                                     if ffma else
+                                     f"{info['sm_count']} SMs x 128 FP32 lanes x 2 x sm_max_mhz {max_mhz} "
+                                     "(MEASURED_PEAKS.json clocks)") + "; FFMA-bound path (no HBM/tensor bound)",
+                     "frac_of_nominal": achieved / fp32_nominal},
         "clocks": clocks,
         "epoch_mean_loss": losses,
     }
@@ -377,14 +410,11 @@ def run_ours(args):
         result["parity"] = {"epoch_loss_max_rel_vs_reference": rel, "tolerance": 1e-4,
                             "bitwise": all("%.17g" % a == "%.17g" % b for a, b in zip(losses, gl))}
 
-    # end-to-end through the public host API (net::train with host buffers; H2D + D2H inside)
-    if not args.no_e2e and world == 1:
+    # end-to-end through the public host API with host buffers, H2D + D2H inside the timed region
+    if not args.no_e2e:
         pin_x = torch.from_numpy(images).pin_memory()
         pin_y = torch.from_numpy(labels).pin_memory()
         px, py = pin_x.numpy(), pin_y.numpy()
-        p = p0.copy()
-        ctx.train(p, px, py, rate=0.05, epochs=1, batch=B)  # warm-up (allocations)
-        torch.cuda.synchronize()
         # this box's pinned host->device bandwidth for the step's image bytes (the e2e ingestion bound)
         d_probe = torch.empty_like(pin_x, device=dev)
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -397,28 +427,64 @@ def run_ours(args):
         h2d_gbps = 3 * images.nbytes / (h0.elapsed_time(h1) * 1e-3) / 1e9
         del d_probe
         times = []
-        p = p0.copy()
-        for s in range(args.steps):
-            flush.fill_(float(s))
+        if not dp:  # net::train (tlb_train): host images/labels/params in, params + losses out
+            p = p0.copy()
+            ctx.train(p, px, py, rate=0.05, epochs=1, batch=B)  # warm-up (allocations)
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            p, _ = ctx.train(p, px, py, rate=0.05, epochs=1, batch=B)
-            times.append(time.perf_counter() - t0)
-        result["e2e"] = {"value": args.steps * n_total / sum(times), "unit": "images/s",
-                         "h2d_bytes_per_step": images.nbytes + labels.nbytes + 3898 * 4,
-                         "d2h_bytes_per_step": 3898 * 4 + 8,
-                         "api": "tlb_train (net::train) on pinned host buffers, wall clock per call",
+            p = p0.copy()
+            for s in range(args.steps):
+                flush.fill_(float(s))
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                p, _ = ctx.train(p, px, py, rate=0.05, epochs=1, batch=B)
+                times.append(time.perf_counter() - t0)
+            api = "tlb_train (net::train) on pinned host buffers, wall clock per call"
+            h2d = images.nbytes + labels.nbytes + 3898 * 4
+            d2h = 3898 * 4 + 8
+            e2e_launches = args.steps
+        else:  # every rank: its shards H2D, the data-parallel epoch, loss (+ params on rank 0) D2H
+            pin_p = torch.from_numpy(np.pad(p0, (0, 6))).pin_memory()
+            out_p = torch.empty(3904).pin_memory()
+            out_l = torch.empty(1, dtype=torch.float64).pin_memory()
+            for s in range(args.warmup + args.steps):
+                flush.fill_(float(s))
+                torch.cuda.synchronize()
+                dist.barrier()
+                t0 = time.perf_counter()
+                d_x.copy_(pin_x, non_blocking=True)
+                d_y.copy_(pin_y, non_blocking=True)
+                d_p.copy_(pin_p, non_blocking=True)
+                epoch(0)
+                out_l.copy_(d_loss[0:1], non_blocking=True)
+                if rank == 0:
+                    out_p.copy_(d_p, non_blocking=True)
+                torch.cuda.synchronize()
+                if s >= args.warmup:
+                    times.append(time.perf_counter() - t0)
+            api = (f"per rank: its shards (1/{world} of the corpus) pinned H2D + params H2D, the data-parallel "
+                   "epoch, epoch loss D2H (+ params D2H on rank 0); wall clock per step, max over ranks")
+            h2d = world * (images.nbytes + labels.nbytes + 3904 * 4)
+            d2h = world * 8 + 3904 * 4
+            e2e_launches = launches_per_step * args.steps
+        e2e_s = sum(times)
+        if dp:
+            e2e_s = all_max(e2e_s)
+        result["e2e"] = {"value": args.steps * n_total / e2e_s, "unit": "images/s",
+                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": api,
                          "h2d_GBps_measured": h2d_gbps,
                          "call_ms": {"median": 1e3 * sorted(times)[len(times) // 2], "min": 1e3 * min(times),
                                      "max": 1e3 * max(times)}}
-        result["gpu_launches"] += args.steps
+        result["gpu_launches"] += e2e_launches
 
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, meta = reference_epochs(n_per, 10.0, 3, min(B * world, n_per))
-        result["cpu_baseline"] = {"value": v, "unit": "images/s", "cores": meta["cores"], "kind": "reference",
-                                  "sample": f"{meta['epochs']} epoch(s) x {n_per} images at batch {B}, reference "
-                                            f"net::train (oracle/_ref) with {meta['cores']} workers, "
-                                            f"{meta['seconds']:.1f} s"}
+    if not args.no_cpu_baseline:
+        if rank == 0:  # the reference's net::train on this box's host cores, a bounded sample
+            v, meta = reference_epochs(n_per, 10.0, 3, min(B * world, n_per))
+            result["cpu_baseline"] = {"value": v, "unit": "images/s", "cores": meta["cores"], "kind": "reference",
+                                      "sample": f"{meta['epochs']} epoch(s) x {n_per} images at batch "
+                                                f"{min(B * world, n_per)}, reference net::train (oracle/_ref) with "
+                                                f"{meta['cores']} workers, {meta['seconds']:.1f} s"}
+        if dp:
+            dist.barrier()
     if real_stdout is not None:
         sys.stdout.flush()
         os.dup2(real_stdout, 1)
@@ -427,6 +493,17 @@ def run_ours(args):
     ctx.close()
     if dp:
         dist.destroy_process_group()
+
+
+def measured_ffma_peak():
+    """The FP32 FFMA roofline measured on this pool's B200 (scripts/ffma_peak.cu, profiles/r2/ffma_peak_r2a.json):
+    MEASURED_PEAKS.json (driver-written) has HBM and bf16 only."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2", "ffma_peak_r2a.json")) as f:
+            rec = json.load(f)
+        return {"tflops": float(rec["tflops_best"]), "source": "profiles/r2/ffma_peak_r2a.json, best of 20"}
+    except Exception:
+        return None
 
 
 def ensure_ranks(args) -> None:
@@ -440,8 +517,11 @@ def ensure_ranks(args) -> None:
             with socket.socket() as sk:
                 sk.bind(("127.0.0.1", 0))
                 port = sk.getsockname()[1]
+            # the ranks get this command's arguments through the environment: torchrun's own parser would
+            # claim abbreviations of its options (--n -> --nnodes / --nproc-per-node ...)
+            os.environ["TLB_BENCH_ARGV"] = json.dumps(sys.argv[1:])
             cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-                   "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+                   "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)]
             sys.stdout.flush()
             os.execv(sys.executable, cmd)
         return
@@ -452,8 +532,17 @@ def ensure_ranks(args) -> None:
 
 
 def main():
+    if "TLB_BENCH_ARGV" in os.environ and len(sys.argv) == 1:  # a rank spawned by ensure_ranks
+        sys.argv[1:] = json.loads(os.environ["TLB_BENCH_ARGV"])
     args = parse()
+    if args.n < args.batch:  # configs[3] sweeps: at least two SGD groups per epoch per GPU
+        args.n = 2 * args.batch
     ensure_ranks(args)
+    if args.plan:
+        print(json.dumps({"rank": int(os.environ.get("RANK", "0")), "world": int(os.environ.get("WORLD_SIZE", "1")),
+                          "local_rank": int(os.environ.get("LOCAL_RANK", "0")), "gpus": args.gpus,
+                          "impl": args.impl, "batch_per_gpu": args.batch, "n_per_gpu": args.n}), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

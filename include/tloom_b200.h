@@ -76,6 +76,11 @@ int tlb_ctx_set_cluster(tlb_ctx* ctx, int enable);
  * images per CTA round, batch_train.cu) from 4 x SM-count examples per group (env TLB_BATCHED=0/1
  * overrides), 0 the one-image-per-CTA flat kernel, 1 the batched kernel for every such group. */
 int tlb_ctx_set_batched(tlb_ctx* ctx, int mode);
+/* Data layout of the images/labels given to tlb_train_shard_device / tlb_train_dp_device: 0 (default) = the
+ * whole dataset (every rank holds every group); > 0 = only this rank's shards, the shard of SGD group g
+ * (static_chunk of the group, runtime.cpp:138-145) starting at example g * local_stride -- each rank then
+ * uploads and keeps 1/world of the corpus. */
+int tlb_ctx_set_shard_layout(tlb_ctx* ctx, int64_t local_stride);
 /* CTA size of the flat train / forward kernels: 0 = automatic (default: 256 = two independent CTAs per SM
  * whose barrier stalls overlap once a launch has more than one item per SM, else 512), or forced 256 / 512.
  * Env TLB_FAST_THREADS. */

@@ -41,6 +41,7 @@ _SIGS = {
     "tlb_ctx_set_trace": (C.c_int, [vp, vp]),
     "tlb_ctx_set_cluster": (C.c_int, [vp, C.c_int]),
     "tlb_ctx_set_batched": (C.c_int, [vp, C.c_int]),
+    "tlb_ctx_set_shard_layout": (C.c_int, [vp, C.c_int64]),
     "tlb_ctx_set_threads": (C.c_int, [vp, C.c_int]),
     "tlb_dp_workspace_bytes": (C.c_size_t, []),
     "tlb_train_dp_device": (C.c_int, [vp, vp, vp, C.c_int64, vp, C.c_float, C.c_int32, C.c_int32, C.c_int64, vp,

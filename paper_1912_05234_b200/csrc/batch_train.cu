@@ -423,7 +423,7 @@ template <int NI>
 __device__ __forceinline__ void issue_round(const TrainArgs& a, float* ring, int* lab, uint64_t* bar, int buf,
                                             const Round& r) {
   const int cnt = (int)min((int64_t)NI, r.hi - r.e);
-  const int64_t first = umod(r.step, a.steps_per_epoch) * a.batch + local_offset(a, r.step) + r.e;
+  const int64_t first = example_index(a, r.step, r.e);
   for (int q = 0; q < cnt; ++q) wait_ready_at(a, r.step, first + q);
   for (int q = 0; q < cnt; ++q) cp_async4(lab + buf * NI + q, a.labels + first + q);
   fence_proxy_async_smem();

@@ -106,6 +106,7 @@ struct tlb_ctx {
   int threads_override = 0;
   int max_clusters = 0;    // co-resident 8-CTA clusters of train_cluster_kernel (0 = unavailable)
   bool use_cluster = true;
+  int64_t shard_stride = 0;  // DP shard layout of the images/labels passed to the shard / fused-DP entry points
   int batched = -1;  // batched fast train kernel: -1 auto (TLB_BATCHED or the group-size rule), 0 off, 1 on
   DevBuf work, losses, loss_part, barrier;  // persistent-train workspaces
   DevBuf stage[8];                 // host-API staging buffers
@@ -454,6 +455,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.dp_error = static_cast<unsigned int*>(c->dev_err.p);        // single GPU: abort word of the bounded waits
   a.fix_err = static_cast<unsigned int*>(c->dev_err.p) + 1;
   a.dp_timeout_cycles = (long long)(kWaitLimitSeconds * 2.0e9);  // ~2 GHz SM clock
+  a.local_stride = (dp || grad_out) ? c->shard_stride : 0;
   if (clustered) {
     if (dp) {  // fused data parallelism: slice s lives on rank s % world (peer memory)
       a.dp_world = dp->world;
@@ -599,6 +601,13 @@ int tlb_ctx_set_threads(tlb_ctx* c, int threads) {
   if (threads != 0 && threads != 256 && threads != 512)
     return fail(TLB_ERR_ARG, "tlb_ctx_set_threads: 0 (automatic), 256 or 512");
   c->threads_override = threads;
+  return TLB_OK;
+}
+
+int tlb_ctx_set_shard_layout(tlb_ctx* c, int64_t local_stride) {
+  if (!c) return fail(TLB_ERR_ARG, "null context");
+  if (local_stride < 0) return fail(TLB_ERR_ARG, "tlb_ctx_set_shard_layout: negative stride");
+  c->shard_stride = local_stride;
   return TLB_OK;
 }
 

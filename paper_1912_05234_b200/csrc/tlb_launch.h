@@ -56,6 +56,10 @@ struct TrainArgs {
                                      // the abort word of the guarded cluster waits (mbar_wait_cluster_guarded)
   long long dp_timeout_cycles;       // bound of every cross-CTA / cross-GPU wait
   unsigned int* fix_err;             // set when a cluster's gradient sum left the fixed-point range (clamped)
+  // Shard layout (DP shard / fused DP modes, tlb_ctx_set_shard_layout): 0 = `images`/`labels` hold the whole
+  // dataset (example e of group g at g * batch + e); > 0 = they hold only this rank's shards, the shard of
+  // group g starting at g * local_stride (the local example e of it at g * local_stride + e).
+  int64_t local_stride;
 };
 
 struct CellArgs {

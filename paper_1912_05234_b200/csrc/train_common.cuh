@@ -71,9 +71,13 @@ __device__ __forceinline__ bool next_job(const TrainArgs& a, Job& j) {
   return first_job(a, j.step + 1, j);
 }
 
-__device__ __forceinline__ int64_t job_index(const TrainArgs& a, const Job& j) {
-  return umod(j.step, a.steps_per_epoch) * a.batch + local_offset(a, j.step) + j.e;
+// Dataset index of the launch-local example e of step st (whole-dataset or shard layout).
+__device__ __forceinline__ int64_t example_index(const TrainArgs& a, int64_t st, int64_t e) {
+  const int64_t ks = umod(st, a.steps_per_epoch);
+  return a.local_stride > 0 ? ks * a.local_stride + e : ks * a.batch + local_offset(a, st) + e;
 }
+
+__device__ __forceinline__ int64_t job_index(const TrainArgs& a, const Job& j) { return example_index(a, j.step, j.e); }
 
 __device__ __forceinline__ const float* job_image(const TrainArgs& a, const Job& j) {
   return a.images + job_index(a, j) * kImg;

@@ -32,9 +32,10 @@ namespace tlb {
 // The issuer completes the copy (cp_async_wait_all) when the job starts, before issuing the next one;
 // the forward pass reads s.lab[buf] only after its first CTA barrier (forward_image's `lab`).
 __device__ __forceinline__ void issue_job(const Smem& s, const TrainArgs& a, int buf, const Job& j) {
-  wait_ready(a, j);
-  cp_async4(s.lab + buf, a.labels + job_index(a, j));
-  issue_image(s, buf, job_image(a, j));
+  const int64_t idx = job_index(a, j);  // once: the index math is a serial chain on the issuer lane
+  wait_ready_at(a, j.step, idx);
+  cp_async4(s.lab + buf, a.labels + idx);
+  issue_image(s, buf, a.images + idx * kImg);
 }
 
 // sgd_step (network.cpp:171-180) for one parameter, or the shard's gradient sum in DP mode.

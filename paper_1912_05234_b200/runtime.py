@@ -170,6 +170,11 @@ class Context:
         one-image-per-CTA flat kernel, 1 the batched kernel (NI images per CTA round) for every such group."""
         _check(self._L.tlb_ctx_set_batched(self._h, int(mode)))
 
+    def set_shard_layout(self, local_stride: int) -> None:
+        """Data-parallel entry points (train_shard_device / train_dp_device): 0 = the image/label buffers hold
+        the whole dataset; > 0 = only this rank's shards, the shard of group g at example g * local_stride."""
+        _check(self._L.tlb_ctx_set_shard_layout(self._h, int(local_stride)))
+
     def set_trace(self, d_trace_ptr: int) -> None:
         """Per-stage clock64 stamps of CTA 0 into a device buffer of [steps][16] uint64 (0 disables)."""
         _check(self._L.tlb_ctx_set_trace(self._h, C.c_void_p(d_trace_ptr or None)))

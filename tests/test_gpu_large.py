@@ -140,3 +140,41 @@ def test_dp_shards_batched_sum_to_the_full_group(orc, zhang_sets):
         torch.cuda.synchronize()
         got_p = d_p[:3898].cpu().numpy()
     check_weights(got_p, want_p)
+
+
+@pytest.mark.parametrize("n,batch,world", [(2048, 1024, 2), (1030, 100, 4), (4100, 2048, 2)])
+def test_shard_layout_matches_whole_dataset_layout(orc, zhang_sets, n, batch, world):
+    """tlb_ctx_set_shard_layout: a rank that holds only its static_chunk shards (shard of group g at
+    g * ceil(batch / world)) computes bit-identical shard gradient sums to a rank holding the whole dataset
+    -- for every group, including the ragged last one, flat (small shards) and batched (large) kernels."""
+    import torch
+    from paper_1912_05234_b200 import Context
+    from paper_1912_05234_b200.parallel import groups, static_chunk
+    (tr_x, tr_y), _ = zhang_sets
+    x, y = tr_x[:n], tr_y[:n]
+    dev = torch.device("cuda:0")
+    p0 = orc.init_params(42)
+    stride = -(-batch // world)
+    for rank in range(world):
+        rows = np.concatenate([np.arange(s + static_chunk(m, world, rank)[0], s + static_chunk(m, world, rank)[1])
+                               for s, m in groups(n, batch)])
+        with Context(0, mode="fast") as c:
+            c.set_stream(torch.cuda.current_stream().cuda_stream)
+            d_p = torch.zeros(3904, device=dev)
+            d_p[:3898] = torch.from_numpy(p0).to(dev)
+            full_x, full_y = torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev)
+            loc_x = torch.from_numpy(np.ascontiguousarray(x[rows])).to(dev)
+            loc_y = torch.from_numpy(np.ascontiguousarray(y[rows])).to(dev)
+            for g, (_, m) in enumerate(groups(n, batch)):
+                lo, hi = static_chunk(m, world, rank)
+                outs = []
+                for layout, (dx, dy) in ((0, (full_x, full_y)), (stride, (loc_x, loc_y))):
+                    c.set_shard_layout(layout)
+                    gsum = torch.zeros(3904, device=dev)
+                    lsum = torch.zeros(1, dtype=torch.float64, device=dev)
+                    c.train_shard_device(dx.data_ptr(), dy.data_ptr(), n, batch, g, lo, hi, d_p.data_ptr(),
+                                         gsum.data_ptr(), lsum.data_ptr())
+                    torch.cuda.synchronize()
+                    outs.append((gsum.cpu().numpy(), float(lsum.cpu())))
+                assert np.array_equal(bits(outs[0][0]), bits(outs[1][0])), (rank, g)
+                assert outs[0][1] == outs[1][1]
