@@ -104,6 +104,9 @@ int tlb_synth_make_digits(int64_t n, uint64_t seed, uint8_t* pixels_out, int32_t
 int tlb_synth_make_digits_device(tlb_ctx* ctx, int64_t n, uint64_t seed, uint8_t* d_pixels, int32_t* d_labels);
 int tlb_synth_make_set_device(tlb_ctx* ctx, int64_t n, uint64_t seed, float* d_images, int32_t* d_labels);
 int tlb_synth_make_set(int64_t n, uint64_t seed, float* images_out, int32_t* labels_out);
+/* Device half of the byte ingestion: d_images[i] = d_pixels[i] / 255.0f for `count` bytes (mnist.cpp:57),
+ * on the context stream. */
+int tlb_pixels_to_images_device(tlb_ctx* ctx, const uint8_t* d_pixels, int64_t count, float* d_images);
 /* mnist::make_set invariants (mnist.cpp:126-154): pixels in [0,1], labels in 0..9 (ValueError). */
 int tlb_validate_set(const float* images, const int32_t* labels, int64_t n);
 
@@ -114,6 +117,22 @@ int tlb_train(tlb_ctx* ctx, const float* images, const int32_t* labels, int64_t 
               float rate, int32_t epochs, int64_t batch, double* epoch_loss, tlb_epoch_cb on_epoch,
               void* user);
 /* net::forward (network.cpp:81-95) for n images: yhat [n][10]; acts [n][TLB_NACT] (nullable). */
+/* net::train on the raw pixel bytes the fp32 images are made from (the IDX payload, mnist.cpp:41-61, or
+ * synth::make_digits, synth.cpp:117-153): the bytes cross the host link (1/4 of the fp32 volume) and are
+ * converted on the device as pixel / 255.0f -- bit-identical to mnist::load_images / synth::make_set, so the
+ * result equals tlb_train on the converted images bit for bit. */
+int tlb_train_u8(tlb_ctx* ctx, const uint8_t* pixels /* n x 784 */, const int32_t* labels, int64_t n, float* params,
+                 float rate, int32_t epochs, int64_t batch, double* epoch_loss_out, tlb_epoch_cb on_epoch, void* user);
+/* net::train straight from the bytes of an IDX image file and an IDX label file (mnist::load_images /
+ * load_labels + make_set): headers validated with the reference's FormatError / ValueError messages, the
+ * image payload ingested as bytes (tlb_train_u8). */
+int tlb_train_idx(tlb_ctx* ctx, const uint8_t* image_file, size_t image_bytes, const uint8_t* label_file,
+                  size_t label_bytes, float* params, float rate, int32_t epochs, int64_t batch,
+                  double* epoch_loss_out, tlb_epoch_cb on_epoch, void* user);
+/* IDX header check (no device): kind 0 = images (magic 2051: count, rows, cols), 1 = labels (magic 2049:
+ * count); dims_out[3] (unused dims 1), *payload_offset = first payload byte.  TLB_ERR_FORMAT with the
+ * reference's message on a bad magic, truncated header/payload or trailing bytes (mnist.cpp:14-61). */
+int tlb_idx_parse(const uint8_t* bytes, size_t len, int kind, int64_t* dims_out, size_t* payload_offset);
 int tlb_forward(tlb_ctx* ctx, const float* images, int64_t n, const float* params, float* yhat,
                 float* acts);
 /* forward + net::backward + net::loss per example: cells [n][TLB_CELL] (3898 grads + loss).

@@ -63,6 +63,11 @@ _SIGS = {
     "tlb_validate_set": (C.c_int, [f32p, i32p, C.c_int64]),
     # raw addresses (c_void_p) on the e2e path: ~4 us per ctypes pointer conversion avoided per call
     "tlb_train": (C.c_int, [vp, vp, vp, C.c_int64, vp, C.c_float, C.c_int32, C.c_int64, vp, EPOCH_CB, vp]),
+    "tlb_train_u8": (C.c_int, [vp, vp, vp, C.c_int64, vp, C.c_float, C.c_int32, C.c_int64, vp, EPOCH_CB, vp]),
+    "tlb_train_idx": (C.c_int, [vp, vp, C.c_size_t, vp, C.c_size_t, vp, C.c_float, C.c_int32, C.c_int64, vp,
+                                EPOCH_CB, vp]),
+    "tlb_idx_parse": (C.c_int, [vp, C.c_size_t, C.c_int, vp, vp]),
+    "tlb_pixels_to_images_device": (C.c_int, [vp, vp, C.c_int64, vp]),
     "tlb_forward": (C.c_int, [vp, f32p, C.c_int64, f32p, f32p, f32p]),
     "tlb_forward_backward": (C.c_int, [vp, f32p, i32p, f32p, C.c_int64, f32p, f32p, f32p]),
     "tlb_backward": (C.c_int, [vp, f32p, f32p, f32p, C.c_int64, f32p, f32p]),

@@ -63,7 +63,9 @@ struct Layout {
   static constexpr int kLab = kRing + 2 * NI * kImg;   // [2][NI] labels (ints)
   static constexpr int kImgs = kLab + 16;
   static constexpr int kFloats = kImgs + NI * kImgRegion;
-  static constexpr size_t kBytes = (size_t)kFloats * sizeof(float) + 2 * sizeof(uint64_t);
+  // + 2 mbarriers, 2 int64 round indices and the [2][NI][784] pixel-byte ring (byte ingestion)
+  static constexpr size_t kBytes = (size_t)kFloats * sizeof(float) + 2 * sizeof(uint64_t) + 2 * sizeof(int64_t) +
+                                   2 * NI * kImg + 4 * sizeof(int);
   static_assert(kRing % 4 == 0 && kImgs % 4 == 0, "16-byte aligned regions");
   static_assert(2 * NI <= 16, "label slots");
 };
@@ -419,14 +421,30 @@ __device__ __forceinline__ bool next_round(const TrainArgs& a, Round& r) {
 }
 
 // Issuer: the round's labels (cp.async, completed at the round's start) and ONE bulk copy of its images.
+// Byte-ingestion state of the two ring buffers (shared memory): first example index, byte flag, count.
+struct RoundBytes {
+  int64_t* idx;
+  int* bst;
+  int* cnt;
+};
+
 template <int NI>
-__device__ __forceinline__ void issue_round(const TrainArgs& a, float* ring, int* lab, uint64_t* bar, int buf,
-                                            const Round& r) {
+__device__ __forceinline__ void issue_round(const TrainArgs& a, float* ring, uint8_t* pxring, const RoundBytes& rb,
+                                            int* lab, uint64_t* bar, int buf, const Round& r) {
   const int cnt = (int)min((int64_t)NI, r.hi - r.e);
   const int64_t first = example_index(a, r.step, r.e);
   for (int q = 0; q < cnt; ++q) wait_ready_at(a, r.step, first + q);
   for (int q = 0; q < cnt; ++q) cp_async4(lab + buf * NI + q, a.labels + first + q);
   fence_proxy_async_smem();
+  rb.bst[buf] = step_bytes(a, r.step) ? 1 : 0;
+  if (rb.bst[buf]) {  // byte ingestion: the round's bytes, converted during the previous round's S3
+    rb.idx[buf] = first;
+    rb.cnt[buf] = cnt;
+    mbar_arrive_expect_tx(&bar[buf], (uint32_t)(cnt * kImg));
+    tma_load_1d(pxring + buf * NI * kImg, a.pixels + first * kImg, (uint32_t)(cnt * kImg), &bar[buf]);
+    return;
+  }
+  if (a.pixels) asm volatile("fence.proxy.async.global;" ::: "memory");  // fp32 written back in epoch 1
   mbar_arrive_expect_tx(&bar[buf], (uint32_t)(cnt * kImg * sizeof(float)));
   tma_load_1d(ring + buf * NI * kImg, a.images + first * kImg, (uint32_t)(cnt * kImg * sizeof(float)), &bar[buf]);
 }
@@ -443,6 +461,10 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
   int* const lab = reinterpret_cast<int*>(bt_smem + L::kLab);
   float* const regs = bt_smem + L::kImgs;
   uint64_t* const bar = reinterpret_cast<uint64_t*>(bt_smem + L::kFloats);
+  int64_t* const ridx = reinterpret_cast<int64_t*>(bar + 2);
+  uint8_t* const pxring = reinterpret_cast<uint8_t*>(ridx + 2);
+  int* const rbst = reinterpret_cast<int*>(pxring + 2 * NI * kImg);
+  const RoundBytes rb{ridx, rbst, rbst + 2};
   const int t = threadIdx.x, nb = gridDim.x;
   unsigned int target = 0;
 
@@ -456,7 +478,13 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
   const bool issuer = t == T - 32;  // lane 0 of the last warp (idle in S2/S6 of a full round)
   Round pf;
   bool pf_valid = first_round<NI>(a, a.step_begin, pf);
-  if (issuer && pf_valid) issue_round<NI>(a, ring, lab, bar, 0, pf);
+  if (issuer && pf_valid) issue_round<NI>(a, ring, pxring, rb, lab, bar, 0, pf);
+  if (pf_valid && step_bytes(a, pf.step)) {  // the first round's bytes: converted by every thread
+    __syncthreads();
+    mbar_wait(&bar[0], 0);
+    convert_pixels(pxring, ring, a.images_wb + ridx[0] * kImg, rb.cnt[0], t, T);
+    __syncthreads();
+  }
   uint32_t consumed = 0;
 
   int64_t ks = umod(a.step_begin, a.steps_per_epoch), ep = udiv(a.step_begin, a.steps_per_epoch);
@@ -494,10 +522,11 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
       mbar_wait(&bar[buf], (consumed >> 1) & 1);
       if (issuer) {
         cp_async_wait_all();  // this round's labels (published by S1's barrier)
+        rbst[buf ^ 1] = 0;    // (issue_round sets it for a next round that arrives as bytes)
         if (pf_valid) {
           Round nx = pf;
           if (next_round<NI>(a, nx)) {
-            issue_round<NI>(a, ring, lab, bar, buf ^ 1, nx);  // buf^1 was last read by the previous round's S6
+            issue_round<NI>(a, ring, pxring, rb, lab, bar, buf ^ 1, nx);  // buf^1 was last read by the previous round's S6
             pf = nx;
           } else {
             pf_valid = false;
@@ -513,7 +542,17 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
       for (int it = t; it < cnt * 192; it += T) conv2_item(P, W2, regs, it);
       __syncthreads();
       // S3
-      for (int it = t; it < (cnt * 80 + 31) / 32 * 32; it += T) fc_item(P, regs, rl, it, it < cnt * 80);
+      {
+        const int nfc = (cnt * 80 + 31) / 32 * 32;
+        for (int it = t; it < nfc; it += T) fc_item(P, regs, rl, it, it < cnt * 80);
+        // byte ingestion: the idle threads convert the NEXT round's bytes (landed during S1/S2)
+        const int nb = buf ^ 1;
+        if (t >= nfc && rbst[nb]) {
+          mbar_wait(&bar[nb], ((consumed + 1) >> 1) & 1);
+          convert_pixels(pxring + nb * NI * kImg, ring + nb * NI * kImg, a.images_wb + ridx[nb] * kImg, rb.cnt[nb],
+                         t - nfc, T - nfc);
+        }
+      }
       __syncthreads();
       // S4: d_s2 = fc^T dz -> dz2 = (d_s2 / 4) g2 in place; thread 0 adds the round's losses
       if (t == 0) {

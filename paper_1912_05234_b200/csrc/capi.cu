@@ -317,7 +317,15 @@ int64_t geo_chunk_start(int64_t k) {
 // fixed chunks of `chunk` images; chunk == 0 = geometric chunks of SGD groups (groups 0 and 1, then
 // the halves of each [2^e, 2^(e+1))), see TrainArgs::chunk.  The copy stream first waits for all earlier work on the
 // context stream (buffer reuse).
-int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t chunk, int64_t batch,
+// Host pixel source of the ingestion: fp32 images (mnist::MnistSet) or the raw bytes they are made from
+// (IDX payload / synth::make_digits), converted on the device by pixel / 255.0f (mnist.cpp:57, synth.cpp:158).
+struct HostImages {
+  const float* f32 = nullptr;
+  const uint8_t* u8 = nullptr;
+  uint8_t* d_u8 = nullptr;  // device byte staging (u8 source)
+};
+
+int ingest_images(tlb_ctx* c, const HostImages& host, float* dev, int64_t n, int64_t chunk, int64_t batch,
                   unsigned int token) {
   TLB_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));  // recorded by the caller
   static const bool two = [] {
@@ -332,8 +340,11 @@ int ingest_images(tlb_ctx* c, const float* host, float* dev, int64_t n, int64_t 
     const int64_t cnt = std::min(hi, n) - lo;
     // (two streams: the first chunks stay on one stream so the first step's data is not slowed)
     cudaStream_t cs = (two && k >= 3 && (k & 1)) ? c->copy_stream2 : c->copy_stream;
-    TLB_CUDA(cudaMemcpyAsync(dev + lo * 784, host + lo * 784, (size_t)cnt * 784 * sizeof(float),
-                             cudaMemcpyHostToDevice, cs));
+    if (host.u8)  // bytes: the train kernel converts them (TrainArgs::pixels)
+      TLB_CUDA(cudaMemcpyAsync(host.d_u8 + lo * 784, host.u8 + lo * 784, (size_t)cnt * 784, cudaMemcpyHostToDevice, cs));
+    else
+      TLB_CUDA(cudaMemcpyAsync(dev + lo * 784, host.f32 + lo * 784, (size_t)cnt * 784 * sizeof(float),
+                               cudaMemcpyHostToDevice, cs));
     const CUresult r = write_value32()(reinterpret_cast<CUstream>(cs),
                                        reinterpret_cast<CUdeviceptr>(flags + k), token, CU_STREAM_WRITE_VALUE_DEFAULT);
     if (r != CUDA_SUCCESS) return fail(TLB_ERR_CUDA, "cuStreamWriteValue32 failed: " + std::to_string((int)r));
@@ -397,7 +408,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
                   float rate, int32_t epoch_begin, int32_t epochs, int64_t batch, double* d_epoch_loss,
                   int64_t shard_lo = 0, int64_t shard_hi = 0, int64_t group = -1, float* grad_out = nullptr,
                   double* loss_out = nullptr, const unsigned int* ready = nullptr, unsigned int token = 0,
-                  int64_t chunk = 1, const DpArgs* dp = nullptr) {
+                  int64_t chunk = 1, const DpArgs* dp = nullptr, const uint8_t* pixels = nullptr) {
   const int64_t spe = (n + batch - 1) / batch;
   const int64_t m_max = std::min<int64_t>(batch, n);
   const int64_t m_local = grad_out ? std::max<int64_t>(0, std::min(shard_hi, m_max) - shard_lo) : m_max;
@@ -456,6 +467,8 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.fix_err = static_cast<unsigned int*>(c->dev_err.p) + 1;
   a.dp_timeout_cycles = (long long)(kWaitLimitSeconds * 2.0e9);  // ~2 GHz SM clock
   a.local_stride = (dp || grad_out) ? c->shard_stride : 0;
+  a.pixels = ready ? pixels : nullptr;  // bytes only while the ingestion flags are live (the first epoch)
+  a.images_wb = const_cast<float*>(d_images);
   if (clustered) {
     if (dp) {  // fused data parallelism: slice s lives on rank s % world (peer memory)
       a.dp_world = dp->world;
@@ -666,8 +679,9 @@ struct HostTrace {
   }
 };
 
-int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n, float* params, float rate,
-              int32_t epochs, int64_t batch, double* epoch_loss, tlb_epoch_cb on_epoch, void* user) {
+static int train_host(tlb_ctx* c, HostImages src, const int32_t* labels, int64_t n, float* params, float rate,
+                      int32_t epochs, int64_t batch, double* epoch_loss, tlb_epoch_cb on_epoch, void* user) {
+  const void* images = src.u8 ? static_cast<const void*>(src.u8) : static_cast<const void*>(src.f32);
   HostTrace ht;
   if (!c || !params) return fail(TLB_ERR_ARG, "tlb_train: null argument");
   TLB_TRY(check_train_args(n, epochs, rate, batch));
@@ -698,8 +712,13 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   while (cap * group_bytes < (int64_t)(1 << 20)) cap *= 2;
   const int64_t chunk = chunk_env >= 0 ? chunk_env : -cap;
   const int64_t nchunks = ingest_chunks(n, chunk, batch);
+  // Byte source: the chunks of bytes (1/4 of the fp32 volume) stream in like fp32 chunks and the train
+  // kernel converts each image where it is trained (a separate conversion kernel could not run beside a
+  // persistent train kernel that may hold every SM); without stream memory operations the bytes land and
+  // are converted before the kernel.
   const bool overlap = write_value32() != nullptr;
   TLB_TRY(stage_out(c, 0, (size_t)n * 784, &d_img));
+  if (src.u8) TLB_TRY(stage_out(c, 4, (size_t)n * 784, &src.d_u8));
   if (overlap) {
     if ((size_t)nchunks * sizeof(unsigned int) > c->ready.cap) {
       TLB_CUDA(cudaStreamSynchronize(c->copy_stream));
@@ -717,8 +736,11 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
     // The copy stream may only overwrite the staging buffer after all earlier work on the context
     // stream: gate it on an event recorded now, before this call's kernel (which waits on the copies).
     TLB_CUDA(cudaEventRecord(c->copy_gate, c->stream));
+  } else if (n && src.u8) {  // no stream memory operations: bytes first, converted before the kernel
+    TLB_CUDA(cudaMemcpyAsync(src.d_u8, src.u8, (size_t)n * 784, cudaMemcpyHostToDevice, c->stream));
+    TLB_CUDA(tlb::launch_pixels_to_f32(src.d_u8, d_img, n * 784, c->stream));
   } else if (n) {
-    TLB_CUDA(cudaMemcpyAsync(d_img, images, (size_t)n * 784 * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    TLB_CUDA(cudaMemcpyAsync(d_img, src.f32, (size_t)n * 784 * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   }
   const unsigned int* rdy = overlap ? static_cast<const unsigned int*>(c->ready.p) : nullptr;
   TLB_TRY(stage_in(c, 1, labels, (size_t)n, &d_lab));
@@ -738,18 +760,18 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   // driver stages pageable memory synchronously on the host.
   ht.mark("staged");
   const bool copies_first = overlap && !is_pinned(images);
-  if (copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token));
+  if (copies_first) TLB_TRY(ingest_images(c, src, d_img, n, chunk, batch, c->ready_token));
   if (!on_epoch) {
     TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, 0, epochs, batch, d_loss, 0, 0, -1, nullptr, nullptr,
-                          rdy, c->ready_token, chunk));
+                          rdy, c->ready_token, chunk, nullptr, src.d_u8));
     ht.mark("launched");
-    if (overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token));
+    if (overlap && !copies_first) TLB_TRY(ingest_images(c, src, d_img, n, chunk, batch, c->ready_token));
     ht.mark("ingest_enqueued");
   } else {
     for (int32_t e = 0; e < epochs; ++e) {
       TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, e, 1, batch, d_loss, 0, 0, -1, nullptr, nullptr,
-                            e == 0 ? rdy : nullptr, c->ready_token, chunk));
-      if (e == 0 && overlap && !copies_first) TLB_TRY(ingest_images(c, images, d_img, n, chunk, batch, c->ready_token));
+                            e == 0 ? rdy : nullptr, c->ready_token, chunk, nullptr, src.d_u8));
+      if (e == 0 && overlap && !copies_first) TLB_TRY(ingest_images(c, src, d_img, n, chunk, batch, c->ready_token));
       double mean = 0.0;
       TLB_TRY(fetch(c, &mean, d_loss + e, 1));
       on_epoch(e + 1, mean, user);
@@ -780,6 +802,47 @@ int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n,
   }
   ht.mark("done");
   return TLB_OK;
+}
+
+int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n, float* params, float rate,
+              int32_t epochs, int64_t batch, double* epoch_loss, tlb_epoch_cb on_epoch, void* user) {
+  if (c && params && !images && n > 0) return fail(TLB_ERR_ARG, "tlb_train: null dataset");
+  HostImages src;
+  src.f32 = images;
+  return train_host(c, src, labels, n, params, rate, epochs, batch, epoch_loss, on_epoch, user);
+}
+
+int tlb_train_u8(tlb_ctx* c, const uint8_t* pixels, const int32_t* labels, int64_t n, float* params, float rate,
+                 int32_t epochs, int64_t batch, double* epoch_loss, tlb_epoch_cb on_epoch, void* user) {
+  if (c && params && !pixels && n > 0) return fail(TLB_ERR_ARG, "tlb_train_u8: null dataset");
+  HostImages src;
+  src.u8 = pixels;
+  return train_host(c, src, labels, n, params, rate, epochs, batch, epoch_loss, on_epoch, user);
+}
+
+int tlb_train_idx(tlb_ctx* c, const uint8_t* image_file, size_t image_bytes, const uint8_t* label_file,
+                  size_t label_bytes, float* params, float rate, int32_t epochs, int64_t batch, double* epoch_loss,
+                  tlb_epoch_cb on_epoch, void* user) {
+  if (!c || !params || !image_file || !label_file) return fail(TLB_ERR_ARG, "tlb_train_idx: null argument");
+  int64_t idim[3], ldim[3];
+  size_t ioff = 0, loff = 0;
+  TLB_TRY(tlb_idx_parse(image_file, image_bytes, 0, idim, &ioff));
+  TLB_TRY(tlb_idx_parse(label_file, label_bytes, 1, ldim, &loff));
+  if (idim[1] != 28 || idim[2] != 28)  // mnist::MnistSet geometry (mnist.hpp:14-19)
+    return fail(TLB_ERR_FORMAT, "dataset: images have shape [" + std::to_string(idim[0]) + "," +
+                                    std::to_string(idim[1]) + "," + std::to_string(idim[2]) + "], expected [n,28,28]");
+  if (idim[0] != ldim[0])
+    return fail(TLB_ERR_FORMAT, "dataset: " + std::to_string(idim[0]) + " images but " + std::to_string(ldim[0]) +
+                                    " labels");
+  std::vector<int32_t> labels((size_t)ldim[0]);
+  for (int64_t i = 0; i < ldim[0]; ++i) {
+    labels[(size_t)i] = label_file[loff + (size_t)i];
+    if (labels[(size_t)i] > 9)
+      return fail(TLB_ERR_VALUE, "idx: label " + std::to_string(labels[(size_t)i]) + " at offset " +
+                                     std::to_string(loff + (size_t)i) + " out of range 0..9");
+  }
+  return tlb_train_u8(c, image_file + ioff, labels.data(), idim[0], params, rate, epochs, batch, epoch_loss, on_epoch,
+                      user);
 }
 
 static int run_cells(tlb_ctx* c, const float* images, const int32_t* labels, const float* targets, int64_t n,
@@ -1138,6 +1201,14 @@ int tlb_synth_make_digits_device(tlb_ctx* c, int64_t n, uint64_t seed, uint8_t* 
 
 int tlb_synth_make_set_device(tlb_ctx* c, int64_t n, uint64_t seed, float* d_images, int32_t* d_labels) {
   return synth_device(c, n, seed, nullptr, d_images, d_labels);
+}
+
+int tlb_pixels_to_images_device(tlb_ctx* c, const uint8_t* d_pixels, int64_t count, float* d_images) {
+  if (!c || (count > 0 && (!d_pixels || !d_images))) return fail(TLB_ERR_ARG, "tlb_pixels_to_images_device: null argument");
+  if (count < 0) return fail(TLB_ERR_ARG, "tlb_pixels_to_images_device: negative count");
+  TLB_TRY(set_device(c));
+  TLB_CUDA(tlb::launch_pixels_to_f32(d_pixels, d_images, count, c->stream));
+  return TLB_OK;
 }
 
 // ---- widened CNN (BASELINE configs[4]) -------------------------------------------------------------------

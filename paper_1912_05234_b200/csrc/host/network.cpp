@@ -44,15 +44,6 @@ T unflat(const float* v) {
   return T{parts[0], parts[1], parts[2], parts[3], parts[4], parts[5]};
 }
 
-std::vector<float> dataset_images(const mnist::MnistSet& data) {
-  const auto px = data.images.data();
-  return std::vector<float>(px.begin(), px.end());
-}
-
-std::vector<std::int32_t> dataset_labels(const mnist::MnistSet& data) {
-  return std::vector<std::int32_t>(data.labels.begin(), data.labels.end());
-}
-
 }  // namespace
 
 void Params::validate() const {
@@ -151,12 +142,15 @@ TrainResult train(const Params& p, const mnist::MnistSet& data, const Hyper& h,
   if (!(h.rate > 0.0f)) throw Error("train: rate must be > 0");
   if (h.batch < 1) throw Error("batches: size must be >= 1, got " + std::to_string(h.batch));
   std::vector<float> w = flat(p);
-  const std::vector<float> images = dataset_images(data);
-  const std::vector<std::int32_t> labels = dataset_labels(data);
+  // The dataset goes to the device straight from the MnistSet's own storage (no host copy): the image
+  // tensor's contiguous floats and the label vector (int is int32_t here).
+  static_assert(sizeof(int) == sizeof(std::int32_t), "labels are passed as int32");
+  const std::span<const float> images = data.images.data();
+  const auto* labels = reinterpret_cast<const std::int32_t*>(data.labels.data());
   std::vector<double> losses(static_cast<std::size_t>(h.epochs));
   {
     auto dev = detail::device();
-    detail::check(tlb_train(dev.ctx, images.data(), labels.data(), data.size(), w.data(), h.rate, h.epochs, h.batch,
+    detail::check(tlb_train(dev.ctx, images.data(), labels, data.size(), w.data(), h.rate, h.epochs, h.batch,
                             losses.data(), on_epoch ? epoch_trampoline : nullptr,
                             const_cast<std::function<void(int, double)>*>(&on_epoch)));
   }
@@ -176,11 +170,11 @@ double evaluate(const Params& p, const mnist::MnistSet& data) {
   p.validate();
   if (data.size() == 0) throw Error("evaluate: empty dataset");
   const std::vector<float> w = flat(p);
-  const std::vector<float> images = dataset_images(data);
-  const std::vector<std::int32_t> labels = dataset_labels(data);
+  const std::span<const float> images = data.images.data();
+  const auto* labels = reinterpret_cast<const std::int32_t*>(data.labels.data());
   std::int64_t correct = 0;
   auto dev = detail::device();
-  detail::check(tlb_evaluate(dev.ctx, images.data(), labels.data(), data.size(), w.data(), nullptr, &correct));
+  detail::check(tlb_evaluate(dev.ctx, images.data(), labels, data.size(), w.data(), nullptr, &correct));
   return static_cast<double>(correct) / static_cast<double>(data.size());
 }
 

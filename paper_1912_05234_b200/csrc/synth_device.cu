@@ -16,6 +16,8 @@
 // 1 M images take ~0.15 s on one B200 against ~33 s on the host.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <cstdint>
 
 #include "tlb_common.cuh"
@@ -181,4 +183,41 @@ cudaError_t make_digits(int64_t n, uint64_t seed, uint64_t* snaps, uint8_t* pixe
 }
 
 }  // namespace synth
+// ---- byte ingestion: pixel bytes -> fp32 images ------------------------------------------------------
+// pixel / 255.0f with IEEE division (mnist.cpp:57, synth.cpp:158): bit-identical to the host conversion.
+// HBM-bound: each thread takes 16 bytes (one 128-bit load) and writes four float4s.
+__global__ void __launch_bounds__(256) pixels_to_f32_kernel(const uint8_t* __restrict__ src, float* __restrict__ dst,
+                                                            int64_t count) {
+  const int64_t nvec = count >> 4;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(src) + v);
+    const uint32_t word[4] = {w.x, w.y, w.z, w.w};
+    float4* d = reinterpret_cast<float4*>(dst) + 4 * v;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      d[q] = make_float4(__fdiv_rn((float)(word[q] & 0xffu), 255.0f), __fdiv_rn((float)((word[q] >> 8) & 0xffu), 255.0f),
+                         __fdiv_rn((float)((word[q] >> 16) & 0xffu), 255.0f), __fdiv_rn((float)(word[q] >> 24), 255.0f));
+  }
+  // tail (count % 16 bytes) and unaligned callers are handled bytewise by the first threads
+  for (int64_t i = (nvec << 4) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __fdiv_rn((float)src[i], 255.0f);
+}
+
+__global__ void __launch_bounds__(256) pixels_to_f32_scalar(const uint8_t* __restrict__ src, float* __restrict__ dst,
+                                                            int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __fdiv_rn((float)src[i], 255.0f);
+}
+
+cudaError_t launch_pixels_to_f32(const uint8_t* src, float* dst, int64_t count, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const int64_t work = (count + 15) / 16;
+  const int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 8);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+  if (aligned) pixels_to_f32_kernel<<<grid, 256, 0, st>>>(src, dst, count);
+  else pixels_to_f32_scalar<<<grid, 256, 0, st>>>(src, dst, count);
+  return cudaGetLastError();
+}
+
 }  // namespace tlb

@@ -60,6 +60,12 @@ struct TrainArgs {
   // dataset (example e of group g at g * batch + e); > 0 = they hold only this rank's shards, the shard of
   // group g starting at g * local_stride (the local example e of it at g * local_stride + e).
   int64_t local_stride;
+  // Byte ingestion (tlb_train_u8 / tlb_train_idx): during the steps < ready_step_end the images arrive as
+  // pixel bytes in `pixels` (chunked, ready flags as above); the CTA that trains an image loads its 784
+  // bytes, converts them in shared memory (pixel / 255.0f, mnist.cpp:57) and writes the fp32 image back to
+  // images_wb (== images) for the later epochs of the launch.  nullptr = fp32 images throughout.
+  const uint8_t* pixels;
+  float* images_wb;
 };
 
 struct CellArgs {
@@ -119,6 +125,9 @@ cudaError_t nn_loss(const float* yhat, const float* y, int64_t n, float* out, cu
 cudaError_t nn_sum_all(const float* x, int64_t n, float* out, cudaStream_t st);
 cudaError_t nn_expf(const float* x, int64_t n, float* out, cudaStream_t st);
 cudaError_t nn_expf_range(uint32_t start_bits, int64_t n, float* out, cudaStream_t st);
+
+// Pixel bytes -> fp32 images, pixel / 255.0f (mnist.cpp:57): the device half of the byte ingestion.
+cudaError_t launch_pixels_to_f32(const uint8_t* src, float* dst, int64_t count, cudaStream_t st);
 
 // Device synthetic corpus (synth_device.cu)
 namespace synth {

@@ -123,4 +123,22 @@ __device__ __forceinline__ void wait_ready_at(const TrainArgs& a, int64_t step, 
 
 __device__ __forceinline__ void wait_ready(const TrainArgs& a, const Job& j) { wait_ready_at(a, j.step, job_index(a, j)); }
 
+// Byte ingestion: does step st take its images as pixel bytes (TrainArgs::pixels)?
+__device__ __forceinline__ bool step_bytes(const TrainArgs& a, int64_t st) {
+  return a.pixels != nullptr && st < a.ready_step_end;
+}
+
+// nimg images of pixel bytes in shared memory -> fp32 (pixel / 255.0f, IEEE division: bit-identical to
+// mnist::load_images / synth::make_set) into shared `img` and back to global `wb` (the launch's later
+// epochs read the fp32 copy).  Threads t of T; the caller publishes with a CTA barrier.
+__device__ __forceinline__ void convert_pixels(const uint8_t* px, float* img, float* wb, int nimg, int t, int T) {
+  for (int q = t; q < nimg * (kImg / 4); q += T) {
+    const uint32_t w = reinterpret_cast<const uint32_t*>(px)[q];
+    const float4 v = make_float4(__fdiv_rn((float)(w & 0xffu), 255.0f), __fdiv_rn((float)((w >> 8) & 0xffu), 255.0f),
+                                 __fdiv_rn((float)((w >> 16) & 0xffu), 255.0f), __fdiv_rn((float)(w >> 24), 255.0f));
+    reinterpret_cast<float4*>(img)[q] = v;
+    __stcg(reinterpret_cast<float4*>(wb) + q, v);
+  }
+}
+
 }  // namespace tlb

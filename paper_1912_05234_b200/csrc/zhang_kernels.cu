@@ -35,7 +35,27 @@ __device__ __forceinline__ void issue_job(const Smem& s, const TrainArgs& a, int
   const int64_t idx = job_index(a, j);  // once: the index math is a serial chain on the issuer lane
   wait_ready_at(a, j.step, idx);
   cp_async4(s.lab + buf, a.labels + idx);
-  issue_image(s, buf, a.images + idx * kImg);
+  s.bst[buf] = step_bytes(a, j.step) ? 1 : 0;
+  if (s.bst[buf]) {  // byte ingestion: the image's 784 bytes (converted while the previous job runs conv2)
+    s.jidx[buf] = idx;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&s.bar[buf], kImg);
+    tma_load_1d(s.px + buf * kImg, a.pixels + idx * kImg, kImg, &s.bar[buf]);
+  } else {
+    // a byte-ingesting launch wrote this fp32 image back with generic stores in its first epoch
+    if (a.pixels) asm volatile("fence.proxy.async.global;" ::: "memory");
+    issue_image(s, buf, a.images + idx * kImg);
+  }
+}
+
+// Byte ingestion, the launch's first job of this CTA (no previous job converted it): every thread waits
+// for its bytes and converts them.  Later jobs are converted during their predecessor's conv2.
+__device__ __forceinline__ void first_bytes(const Smem& s, const TrainArgs& a, bool valid, const Job& j) {
+  if (!valid || !step_bytes(a, j.step)) return;
+  __syncthreads();  // the issuer's s.jidx[0]
+  mbar_wait(&s.bar[0], 0);
+  convert_pixels(s.px, s.img, a.images_wb + s.jidx[0] * kImg, 1, threadIdx.x, blockDim.x);
+  __syncthreads();
 }
 
 // sgd_step (network.cpp:171-180) for one parameter, or the shard's gradient sum in DP mode.
@@ -153,6 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
   // the next job's index math, label copy and TMA issue stay off the first stage's critical path.
   const bool issuer = threadIdx.x == blockDim.x - 32;
   if (issuer && pf_valid) issue_job(s, a, 0, pf);
+  first_bytes(s, a, pf_valid, pf);
   uint32_t consumed = 0;
 
   // group index within the epoch and epoch of step st, advanced incrementally (no per-step division)
@@ -179,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
       mark(s, 2);
       if (issuer) {
         cp_async_wait_all();  // this job's label (published by conv1's barrier)
+        s.bst[buf ^ 1] = 0;   // (issue_job sets it for a next job that arrives as bytes)
         if (pf_valid) {
           Job nx = pf;
           if (next_job(a, nx)) {
@@ -189,7 +211,9 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
           }
         }
       }
-      forward_image<EXACT>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf);
+      const NextBytes nb{buf ^ 1, ((consumed + 1) >> 1) & 1, a.images_wb};
+      forward_image<EXACT>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf, nullptr, 0, 0, nullptr,
+                           a.pixels ? &nb : nullptr);
       if (threadIdx.x == 0) {
         const float l = example_loss(s, s.lab[buf], nullptr);
         if constexpr (EXACT) a.losses[e] = l;
@@ -334,6 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
   // the next job's index math, label copy and TMA issue stay off the first stage's critical path.
   const bool issuer = threadIdx.x == blockDim.x - 32;
   if (issuer && pf_valid) issue_job(s, a, 0, pf);
+  first_bytes(s, a, pf_valid, pf);
   uint32_t consumed = 0;
   load_params(s, a.params);  // once: afterwards the parameters live in shared memory
 
@@ -366,6 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       mark(s, 2);
       if (issuer) {
         cp_async_wait_all();  // this job's label (published by conv1's barrier)
+        s.bst[buf ^ 1] = 0;   // (issue_job sets it for a next job that arrives as bytes)
         if (pf_valid) {
           Job nx = pf;
           if (next_job(a, nx)) {
@@ -378,8 +404,9 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       }
       // (single GPU: parameter slices 1-7 of the previous step's update land during conv1)
       const bool pending = !dp && ls > 0;
+      const NextBytes nb{buf ^ 1, ((consumed + 1) >> 1) & 1, a.images_wb};
       forward_image<false>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf, pending ? &xbar[2] : nullptr,
-                           (uint32_t)((ls - 1) & 1), a.dp_timeout_cycles, a.dp_error);
+                           (uint32_t)((ls - 1) & 1), a.dp_timeout_cycles, a.dp_error, a.pixels ? &nb : nullptr);
       if (threadIdx.x == 0) cta_loss = __dadd_rn(cta_loss, (double)example_loss(s, s.lab[buf], nullptr));
       backward_image<false, true>(s, s.img + buf * kImg, nullptr);
       ++consumed;

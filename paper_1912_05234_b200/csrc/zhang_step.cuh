@@ -81,6 +81,9 @@ struct Smem {
   int* lab;    // labels of the two image buffers (train kernels; aliases out[12..13], unused by the FC)
   uint64_t* tab;
   uint64_t* bar;
+  int64_t* jidx;  // dataset index of the job in each image buffer (byte ingestion write-back)
+  uint8_t* px;    // [2][784] pixel bytes of the two image buffers (byte ingestion)
+  int* bst;       // [2] 1 = the job in this buffer arrives as bytes (set by the issuer)
   unsigned long long* tr;  // optional per-stage clock64 trace (CTA 0 only), nullptr otherwise
 };
 
@@ -119,7 +122,10 @@ __device__ __forceinline__ int sh_at(int v, int y) { return v * kShPlane + y * 2
 // two tails alias: no kernel uses both) -- then the clustered kernel's DSMEM receive buffer (`term`).
 // Kernels allocate only what they touch, so both the fast and the EXACT flat kernels fit two CTAs per SM.
 constexpr int kPrefixFloats = kPStride + kKp + 2 * kImg + kC1Floats + 864 + 768 + 192 + 16 + 16 + kDzp;
-constexpr size_t kPrefixBytes = ((sizeof(float) * kPrefixFloats + 34 * sizeof(uint64_t)) + 15) / 16 * 16;
+// + 2 x 784 B pixel-byte staging and 2 int64 job indices (byte ingestion, see TrainArgs::pixels)
+constexpr size_t kPrefixBytes =
+    ((sizeof(float) * kPrefixFloats + 34 * sizeof(uint64_t) + 2 * sizeof(int64_t) + 2 * kImg + 2 * sizeof(int)) + 15) /
+    16 * 16;
 constexpr int kFastTailFloats = kRed + kPStride;
 constexpr int kExactTailFloats = kSh + 1920;
 constexpr int kTailFloats = kFastTailFloats > kExactTailFloats ? kFastTailFloats : kExactTailFloats;
@@ -149,6 +155,9 @@ __device__ __forceinline__ Smem carve_smem(float* base) {
   s.dzp = p; p += kDzp;
   s.tab = reinterpret_cast<uint64_t*>(p);
   s.bar = s.tab + 32;
+  s.jidx = reinterpret_cast<int64_t*>(s.bar + 2);
+  s.px = reinterpret_cast<uint8_t*>(s.jidx + 2);  // 16-byte aligned (the prefix floats are a 16-B multiple)
+  s.bst = reinterpret_cast<int*>(s.px + 2 * kImg);
   float* const tail = base + kPrefixBytes / sizeof(float);
   s.red = tail;                   // fast tail
   s.G = tail + kRed;
@@ -1681,11 +1690,37 @@ __device__ __noinline__ void call_conv1_back(const float* img, float* row) {
 // Whole forward pass of one image (image already in shared memory).  `lab` (train kernels): the label
 // sits in shared memory, written by an async copy that thread 0 completed before conv1; it is read only
 // after conv1's barrier.
+// Byte ingestion (TrainArgs::pixels): the NEXT job's pixel bytes, converted while this job runs conv2.
+struct NextBytes {
+  int buf;          // its image buffer
+  uint32_t parity;  // the mbarrier phase its bytes complete
+  float* wb;        // fp32 write-back base (TrainArgs::images_wb); the job index is s.jidx[buf]
+};
+constexpr int kConv2Lanes = 192;  // conv2 (both modes' variants) runs on threads [0, 192): the rest are idle
+
+// Threads [kConv2Lanes, blockDim) during conv2: if the next job arrives as bytes, wait for them and convert
+// (pixel / 255.0f) into its fp32 buffer and the global write-back -- off the critical path of both jobs.
+__device__ __forceinline__ void convert_next_bytes(const Smem& s, const NextBytes* nb) {
+  if (!nb || (int)threadIdx.x < kConv2Lanes || !s.bst[nb->buf]) return;
+  mbar_wait(&s.bar[nb->buf], nb->parity);
+  const int t = threadIdx.x - kConv2Lanes, T = blockDim.x - kConv2Lanes;
+  const uint32_t* px = reinterpret_cast<const uint32_t*>(s.px + nb->buf * kImg);
+  float4* img = reinterpret_cast<float4*>(s.img + nb->buf * kImg);
+  float4* wb = reinterpret_cast<float4*>(nb->wb + s.jidx[nb->buf] * kImg);
+  for (int q = t; q < kImg / 4; q += T) {
+    const uint32_t w = px[q];
+    const float4 v = make_float4(__fdiv_rn((float)(w & 0xffu), 255.0f), __fdiv_rn((float)((w >> 8) & 0xffu), 255.0f),
+                                 __fdiv_rn((float)((w >> 16) & 0xffu), 255.0f), __fdiv_rn((float)(w >> 24), 255.0f));
+    img[q] = v;
+    __stcg(wb + q, v);
+  }
+}
+
 template <bool EXACT>
 __device__ __forceinline__ void forward_image(const Smem& s, const float* img, int label, const float* y,
                                               bool want_dz, const int* lab = nullptr, uint64_t* post_conv1 = nullptr,
                                               uint32_t post_conv1_parity = 0, long long wait_limit = 0,
-                                              unsigned int* abort = nullptr) {
+                                              unsigned int* abort = nullptr, const NextBytes* next_bytes = nullptr) {
   call_conv1<EXACT>(img);
   __syncthreads();
   if (lab) label = *lab;
@@ -1693,6 +1728,7 @@ __device__ __forceinline__ void forward_image(const Smem& s, const float* img, i
   if (post_conv1) mbar_wait_cluster_guarded(post_conv1, post_conv1_parity, wait_limit, abort);
   mark(s, 3);
   call_conv2<EXACT>();  // includes avgpool
+  convert_next_bytes(s, next_bytes);
   __syncthreads();
   mark(s, 4);
   mark(s, 5);

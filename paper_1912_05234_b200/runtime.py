@@ -71,6 +71,17 @@ def init_params(seed: int) -> np.ndarray:
     return p
 
 
+def idx_parse(data: bytes, kind: str):
+    """IDX header check (mnist.cpp:14-61 messages; no device): kind 'images' -> (count, rows, cols, payload
+    offset), 'labels' -> (count, payload offset)."""
+    buf = np.frombuffer(data, np.uint8)
+    dims = np.zeros(3, np.int64)
+    off = C.c_size_t()
+    _check(_lib.lib().tlb_idx_parse(buf.ctypes.data if buf.size else None, buf.size, 0 if kind == "images" else 1,
+                                    dims.ctypes.data, C.byref(off)))
+    return (int(dims[0]), int(dims[1]), int(dims[2]), off.value) if kind == "images" else (int(dims[0]), off.value)
+
+
 def synth_make_digits(n: int, seed: int):
     """synth::make_digits (synth.cpp:117-153): uint8 pixels [n,784], labels [n]."""
     px = np.zeros((max(n, 1), 784), np.uint8)
@@ -202,6 +213,36 @@ class Context:
                                  epochs, batch, losses.ctypes.data, cb, None))
         return p, losses[: max(epochs, 0)]
 
+    def train_u8(self, params, pixels, labels, rate: float = 0.05, epochs: int = 10, batch: int = 100,
+                 on_epoch: Optional[Callable[[int, float], None]] = None):
+        """net::train on the pixel BYTES the images are made from (IDX payload / synth::make_digits): the
+        bytes cross the host link and become pixel / 255.0f on the device -- bit-identical to train() on
+        the converted images (tlb_train_u8)."""
+        p = np.array(params, np.float32, copy=True).reshape(-1)
+        px = np.ascontiguousarray(pixels, np.uint8).reshape(-1)
+        labels = np.ascontiguousarray(labels, np.int32).reshape(-1)
+        _check_params(p, "train_u8")
+        if px.size != len(labels) * 784:
+            raise_for(2, f"train_u8: pixels hold {px.size} bytes, expected {len(labels)} x 784")
+        losses = np.zeros(max(epochs, 1), np.float64)
+        cb = _lib.EPOCH_CB(lambda e, l, _u: on_epoch(e, l)) if on_epoch else _NO_EPOCH_CB
+        _check(self._L.tlb_train_u8(self._h, px.ctypes.data, labels.ctypes.data, len(labels), p.ctypes.data, rate,
+                                    epochs, batch, losses.ctypes.data, cb, None))
+        return p, losses[: max(epochs, 0)]
+
+    def train_idx(self, params, image_file: bytes, label_file: bytes, rate: float = 0.05, epochs: int = 10,
+                  batch: int = 100, on_epoch: Optional[Callable[[int, float], None]] = None):
+        """net::train straight from the bytes of an IDX image file and an IDX label file (tlb_train_idx)."""
+        p = np.array(params, np.float32, copy=True).reshape(-1)
+        _check_params(p, "train_idx")
+        img = np.frombuffer(image_file, np.uint8)
+        lab = np.frombuffer(label_file, np.uint8)
+        losses = np.zeros(max(epochs, 1), np.float64)
+        cb = _lib.EPOCH_CB(lambda e, l, _u: on_epoch(e, l)) if on_epoch else _NO_EPOCH_CB
+        _check(self._L.tlb_train_idx(self._h, img.ctypes.data, img.size, lab.ctypes.data, lab.size, p.ctypes.data,
+                                     rate, epochs, batch, losses.ctypes.data, cb, None))
+        return p, losses[: max(epochs, 0)]
+
     def forward(self, images, params, acts: bool = False):
         """net::forward for n images -> yhat [n,10] (and activations [n,5290])."""
         images = _images_2d(images, "forward")
@@ -256,6 +297,10 @@ class Context:
                                         batch, d_epoch_loss))
 
     # ---- device synthetic corpus ------------------------------------------------------------------------
+    def pixels_to_images_device(self, d_pixels: int, count: int, d_images: int) -> None:
+        """d_images[i] = d_pixels[i] / 255.0f on the context stream (the device half of the byte ingestion)."""
+        _check(self._L.tlb_pixels_to_images_device(self._h, d_pixels, count, d_images))
+
     def synth_make_set_device(self, n: int, seed: int, d_images: int, d_labels: int) -> None:
         """synth::make_set(n, seed) generated on the device into [n][784] fp32 / [n] int32 buffers."""
         _check(self._L.tlb_synth_make_set_device(self._h, n, seed, C.c_void_p(d_images or None),
