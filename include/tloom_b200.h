@@ -59,6 +59,15 @@ const char* tlb_version(void);
 /* ---- context: device, stream, mode, workspaces ------------------------------------------------ */
 int tlb_ctx_create(int device, tlb_ctx** out);
 int tlb_ctx_destroy(tlb_ctx* ctx);
+/* A context over several local GPUs in one process: tlb_train / tlb_train_u8 /
+ * tlb_train_idx split every SGD group over the devices with the reference's static_chunk rule
+ * (runtime.cpp:138-145) -- each device keeps its shard of the data -- and reduce the gradient over all of
+ * them at every step through peer memory (one persistent kernel per device).  EXACT mode: bit-identical to
+ * one device and to the reference, for any device count (as the reference is for any worker count); fast
+ * mode: deterministic for a given count, within the 1e-4 tolerance.  A device may be listed more than once
+ * (the kernels then share it).  Other entry points run on devices[0]. */
+int tlb_ctx_create_multi(const int* devices, int n_devices, tlb_ctx** out);
+int tlb_ctx_device_count(const tlb_ctx* ctx, int* n_devices);
 /* Enqueue on a caller-owned cudaStream_t (NULL = the legacy default stream).  A new context uses
  * its own non-blocking stream. */
 int tlb_ctx_set_stream(tlb_ctx* ctx, void* cuda_stream);

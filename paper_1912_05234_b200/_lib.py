@@ -33,6 +33,8 @@ _SIGS = {
     "tlb_last_error": (C.c_char_p, []),
     "tlb_version": (C.c_char_p, []),
     "tlb_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+    "tlb_ctx_create_multi": (C.c_int, [vp, C.c_int, C.POINTER(vp)]),
+    "tlb_ctx_device_count": (C.c_int, [vp, vp]),
     "tlb_ctx_destroy": (C.c_int, [vp]),
     "tlb_ctx_set_stream": (C.c_int, [vp, vp]),
     "tlb_ctx_set_mode": (C.c_int, [vp, C.c_int]),

@@ -128,6 +128,10 @@ struct tlb_ctx {
   DevBuf wide[12];
   int64_t wide_cap = 0;
   tlb::wide::StepArgs wide_last{};
+  // In-process multi-GPU (tlb_ctx_create_multi): the contexts of devices[1..] (this one is devices[0]);
+  // each keeps its shard of the data, its parameter copy and its rows in md_* (see train_multi).
+  std::vector<tlb_ctx*> peers;
+  DevBuf md_img, md_lab, md_u8, md_p, md_loss, md_work, md_losses, md_lpart, md_bar;
 };
 
 namespace {
@@ -560,7 +564,12 @@ int tlb_ctx_create(int device, tlb_ctx** out) {
 
 int tlb_ctx_destroy(tlb_ctx* c) {
   if (!c) return TLB_OK;
+  for (tlb_ctx* p : c->peers) tlb_ctx_destroy(p);
+  c->peers.clear();
   cudaSetDevice(c->device);
+  for (DevBuf* b : {&c->md_img, &c->md_lab, &c->md_u8, &c->md_p, &c->md_loss, &c->md_work, &c->md_losses, &c->md_lpart,
+                    &c->md_bar})
+    b->release();
   cudaStreamSynchronize(c->stream);
   c->work.release();
   c->losses.release();
@@ -594,6 +603,52 @@ int tlb_ctx_set_mode(tlb_ctx* c, int mode) {
   if (mode != TLB_MODE_EXACT && mode != TLB_MODE_FAST)
     return fail(TLB_ERR_ARG, "tlb_ctx_set_mode: unknown mode " + std::to_string(mode));
   c->mode = mode;
+  for (tlb_ctx* p : c->peers) p->mode = mode;
+  return TLB_OK;
+}
+
+int tlb_ctx_create_multi(const int* devices, int n_devices, tlb_ctx** out) {
+  if (!out || !devices) return fail(TLB_ERR_ARG, "tlb_ctx_create_multi: null argument");
+  *out = nullptr;
+  if (n_devices < 1 || n_devices > 8) return fail(TLB_ERR_ARG, "tlb_ctx_create_multi: 1..8 devices");
+  tlb_ctx* c = nullptr;
+  TLB_TRY(tlb_ctx_create(devices[0], &c));
+  for (int i = 1; i < n_devices; ++i) {
+    tlb_ctx* p = nullptr;
+    const int rc = tlb_ctx_create(devices[i], &p);
+    if (rc != TLB_OK) {
+      tlb_ctx_destroy(c);
+      return rc;
+    }
+    c->peers.push_back(p);
+  }
+  // peer access between distinct devices (the reduction reads every device's rows, writes every copy)
+  for (int i = 0; i < n_devices; ++i)
+    for (int j = 0; j < n_devices; ++j) {
+      if (devices[i] == devices[j]) continue;
+      int ok = 0;
+      cudaDeviceCanAccessPeer(&ok, devices[i], devices[j]);
+      if (!ok) {
+        tlb_ctx_destroy(c);
+        return fail(TLB_ERR_CUDA, "tlb_ctx_create_multi: device " + std::to_string(devices[i]) +
+                                      " cannot access device " + std::to_string(devices[j]) + " (no P2P)");
+      }
+      cudaSetDevice(devices[i]);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        tlb_ctx_destroy(c);
+        return fail(TLB_ERR_CUDA, std::string("tlb_ctx_create_multi: ") + cudaGetErrorString(e));
+      }
+      (void)cudaGetLastError();
+    }
+  cudaSetDevice(devices[0]);
+  *out = c;
+  return TLB_OK;
+}
+
+int tlb_ctx_device_count(const tlb_ctx* c, int* n) {
+  if (!c || !n) return fail(TLB_ERR_ARG, "null argument");
+  *n = 1 + (int)c->peers.size();
   return TLB_OK;
 }
 
@@ -679,6 +734,157 @@ struct HostTrace {
   }
 };
 
+// In-process multi-GPU net::train (tlb_ctx_create_multi): device d trains
+// static_chunk(m, N, d) of every SGD group (runtime.cpp:138-145) on its shard of the data (shard layout,
+// stride ceil(batch / N)); one flat persistent kernel per device, launched together, meets the others at a
+// grid barrier over every CTA of every device, and the reduction phase sums ALL devices' rows -- EXACT: the
+// per-example rows in example order, so the result is bit-identical to one device (and to the reference)
+// for any device count, as the reference is for any worker count; fast: CTA partials in (device, CTA)
+// order (deterministic for a given N).  Every device's parameter copy receives the update.
+static int train_multi(tlb_ctx* c, HostImages src, const int32_t* labels, int64_t n, float* params, float rate,
+                       int32_t epochs, int64_t batch, double* epoch_loss, tlb_epoch_cb on_epoch, void* user) {
+  std::vector<tlb_ctx*> dv{c};
+  for (tlb_ctx* p : c->peers) dv.push_back(p);
+  const int N = (int)dv.size();
+  const bool ex = exact(c);
+  const int64_t spe = (n + batch - 1) / batch, full = n / batch, last = n - full * batch;
+  const int64_t S = (batch + N - 1) / N;  // shard stride
+  auto static_chunk = [](int64_t m, int workers, int w, int64_t& lo, int64_t& hi) {  // runtime.cpp:138-145
+    const int64_t block = (m + workers - 1) / workers;
+    lo = std::min<int64_t>((int64_t)w * block, m);
+    hi = std::min<int64_t>(lo + block, m);
+  };
+  const int threads = 512;
+  // co-residency: devices listed more than once (one-GPU tests) share its SMs
+  int G = 1 << 30;
+  for (int d = 0; d < N; ++d) {
+    int share = 0;
+    for (int e = 0; e < N; ++e) share += dv[e]->device == dv[d]->device;
+    const int occ = std::max(1, dv[d]->occ_train[ex ? 1 : 0][1]);
+    G = std::min(G, std::max(1, occ * dv[d]->sm_count / share));
+  }
+  const int64_t rows = ex ? S : G;
+  const size_t elem = src.u8 ? 1 : sizeof(float);
+  const void* img_host = src.u8 ? static_cast<const void*>(src.u8) : static_cast<const void*>(src.f32);
+  std::vector<float> h_par(TLB_PSTRIDE, 0.0f);
+  std::memcpy(h_par.data(), params, TLB_NPARAM * sizeof(float));
+  // per-device buffers and the shard upload (one 2-D copy for the full groups, one for the ragged tail)
+  for (int d = 0; d < N; ++d) {
+    tlb_ctx* x = dv[d];
+    TLB_TRY(set_device(x));
+    TLB_CUDA(x->md_img.ensure((size_t)spe * S * 784 * sizeof(float)));
+    TLB_CUDA(x->md_lab.ensure((size_t)spe * S * sizeof(int32_t)));
+    if (src.u8) TLB_CUDA(x->md_u8.ensure((size_t)spe * S * 784));
+    TLB_CUDA(x->md_p.ensure(TLB_PSTRIDE * sizeof(float)));
+    TLB_CUDA(x->md_loss.ensure((size_t)std::max(epochs, 1) * sizeof(double)));
+    TLB_CUDA(x->md_work.ensure((size_t)std::max<int64_t>(rows, 1) * TLB_PSTRIDE * sizeof(float)));
+    TLB_CUDA(x->md_losses.ensure((size_t)S * sizeof(float)));
+    TLB_CUDA(x->md_lpart.ensure((size_t)G * sizeof(double)));
+    void* dst = src.u8 ? x->md_u8.p : x->md_img.p;
+    int64_t lo, hi;
+    static_chunk(batch, N, d, lo, hi);
+    if (full > 0 && hi > lo) {
+      TLB_CUDA(cudaMemcpy2DAsync(dst, S * 784 * elem, static_cast<const char*>(img_host) + lo * 784 * elem,
+                                 batch * 784 * elem, (hi - lo) * 784 * elem, full, cudaMemcpyHostToDevice, x->stream));
+      TLB_CUDA(cudaMemcpy2DAsync(x->md_lab.p, S * sizeof(int32_t), labels + lo, batch * sizeof(int32_t),
+                                 (hi - lo) * sizeof(int32_t), full, cudaMemcpyHostToDevice, x->stream));
+    }
+    if (last > 0) {
+      static_chunk(last, N, d, lo, hi);
+      if (hi > lo) {
+        TLB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + full * S * 784 * elem,
+                                 static_cast<const char*>(img_host) + (full * batch + lo) * 784 * elem,
+                                 (hi - lo) * 784 * elem, cudaMemcpyHostToDevice, x->stream));
+        TLB_CUDA(cudaMemcpyAsync(static_cast<int32_t*>(x->md_lab.p) + full * S, labels + full * batch + lo,
+                                 (hi - lo) * sizeof(int32_t), cudaMemcpyHostToDevice, x->stream));
+      }
+    }
+    if (src.u8)
+      TLB_CUDA(tlb::launch_pixels_to_f32(static_cast<const uint8_t*>(x->md_u8.p), static_cast<float*>(x->md_img.p),
+                                         spe * S * 784, x->stream));
+    TLB_CUDA(cudaMemcpyAsync(x->md_p.p, h_par.data(), TLB_PSTRIDE * sizeof(float), cudaMemcpyHostToDevice, x->stream));
+    TLB_CUDA(cudaMemsetAsync(x->dev_err.p, 0, 4 * sizeof(unsigned int), x->stream));
+  }
+  TLB_TRY(set_device(c));
+  TLB_CUDA(c->md_bar.ensure(sizeof(unsigned int)));
+  auto launch = [&](int32_t e0, int32_t ne) -> int {
+    for (tlb_ctx* x : dv) {
+      TLB_CUDA(cudaSetDevice(x->device));
+      TLB_CUDA(cudaStreamSynchronize(x->stream));
+    }
+    TLB_TRY(set_device(c));
+    TLB_CUDA(cudaMemset(c->md_bar.p, 0, sizeof(unsigned int)));  // the kernels meet on it from step 0
+    TLB_CUDA(cudaDeviceSynchronize());
+    for (int d = 0; d < N; ++d) {
+      tlb_ctx* x = dv[d];
+      TLB_TRY(set_device(x));
+      tlb::TrainArgs a{};
+      a.images = static_cast<const float*>(x->md_img.p);
+      a.images_wb = static_cast<float*>(x->md_img.p);
+      a.labels = static_cast<const int32_t*>(x->md_lab.p);
+      a.n = n;
+      a.batch = batch;
+      a.rate = rate;
+      a.steps_per_epoch = spe;
+      a.step_begin = (int64_t)e0 * spe;
+      a.step_end = (int64_t)(e0 + ne) * spe;
+      a.params = static_cast<float*>(x->md_p.p);
+      a.work = static_cast<float*>(x->md_work.p);
+      a.losses = static_cast<float*>(x->md_losses.p);
+      a.loss_part = static_cast<double*>(x->md_lpart.p);
+      a.epoch_loss = static_cast<double*>(x->md_loss.p);
+      a.barrier = static_cast<unsigned int*>(c->md_bar.p);
+      a.dp_world = N;
+      a.dp_rank = d;
+      a.local_stride = S;
+      a.md_n = N;
+      for (int e = 0; e < N; ++e) {
+        a.md_work[e] = static_cast<float*>(dv[e]->md_work.p);
+        a.md_losses[e] = static_cast<float*>(dv[e]->md_losses.p);
+        a.md_loss_part[e] = static_cast<double*>(dv[e]->md_lpart.p);
+        a.md_params[e] = static_cast<float*>(dv[e]->md_p.p);
+        a.md_epoch_loss[e] = static_cast<double*>(dv[e]->md_loss.p);
+      }
+      a.md_bar = static_cast<unsigned int*>(c->md_bar.p);
+      a.dp_error = static_cast<unsigned int*>(x->dev_err.p);
+      a.fix_err = static_cast<unsigned int*>(x->dev_err.p) + 1;
+      a.dp_timeout_cycles = (long long)(kWaitLimitSeconds * 2.0e9);
+      TLB_CUDA(tlb::launch_train(ex, a, G, threads, x->stream));
+    }
+    for (tlb_ctx* x : dv) {
+      TLB_CUDA(cudaSetDevice(x->device));
+      TLB_CUDA(cudaStreamSynchronize(x->stream));
+    }
+    for (int d = 0; d < N; ++d) {
+      unsigned int w[4];
+      TLB_CUDA(cudaSetDevice(dv[d]->device));
+      TLB_CUDA(cudaMemcpy(w, dv[d]->dev_err.p, sizeof(w), cudaMemcpyDeviceToHost));
+      if (w[0] || w[1]) {
+        TLB_CUDA(cudaMemset(dv[d]->dev_err.p, 0, sizeof(w)));
+        return fail(TLB_ERR_CUDA, "train: device " + std::to_string(dv[d]->device) + " (rank " + std::to_string(d) +
+                                      ") timed out at the cross-device grid barrier (another device never arrived)");
+      }
+    }
+    return TLB_OK;
+  };
+  std::vector<double> losses((size_t)std::max(epochs, 1));
+  if (!on_epoch) {
+    TLB_TRY(launch(0, epochs));
+  } else {
+    for (int32_t e = 0; e < epochs; ++e) {
+      TLB_TRY(launch(e, 1));
+      TLB_TRY(set_device(c));
+      TLB_CUDA(cudaMemcpy(&losses[(size_t)e], static_cast<double*>(c->md_loss.p) + e, sizeof(double),
+                          cudaMemcpyDeviceToHost));
+      on_epoch(e + 1, losses[(size_t)e], user);
+    }
+  }
+  TLB_TRY(set_device(c));
+  TLB_CUDA(cudaMemcpy(params, c->md_p.p, TLB_NPARAM * sizeof(float), cudaMemcpyDeviceToHost));
+  if (epoch_loss) TLB_CUDA(cudaMemcpy(epoch_loss, c->md_loss.p, epochs * sizeof(double), cudaMemcpyDeviceToHost));
+  return TLB_OK;
+}
+
 static int train_host(tlb_ctx* c, HostImages src, const int32_t* labels, int64_t n, float* params, float rate,
                       int32_t epochs, int64_t batch, double* epoch_loss, tlb_epoch_cb on_epoch, void* user) {
   const void* images = src.u8 ? static_cast<const void*>(src.u8) : static_cast<const void*>(src.f32);
@@ -692,6 +898,7 @@ static int train_host(tlb_ctx* c, HostImages src, const int32_t* labels, int64_t
   TLB_TRY(set_device(c));
   ht.mark("checked");
   if (epochs == 0) return TLB_OK;
+  if (!c->peers.empty()) return train_multi(c, src, labels, n, params, rate, epochs, batch, epoch_loss, on_epoch, user);
   float* d_img;
   int32_t* d_lab;
   float* d_p;

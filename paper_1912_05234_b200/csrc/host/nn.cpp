@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "device.hpp"
 #include "tloom_b200.h"
@@ -35,8 +36,21 @@ void check(int status) { raise(status); }
 DeviceLock device() {
   std::unique_lock<std::mutex> lk(g_mutex);
   if (!g_ctx) {
-    const char* dev = std::getenv("TLOOM_B200_DEVICE");
-    check(tlb_ctx_create(dev ? std::atoi(dev) : 0, &g_ctx));
+    // TLOOM_B200_DEVICES=0,1,2,3: one context over several GPUs (net::train splits every group over them);
+    // else TLOOM_B200_DEVICE (default 0)
+    if (const char* list = std::getenv("TLOOM_B200_DEVICES")) {
+      std::vector<int> devs;
+      for (const char* p = list; *p;) {
+        char* end = nullptr;
+        devs.push_back(static_cast<int>(std::strtol(p, &end, 10)));
+        p = (*end == ',') ? end + 1 : end;
+        if (end == p && *p) break;
+      }
+      check(tlb_ctx_create_multi(devs.data(), static_cast<int>(devs.size()), &g_ctx));
+    } else {
+      const char* dev = std::getenv("TLOOM_B200_DEVICE");
+      check(tlb_ctx_create(dev ? std::atoi(dev) : 0, &g_ctx));
+    }
     const char* mode = std::getenv("TLOOM_B200_MODE");
     if (mode && std::strcmp(mode, "fast") == 0) check(tlb_ctx_set_mode(g_ctx, TLB_MODE_FAST));
   }

@@ -11,7 +11,7 @@
 #include <cstdio>
 #include <vector>
 
-#include "zhang_step.cuh"
+#include "stage_variants.cuh"
 
 using namespace tlb;
 
@@ -65,31 +65,31 @@ __device__ __forceinline__ void run_stage(const Smem& s, float* row) {
   else if constexpr (STAGE == kConv2V2) stage_conv2<EXACT, 2>(s);
   else if constexpr (STAGE == kFc) stage_fc<EXACT>(s, 3, nullptr, true);
   else if constexpr (STAGE == kFcBack) stage_fc_back<EXACT, A>(s, row);
-  else if constexpr (STAGE == kC2BackV0) stage_conv2_back<EXACT, A, 0>(s, row);
-  else if constexpr (STAGE == kC2BackV1) stage_conv2_back<EXACT, A, 1>(s, row);
-  else if constexpr (STAGE == kC2BackV2) stage_conv2_back<EXACT, A, 2>(s, row);
-  else if constexpr (STAGE == kC2BackV3) stage_conv2_back<EXACT, A, 3>(s, row);
+  else if constexpr (STAGE == kC2BackV0) stage_conv2_back_legacy<EXACT, A, 0>(s, row);
+  else if constexpr (STAGE == kC2BackV1) stage_conv2_back_legacy<EXACT, A, 1>(s, row);
+  else if constexpr (STAGE == kC2BackV2) stage_conv2_back_legacy<EXACT, A, 2>(s, row);
+  else if constexpr (STAGE == kC2BackV3) stage_conv2_back_legacy<EXACT, A, 3>(s, row);
   else if constexpr (STAGE == kC1Back) stage_conv1_back<EXACT, A>(s, s.img, row);
   else if constexpr (STAGE == kForward) forward_image<EXACT>(s, s.img, 3, nullptr, true);
-  else if constexpr (STAGE == kBackinV4) stage_conv2_back<EXACT, A, 4>(s, row);
-  else if constexpr (STAGE == kBackinV5) stage_conv2_back<EXACT, A, 5>(s, row);
-  else if constexpr (STAGE == kC1BackGk2) stage_conv1_back_gk2<EXACT, A>(s, s.img, row);
+  else if constexpr (STAGE == kBackinV4) stage_conv2_back_legacy<EXACT, A, 4>(s, row);
+  else if constexpr (STAGE == kBackinV5) stage_conv2_back_legacy<EXACT, A, 5>(s, row);
+  else if constexpr (STAGE == kC1BackGk2) stage_conv1_back_gk2_legacy<EXACT, A>(s, s.img, row);
   else if constexpr (STAGE == kC2BackV6 || STAGE == kC2BackV7) {
-    if constexpr (!EXACT) stage_conv2_back<false, A, STAGE == kC2BackV6 ? 6 : 7>(s, row);
+    if constexpr (!EXACT) stage_conv2_back_legacy<false, A, STAGE == kC2BackV6 ? 6 : 7>(s, row);
   } else if constexpr (STAGE == kBackwardV6 || STAGE == kBackwardV7 || STAGE == kBackwardV8) {
     if constexpr (!EXACT) {
       stage_fc_back<EXACT, A>(s, row);
       __syncthreads();
-      stage_conv2_back<false, A, STAGE == kBackwardV6 ? 6 : STAGE == kBackwardV7 ? 7 : 8>(s, row);
+      stage_conv2_back_legacy<false, A, STAGE == kBackwardV6 ? 6 : STAGE == kBackwardV7 ? 7 : 8>(s, row);
       __syncthreads();
       stage_conv1_back<EXACT, A>(s, s.img, row);
     }
   } else if constexpr (STAGE == kC2BackV8) {
-    if constexpr (!EXACT) stage_conv2_back<false, A, 8>(s, row);
+    if constexpr (!EXACT) stage_conv2_back_legacy<false, A, 8>(s, row);
   } else if constexpr (STAGE == kBackinV9) {
-    if constexpr (!EXACT) stage_conv2_back<false, A, 9>(s, row);
+    if constexpr (!EXACT) stage_conv2_back_legacy<false, A, 9>(s, row);
   } else if constexpr (STAGE == kC2BackV10) {
-    if constexpr (!EXACT) stage_conv2_back<false, A, 10>(s, row);
+    if constexpr (!EXACT) stage_conv2_back_legacy<false, A, 10>(s, row);
   } else if constexpr (STAGE == kBackwardV9 || STAGE == kBackwardV10 || STAGE == kBackwardV11 ||
                        STAGE == kBackwardV12 || STAGE == kBackwardV13 || STAGE == kBackwardV14) {
     if constexpr (!EXACT) {
@@ -97,27 +97,27 @@ __device__ __forceinline__ void run_stage(const Smem& s, float* row) {
                       : STAGE == kBackwardV12 ? 12 : STAGE == kBackwardV13 ? 13 : 14;
       stage_fc_back<EXACT, A>(s, row);
       __syncthreads();
-      stage_conv2_back<false, A, V>(s, row);
+      stage_conv2_back_legacy<false, A, V>(s, row);
       __syncthreads();
-      stage_conv1_back_gk2<false, A, gk2_split_lanes(V), V == 14>(s, s.img, row);
+      stage_conv1_back_gk2_legacy<false, A, gk2_split_lanes(V), V == 14>(s, s.img, row);
     }
   }
   else if constexpr (STAGE == kBackwardV4 || STAGE == kBackwardV5) {
     stage_fc_back<EXACT, A>(s, row);
     __syncthreads();
-    stage_conv2_back<EXACT, A, STAGE == kBackwardV4 ? 4 : 5>(s, row);
+    stage_conv2_back_legacy<EXACT, A, STAGE == kBackwardV4 ? 4 : 5>(s, row);
     __syncthreads();
-    stage_conv1_back_gk2<EXACT, A>(s, s.img, row);
+    stage_conv1_back_gk2_legacy<EXACT, A>(s, s.img, row);
   } else if constexpr (STAGE == kBackwardV0) {
     stage_fc_back<EXACT, A>(s, row);
     __syncthreads();
-    stage_conv2_back<EXACT, A, 0>(s, row);
+    stage_conv2_back_legacy<EXACT, A, 0>(s, row);
     __syncthreads();
     stage_conv1_back<EXACT, A>(s, s.img, row);
   } else {
     stage_fc_back<EXACT, A>(s, row);
     __syncthreads();
-    stage_conv2_back<EXACT, A, 1>(s, row);
+    stage_conv2_back_legacy<EXACT, A, 1>(s, row);
     __syncthreads();
     stage_conv1_back<EXACT, A>(s, s.img, row);
   }

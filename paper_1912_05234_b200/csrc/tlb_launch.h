@@ -66,6 +66,19 @@ struct TrainArgs {
   // images_wb (== images) for the later epochs of the launch.  nullptr = fp32 images throughout.
   const uint8_t* pixels;
   float* images_wb;
+  // In-process multi-GPU (tlb_ctx_create_multi): md_n > 1 devices run the flat train kernel at once, device
+  // dp_rank on static_chunk(m, md_n, dp_rank) of every group (dp_world = md_n, shard layout).  Phase 2 spans
+  // every device: global CTA (dp_rank * grid + cta) reduces its parameter slice over ALL devices' rows in
+  // example order (EXACT: bit-identical to one device) or (device, CTA) order (fast), reading peers' rows
+  // through their pointers, and writes the update into every device's parameter copy; the grid barrier
+  // counts every CTA of every device on md_bar (device 0).  md_n == 0: single device.
+  int md_n;
+  float* md_work[8];
+  float* md_losses[8];
+  double* md_loss_part[8];
+  float* md_params[8];
+  double* md_epoch_loss[8];
+  unsigned int* md_bar;
 };
 
 struct CellArgs {

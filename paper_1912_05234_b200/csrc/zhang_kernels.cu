@@ -159,6 +159,137 @@ __device__ __forceinline__ void reduce_loss(const Smem& s, const TrainArgs& a, i
 }
 
 
+// ---- in-process multi-GPU (TrainArgs::md_n > 1) -----------------------------------------------------
+// Grid barrier over every CTA of every device: arrivals on device 0's counter (system scope: the peers
+// reach it over NVLink), bounded by dp_timeout_cycles -- a device that never arrives sets dp_error and the
+// host call fails instead of hanging.
+__device__ __forceinline__ void md_sync(const TrainArgs& a, unsigned int& target) {
+  __syncthreads();
+  target += gridDim.x * (unsigned int)a.md_n;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(a.md_bar) : "memory");
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.md_bar) : "memory");
+    const long long t0 = clock64();
+    while ((int)(v - target) < 0) {
+      if (clock64() - t0 > a.dp_timeout_cycles) {
+        atomicExch(a.dp_error, 1u);
+        break;
+      }
+      __nanosleep(64);
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.md_bar) : "memory");
+    }
+  }
+  __syncthreads();
+}
+
+// Row r (0 <= r < total) of the step's gradient rows across devices: EXACT = example r of the group (device
+// d holds static_chunk(m, md_n, d) of it, local row r - lo_d); fast = the CTA partials of device 0, then of
+// device 1, ... (nrows_d = CTAs with examples on device d).  Returns the row's base pointer.
+template <bool EXACT>
+__device__ __forceinline__ const float* md_row(const TrainArgs& a, int64_t m, int64_t r) {
+  int d = 0;
+  for (; d < a.md_n - 1; ++d) {
+    int64_t lo, hi;
+    static_chunk(m, a.md_n, d, lo, hi);
+    int64_t cnt = hi - lo;
+    if constexpr (!EXACT) {  // CTA partial rows of device d
+      const int64_t block = cnt > 0 ? udiv(cnt + gridDim.x - 1, gridDim.x) : 1;
+      cnt = cnt > 0 ? udiv(cnt + block - 1, block) : 0;
+    }
+    if (r < cnt) break;
+    r -= cnt;
+  }
+  return a.md_work[d] + r * kPStride;
+}
+
+__device__ __forceinline__ int64_t md_total_rows(const TrainArgs& a, int64_t m, bool exact) {
+  if (exact) return m;
+  int64_t total = 0;
+  for (int d = 0; d < a.md_n; ++d) {
+    int64_t lo, hi;
+    static_chunk(m, a.md_n, d, lo, hi);
+    const int64_t cnt = hi - lo;
+    const int64_t block = cnt > 0 ? udiv(cnt + gridDim.x - 1, gridDim.x) : 1;
+    total += cnt > 0 ? udiv(cnt + block - 1, block) : 0;
+  }
+  return total;
+}
+
+// Phase 2 across devices: global CTA gb owns parameters static_chunk(3898, md_n * grid, gb); rows are staged
+// through shared memory (one L2/NVLink round trip per chunk), then each parameter's sum runs in row order
+// (EXACT: a single fp32 chain in example order = the reference's; fast: 8 lanes + a fixed tree) and the
+// update goes to every device's parameter copy.
+template <bool EXACT>
+__device__ __forceinline__ void md_reduce_slice(const Smem& s, const TrainArgs& a, int64_t m) {
+  const int Gt = gridDim.x * a.md_n, gb = a.dp_rank * gridDim.x + blockIdx.x;
+  int64_t j0, j1;
+  static_chunk(kNParam, Gt, gb, j0, j1);
+  const int64_t nrows = md_total_rows(a, m, EXACT);
+  constexpr int kLanes = EXACT ? 1 : 8;
+  float* stage = s.c1;  // c1|s1|c2|s2 are contiguous: >= 5,280 free floats
+  const int t = threadIdx.x, per = blockDim.x / kLanes;
+  for (int64_t jb = j0; jb < j1; jb += per) {
+    const int W = (int)min((int64_t)per, j1 - jb);
+    const int R = 5280 / W;
+    const int j = t / kLanes, l = t % kLanes;
+    float acc = 0.0f;
+    for (int64_t r0 = 0; r0 < nrows; r0 += R) {
+      const int rr = (int)min((int64_t)R, nrows - r0);
+      __syncthreads();
+      for (int q = t; q < rr * W; q += blockDim.x) {
+        const int rw = q / W, c = q - rw * W;
+        stage[rw * W + c] = __ldcg(md_row<EXACT>(a, m, r0 + rw) + jb + c);
+      }
+      __syncthreads();
+      if (j < W) {
+        if constexpr (EXACT) {
+          for (int r = 0; r < rr; ++r) acc = fadd(acc, stage[r * W + j]);
+        } else {
+          for (int r = l; r < rr; r += kLanes) acc += stage[r * W + j];
+        }
+      }
+    }
+    if constexpr (!EXACT) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    }
+    if (j < W && l == 0) {
+      const int pj = (int)jb + j;
+      if (a.grad_out) {
+        a.grad_out[pj] = acc;
+      } else {
+        const float w = fsub(s.P[pj], fmul(a.rate, __fdiv_rn(acc, (float)m)));
+        for (int d = 0; d < a.md_n; ++d) __stcg(a.md_params[d] + pj, w);
+      }
+    }
+  }
+}
+
+// fp64 loss of the group across devices (global CTA md_n * grid - 1): EXACT per-example losses in example
+// order, fast CTA partials in (device, CTA) order; the epoch value goes to every device's epoch_loss.
+template <bool EXACT>
+__device__ __forceinline__ void md_reduce_loss(const Smem& s, const TrainArgs& a, int64_t m, int64_t ks, int64_t ep) {
+  if (threadIdx.x != 0) return;
+  double l = ks != 0 ? a.epoch_loss[ep] : 0.0;
+  for (int d = 0; d < a.md_n; ++d) {
+    int64_t lo, hi;
+    static_chunk(m, a.md_n, d, lo, hi);
+    const int64_t cnt = hi - lo;
+    if constexpr (EXACT) {
+      for (int64_t e = 0; e < cnt; ++e) l = __dadd_rn(l, (double)__ldcg(a.md_losses[d] + e));
+    } else {
+      const int64_t block = cnt > 0 ? udiv(cnt + gridDim.x - 1, gridDim.x) : 1;
+      const int64_t rows = cnt > 0 ? udiv(cnt + block - 1, block) : 0;
+      for (int64_t r = 0; r < rows; ++r) l = __dadd_rn(l, __ldcg(a.md_loss_part[d] + r));
+    }
+  }
+  const double v = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(l, (double)a.n) : l;
+  for (int d = 0; d < a.md_n; ++d) a.md_epoch_loss[d][ep] = v;
+}
+
 template <bool EXACT>
 __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
   Smem s = carve_smem(tlb_smem);
@@ -231,6 +362,15 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
       }
     }
     mark(s, 10);
+    if (a.md_n > 1) {  // in-process multi-GPU: the reduction spans every device (see md_reduce_slice)
+      const int64_t mg = group_size_k(a, ks);
+      md_sync(a, target);
+      md_reduce_slice<EXACT>(s, a, mg);
+      if (a.dp_rank == a.md_n - 1 && blockIdx.x == G - 1) md_reduce_loss<EXACT>(s, a, mg, ks, ep);
+      __syncthreads();
+      md_sync(a, target);
+      continue;
+    }
     grid_sync(a.barrier, target);
     mark(s, 11);
 
@@ -709,6 +849,12 @@ cudaError_t train_occupancy(bool exact, int threads, int* occ) {
 
 // 256-thread CTAs (two per SM: the stages loop over their lanes) or 512 (one per SM).
 cudaError_t launch_train(bool exact, const TrainArgs& a, int grid, int threads, cudaStream_t st) {
+  if (a.md_n > 1) {  // multi-GPU: the devices' kernels meet at md_bar (zeroed by the host beforehand);
+    // plain launches, grids sized by the host so every device's CTAs are co-resident (bounded waits)
+    if (exact) train_kernel<true><<<grid, threads, kSmemExactBytes, st>>>(a);
+    else train_kernel<false><<<grid, threads, kSmemFastBytes, st>>>(a);
+    return cudaGetLastError();
+  }
   cudaError_t e = cudaMemsetAsync(a.barrier, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return e;
   void* args[] = {const_cast<TrainArgs*>(&a)};

@@ -126,13 +126,25 @@ def wide_make_set(n: int, seed: int):
 class Context:
     """One device context of the CUDA library (tlb_ctx)."""
 
-    def __init__(self, device: int = 0, mode: str = "exact"):
+    def __init__(self, device: int = 0, mode: str = "exact", devices=None):
+        """devices: several local GPUs in one context (tlb_ctx_create_multi) -- train() then splits every SGD
+        group over them (EXACT: bit-identical to one device); `device` is ignored when given."""
         self._L = _lib.lib()
         h = C.c_void_p()
-        _check(self._L.tlb_ctx_create(device, C.byref(h)))
+        if devices is not None:
+            devs = np.ascontiguousarray(list(devices), np.int32)
+            _check(self._L.tlb_ctx_create_multi(devs.ctypes.data, len(devs), C.byref(h)))
+            device = int(devs[0])
+        else:
+            _check(self._L.tlb_ctx_create(device, C.byref(h)))
         self._h = h
         self.device = device
         self.mode = mode
+
+    def device_count(self) -> int:
+        n = C.c_int()
+        _check(self._L.tlb_ctx_device_count(self._h, C.byref(n)))
+        return n.value
 
     def close(self) -> None:
         if getattr(self, "_h", None):

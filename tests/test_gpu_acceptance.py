@@ -14,10 +14,16 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.skipif(not os.path.exists(EXE), reason="acceptance_b200 not built (needs /root/reference at build time)")
-def test_reference_acceptance_gate_on_b200():
+@pytest.mark.parametrize("devices", [None, "0,0"])
+def test_reference_acceptance_gate_on_b200(devices):
+    """devices: TLOOM_B200_DEVICES -- the same gate through a multi-device context (net::train splits every
+    group over the listed devices)."""
     env = dict(os.environ, LD_LIBRARY_PATH=os.path.join(ROOT, "paper_1912_05234_b200", "lib"))
+    if devices:
+        env["TLOOM_B200_DEVICES"] = devices
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    log_path = os.path.join(ROOT, "gpurun_out", "acceptance_b200.log")
+    log_path = os.path.join(ROOT, "gpurun_out", "acceptance_b200%s.log" % ("_devices_" + devices.replace(",", "_")
+                                                                            if devices else ""))
     # line-buffered straight into the log, so a stuck step is visible even when the timeout fires
     with open(log_path, "w") as f:
         try:

@@ -85,17 +85,22 @@ def test_cli_format_errors_exit_3(tmp_path, corpus):
 
 @pytest.mark.gpu
 @needs_tools
-def test_cli_train_checkpoint_eval_vs_reference(tmp_path, corpus):
+@pytest.mark.parametrize("devices", [None, "0,0", "0,0,0,0"])
+def test_cli_train_checkpoint_eval_vs_reference(tmp_path, corpus, devices):
     """EXACT mode: the CLI's trained weights (TLM1 checkpoint) equal the reference library's own training
     run bit for bit, the reference's load_params reads the file, and train/eval report the reference's
-    accuracy."""
+    accuracy -- on one device and through tloom::net::train over a multi-device context
+    (TLOOM_B200_DEVICES: every group split over the devices, reduced across them every step)."""
     if not os.path.exists(REF_SO):
         pytest.skip("reference library not built")
     from oracle import Reference
     ref = Reference()
     ck = tmp_path / "w.tlm"
+    env = dict(os.environ)
+    if devices:
+        env["TLOOM_B200_DEVICES"] = devices
     r = run([CLI, "train", "--epochs", "2", "--batch", "50", "--limit-train", "600", "--limit-test", "300",
-             "--checkpoint", str(ck)] + files(corpus))
+             "--checkpoint", str(ck)] + files(corpus), env=env)
     assert r.returncode == 0, r.stderr
     out = dict(line.split() for line in r.stdout.strip().splitlines())
     tr_x, tr_y = ref.load_set(str(corpus / "train-images-idx3-ubyte"), str(corpus / "train-labels-idx1-ubyte"), 600)
