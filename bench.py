@@ -19,6 +19,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -493,6 +494,11 @@ def run_ours(args):
                          "call_ms": {"median": 1e3 * sorted(times)[len(times) // 2], "min": 1e3 * min(times),
                                      "max": 1e3 * max(times)}}
         result["gpu_launches"] += e2e_launches
+        if not dp:
+            cpp = cpp_e2e(args, n_total, B)
+            if cpp is not None:
+                result["e2e_cpp"] = cpp
+                result["gpu_launches"] += args.steps
 
     if not args.no_cpu_baseline:
         if rank == 0:  # the reference's net::train on this box's host cores, a bounded sample
@@ -511,6 +517,25 @@ def run_ours(args):
     ctx.close()
     if dp:
         dist.destroy_process_group()
+
+
+def cpp_e2e(args, n, batch):
+    """The same epoch through the C++ drop-in (tloom::net::train on a host MnistSet in pageable memory, as the
+    reference's callers hold it), timed by tools/e2e_bench.cpp in its own process: wall clock per call,
+    dataset H2D and parameters D2H inside every call."""
+    exe = os.path.join(ROOT, "paper_1912_05234_b200", "bin", "tloom-e2e-bench")
+    if not os.path.exists(exe):
+        return None
+    cmd = [exe, "--n", str(n), "--batch", str(batch), "--steps", str(args.steps), "--warmup", str(args.warmup),
+           "--mode", args.mode]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        rec = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # reported, never fatal to the bench line
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+    return {"value": rec["images_per_s"], "unit": "images/s", "h2d_bytes_per_step": rec["h2d_bytes_per_step"],
+            "d2h_bytes_per_step": rec["d2h_bytes_per_step"], "api": rec["api"], "call_ms": rec["call_ms"],
+            "epoch_loss": rec["epoch_loss"]}
 
 
 def measured_ffma_peak():

@@ -110,7 +110,8 @@ def build_variant(tag: str, defines: list[str]) -> str:
     return vlib
 
 
-TOOLS = {"tensorloom": "tools/tensorloom_cli.cpp", "tensorloom-datagen": "tools/datagen.cpp"}
+TOOLS = {"tensorloom": "tools/tensorloom_cli.cpp", "tensorloom-datagen": "tools/datagen.cpp",
+         "tloom-e2e-bench": "tools/e2e_bench.cpp"}
 BINDIR = os.path.join(PKG, "bin")
 
 

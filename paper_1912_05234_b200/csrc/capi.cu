@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "tlb_capi_internal.h"
@@ -122,6 +123,10 @@ struct tlb_ctx {
   // [1] a fixed-point gradient sum was out of range.  Read and cleared by tlb_train / tlb_synchronize.
   DevBuf dev_err;
   HostBuf pin;       // tlb_train: pinned params / losses / watchdog words
+  // Pageable sources (e.g. a C++ MnistSet's std::vector): host worker threads copy each chunk into a
+  // pinned bounce slot, the slot's DMA + ready flag follow on the copy stream (see ingest_pageable).
+  HostBuf bounce;
+  std::vector<cudaEvent_t> bounce_ev;
   unsigned int ready_token = 0;
   DevBuf synth_snaps;  // device synthetic corpus: mt19937_64 state snapshots per segment
   // Widened-network workspaces (capacity `wide_cap` images) and the last group's arguments.
@@ -357,6 +362,99 @@ int ingest_images(tlb_ctx* c, const HostImages& host, float* dev, int64_t n, int
   return TLB_OK;
 }
 
+// Pageable source (the memory a C++ caller's MnistSet lives in): the driver would stage a pageable
+// cudaMemcpyAsync synchronously through its own bounce buffers, one chunk at a time, ahead of the
+// kernel.  Instead W host threads copy the chunks into pinned bounce slots (worker w takes chunks
+// k = w, w + W, ... into its own ring of kBounceRing slots) and each slot's DMA + ready flag follow on
+// the copy stream, so the host copies, the DMA and the running train kernel overlap.  A slot is reused
+// once its previous DMA completed (event).  Called after the kernel launch, like the pinned path.
+constexpr int kBounceRing = 2;
+struct PageablePlan {
+  std::vector<int64_t> lo_of;  // chunk k covers images [lo_of[k], lo_of[k + 1])
+  size_t elem = 0, slot = 0;
+  int workers = 1;
+};
+// The chunk plan (the same ramp the kernel's ready flags follow), the slot size and the worker count;
+// allocates the bounce slots and their events.  Runs BEFORE the kernel launch: growing pinned memory
+// (cudaFreeHost) synchronises the device, which would deadlock against a kernel waiting for the chunks.
+int plan_pageable(tlb_ctx* c, bool u8, int64_t n, int64_t chunk, int64_t batch, PageablePlan* pl) {
+  pl->elem = u8 ? 784 : 784 * sizeof(float);
+  pl->lo_of.clear();
+  for (int64_t k = 0, lo = 0; lo < n; ++k) {
+    pl->lo_of.push_back(lo);
+    const int64_t hi = chunk > 0 ? lo + chunk
+                       : chunk < 0 ? ramp_chunk_start(k + 1, -chunk) * batch : geo_chunk_start(k + 1) * batch;
+    lo = std::min(hi, n);
+  }
+  pl->lo_of.push_back(n);
+  const int64_t nk = (int64_t)pl->lo_of.size() - 1;
+  size_t slot = 0;
+  for (int64_t k = 0; k < nk; ++k) slot = std::max(slot, (size_t)(pl->lo_of[k + 1] - pl->lo_of[k]) * pl->elem);
+  pl->slot = (slot + 4095) / 4096 * 4096;
+  // host copy threads: 4 measured best on the GPU VMs (1: 4.6, 2: 5.7, 4: 6.0, 8: 4.4 M img/s through
+  // tloom::net::train at batch 100; profiles/r2/cpp_e2e_threads_r2i.txt); TLB_INGEST_THREADS overrides
+  static const int env_w = [] {
+    const char* e = std::getenv("TLB_INGEST_THREADS");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  pl->workers = (int)std::max<int64_t>(1, std::min<int64_t>(nk, env_w ? env_w : std::min(4, std::max(1, hw / 2))));
+  TLB_CUDA(c->bounce.ensure((size_t)pl->workers * kBounceRing * pl->slot));
+  while (c->bounce_ev.size() < (size_t)pl->workers * kBounceRing) {
+    cudaEvent_t ev;
+    TLB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    c->bounce_ev.push_back(ev);
+  }
+  return TLB_OK;
+}
+
+int ingest_pageable(tlb_ctx* c, const HostImages& host, float* dev, const PageablePlan& pl, unsigned int token) {
+  TLB_CUDA(cudaStreamWaitEvent(c->copy_stream, c->copy_gate, 0));  // recorded by the caller
+  const std::vector<int64_t>& lo_of = pl.lo_of;
+  const int64_t nk = (int64_t)lo_of.size() - 1;
+  const size_t elem = pl.elem, slot = pl.slot;
+  const int W = pl.workers;
+  unsigned int* flags = static_cast<unsigned int*>(c->ready.p);
+  uint8_t* const base = static_cast<uint8_t*>(c->bounce.p);
+  const uint8_t* const src = host.u8 ? host.u8 : reinterpret_cast<const uint8_t*>(host.f32);
+  uint8_t* const dst = host.u8 ? host.d_u8 : reinterpret_cast<uint8_t*>(dev);
+  std::vector<int> status(W, TLB_OK);
+  std::vector<std::string> why(W);
+  auto worker = [&](int w) {
+    cudaSetDevice(c->device);
+    for (int64_t k = w, j = 0; k < nk; k += W, ++j) {
+      const int s = w * kBounceRing + (int)(j % kBounceRing);
+      uint8_t* b = base + (size_t)s * slot;
+      cudaError_t e = j >= kBounceRing ? cudaEventSynchronize(c->bounce_ev[s]) : cudaSuccess;
+      const size_t off = (size_t)lo_of[k] * elem, bytes = (size_t)(lo_of[k + 1] - lo_of[k]) * elem;
+      if (e == cudaSuccess) {
+        std::memcpy(b, src + off, bytes);
+        e = cudaMemcpyAsync(dst + off, b, bytes, cudaMemcpyHostToDevice, c->copy_stream);
+      }
+      if (e == cudaSuccess) e = cudaEventRecord(c->bounce_ev[s], c->copy_stream);
+      if (e != cudaSuccess) {
+        status[w] = TLB_ERR_CUDA;
+        why[w] = std::string("pageable ingestion: ") + cudaGetErrorString(e);
+        return;  // the kernel's ready-flag watchdog fails the call
+      }
+      const CUresult r = write_value32()(reinterpret_cast<CUstream>(c->copy_stream),
+                                         reinterpret_cast<CUdeviceptr>(flags + k), token, CU_STREAM_WRITE_VALUE_DEFAULT);
+      if (r != CUDA_SUCCESS) {
+        status[w] = TLB_ERR_CUDA;
+        why[w] = "cuStreamWriteValue32 failed: " + std::to_string((int)r);
+        return;
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int w = 1; w < W; ++w) pool.emplace_back(worker, w);
+  worker(0);
+  for (auto& t : pool) t.join();
+  for (int w = 0; w < W; ++w)
+    if (status[w] != TLB_OK) return fail(status[w], why[w]);
+  return TLB_OK;
+}
+
 // Number of ingestion chunks for n images (see ingest_images).
 int64_t ingest_chunks(int64_t n, int64_t chunk, int64_t batch) {
   if (chunk > 0) return (n + chunk - 1) / chunk;
@@ -582,6 +680,8 @@ int tlb_ctx_destroy(tlb_ctx* c) {
   c->ready_err.release();
   c->dev_err.release();
   c->pin.release();
+  c->bounce.release();
+  for (cudaEvent_t ev : c->bounce_ev) cudaEventDestroy(ev);
   for (auto& w : c->wide) w.release();
   c->synth_snaps.release();
   if (c->copy_gate) cudaEventDestroy(c->copy_gate);
@@ -962,23 +1062,35 @@ static int train_host(tlb_ctx* c, HostImages src, const int32_t* labels, int64_t
   std::memcpy(h_p, params, TLB_NPARAM * sizeof(float));
   TLB_CUDA(cudaMemcpyAsync(d_p, h_p, TLB_NPARAM * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   TLB_TRY(stage_out(c, 3, (size_t)epochs, &d_loss));
-  // Pinned source: launch the kernel first, then enqueue the chunk copies (the host's ~200 enqueue calls
-  // overlap the running kernel, which polls the ready flags).  Pageable source: copies first -- the
-  // driver stages pageable memory synchronously on the host.
+  // Launch the kernel first, then enqueue the chunk copies (the host's enqueue calls overlap the running
+  // kernel, which polls the ready flags): pinned sources DMA straight from the caller's memory, pageable
+  // ones through the pinned bounce slots filled by host worker threads (ingest_pageable).
+  // TLB_PAGEABLE_COPIES_FIRST=1 restores the earlier pageable policy (copies enqueued before the kernel).
   ht.mark("staged");
-  const bool copies_first = overlap && !is_pinned(images);
+  static const bool pageable_first = [] {
+    const char* e = std::getenv("TLB_PAGEABLE_COPIES_FIRST");
+    return e && std::atoi(e) == 1;
+  }();
+  const bool pageable = overlap && !is_pinned(images);
+  const bool copies_first = pageable && pageable_first;
+  PageablePlan plan;
+  if (pageable && !copies_first) TLB_TRY(plan_pageable(c, src.u8 != nullptr, n, chunk, batch, &plan));
+  auto ingest = [&]() {
+    return pageable && !copies_first ? ingest_pageable(c, src, d_img, plan, c->ready_token)
+                                     : ingest_images(c, src, d_img, n, chunk, batch, c->ready_token);
+  };
   if (copies_first) TLB_TRY(ingest_images(c, src, d_img, n, chunk, batch, c->ready_token));
   if (!on_epoch) {
     TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, 0, epochs, batch, d_loss, 0, 0, -1, nullptr, nullptr,
                           rdy, c->ready_token, chunk, nullptr, src.d_u8));
     ht.mark("launched");
-    if (overlap && !copies_first) TLB_TRY(ingest_images(c, src, d_img, n, chunk, batch, c->ready_token));
+    if (overlap && !copies_first) TLB_TRY(ingest());
     ht.mark("ingest_enqueued");
   } else {
     for (int32_t e = 0; e < epochs; ++e) {
       TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, e, 1, batch, d_loss, 0, 0, -1, nullptr, nullptr,
                             e == 0 ? rdy : nullptr, c->ready_token, chunk, nullptr, src.d_u8));
-      if (e == 0 && overlap && !copies_first) TLB_TRY(ingest_images(c, src, d_img, n, chunk, batch, c->ready_token));
+      if (e == 0 && overlap && !copies_first) TLB_TRY(ingest());
       double mean = 0.0;
       TLB_TRY(fetch(c, &mean, d_loss + e, 1));
       on_epoch(e + 1, mean, user);

@@ -378,15 +378,19 @@ def test_overlapped_ingestion_equals_resident_data(orc, zhang_sets, mode):
     check(orc, tr_x, tr_y, mode)
 
 
-@pytest.mark.parametrize("policy", ["0", "37", "200", "streams2"])
+@pytest.mark.parametrize("policy", ["0", "37", "200", "streams2", "threads1", "threads3", "pageable_first"])
 def test_overlapped_ingestion_chunk_policies(policy):
     """The same check under the other chunk policies (TLB_INGEST_CHUNK: 0 = geometric group chunks,
     N = fixed chunks of N images, not group-aligned; 200 = the former 2-group default; streams2 = the ramp
-    over two copy streams), both modes, in a fresh process."""
+    over two copy streams), the pageable bounce-slot path with 1 and 3 host copy threads (every slot reused
+    several times), and the former copies-first policy for pageable sources, both modes, in a fresh process."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, **({"TLB_INGEST_STREAMS": "2"} if policy == "streams2" else {"TLB_INGEST_CHUNK": policy}))
+    extra = {"streams2": {"TLB_INGEST_STREAMS": "2"}, "threads1": {"TLB_INGEST_THREADS": "1"},
+             "threads3": {"TLB_INGEST_THREADS": "3", "TLB_INGEST_CHUNK": "150"},
+             "pageable_first": {"TLB_PAGEABLE_COPIES_FIRST": "1"}}.get(policy, {"TLB_INGEST_CHUNK": policy})
+    env = dict(os.environ, **extra)
     out = subprocess.run([sys.executable, os.path.join(root, "tests", "_ingest_check.py")], cwd=root, env=env,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
