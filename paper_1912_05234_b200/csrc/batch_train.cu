@@ -232,12 +232,18 @@ __device__ __forceinline__ void fc_item(const float* P, float* regs, const int* 
 // BackinBox (nn.cpp:169-189): u <= pA for row pA, u >= pB - 7 for row pB (6-7 rows per lane for every pp;
 // the column bounds are compile-time).  Tasks run pp-major, so a warp holds at most two pp values.  Epilogue:
 // dz1 = (d_s1 * 0.25) g1 for conv1 rows 2p, 2p+1 of both rows, columns 6ig..6ig+5 (in place of g1).
+template <bool WP>  // WP: weight rows read from P (5 floats per row) instead of the padded W2 copy (8)
 __device__ __forceinline__ void backin_acc(const float* d2i, const float* wrow, int p, int u0, int u1, float (&acc)[12]) {
 #pragma unroll 1
   for (int u = u0; u <= u1; ++u) {
     float d[8], w[5];
     load_row<8>(d2i + (4 + p - u) * 8, d);
-    load5(wrow + u * 8, w);
+    if constexpr (WP) {
+#pragma unroll
+      for (int v = 0; v < 5; ++v) w[v] = wrow[u * 5 + v];
+    } else {
+      load5(wrow + u * 8, w);
+    }
 #pragma unroll
     for (int q = 0; q < 12; ++q)
 #pragma unroll
@@ -263,6 +269,7 @@ __device__ __forceinline__ void backin_dz1(float* g1c, int p, int ig, const floa
   }
 }
 
+template <bool WP = false>  // WP: W2 is P (unpadded k2), see backin_acc
 __device__ __forceinline__ void backin_item(const float* W2, float* regs, int bi, int cnt, bool valid) {
   const int ig = bi & 3, task = valid ? bi >> 2 : 0;
   const int c = task % 6, kp = task / 6, k = kp % cnt, pp = kp / cnt;
@@ -274,10 +281,10 @@ __device__ __forceinline__ void backin_item(const float* W2, float* regs, int bi
 #pragma unroll 1
   for (int ii = 0; ii < 3; ++ii) {
     const int i = 3 * ig + ii;
-    const float* wrow = W2 + i * kW2Stride + c * 40;
+    const float* wrow = WP ? W2 + kK2 + (i * 6 + c) * 25 : W2 + i * kW2Stride + c * 40;
     const float* d2i = reg + kOffD2 + i * kD2K;
-    backin_acc(d2i, wrow, pA, 0, min(4, pA), accA);
-    backin_acc(d2i, wrow, pB, max(0, pB - 7), 4, accB);
+    backin_acc<WP>(d2i, wrow, pA, 0, min(4, pA), accA);
+    backin_acc<WP>(d2i, wrow, pB, max(0, pB - 7), 4, accB);
   }
 #pragma unroll
   for (int q = 0; q < 12; ++q) {
@@ -394,6 +401,148 @@ __device__ __forceinline__ void gk1_item(float* G, const float* imgs, const floa
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Packed-pair forward items (PAIR = true): conv1 and conv2 run on packed FP32 pairs (__ffma2_rn -> SASS
+// FFMA2, sm_100: the FP32 rate of FFMA at half the issued instructions), one operand a broadcast scalar --
+//   conv1 : pixel (broadcast) x (k1[c], k1[c+3])        -> (c1[c], c1[c+3])
+//   conv2 : s1 (broadcast) x (k2[i][c], k2[i+6][c])     -> (out[i], out[i+6])
+// with the same lane counts as the scalar items; activations keep their canonical layouts, so the backward
+// items are the scalar ones.  Fast-mode arithmetic (summation trees differ; within the 1e-4 tolerance).
+// ------------------------------------------------------------------------------------------------
+constexpr int kW1PFloats = 152, kW2PFloats = 6 * 364;
+static_assert(kW1PFloats <= kW1Floats && kW2PFloats <= kW2Floats, "pair weights fit the padded slots");
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 ld2(const float* p) { return *reinterpret_cast<const float2*>(p); }
+
+// Pair weights from P (once per step, all threads): W1p[ip][t] = (k1[ip][t], k1[ip+3][t]) (ip < 3);
+// W2p[ip][c][ky][kx] = (k2[ip][c][ky][kx], k2[ip+6][c][ky][kx]) (ip < 6; kx = 5 is a zero pad pair).
+__device__ __forceinline__ void build_pair_weights(const float* P, float* W1p, float* W2p, int t, int T) {
+  for (int q = t; q < 75 + 6 * 180; q += T) {
+    if (q < 75) {
+      const int ip = q / 25, tp = q - ip * 25;
+      *reinterpret_cast<float2*>(W1p + 2 * q) = make_float2(P[kK1 + ip * 25 + tp], P[kK1 + (ip + 3) * 25 + tp]);
+    } else {
+      const int q2 = q - 75, ip = q2 / 180, r = q2 - ip * 180, c = r / 30, r2 = r - c * 30, ky = r2 / 6, kx = r2 - ky * 6;
+      const float2 v = kx < 5 ? make_float2(P[kK2 + (ip * 6 + c) * 25 + ky * 5 + kx], P[kK2 + ((ip + 6) * 6 + c) * 25 + ky * 5 + kx])
+                              : make_float2(0.0f, 0.0f);
+      *reinterpret_cast<float2*>(W2p + ip * 364 + c * 60 + ky * 12 + 2 * kx) = v;
+    }
+  }
+}
+
+// S1 pair lane (image k, pooled row py, 6-column strip xs, channel pair ip), ip fastest (the three pair lanes
+// of a (py, xs) read the same image rows): conv rows 2py, 2py+1 x 6 columns x channels (ip, ip+3) = 12 FFMA2
+// accumulators over the 25 taps (300 FFMA2), logistic, g1 = c1(1-c1), 2x2 pool -> s1 (canonical layouts).
+__device__ __forceinline__ void conv1_item_p(const float* P, const float* W1p, const float* imgs, float* regs, int it) {
+  const int k = it / 144, r = it - k * 144;
+  const int ip = r % 3, pos = r / 3, xs = pos & 3, py = pos >> 2;
+  const int y0 = 2 * py, x0 = 6 * xs;
+  const float* img = imgs + k * kImg;
+  float2 a[2][6];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int o = 0; o < 6; ++o) a[q][o] = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int rr = 0; rr < 6; ++rr) {  // image row y0 + rr feeds conv row q with ky = rr - q
+    float in[10];
+#pragma unroll
+    for (int h = 0; h < 5; ++h) {
+      const float2 v = ld2(img + (y0 + rr) * 28 + x0 + 2 * h);
+      in[2 * h] = v.x;
+      in[2 * h + 1] = v.y;
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int ky = rr - q;
+      if (ky < 0 || ky > 4) continue;
+#pragma unroll
+      for (int kx = 0; kx < 5; ++kx) {
+        const float2 w = ld2(W1p + 2 * (ip * 25 + ky * 5 + kx));
+#pragma unroll
+        for (int o = 0; o < 6; ++o) a[q][o] = __ffma2_rn(bc2(in[o + kx]), w, a[q][o]);
+      }
+    }
+  }
+  const float nb[2] = {neg_log2e_times(P[kB1 + ip]), neg_log2e_times(P[kB1 + ip + 3])};
+  float* reg = regs + k * kImgRegion;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // channel ip + 3h
+    const int i = ip + 3 * h;
+    float t[2][6];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int o = 0; o < 6; ++o) t[q][o] = logistic(h ? a[q][o].y : a[q][o].x, nb[h]);
+      float* g1 = reg + i * kG1Plane + (y0 + q) * 24 + x0;
+#pragma unroll
+      for (int o2 = 0; o2 < 3; ++o2)
+        *reinterpret_cast<float2*>(g1 + 2 * o2) =
+            make_float2(t[q][2 * o2] * (1.0f - t[q][2 * o2]), t[q][2 * o2 + 1] * (1.0f - t[q][2 * o2 + 1]));
+    }
+    float* s1 = reg + kOffS1 + (i * 12 + py) * 12 + 3 * xs;
+#pragma unroll
+    for (int px = 0; px < 3; ++px)  // avgpool (nn.cpp:144): ((p00 + p01) + p10) + p11, then * 0.25f
+      s1[px] = (((t[0][2 * px] + t[0][2 * px + 1]) + t[1][2 * px]) + t[1][2 * px + 1]) * 0.25f;
+  }
+}
+
+// S2 pair lane (image k, pooled row py, kernel pair ip, conv row r of the pooling window, channel half h), h
+// fastest: conv row y = 2py + r x 8 columns x kernels (ip, ip+6) over channels 3h..3h+2 -- the s1 value is
+// the broadcast operand, (k2[ip][c], k2[ip+6][c]) the weight pair (600 FFMA2) -- the halves joined by a
+// shuffle (lane ^ 1); lane h finishes kernel ip + 6h: logistic, g2 into the padded dz2 row, and the 2x2
+// pool with the partner row (lane ^ 2).  W2p: [ip][c][ky][6] float2 in 364-float kernel-pair rows.
+constexpr int kW2PRow = 364;
+__device__ __forceinline__ void conv2_item_kp(const float* P, const float* W2p, float* regs, int it) {
+  const int h = it & 1, r = (it >> 1) & 1, rest = it >> 2;
+  const int ip = rest % 6, kp = rest / 6, py = kp & 3, k = kp >> 2;
+  const int y = 2 * py + r;
+  float* reg = regs + k * kImgRegion;
+  const float* s1 = reg + kOffS1;
+  float2 acc[8];
+#pragma unroll
+  for (int o = 0; o < 8; ++o) acc[o] = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+  for (int c = 3 * h; c < 3 * h + 3; ++c) {
+    const float* wc = W2p + ip * kW2PRow + c * 60;
+#pragma unroll
+    for (int ky = 0; ky < 5; ++ky) {
+      float in[12];
+      load_row<12>(s1 + (c * 12 + y + ky) * 12, in);
+      const float4* wr = reinterpret_cast<const float4*>(wc + ky * 12);
+      const float4 w01 = wr[0], w23 = wr[1], w4 = wr[2];
+      const float2 wv[5] = {make_float2(w01.x, w01.y), make_float2(w01.z, w01.w), make_float2(w23.x, w23.y),
+                            make_float2(w23.z, w23.w), make_float2(w4.x, w4.y)};
+#pragma unroll
+      for (int kx = 0; kx < 5; ++kx)
+#pragma unroll
+        for (int o = 0; o < 8; ++o) acc[o] = __ffma2_rn(bc2(in[o + kx]), wv[kx], acc[o]);
+    }
+  }
+  float t[8], u[8];
+  const int i = ip + 6 * h;
+  const float nb = neg_log2e_times(P[kB2 + i]);
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+    const float ox = acc[o].x + __shfl_xor_sync(0xffffffffu, acc[o].x, 1);
+    const float oy = acc[o].y + __shfl_xor_sync(0xffffffffu, acc[o].y, 1);
+    t[o] = logistic(h ? oy : ox, nb);
+  }
+  float* g2 = reg + kOffD2 + i * kD2K + (4 + y) * 8;
+  reinterpret_cast<float4*>(g2)[0] =
+      make_float4(t[0] * (1.0f - t[0]), t[1] * (1.0f - t[1]), t[2] * (1.0f - t[2]), t[3] * (1.0f - t[3]));
+  reinterpret_cast<float4*>(g2)[1] =
+      make_float4(t[4] * (1.0f - t[4]), t[5] * (1.0f - t[5]), t[6] * (1.0f - t[6]), t[7] * (1.0f - t[7]));
+#pragma unroll
+  for (int o = 0; o < 8; ++o) u[o] = __shfl_xor_sync(0xffffffffu, t[o], 2);  // conv row y ^ 1
+  if (r == 0) {  // avgpool (nn.cpp:144): ((p00 + p01) + p10) + p11, then * 0.25f
+    float pv[4];
+#pragma unroll
+    for (int px = 0; px < 4; ++px) pv[px] = (((t[2 * px] + t[2 * px + 1]) + u[2 * px]) + u[2 * px + 1]) * 0.25f;
+    *reinterpret_cast<float4*>(reg + kOffS2 + (i * 4 + py) * 4) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+  }
+}
+
 // Rounds of one CTA: (step, first local example, end of the CTA's chunk).
 struct Round {
   int64_t step, e, hi;
@@ -449,7 +598,7 @@ __device__ __forceinline__ void issue_round(const TrainArgs& a, float* ring, uin
   tma_load_1d(ring + buf * NI * kImg, a.images + first * kImg, (uint32_t)(cnt * kImg * sizeof(float)), &bar[buf]);
 }
 
-template <int NI, int T, int MINB>
+template <int NI, int T, int MINB, bool PAIR>
 __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
   static_assert(T % 32 == 0, "stage loops run whole warps");
   using L = Layout<NI>;
@@ -503,14 +652,18 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
       for (int q = t; q < kPStride; q += T) G[q] = 0.0f;
     }
     __syncthreads();
-    for (int q = t; q < kW1Floats + kW2Floats; q += T) {
-      if (q < kW1Floats) {
-        const int i = q / kW1Stride, rr = q - i * kW1Stride, ky = rr >> 3, kx = rr & 7;
-        W1[q] = (ky < 5 && kx < 5) ? P[kK1 + i * 25 + ky * 5 + kx] : 0.0f;
-      } else {
-        const int q2 = q - kW1Floats, i = q2 / kW2Stride, rr = q2 - i * kW2Stride, c = rr / 40, r2 = rr - c * 40;
-        const int ky = r2 >> 3, kx = r2 & 7;
-        W2[q2] = (c < 6 && kx < 5) ? P[kK2 + (i * 6 + c) * 25 + ky * 5 + kx] : 0.0f;
+    if constexpr (PAIR) {
+      build_pair_weights(P, W1, W2, t, T);
+    } else {
+      for (int q = t; q < kW1Floats + kW2Floats; q += T) {
+        if (q < kW1Floats) {
+          const int i = q / kW1Stride, rr = q - i * kW1Stride, ky = rr >> 3, kx = rr & 7;
+          W1[q] = (ky < 5 && kx < 5) ? P[kK1 + i * 25 + ky * 5 + kx] : 0.0f;
+        } else {
+          const int q2 = q - kW1Floats, i = q2 / kW2Stride, rr = q2 - i * kW2Stride, c = rr / 40, r2 = rr - c * 40;
+          const int ky = r2 >> 3, kx = r2 & 7;
+          W2[q2] = (c < 6 && kx < 5) ? P[kK2 + (i * 6 + c) * 25 + ky * 5 + kx] : 0.0f;
+        }
       }
     }
     __syncthreads();
@@ -536,10 +689,16 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
       const float* imgs = ring + buf * NI * kImg;
       const int* rl = lab + buf * NI;
       // S1
-      for (int it = t; it < cnt * 144; it += T) conv1_item(P, W1, imgs, regs, it);
+      for (int it = t; it < cnt * 144; it += T) {
+        if constexpr (PAIR) conv1_item_p(P, W1, imgs, regs, it);
+        else conv1_item(P, W1, imgs, regs, it);
+      }
       __syncthreads();
       // S2 (cnt * 192 lanes: whole warps)
-      for (int it = t; it < cnt * 192; it += T) conv2_item(P, W2, regs, it);
+      for (int it = t; it < cnt * (PAIR ? 96 : 192); it += T) {  // pair items: 96 lanes per image
+        if constexpr (PAIR) conv2_item_kp(P, W2, regs, it);
+        else conv2_item(P, W2, regs, it);
+      }
       __syncthreads();
       // S3
       {
@@ -591,7 +750,8 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
         const int nbi = (cnt * 144 + 31) / 32 * 32, n2 = nbi + 768, nfc = n2 + 1930;
         for (int it = t; it < nfc; it += T) {
           if (it < nbi) {
-            backin_item(W2, regs, it, cnt, it < cnt * 144);
+            if constexpr (PAIR) backin_item<true>(P, regs, it, cnt, it < cnt * 144);
+            else backin_item(W2, regs, it, cnt, it < cnt * 144);
           } else if (it < n2) {
             gk2_item(G, regs, it - nbi, cnt);
           } else if (it < n2 + 1920) {
@@ -678,18 +838,18 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
   }
 }
 
-template <int NI, int T, int MINB>
+template <int NI, int T, int MINB, bool PAIR>
 cudaError_t prep(int* occ) {
-  auto kern = train_batch_kernel<NI, T, MINB>;
+  auto kern = train_batch_kernel<NI, T, MINB, PAIR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Layout<NI>::kBytes);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, T, Layout<NI>::kBytes);
 }
 
-template <int NI, int T, int MINB>
+template <int NI, int T, int MINB, bool PAIR>
 cudaError_t launch_cfg(const TrainArgs& a, int sm_count, int64_t m_max, cudaStream_t st, int* grid_out) {
   int occ = 0;
-  cudaError_t e = prep<NI, T, MINB>(&occ);
+  cudaError_t e = prep<NI, T, MINB, PAIR>(&occ);
   if (e != cudaSuccess) return e;
   const int64_t cap = (int64_t)std::max(occ, 1) * sm_count;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cap, (m_max + NI - 1) / NI));
@@ -700,36 +860,42 @@ cudaError_t launch_cfg(const TrainArgs& a, int sm_count, int64_t m_max, cudaStre
   e = cudaMemsetAsync(a.barrier, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return e;
   void* args[] = {const_cast<TrainArgs*>(&a)};
-  return cudaLaunchCooperativeKernel((const void*)train_batch_kernel<NI, T, MINB>, dim3(grid), dim3(T), args,
+  return cudaLaunchCooperativeKernel((const void*)train_batch_kernel<NI, T, MINB, PAIR>, dim3(grid), dim3(T), args,
                                      Layout<NI>::kBytes, st);
 }
 
-// TLB_BATCH_CFG = "NIxTHREADSxMINB" picks a measured alternative (A/B); default below.
+// TLB_BATCH_CFG = "[p]NIxTHREADSxMINB" picks a measured alternative (A/B); default below:
+// the packed-pair forward with 4 images per 512-thread CTA (one per SM) for groups of < 8k images per GPU
+// (1k: 17.0 -> 20.3 M img/s), 2 images per 320-thread CTA (two per SM) above (16k: 23.3 -> 25.0, 256k:
+// 24.2 -> 25.9 M img/s; profiles/r2/pair_time_p3.jsonl).
 template <typename F>
-cudaError_t dispatch(F&& f) {
+cudaError_t dispatch(F&& f, int64_t m_max) {
   static const char* cfg = std::getenv("TLB_BATCH_CFG");
   const auto is = [](const char* want) { return cfg && !std::strcmp(cfg, want); };
+  if (is("p2x384x2")) return f.template operator()<2, 384, 2, true>();
+  if (is("p2x256x2")) return f.template operator()<2, 256, 2, true>();
+  if (is("p2x288x2")) return f.template operator()<2, 288, 2, true>();
+  if (is("2x384x2")) return f.template operator()<2, 384, 2>();
   if (is("2x512x1")) return f.template operator()<2, 512, 1>();
-  if (is("3x384x1")) return f.template operator()<3, 384, 1>();
   if (is("4x512x1")) return f.template operator()<4, 512, 1>();
-  if (is("4x768x1")) return f.template operator()<4, 768, 1>();
-  return f.template operator()<2, 384, 2>();
+  if (is("p4x512x1") || (!cfg && m_max < 8192)) return f.template operator()<4, 512, 1, true>();
+  return f.template operator()<2, 320, 2, true>();
 }
 
 struct GridQuery {
   int sm;
   int64_t m;
   int* g;
-  template <int NI, int T, int MINB>
-  cudaError_t operator()() { return launch_cfg<NI, T, MINB>(TrainArgs{}, sm, m, nullptr, g); }
+  template <int NI, int T, int MINB, bool PAIR = false>
+  cudaError_t operator()() { return launch_cfg<NI, T, MINB, PAIR>(TrainArgs{}, sm, m, nullptr, g); }
 };
 struct Launcher {
   const TrainArgs& a;
   int sm;
   int64_t m;
   cudaStream_t st;
-  template <int NI, int T, int MINB>
-  cudaError_t operator()() { return launch_cfg<NI, T, MINB>(a, sm, m, st, nullptr); }
+  template <int NI, int T, int MINB, bool PAIR = false>
+  cudaError_t operator()() { return launch_cfg<NI, T, MINB, PAIR>(a, sm, m, st, nullptr); }
 };
 
 }  // namespace bt
@@ -738,13 +904,13 @@ struct Launcher {
 int batch_train_grid(int sm_count, int64_t m_max) {
   int grid = 0;
   bt::GridQuery q{sm_count, m_max, &grid};
-  if (bt::dispatch(q) != cudaSuccess) return 0;
+  if (bt::dispatch(q, m_max) != cudaSuccess) return 0;
   return grid;
 }
 
 cudaError_t launch_train_batch(const TrainArgs& a, int sm_count, int64_t m_max, cudaStream_t st) {
   bt::Launcher l{a, sm_count, m_max, st};
-  return bt::dispatch(l);
+  return bt::dispatch(l, m_max);
 }
 
 }  // namespace tlb

@@ -17,7 +17,8 @@ using namespace tlb;
 
 enum Stage { kConv1, kConv2V0, kConv2V1, kFc, kFcBack, kC2BackV0, kC2BackV1, kC2BackV2, kC2BackV3, kC1Back, kForward,
              kBackwardV0, kBackwardV1, kBackinV4, kBackinV5, kC1BackGk2, kBackwardV4, kBackwardV5, kC2BackV6, kC2BackV7, kBackwardV6, kBackwardV7, kC2BackV8, kBackwardV8,
-             kBackinV9, kBackwardV9, kC2BackV10, kBackwardV10, kBackwardV11, kBackwardV12, kBackwardV13, kConv2V2, kBackwardV14, kNumStages };
+             kBackinV9, kBackwardV9, kC2BackV10, kBackwardV10, kBackwardV11, kBackwardV12, kBackwardV13, kConv2V2, kBackwardV14,
+             kBackwardProduct, kC2BackProduct, kC1BackProduct, kNumStages };
 static const char* kNames[kNumStages] = {"conv1", "conv2_v0_halves", "conv2_v1_rows", "fc", "fc_back",
                                          "conv2_back_v0_quads", "conv2_back_v1_items", "conv2_back_v2_pairs", "conv2_back_v3_ws", "conv1_back",
                                          "forward_image", "backward_v0", "backward_v1",
@@ -26,7 +27,8 @@ static const char* kNames[kNumStages] = {"conv1", "conv2_v0_halves", "conv2_v1_r
                                          "backward_v6", "backward_v7", "conv2_back_v8_rows4p", "backward_v8",
                                          "backin_only_v9_rows4p", "backward_v9", "conv2_back_v10_split_gk2",
                                          "backward_v10", "backward_v11_gk160", "backward_v12_gk192",
-                                         "backward_v13_gk128", "conv2_v2_rows_p", "backward_v14_gk2rows"};
+                                         "backward_v13_gk128", "conv2_v2_rows_p", "backward_v14_gk2rows",
+                                         "backward_product", "conv2_back_product", "conv1_back_product"};
 
 __device__ __forceinline__ float hrand(unsigned int x) {  // deterministic value in [0, 1)
   x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
@@ -48,6 +50,10 @@ __device__ void fill(const Smem& s) {
     const int row = idx >> 3, k = idx & 7;
     s.Kp[idx] = k < 5 ? s.P[kK2 + row * 5 + k] : 0.0f;
   }
+#if TLB_PAIR
+  __syncthreads();
+  build_k2k(s);  // the fast product conv2 reads the k2 kernel pairs from the Kp slot
+#endif
   for (int q = t; q < 12 * 64; q += n) {
     const int i = q >> 6, y = (q >> 3) & 7, x = q & 7;
     s.dzp[dzp_at(i, y + 4, x + 4)] = (hrand(q + 70000) - 0.5f) * 0.01f;
@@ -59,6 +65,18 @@ __device__ void fill(const Smem& s) {
 template <bool EXACT, int STAGE>
 __device__ __forceinline__ void run_stage(const Smem& s, float* row) {
   constexpr bool A = !EXACT;
+  if constexpr (STAGE == kBackwardProduct) {
+    backward_image<EXACT, A>(s, s.img, row);
+    return;
+  }
+  if constexpr (STAGE == kC2BackProduct) {
+    call_conv2_back<EXACT, A>(row);
+    return;
+  }
+  if constexpr (STAGE == kC1BackProduct) {
+    call_conv1_back<EXACT, A>(s.img, row);
+    return;
+  }
   if constexpr (STAGE == kConv1) stage_conv1<EXACT>(s, s.img);
   else if constexpr (STAGE == kConv2V0) stage_conv2<EXACT, 0>(s);
   else if constexpr (STAGE == kConv2V1) stage_conv2<EXACT, 1>(s);
@@ -226,6 +244,9 @@ void all(float* rows, unsigned long long* d_cycles, int sms, int iters, double m
     measure<EXACT, kBackwardV13>(rows, d_cycles, sms, iters, mhz);
     measure<EXACT, kBackwardV14>(rows, d_cycles, sms, iters, mhz);
   }
+  measure<EXACT, kC2BackProduct>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kC1BackProduct>(rows, d_cycles, sms, iters, mhz);
+  measure<EXACT, kBackwardProduct>(rows, d_cycles, sms, iters, mhz);
 }
 
 int main(int argc, char** argv) {

@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
     mark(s, 0);
 
     // ---- phase 1: per-example forward + backward out of shared memory ----
-    load_params(s, a.params);
+    load_params<EXACT>(s, a.params);
     if constexpr (!EXACT)
       for (int i = threadIdx.x; i < kPStride; i += blockDim.x) s.G[i] = 0.0f;
     __syncthreads();
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
   if (issuer && pf_valid) issue_job(s, a, 0, pf);
   first_bytes(s, a, pf_valid, pf);
   uint32_t consumed = 0;
-  load_params(s, a.params);  // once: afterwards the parameters live in shared memory
+  load_params<false>(s, a.params);  // once: afterwards the parameters live in shared memory
 
   // group index within the epoch and epoch of step st, advanced incrementally (no per-step division)
   int64_t ks = umod(a.step_begin, a.steps_per_epoch), ep = udiv(a.step_begin, a.steps_per_epoch);
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       const bool pending = !dp && ls > 0;
       const NextBytes nb{buf ^ 1, ((consumed + 1) >> 1) & 1, a.images_wb};
       forward_image<false>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf, pending ? &xbar[2] : nullptr,
-                           (uint32_t)((ls - 1) & 1), a.dp_timeout_cycles, a.dp_error, a.pixels ? &nb : nullptr);
+                           (uint32_t)((ls - 1) & 1), a.dp_timeout_cycles, a.dp_error, a.pixels ? &nb : nullptr, ls > 0);
       if (threadIdx.x == 0) cta_loss = __dadd_rn(cta_loss, (double)example_loss(s, s.lab[buf], nullptr));
       backward_image<false, true>(s, s.img + buf * kImg, nullptr);
       ++consumed;
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1) cells_kernel(CellArgs a) {
   smem_setup(s);
   int64_t lo, hi;
   static_chunk(a.n, gridDim.x, blockIdx.x, lo, hi);
-  load_params(s, a.params);
+  load_params<EXACT>(s, a.params);
   if (threadIdx.x == 0 && lo < hi) issue_image(s, 0, a.images + lo * kImg);
   __syncthreads();
   uint32_t k = 0;
@@ -798,7 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(EvalArgs a) {
   smem_setup(s);
   int64_t lo, hi;
   static_chunk(a.n, gridDim.x, blockIdx.x, lo, hi);
-  load_params(s, a.params);
+  load_params<EXACT>(s, a.params);
   if (threadIdx.x == 0 && lo < hi) issue_image(s, 0, a.images + lo * kImg);
   __syncthreads();
   unsigned long long correct = 0;

@@ -37,6 +37,14 @@ namespace tlb {
 
 constexpr int kThreads = 512;
 // backin_rows kernel-loop unroll (A/B: 3 = the three kernels' loads can overlap, +0.7% vs 1)
+// Fast forward on packed FP32 pairs (fma.rn.f32x2 -> FFMA2; see "Packed-pair fast forward" below).
+// 0 = the scalar fast forward stages.
+#ifndef TLB_PAIR
+#define TLB_PAIR 1
+#endif
+#ifndef TLB_C2K
+#define TLB_C2K 8  // pair conv2: columns per lane (8: 96 lanes, 4: 192 lanes)
+#endif
 #ifndef TLB_CONV1_ROWS2
 #define TLB_CONV1_ROWS2 1  // fast conv1: 1 = two rows x 8 columns per lane, 2 = two rows x 4, 0 = row strips
 #endif
@@ -192,6 +200,8 @@ __device__ __forceinline__ void issue_image(const Smem& s, int buf, const float*
 
 // Parameters (3,898 floats, padded) global -> shared, then the padded k2 copy.  __ldcg: other CTAs
 // rewrote them in the previous step's SGD phase, so bypass L1.  Ends with __syncthreads.
+__device__ __forceinline__ void build_k2k(const Smem& s);
+template <bool EXACT = true>
 __device__ __forceinline__ void load_params(const Smem& s, const float* params) {
   const float4* src = reinterpret_cast<const float4*>(params);
   float4* dst = reinterpret_cast<float4*>(s.P);
@@ -206,9 +216,13 @@ __device__ __forceinline__ void load_params(const Smem& s, const float* params) 
       if (base + u * (int)blockDim.x < kPStride / 4) dst[base + u * blockDim.x] = v[u];
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < kKp; idx += blockDim.x) {
-    const int row = idx >> 3, k = idx & 7;
-    s.Kp[idx] = k < 5 ? s.P[kK2 + row * 5 + k] : 0.0f;
+  if constexpr (!EXACT && TLB_PAIR) {
+    build_k2k(s);
+  } else {
+    for (int idx = threadIdx.x; idx < kKp; idx += blockDim.x) {
+      const int row = idx >> 3, k = idx & 7;
+      s.Kp[idx] = k < 5 ? s.P[kK2 + row * 5 + k] : 0.0f;
+    }
   }
   __syncthreads();
 }
@@ -292,8 +306,148 @@ __device__ __forceinline__ void stage_conv1_rows2(const Smem& s, const float* im
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Packed-pair fast forward (TLB_PAIR): the two forward contractions run on packed FP32 pairs (__ffma2_rn,
+// SASS FFMA2: the FP32 rate of FFMA at half the issued instructions -- measured peak 74.1 vs 72.4 TFLOP/s,
+// profiles/r2/ffma2_peak_r2k.json), one operand a broadcast scalar:
+//   conv1 : pixel (broadcast) x (k1[c], k1[c+3])            -> (c1[c], c1[c+3])
+//   conv2 : s1 (broadcast) x (k2[i][c], k2[i+6][c])         -> (out[i], out[i+6])
+// The conv2 weight pairs K2K [6][6][25] float2 live in the Kp slot, rebuilt from P whenever P changes;
+// every activation keeps its canonical layout, so the backward stages are the scalar ones.  (Pair
+// layouts for the backward contractions were measured slower at one image per SM: their weight-pair and
+// dz2-pair loads cost more shared-memory wavefronts than the halved FFMA issue saves; profiles/README.md.)
+// Fast-mode arithmetic (FFMA, fixed summation trees; within the north-star 1e-4); EXACT keeps the scalar
+// ordered stages.
+__device__ __forceinline__ float2 bcast2(float v) { return make_float2(v, v); }
+
+// conv1 pair lane = (channel pair ip, pooled row py, 4-column strip xs), 216 lanes: the two conv rows x 4
+// columns x 2 channels (8 FFMA2 accumulators) over the 25 taps -- 200 FFMA2 for 400 multiply-adds -- with
+// the pixel as the broadcast operand and the (k1[ip], k1[ip+3]) weight pair in registers; logistic, c1
+// pairs, 2x2 pool in registers -> s1 pairs.
+__device__ __forceinline__ void stage_conv1_pair(const Smem& s, const float* img) {
+  const int it = threadIdx.x;
+  if (it >= 216) return;
+  const int ip = it / 72, rem = it - ip * 72, py = rem / 6, xs = rem - py * 6;
+  const int y0 = 2 * py, x0 = 4 * xs;
+  float2 w[25];
+#pragma unroll
+  for (int t = 0; t < 25; ++t) w[t] = make_float2(s.P[kK1 + ip * 25 + t], s.P[kK1 + (ip + 3) * 25 + t]);
+  float2 a[2][4];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int o = 0; o < 4; ++o) a[r][o] = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int rr = 0; rr < 6; ++rr) {  // image row y0 + rr feeds conv row r with ky = rr - r
+    const float4* src = reinterpret_cast<const float4*>(img + (y0 + rr) * 28 + x0);
+    const float4 v0 = src[0], v1 = src[1];
+    const float in[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int ky = rr - r;
+      if (ky < 0 || ky > 4) continue;
+#pragma unroll
+      for (int kx = 0; kx < 5; ++kx)
+#pragma unroll
+        for (int o = 0; o < 4; ++o) a[r][o] = __ffma2_rn(bcast2(in[o + kx]), w[ky * 5 + kx], a[r][o]);
+    }
+  }
+  const float bx = s.P[kB1 + ip], by = s.P[kB1 + ip + 3];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+#pragma unroll
+    for (int o = 0; o < 4; ++o)
+      a[r][o] = make_float2(sigmoid_m<false>(fadd(a[r][o].x, bx), s.tab), sigmoid_m<false>(fadd(a[r][o].y, by), s.tab));
+    *reinterpret_cast<float4*>(s.c1 + c1_at(ip, y0 + r, x0)) = make_float4(a[r][0].x, a[r][1].x, a[r][2].x, a[r][3].x);
+    *reinterpret_cast<float4*>(s.c1 + c1_at(ip + 3, y0 + r, x0)) = make_float4(a[r][0].y, a[r][1].y, a[r][2].y, a[r][3].y);
+  }
+  float2 pv[2];
+#pragma unroll
+  for (int px = 0; px < 2; ++px) {  // avgpool (nn.cpp:144): ((p00 + p01) + p10) + p11, then * 0.25f
+    const float2 p00 = a[0][2 * px], p01 = a[0][2 * px + 1], p10 = a[1][2 * px], p11 = a[1][2 * px + 1];
+    pv[px] = make_float2(fmul(fadd(fadd(fadd(p00.x, p01.x), p10.x), p11.x), 0.25f),
+                         fmul(fadd(fadd(fadd(p00.y, p01.y), p10.y), p11.y), 0.25f));
+  }
+  // s1 stays in the canonical [6][12][12] layout (conv2 and g_k2 broadcast it against kernel pairs)
+  *reinterpret_cast<float2*>(s.s1 + (ip * 12 + py) * 12 + 2 * xs) = make_float2(pv[0].x, pv[1].x);
+  *reinterpret_cast<float2*>(s.s1 + ((ip + 3) * 12 + py) * 12 + 2 * xs) = make_float2(pv[0].y, pv[1].y);
+}
+
+// K2K[(ip*6 + c)*25 + t] = (k2[ip][c][t], k2[ip+6][c][t]): conv2 / backin kernel-pair weights (Kp slot).
+__device__ __forceinline__ void build_k2k(const Smem& s) {
+  for (int q = threadIdx.x; q < 900; q += blockDim.x) {
+    const int ip = q / 150, r = q - ip * 150;
+    reinterpret_cast<float2*>(s.Kp)[q] = make_float2(s.P[kK2 + ip * 150 + r], s.P[kK2 + (ip + 6) * 150 + r]);
+  }
+}
+
+// conv2 on kernel pairs (i, i+6): lane = (channel half h, column block xh, pool row r, kernel pair ip,
+// pooled row py), h fastest.  The s1 row value is the broadcast operand, (k2[i][c], k2[i+6][c]) the weight
+// pair; COLS columns of conv row y = 2py + r over the lane's 3 channels (15 x 5 x COLS FFMA2), the two
+// channel halves joined by a shuffle (lane ^ 1), lane h finishes kernel ip + 6h: sigmoid, c2, and the 2x2
+// pool with the partner row (lane ^ (2 * 8 / COLS)).  COLS = 8: 96 lanes; COLS = 4: 192 lanes.
+template <int COLS>
+__device__ __forceinline__ void stage_conv2_kpair(const Smem& s) {
+  constexpr int XB = 8 / COLS, kLanes = 96 * XB;
+  const int it = threadIdx.x;
+  if (it >= kLanes) return;
+  const int h = it & 1, xh = (it >> 1) % XB, r = (it / (2 * XB)) & 1, rest = it / (4 * XB);
+  const int ip = rest % 6, py = rest / 6, y = 2 * py + r, x0 = COLS * xh;
+  const float2* k2k = reinterpret_cast<const float2*>(s.Kp) + ip * 150;
+  float2 acc[COLS];
+#pragma unroll
+  for (int o = 0; o < COLS; ++o) acc[o] = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+  for (int c = 3 * h; c < 3 * h + 3; ++c) {
+#pragma unroll
+    for (int ky = 0; ky < 5; ++ky) {
+      const float4* src = reinterpret_cast<const float4*>(s.s1 + (c * 12 + y + ky) * 12 + x0);
+      float in[COLS + 4];
+#pragma unroll
+      for (int q = 0; q < (COLS + 4) / 4; ++q) {
+        const float4 v = src[q];
+        in[4 * q] = v.x; in[4 * q + 1] = v.y; in[4 * q + 2] = v.z; in[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int kx = 0; kx < 5; ++kx) {
+        const float2 w = k2k[c * 25 + ky * 5 + kx];
+#pragma unroll
+        for (int o = 0; o < COLS; ++o) acc[o] = __ffma2_rn(bcast2(in[o + kx]), w, acc[o]);
+      }
+    }
+  }
+  float t[COLS], u[COLS];
+  const int i = ip + 6 * h;
+  const float b = s.P[kB2 + i];
+#pragma unroll
+  for (int o = 0; o < COLS; ++o) {
+    const float ox = acc[o].x + __shfl_xor_sync(0xffffffffu, acc[o].x, 1);
+    const float oy = acc[o].y + __shfl_xor_sync(0xffffffffu, acc[o].y, 1);
+    t[o] = sigmoid_m<false>(fadd(h ? oy : ox, b), s.tab);
+  }
+#pragma unroll
+  for (int o = 0; o < COLS; ++o) u[o] = __shfl_xor_sync(0xffffffffu, t[o], 2 * XB);  // conv row y ^ 1
+  float* c2 = s.c2 + (i * 8 + y) * 8 + x0;
+#pragma unroll
+  for (int q = 0; q < COLS / 4; ++q)
+    reinterpret_cast<float4*>(c2)[q] = make_float4(t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
+  if (r == 0) {  // avgpool (nn.cpp:144): ((p00 + p01) + p10) + p11, then * 0.25f
+    float pv[COLS / 2];
+#pragma unroll
+    for (int px = 0; px < COLS / 2; ++px)
+      pv[px] = fmul(fadd(fadd(fadd(t[2 * px], t[2 * px + 1]), u[2 * px]), u[2 * px + 1]), 0.25f);
+    float* s2 = s.s2 + (i * 4 + py) * 4 + (COLS / 2) * xh;
+    if constexpr (COLS == 8) *reinterpret_cast<float4*>(s2) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+    else *reinterpret_cast<float2*>(s2) = make_float2(pv[0], pv[1]);
+  }
+}
+
 template <bool EXACT>
 __device__ __forceinline__ void stage_conv1(const Smem& s, const float* img) {
+  if constexpr (!EXACT && TLB_PAIR) {
+    stage_conv1_pair(s, img);
+    return;
+  }
   if constexpr (!EXACT && TLB_CONV1_ROWS2) {
     stage_conv1_rows2<TLB_CONV1_ROWS2 == 2 ? 4 : 8>(s, img);
     return;
@@ -462,7 +616,8 @@ __device__ __forceinline__ void stage_conv2_halves(const Smem& s) {
 
 template <bool EXACT, int V>
 __device__ __forceinline__ void stage_conv2(const Smem& s) {
-  if constexpr (V == 0) stage_conv2_halves<EXACT>(s);
+  if constexpr (!EXACT && TLB_PAIR) stage_conv2_kpair<TLB_C2K>(s);
+  else if constexpr (V == 0) stage_conv2_halves<EXACT>(s);
   else if constexpr (V == 2) stage_conv2_rows<EXACT, true>(s);
   else stage_conv2_rows<EXACT>(s);
 }
@@ -1175,12 +1330,19 @@ template <bool EXACT>
 __device__ __forceinline__ void forward_image(const Smem& s, const float* img, int label, const float* y,
                                               bool want_dz, const int* lab = nullptr, uint64_t* post_conv1 = nullptr,
                                               uint32_t post_conv1_parity = 0, long long wait_limit = 0,
-                                              unsigned int* abort = nullptr, const NextBytes* next_bytes = nullptr) {
+                                              unsigned int* abort = nullptr, const NextBytes* next_bytes = nullptr,
+                                              bool rebuild_k2p = false) {
   call_conv1<EXACT>(img);
   __syncthreads();
   if (lab) label = *lab;
   // clustered kernel: the parameters conv2 and later stages read may still be arriving during conv1
   if (post_conv1) mbar_wait_cluster_guarded(post_conv1, post_conv1_parity, wait_limit, abort);
+  if constexpr (!EXACT && TLB_PAIR) {
+    if (rebuild_k2p) {  // clustered kernel: P changed in the last exchange -> the conv2 weight pairs
+      build_k2k(s);
+      __syncthreads();
+    }
+  }
   mark(s, 3);
   call_conv2<EXACT>();  // includes avgpool
   convert_next_bytes(s, next_bytes);

@@ -31,7 +31,7 @@ def parity():
     p0 = init_params(42)
     for n, batch, epochs in ((2048, 1024, 2), (4100, 2048, 1), (1500, 700, 1)):
         want_p, want_l = orc.train(x[:n], y[:n], p0, epochs=epochs, batch=batch)
-        for mode in (1, 0):
+        for mode in ((1,) if os.environ.get("TLB_BT_ONLY") else (1, 0)):
             with Context(0, mode="fast") as c:
                 c.set_batched(mode)
                 gp, gl = c.train(p0, x[:n], y[:n], epochs=epochs, batch=batch)
@@ -40,7 +40,8 @@ def parity():
             print(json.dumps({"n": n, "batch": batch, "epochs": epochs, "kernel": "batched" if mode else "flat",
                               "params_max_rel": rel(gp, want_p), "params_max_rel_w_ge_1e-3": rel(gp[big], want_p[big]),
                               "params_max_abs_over_max_w": float(np.max(np.abs(gp - want_p)) / np.max(np.abs(want_p))),
-                              "loss_max_rel": rel(gl, want_l), "deterministic": bool(np.array_equal(gp, gp2))}),
+                              "loss_max_rel": rel(gl, want_l), "deterministic": bool(np.array_equal(gp, gp2)),
+                              "cfg": os.environ.get("TLB_BATCH_CFG", "default")}),
                   flush=True)
 
 
@@ -52,7 +53,7 @@ def timing(batches):
         n = max(2 * B, 32768)
         x = torch.empty(n, 784, device=dev)
         y = torch.empty(n, dtype=torch.int32, device=dev)
-        for mode in (1, 0):
+        for mode in ((1,) if os.environ.get("TLB_BT_ONLY") else (1, 0)):
             ctx = Context(0, mode="fast")
             ctx.set_stream(st.cuda_stream)
             ctx.set_batched(mode)
