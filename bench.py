@@ -192,13 +192,19 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+NCU_CAPTURES = {  # (mode, batch, n) -> committed `ncu --set full` key metrics of that exact launch
+    ("fast", 100, 10000): "profiles/r2/ncu_train_cluster_r2n_keymetrics.csv",   # train_cluster_kernel
+    ("fast", 16384, 32768): "profiles/r2/ncu_batch16k_r2m_keymetrics.csv",     # train_batch_kernel<2,320,2,1>
+}
+
+
 def ncu_traffic(mode: str, batch: int, n: int, world: int):
-    """DRAM bytes per launch (read + write) of the train kernel from the committed `ncu --set full` capture
-    of this exact workload (profiles/r1/ncu_train_cluster_keymetrics.csv: fast mode, batch 100, 10k images,
-    one epoch per launch); None for any other configuration."""
-    path = os.path.join(ROOT, "profiles", "r1", "ncu_train_cluster_keymetrics.csv")
-    if not (mode == "fast" and batch == 100 and n == 10000 and world == 1 and os.path.exists(path)):
-        return None
+    """(DRAM bytes per launch (read + write), source file) of the train kernel from the committed
+    `ncu --set full` capture of this exact workload (one epoch per launch); (None, None) otherwise."""
+    rel = NCU_CAPTURES.get((mode, batch, n)) if world == 1 else None
+    path = os.path.join(ROOT, rel) if rel else None
+    if not path or not os.path.exists(path):
+        return None, None
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     total = 0.0
     import csv
@@ -206,7 +212,7 @@ def ncu_traffic(mode: str, batch: int, n: int, world: int):
         for row in csv.DictReader(f):
             if row["metric"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 total += float(row["value"]) * scale.get(row["unit"], 1)
-    return total
+    return total, rel
 
 
 # ---- our arm ----------------------------------------------------------------------------------------
@@ -377,6 +383,7 @@ def run_ours(args):
     achieved = flop_per_launch / (total_ms / args.steps / 1e3) / 1e12
     clocks = clk.summary()
 
+    traffic, traffic_src = (None, None) if dp else ncu_traffic(args.mode, B, n_per, world)
     result = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -393,9 +400,10 @@ def run_ours(args):
                        dp_note=dp_note),
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp32_peak, "traffic": None if dp else ncu_traffic(args.mode, B, n_per, world),
-                     "traffic_note": "DRAM bytes/launch from profiles/r1/ncu_train_cluster_keymetrics.csv; "
-                                     f"algorithmic input bytes/launch = {n_per * 3136}",
+                     "frac": achieved / fp32_peak, "traffic": traffic,
+                     "traffic_note": (f"DRAM bytes/launch from {traffic_src}" if traffic_src else
+                                      "no committed ncu capture of this exact launch") +
+                                     f"; algorithmic input bytes/launch = {n_per * 3136}",
                      "per_launch": f"{n_per} images x {FLOP_PER_TRAIN_IMAGE} algorithmic FLOP",
                      "peak_source": (f"measured FFMA peak {ffma['tflops']:.2f} TFLOP/s ({ffma['source']}); nominal "
                                      f"{fp32_nominal:.2f} = {info['sm_count']} SMs x 128 lanes x 2 x {max_mhz} MHz"
