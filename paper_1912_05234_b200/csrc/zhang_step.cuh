@@ -42,6 +42,12 @@ constexpr int kThreads = 512;
 #ifndef TLB_PAIR
 #define TLB_PAIR 1
 #endif
+#ifndef TLB_GK2K
+#define TLB_GK2K 1  // fast g_k2 on kernel pairs (FFMA2): TLB_GK2K_SPLIT lanes beside backin, the rest beside g_k1
+#endif
+#ifndef TLB_GK2K_SPLIT
+#define TLB_GK2K_SPLIT 96
+#endif
 #ifndef TLB_C2K
 #define TLB_C2K 8  // pair conv2: columns per lane (8: 96 lanes, 4: 192 lanes)
 #endif
@@ -119,6 +125,12 @@ constexpr int kRed = 144 * 26;          // fast C1 weight-gradient row partials
 constexpr int kTerm = 12 * 864;         // backin per-kernel terms
 
 __device__ __forceinline__ int dzp_at(int i, int R, int col) { return i * kDzpK + R * kDzpRow + col; }
+// Fast mode (TLB_GK2K): a second copy of dz2 as kernel pairs (dz2[ip], dz2[ip+6]) [6][8][8] float2 for the
+// packed-pair g_k2, in the Kp slot after the conv2 weight pairs; rows padded to 20 floats and pair planes to
+// 164 (both 4 mod 32 banks in 16-byte units: a warp's row loads of different rows / pairs do not collide).
+constexpr int kDzkOff = 1800, kDzkRow = 20, kDzkPlane = 8 * kDzkRow + 4;
+static_assert(kDzkOff + 6 * kDzkPlane <= kKp, "dz2 pairs fit the Kp slot after K2K");
+__device__ __forceinline__ int dzk_at(int ip, int y, int x) { return kDzkOff + ip * kDzkPlane + y * kDzkRow + 2 * x; }
 // c1 / dz1 channel planes padded 576 -> 580 floats: the six channel rows of one y start in six different
 // bank groups (580 mod 32 = 4), so the C1 weight-gradient lanes read them conflict-free.
 constexpr int kC1Plane = 580;
@@ -701,7 +713,9 @@ __device__ __forceinline__ void fc_back_dz2(const Smem& s, int j) {
     for (int dx = 0; dx < 2; ++dx) {
       const int yy = 2 * py + dy, xx = 2 * px + dx;
       const float o = s.c2[(c * 8 + yy) * 8 + xx];
-      s.dzp[dzp_at(c, yy + 4, xx + 4)] = fmul(fmul(dc, o), fsub(1.0f, o));
+      const float d = fmul(fmul(dc, o), fsub(1.0f, o));
+      s.dzp[dzp_at(c, yy + 4, xx + 4)] = d;
+      if constexpr (TLB_PAIR && TLB_GK2K) s.Kp[dzk_at(c % 6, yy, xx) + c / 6] = d;
     }
 }
 
@@ -754,7 +768,9 @@ __device__ __forceinline__ void stage_fc_back(const Smem& s, float* row) {
       for (int dx = 0; dx < 2; ++dx) {
         const int yy = 2 * py + dy, xx = 2 * px + dx;
         const float o = s.c2[(c * 8 + yy) * 8 + xx];
-        s.dzp[dzp_at(c, yy + 4, xx + 4)] = fmul(fmul(dc, o), fsub(1.0f, o));
+        const float d = fmul(fmul(dc, o), fsub(1.0f, o));
+        s.dzp[dzp_at(c, yy + 4, xx + 4)] = d;
+        if constexpr (!EXACT && TLB_PAIR && TLB_GK2K) s.Kp[dzk_at(c % 6, yy, xx) + c / 6] = d;
       }
   }
 }
@@ -974,6 +990,52 @@ __device__ __forceinline__ void backin_rows_exact(const Smem& s, int t) {
   }
 }
 
+// Fast g_k2 on kernel pairs (TLB_GK2K): lane j < 180 = (channel c, row u) = j / 6, kernel pair ip = j % 6 (the
+// six pair lanes of a (c, u) read the same s1 rows: broadcast); five outputs v over the 64 taps (y, x):
+// s1[c][u+y][v+x] (broadcast) x (dz2[ip][y][x], dz2[ip+6][y][x]) -> (g_k2[ip][c][u][v], g_k2[ip+6][c][u][v])
+// with FFMA2; the (c, u) = (0, 0) lanes also form (g_b2[ip], g_b2[ip+6]).
+template <bool ACCUM>
+__device__ __forceinline__ void gk2_kpair(const Smem& s, float* row, int j) {
+  const int cu = j / 6, ip = j - cu * 6, c = cu / 5, u = cu - c * 5;
+  float2 acc[5];
+#pragma unroll
+  for (int v = 0; v < 5; ++v) acc[v] = make_float2(0.0f, 0.0f);
+  float2 bsum = make_float2(0.0f, 0.0f);
+#pragma unroll 2
+  for (int y = 0; y < 8; ++y) {
+    const float4* sp = reinterpret_cast<const float4*>(s.s1 + (c * 12 + u + y) * 12);
+    const float4 a = sp[0], b = sp[1], cc = sp[2];
+    const float sr[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, cc.x, cc.y, cc.z, cc.w};
+    const float4* dp = reinterpret_cast<const float4*>(s.Kp + dzk_at(ip, y, 0));
+    float2 d[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 v = dp[q];
+      d[2 * q] = make_float2(v.x, v.y);
+      d[2 * q + 1] = make_float2(v.z, v.w);
+    }
+#pragma unroll
+    for (int x = 0; x < 8; ++x)
+#pragma unroll
+      for (int v = 0; v < 5; ++v) acc[v] = __ffma2_rn(bcast2(sr[v + x]), d[x], acc[v]);
+    if (cu == 0) {
+      const float2 r0 = make_float2((d[0].x + d[1].x) + (d[2].x + d[3].x), (d[0].y + d[1].y) + (d[2].y + d[3].y));
+      const float2 r1 = make_float2((d[4].x + d[5].x) + (d[6].x + d[7].x), (d[4].y + d[5].y) + (d[6].y + d[7].y));
+      bsum = make_float2(bsum.x + (r0.x + r1.x), bsum.y + (r0.y + r1.y));
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < 5; ++v) {
+    const int idx = kK2 + ((ip * 6 + c) * 5 + u) * 5 + v;
+    put<ACCUM>(s, row, idx, acc[v].x);
+    put<ACCUM>(s, row, idx + 900, acc[v].y);  // kernel ip + 6: 6 x 150 floats further
+  }
+  if (cu == 0) {
+    put<ACCUM>(s, row, kB2 + ip, bsum.x);
+    put<ACCUM>(s, row, kB2 + ip + 6, bsum.y);
+  }
+}
+
 // g_k2 lanes done beside the scatter-form backin in conv2_back V14 / V15 (and the variants 10..13).
 __host__ __device__ constexpr int gk2_split_lanes(int V) {
   return V == 10 ? 224 : V == 11 ? 160 : V == 12 ? 192 : V == 13 ? 128 : V == 14 ? TLB_GK2R_SPLIT
@@ -989,10 +1051,14 @@ __host__ __device__ constexpr int gk2_split_lanes(int V) {
 template <bool EXACT, bool ACCUM, int V>
 __device__ __forceinline__ void stage_conv2_back(const Smem& s, float* row) {
   static_assert(EXACT ? V == 15 : V == 14, "product schedules: V14 (fast), V15 (EXACT)");
-  for (int it = threadIdx.x; it < 288 + gk2_split_lanes(V); it += blockDim.x) {  // whole warps per round
+  constexpr int kBeside = (!EXACT && TLB_PAIR && TLB_GK2K) ? (TLB_GK2K_SPLIT + 31) / 32 * 32 : gk2_split_lanes(V);
+  for (int it = threadIdx.x; it < 288 + kBeside; it += blockDim.x) {  // whole warps per round
     if constexpr (EXACT) {
       if (it < 288) backin_rows_exact(s, it);
       else gk2_exact<ACCUM>(s, row, it - 288);
+    } else if constexpr (TLB_PAIR && TLB_GK2K) {
+      if (it < 288) backin_rows<4, true>(s, it);
+      else if (it - 288 < TLB_GK2K_SPLIT) gk2_kpair<ACCUM>(s, row, it - 288);
     } else {
       if (it < 288) backin_rows<4, true>(s, it);
       else gk2_rows<ACCUM>(s, row, it - 288);
@@ -1224,6 +1290,17 @@ template <bool EXACT, bool ACCUM, int GLO = 0, bool ROWS = false>
 __device__ __forceinline__ void stage_conv1_back_gk2(const Smem& s, const float* img, float* row) {
   constexpr int kGk2 = EXACT ? 372 : ROWS ? 360 : 288;
   const int t = threadIdx.x;
+  if constexpr (!EXACT && TLB_PAIR && TLB_GK2K) {  // the C1 gradient beside the remaining g_k2 pair lanes
+    if (blockDim.x >= 512) {
+      if (t < 288) conv1_back_fast_group2<ACCUM>(s, img, row);
+      else for (int j = TLB_GK2K_SPLIT + t - 288; j < 180; j += blockDim.x - 288) gk2_kpair<ACCUM>(s, row, j);
+    } else if (t < 160) {
+      conv1_back_fast_group<ACCUM>(s, img, row);
+    } else {
+      for (int j = TLB_GK2K_SPLIT + t - 160; j < 180; j += blockDim.x - 160) gk2_kpair<ACCUM>(s, row, j);
+    }
+    return;
+  }
   if constexpr (!EXACT && TLB_C1BACK_GROUP2) {
     if (blockDim.x >= 512) {  // C1 gradient on warps 0-8, the remaining g_k2 lanes on warps 9+
       if (t < 288) {
