@@ -48,6 +48,7 @@ constexpr int kThreads = 512;
 #ifndef TLB_GK2K_SPLIT
 #define TLB_GK2K_SPLIT 96
 #endif
+
 #ifndef TLB_C2K
 #define TLB_C2K 8  // pair conv2: columns per lane (8: 96 lanes, 4: 192 lanes)
 #endif
