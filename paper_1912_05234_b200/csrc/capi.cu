@@ -575,7 +575,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
     if (dp) {  // fused data parallelism: slice s lives on rank s % world (peer memory)
       a.dp_world = dp->world;
       a.dp_rank = dp->rank;
-      for (int sl = 0; sl < 8; ++sl) {
+      for (int sl = 0; sl < tlb::cluster_size(); ++sl) {
         char* base = static_cast<char*>(dp->peer_ws[sl % dp->world]);
         a.slice_acc[sl] = reinterpret_cast<unsigned long long*>(base);
         a.slice_cnt[sl] = reinterpret_cast<unsigned int*>(base + tlb::dp_counter_offset()) + sl;
@@ -583,10 +583,10 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
       a.loss_acc = reinterpret_cast<unsigned long long*>(static_cast<char*>(dp->peer_ws[0]) + 3 * TLB_PSTRIDE * 8);
       a.seq_base = dp->seq_base;
       a.dp_error = reinterpret_cast<unsigned int*>(static_cast<char*>(dp->peer_ws[dp->rank]) +
-                                                   tlb::dp_counter_offset()) + 8;
+                                                   tlb::dp_counter_offset()) + tlb::cluster_size();
       a.dp_timeout_cycles = dp->timeout_cycles;
     } else {
-      for (int sl = 0; sl < 8; ++sl) {
+      for (int sl = 0; sl < tlb::cluster_size(); ++sl) {
         a.slice_acc[sl] = static_cast<unsigned long long*>(c->work.p);
         a.slice_cnt[sl] = static_cast<unsigned int*>(c->barrier.p) + sl;
       }

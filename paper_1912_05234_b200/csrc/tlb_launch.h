@@ -48,8 +48,8 @@ struct TrainArgs {
   // accumulator on rank 0 (symmetric buffers, peer pointers).  seq_base = steps run on these buffers
   // since they were zeroed (triple-buffer phase and counter targets continue across launches).
   int dp_world, dp_rank;
-  unsigned long long* slice_acc[8];  // [3][3904] u64 accumulator holding slice s (local or peer)
-  unsigned int* slice_cnt[8];        // arrival counter of slice s
+  unsigned long long* slice_acc[16];  // [3][3904] u64 accumulator holding slice s (local or peer)
+  unsigned int* slice_cnt[16];        // arrival counter of slice s (cluster_size() entries used)
   unsigned long long* loss_acc;      // [3] u64 loss accumulators
   uint64_t seq_base;
   unsigned int* dp_error;            // set when a peer wait times out (the kernel then exits); single GPU:

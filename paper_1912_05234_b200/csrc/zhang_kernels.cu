@@ -412,7 +412,11 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
 // (every CTA that adds into it in step s+1 has observed that signal); packed words are never zeroed.
 // Not the reference's example-order chain: EXACT mode keeps train_kernel<true>.
 // ------------------------------------------------------------------------------------------------
-constexpr int kCluster = 8;
+#ifndef TLB_CLUSTER
+#define TLB_CLUSTER 8  // CTAs per cluster (16 = the non-portable cluster size: A/B)
+#endif
+constexpr int kCluster = TLB_CLUSTER;
+static_assert(kCluster == 8 || kCluster == 16, "cluster of 8 or 16 CTAs");
 constexpr int kSlice = kPStride / kCluster;  // 488 floats per owner CTA
 constexpr int kSlice4 = kSlice / 4;
 static_assert(kSlice % 4 == 0, "slice must be float4-aligned");
@@ -867,6 +871,10 @@ cudaError_t cluster_train_capacity(int* max_clusters) {
   *max_clusters = 0;
   cudaError_t e = cudaFuncSetAttribute(train_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
   if (e != cudaSuccess) return e;
+  if (kCluster > 8) {
+    e = cudaFuncSetAttribute(train_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kCluster);
   cfg.blockDim = dim3(kThreads);
@@ -885,7 +893,7 @@ int cluster_size() { return kCluster; }
 size_t cluster_work_bytes() { return kAccWords * sizeof(unsigned long long); }
 // Fused-DP symmetric workspace per rank: [3][kPStride] u64 accumulators | [3] u64 loss | pad |
 // [kCluster] u32 slice counters | u32 watchdog flag.
-size_t dp_workspace_bytes() { return kAccWords * sizeof(unsigned long long) + 8 + 64; }
+size_t dp_workspace_bytes() { return kAccWords * sizeof(unsigned long long) + 8 + 4 * kCluster + 16; }
 size_t dp_counter_offset() { return kAccWords * sizeof(unsigned long long) + 8; }
 
 // Grid = clusters * 8 CTAs, all co-resident (clusters <= cluster_train_capacity): the kernel's grid
