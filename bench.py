@@ -304,6 +304,15 @@ def run_ours(args):
             except Exception as exc:  # symmetric memory unavailable: NCCL path
                 dp_note = f"fused NVLink step unavailable ({type(exc).__name__}: {exc}); NCCL fallback"
                 print(dp_note, file=sys.stderr)
+            # every rank must take the same path: if the fused step could not be set up on ANY rank, all
+            # ranks use NCCL (a rank running the fused kernel alone would wait for peers that never arrive)
+            agree = torch.tensor([0.0 if step is not None else 1.0], dtype=torch.float64,
+                                 device="cpu" if same_gpu else dev)
+            dist.all_reduce(agree, op=dist.ReduceOp.MAX)
+            if float(agree) > 0 and step is not None:
+                step, dp_used = None, "nccl"
+                dp_note = "fused NVLink step unavailable on another rank; NCCL fallback on every rank"
+                print(dp_note, file=sys.stderr)
         if step is None:
             step = DeviceShardStep(ctx, d_x, d_y, n_total, Bg, world, rank, graph=not (args.no_graph or same_gpu))
 
