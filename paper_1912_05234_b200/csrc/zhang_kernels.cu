@@ -416,6 +416,9 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
 #define TLB_CLUSTER 8  // CTAs per cluster (16 = the non-portable cluster size: A/B)
 #endif
 constexpr int kCluster = TLB_CLUSTER;
+#ifndef TLB_PUSH_EARLY
+#define TLB_PUSH_EARLY 1  // single GPU: each owner thread pushes its updated parameter as soon as its word completed
+#endif
 static_assert(kCluster == 8 || kCluster == 16, "cluster of 8 or 16 CTAs");
 constexpr int kSlice = kPStride / kCluster;  // 488 floats per owner CTA
 constexpr int kSlice4 = kSlice / 4;
@@ -566,6 +569,9 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       st_async_v4(dsmem_map(rx + (int)rank * kSlice + o, q), *reinterpret_cast<const float4*>(s.G + q * kSlice + o),
                   dsmem_map(&xbar[0], q));
     }
+    // Early push (below): no CTA barrier follows the exchange any more, so order every thread's reads of G
+    // here before any thread can reach the next step's zeroing of G (the threads wait for xbar[0] next anyway).
+    if (packed && TLB_PUSH_EARLY) __syncthreads();
     mark(s, 9);
     if (threadIdx.x == 0)
       mbar_arrive_expect_tx(&xbar[0], kCluster * kSlice * sizeof(float) + (rank == 0 ? kCluster * sizeof(double) : 0));
@@ -642,6 +648,17 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
         s.P[j] = fsub(s.P[j], fmul(a.rate, __fdiv_rn(gsum, (float)m_global)));
         if (cid == 0) __stcg(a.params + j, s.P[j]);
       }
+      if (TLB_PUSH_EARLY && threadIdx.x < kSlice) {
+        // ---- 5 (early). push this parameter into the 7 peers right away (no CTA barrier between the
+        // per-word polls and the push): slice 0 to the peers' xbar[1], slices 1-7 to their xbar[2]
+        const float v = s.P[j];
+        uint64_t* const pbar = rank == 0 ? &xbar[1] : &xbar[2];
+#pragma unroll
+        for (int qi = 0; qi < kCluster - 1; ++qi) {
+          const int q = qi < (int)rank ? qi : qi + 1;
+          st_async_f32(dsmem_map(s.P + j, q), v, dsmem_map(pbar, q));
+        }
+      }
       if (blockIdx.x == 0 && threadIdx.x == kSlice) {
         const double l = (double)dsum * kPackUnfix;
         loss_run = (ks != 0 ? loss_run : 0.0) + l;
@@ -700,12 +717,13 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
         }
       }
     }
-    __syncthreads();
+    const bool pushed = packed && TLB_PUSH_EARLY;
+    if (!pushed) __syncthreads();
     mark(s, 12);
-    // ---- 5. push the updated slice into the other CTAs of the cluster ----
+    // ---- 5. push the updated slice into the other CTAs of the cluster (unless pushed early above) ----
     // slice 0 goes to the peers' xbar[1], slices 1-7 to their xbar[2]
     uint64_t* const pbar = rank == 0 ? &xbar[1] : &xbar[2];
-    for (int i = threadIdx.x; i < (kCluster - 1) * kSlice4; i += blockDim.x) {
+    for (int i = threadIdx.x; !pushed && i < (kCluster - 1) * kSlice4; i += blockDim.x) {
       const int qi = i / kSlice4, q = qi < (int)rank ? qi : qi + 1;
       const int o = (int)rank * kSlice + 4 * (i - qi * kSlice4);
       st_async_v4(dsmem_map(s.P + o, q), *reinterpret_cast<const float4*>(s.P + o), dsmem_map(pbar, q));
@@ -893,7 +911,8 @@ int cluster_size() { return kCluster; }
 size_t cluster_work_bytes() { return kAccWords * sizeof(unsigned long long); }
 // Fused-DP symmetric workspace per rank: [3][kPStride] u64 accumulators | [3] u64 loss | pad |
 // [kCluster] u32 slice counters | u32 watchdog flag.
-size_t dp_workspace_bytes() { return kAccWords * sizeof(unsigned long long) + 8 + 4 * kCluster + 16; }
+// (the watchdog flag sits at dp_workspace_bytes() - 32 = right after the slice counters: parallel.FusedDPStep)
+size_t dp_workspace_bytes() { return kAccWords * sizeof(unsigned long long) + 8 + 4 * kCluster + 32; }
 size_t dp_counter_offset() { return kAccWords * sizeof(unsigned long long) + 8; }
 
 // Grid = clusters * 8 CTAs, all co-resident (clusters <= cluster_train_capacity): the kernel's grid

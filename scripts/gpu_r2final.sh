@@ -1,0 +1,28 @@
+#!/bin/bash
+# Full evidence session at HEAD (round 2): GPU tests, smoke, bench (+ reference arm), configs[3] line,
+# sweeps, widened engines, same-GPU N=2 plumbing check, ncu launch list.
+TAG=${1:-r2z}
+OUT=gpurun_out; mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/nvsmi_$TAG.txt 2>&1
+(nproc; lscpu | grep "Model name") > $OUT/host_$TAG.txt
+timeout 1200 python -u -m pytest tests -m gpu -x -q --timeout 400 > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu_$TAG.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke_$TAG.log
+timeout 600 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
+timeout 600 python bench.py --mode exact --no-cpu-baseline --no-e2e > $OUT/bench_exact_$TAG.json 2> $OUT/bench_exact_$TAG.err
+timeout 600 python bench.py --batch 16384 --n 32768 --steps 5 --no-cpu-baseline > $OUT/bench16k_$TAG.json 2> $OUT/bench16k_$TAG.err
+TLB_BENCH_SAME_GPU=1 timeout 600 python bench.py --gpus 2 --batch 16 --n 800 --steps 3 --warmup 3 > $OUT/bench_same2_$TAG.json 2> $OUT/bench_same2_$TAG.err
+timeout 300 python scripts/trace_step.py --mode fast > $OUT/trace_fast_$TAG.json 2>&1
+timeout 900 python scripts/sweep.py --out $OUT/sweep_$TAG.json > $OUT/sweep_$TAG.log 2>&1
+timeout 600 python scripts/wide_bench.py --batch 100 --n 1000 --steps 3 --out $OUT/wide_$TAG.jsonl > $OUT/wide_$TAG.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
+  python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch_$TAG.log 2>&1
+tail -3 $OUT/pytest_gpu_$TAG.log; tail -2 $OUT/smoke_$TAG.log
+for f in bench bench_ref bench_exact bench16k bench_same2; do python -c "
+import json
+try:
+  d=json.loads(open('$OUT/${f}_$TAG.json').read().strip().splitlines()[-1])
+  print('$f', d.get('value'), d.get('n_gpus'), d.get('ms_per_step'), (d.get('e2e') or {}).get('value'), (d.get('e2e_cpp') or {}).get('value'), (d.get('roofline') or {}).get('frac'), (d.get('cpu_baseline') or {}).get('value'), (d.get('impl_config') or {}).get('dp_note'))
+except Exception as e: print('$f ERR', e)
+"; done
+cat $OUT/trace_fast_$TAG.json; tail -4 $OUT/wide_$TAG.log
