@@ -126,3 +126,28 @@ def test_cli_bench_csv_and_determinism(corpus):
     lines = r.stdout.strip().splitlines()
     assert lines[0] == "workers,seconds,speedup_vs_1" and [l.split(",")[0] for l in lines[1:]] == ["1", "4"]
     assert "determinism: final params identical" in r.stderr
+
+
+E2E = os.path.join(BIN, "tloom-e2e-bench")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(E2E), reason="tools not built")
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_cpp_e2e_tool_trains_the_protocol(mode):
+    """tools/e2e_bench.cpp drives tloom::net::train on a host MnistSet (pageable memory: the bounce-slot
+    ingestion) one epoch per call from init_params(42): its 10 epoch losses are the reference's golden
+    protocol losses -- bitwise in EXACT mode, within the north-star 1e-4 in FAST mode."""
+    import json
+    with open(os.path.join(ROOT, "tests", "golden", "protocol.json")) as f:
+        want = [float(v) for v in json.load(f)["epoch_mean_loss"]]
+    r = subprocess.run([E2E, "--steps", "10", "--warmup", "0", "--mode", mode], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr
+    rec = json.loads(r.stdout.strip().splitlines()[-1])
+    got = rec["epoch_loss"]
+    assert len(got) == 10 and rec["images_per_s"] > 0
+    if mode == "exact":
+        assert got == want, (got, want)
+    else:
+        assert np.allclose(got, want, rtol=1e-4, atol=0), (got, want)
