@@ -7,11 +7,14 @@ starts from init_params(42), so its epoch losses are checked against the referen
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--mode fast|exact] [--impl ours|reference]
 
-N > 1 (torchrun, one rank per GPU, NCCL): weak scaling -- every rank owns a 100-image shard of each
-global group of 100*N images (static_chunk, runtime.cpp:138-145) over a 10k*N-image corpus; per group:
-shard forward/backward/reduction kernel -> ncclAllReduce of the 3,898-float gradient sum (+ fp64 loss)
--> sgd kernel.  ``--impl reference`` times the reference's own CPU net::train (oracle/_ref, the
-unmodified tensorloom library) with all host threads on the same workload; rank 0 only.
+N > 1 (``--gpus N`` spawns N ranks under torch.distributed.run, one per GPU): weak scaling -- every rank
+owns a 100-image shard of each global group of 100*N images (static_chunk, runtime.cpp:138-145) over a
+10k*N-image corpus.  Default exchange: fused into the clustered train kernel over NVLink peer memory
+(fixed-point gradient slices added into the owning rank's accumulator, no collective call); fallback
+(all ranks together): shard kernel -> ncclAllReduce of the 3,904-float gradient sum -> sgd kernel.
+Every N>1 line carries its own e2e (per-rank shard bytes in) and the rank-0 cpu_baseline.
+``--impl reference`` times the reference's own CPU net::train (oracle/_ref, the unmodified tensorloom
+library) with all host threads on the same workload; rank 0 only.
 """
 from __future__ import annotations
 
@@ -120,12 +123,12 @@ def golden_losses():
 
 
 # ---- reference CPU path (oracle/_ref = the unmodified tensorloom library) ---------------------------
-def reference_epochs(n: int, epochs_budget_s: float, max_epochs: int, batch: int):
+def reference_epochs(n: int, epochs_budget_s: float, max_epochs: int, batch: int, workers: int = 0):
     """Times the reference's own net::train (oracle/_ref) on whole epochs of its own synth::make_set(n, 1)
-    from its own init_params(42), with all host threads; returns (img/s, info)."""
+    from its own init_params(42), with `workers` host threads (0 = all); returns (img/s, info)."""
     from oracle import Reference  # reference arm / cpu_baseline only
     R = Reference()
-    cores = os.cpu_count() or 1
+    cores = workers or os.cpu_count() or 1
     R.set_workers(cores)
     images, labels = R.make_set(n, 1)
     p = R.init_params(42)
@@ -138,6 +141,17 @@ def reference_epochs(n: int, epochs_budget_s: float, max_epochs: int, batch: int
         if t_total >= epochs_budget_s:
             break
     return done * n / t_total, {"cores": cores, "epochs": done, "seconds": t_total}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def workload_config(args, world: int) -> dict:
@@ -523,7 +537,14 @@ def run_ours(args):
             result["cpu_baseline"] = {"value": v, "unit": "images/s", "cores": meta["cores"], "kind": "reference",
                                       "sample": f"{meta['epochs']} epoch(s) x {n_per} images at batch "
                                                 f"{min(B * world, n_per)}, reference net::train (oracle/_ref) with "
-                                                f"{meta['cores']} workers, {meta['seconds']:.1f} s"}
+                                                f"{meta['cores']} workers, {meta['seconds']:.1f} s",
+                                      "cpu_model": cpu_model()}
+            # the reference at one worker too (a bounded sample: 1 epoch of <= 2000 images)
+            n1 = min(n_per, 2000)
+            v1, meta1 = reference_epochs(n1, 1.0, 1, min(B * world, n1), workers=1)
+            result["cpu_baseline_w1"] = {"value": v1, "unit": "images/s", "cores": 1, "kind": "reference",
+                                         "sample": f"1 epoch x {n1} images at batch {min(B * world, n1)}, reference "
+                                                   f"net::train with 1 worker, {meta1['seconds']:.1f} s"}
         if dp:
             dist.barrier()
     if real_stdout is not None:
