@@ -21,7 +21,7 @@
 //   S4 d_s2 = fc^T dz, dz2 = (d_s2/4) g2                               192 lanes
 //   S5 backin (36 row pairs x 4 kernel-group lanes, valid taps only: 720-840 FFMA each), whose epilogue
 //      writes dz1 = (d_s1/4) g1 in place of g1; g_k2 + g_b2 (720 + 24 lanes over the round's images,
-//      320 FFMA per image); g_fc + g_b (1,930 output lanes)
+//      320 FFMA per image); g_fc (480 lanes, 4 columns each) + g_b (10 lanes)
 //   S6 g_k1 (30 outputs x 8 row-chunk lanes over the round's images), g_b1
 // Arithmetic is the fast mode's (FFMA, ex2/rcp MUFU logistic; fixed summation trees), within the
 // north-star 1e-4 tolerance; EXACT mode never runs here.
@@ -747,23 +747,31 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
       // S5: backin (heaviest items first; 4-lane groups, whole warps) | g_k2 + g_b2 (lane pairs, whole
       // warps) | g_fc + g_b (one lane per output, light items that fill the tail)
       {
-        const int nbi = (cnt * 144 + 31) / 32 * 32, n2 = nbi + 768, nfc = n2 + 1930;
+        const int nbi = (cnt * 144 + 31) / 32 * 32, n2 = nbi + 768, nfc = n2 + 490;
         for (int it = t; it < nfc; it += T) {
           if (it < nbi) {
             if constexpr (PAIR) backin_item<true>(P, regs, it, cnt, it < cnt * 144);
             else backin_item(W2, regs, it, cnt, it < cnt * 144);
           } else if (it < n2) {
             gk2_item(G, regs, it - nbi, cnt);
-          } else if (it < n2 + 1920) {
-            const int o = it - n2, i = o / 192, j = o - i * 192;
-            float g = 0.0f;
+          } else if (it < n2 + 480) {  // g_fc, four columns per lane (float4 s2 / G)
+            const int o4 = it - n2, i = o4 / 48, j4 = o4 - i * 48;
+            float4 g = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
             for (int k = 0; k < cnt; ++k) {
               const float* reg = regs + k * kImgRegion;
-              g = __fmaf_rn(reg[kOffS2 + j], reg[kOffOd + 16 + i], g);
+              const float4 sv = reinterpret_cast<const float4*>(reg + kOffS2)[j4];
+              const float d = reg[kOffOd + 16 + i];
+              g.x = __fmaf_rn(sv.x, d, g.x);
+              g.y = __fmaf_rn(sv.y, d, g.y);
+              g.z = __fmaf_rn(sv.z, d, g.z);
+              g.w = __fmaf_rn(sv.w, d, g.w);
             }
-            G[kFC + o] += g;
+            float4* gp = reinterpret_cast<float4*>(G + kFC) + o4;
+            float4 gv = *gp;
+            gv.x += g.x; gv.y += g.y; gv.z += g.z; gv.w += g.w;
+            *gp = gv;
           } else {
-            const int i = it - n2 - 1920;
+            const int i = it - n2 - 480;
             float g = 0.0f;
             for (int k = 0; k < cnt; ++k) g += regs[k * kImgRegion + kOffOd + 16 + i];
             G[kB + i] += g;

@@ -26,3 +26,6 @@ try:
 except Exception as e: print('$f ERR', e)
 "; done
 cat $OUT/trace_fast_$TAG.json; tail -4 $OUT/wide_$TAG.log
+TLB_CLUSTER_COOP=0 bash scripts/ncu_one.sh ncu_cluster_$TAG train_cluster_kernel python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+python scripts/ncu_lines.py $OUT/ncu_cluster_$TAG.ncu-rep 40 > $OUT/ncu_cluster_${TAG}_lines.txt 2>&1
+grep -E "time_duration|dram__bytes|fma_cycles|issue_active" $OUT/ncu_cluster_${TAG}_keymetrics.csv | cut -d, -f2- | cut -c1-100
