@@ -36,6 +36,10 @@
 #include "tlb_launch.h"
 #include "train_common.cuh"
 
+#ifndef TLB_GK2_FULL
+#define TLB_GK2_FULL 1  // batched g_k2: one lane per output row over all 8 tap rows (0: two row-half lanes)
+#endif
+
 namespace tlb {
 namespace bt {
 
@@ -346,6 +350,46 @@ __device__ __forceinline__ void gk2_item(float* G, const float* regs, int it, in
     } else if (task < 372) {
       G[kB2 + task - 360] += acc[0];
     }
+  }
+}
+
+// S5 g_k2 lane over all 8 rows (TLB_GK2_FULL): task (kernel i, channel c, row u), i fastest (the twelve
+// kernel lanes of a (c, u) read the same s1 rows: broadcast) -- 5 outputs over the 64 taps per image, no
+// row-half shuffle; tasks 360..371: g_b2[i].  372 lanes (half the items of gk2_item, twice the work each).
+__device__ __forceinline__ void gk2_item_full(float* G, const float* regs, int task, int cnt) {
+  float acc[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+  if (task < 360) {
+    const int i = task % 12, cu = task / 12, c = cu / 5, u = cu - c * 5;
+#pragma unroll 1
+    for (int k = 0; k < cnt; ++k) {
+      const float* reg = regs + k * kImgRegion;
+      const float* s1 = reg + kOffS1 + (c * 12 + u) * 12;
+      const float* d2 = reg + kOffD2 + i * kD2K + 4 * 8;
+#pragma unroll 2
+      for (int y = 0; y < 8; ++y) {
+        float in[12], d[8];
+        load_row<12>(s1 + y * 12, in);
+        load_row<8>(d2 + y * 8, d);
+#pragma unroll
+        for (int v = 0; v < 5; ++v)
+#pragma unroll
+          for (int x = 0; x < 8; ++x) acc[v] = __fmaf_rn(in[v + x], d[x], acc[v]);
+      }
+    }
+    float* g = G + kK2 + ((i * 6 + c) * 5 + u) * 5;
+#pragma unroll
+    for (int v = 0; v < 5; ++v) g[v] += acc[v];
+  } else if (task < 372) {
+    const int i = task - 360;
+    for (int k = 0; k < cnt; ++k) {
+      const float4* d = reinterpret_cast<const float4*>(regs + k * kImgRegion + kOffD2 + i * kD2K + 4 * 8);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const float4 v = d[q];
+        acc[0] += (v.x + v.y) + (v.z + v.w);
+      }
+    }
+    G[kB2 + i] += acc[0];
   }
 }
 
@@ -747,13 +791,14 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
       // S5: backin (heaviest items first; 4-lane groups, whole warps) | g_k2 + g_b2 (lane pairs, whole
       // warps) | g_fc + g_b (one lane per output, light items that fill the tail)
       {
-        const int nbi = (cnt * 144 + 31) / 32 * 32, n2 = nbi + 768, nfc = n2 + 490;
+        const int nbi = (cnt * 144 + 31) / 32 * 32, n2 = nbi + (TLB_GK2_FULL ? 384 : 768), nfc = n2 + 490;
         for (int it = t; it < nfc; it += T) {
           if (it < nbi) {
             if constexpr (PAIR) backin_item<true>(P, regs, it, cnt, it < cnt * 144);
             else backin_item(W2, regs, it, cnt, it < cnt * 144);
           } else if (it < n2) {
-            gk2_item(G, regs, it - nbi, cnt);
+            if constexpr (TLB_GK2_FULL) gk2_item_full(G, regs, it - nbi, cnt);
+            else gk2_item(G, regs, it - nbi, cnt);
           } else if (it < n2 + 480) {  // g_fc, four columns per lane (float4 s2 / G)
             const int o4 = it - n2, i = o4 / 48, j4 = o4 - i * 48;
             float4 g = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
