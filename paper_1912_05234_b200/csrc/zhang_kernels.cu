@@ -419,6 +419,9 @@ constexpr int kCluster = TLB_CLUSTER;
 #ifndef TLB_PUSH_EARLY
 #define TLB_PUSH_EARLY 1  // single GPU: each owner thread pushes its updated parameter as soon as its word completed
 #endif
+#ifndef TLB_STEP_NOBAR
+#define TLB_STEP_NOBAR 1  // with TLB_PUSH_EARLY: no CTA barrier at the step start (G zeroed after the push)
+#endif
 static_assert(kCluster == 8 || kCluster == 16, "cluster of 8 or 16 CTAs");
 constexpr int kSlice = kPStride / kCluster;  // 488 floats per owner CTA
 constexpr int kSlice4 = kSlice / 4;
@@ -508,6 +511,15 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
   first_bytes(s, a, pf_valid, pf);
   uint32_t consumed = 0;
   load_params<false>(s, a.params);  // once: afterwards the parameters live in shared memory
+  // Barrier-free step start (single GPU, early push): G is zeroed right after each step's gradient push
+  // (here for the first step) and rank 0 pushes its own slice 0 to itself as well, so a CTA starts the next
+  // conv1 as soon as slice 0 has landed -- its own owner threads still finishing their slices do not hold
+  // it back (their own-slice writes are ordered before conv2 by conv1's barrier).
+  const bool nobar = TLB_PUSH_EARLY && TLB_STEP_NOBAR && TLB_PACKED_ACC && !dp && a.grad_out == nullptr;
+  if (nobar) {
+    for (int i = threadIdx.x; i < kPStride; i += blockDim.x) s.G[i] = 0.0f;
+    __syncthreads();
+  }
 
   // group index within the epoch and epoch of step st, advanced incrementally (no per-step division)
   int64_t ks = umod(a.step_begin, a.steps_per_epoch), ep = udiv(a.step_begin, a.steps_per_epoch);
@@ -528,8 +540,10 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     static_chunk(m, G, blockIdx.x, lo, hi);
     s.tr = trace ? trace + ls * 16 : nullptr;
     mark(s, 0);
-    for (int i = threadIdx.x; i < kPStride; i += blockDim.x) s.G[i] = 0.0f;
-    __syncthreads();
+    if (!nobar) {
+      for (int i = threadIdx.x; i < kPStride; i += blockDim.x) s.G[i] = 0.0f;
+      __syncthreads();
+    }
     mark(s, 1);
     double cta_loss = 0.0;
     for (int64_t e = lo; e < hi; ++e) {
@@ -562,6 +576,8 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     // re-arms that barrier below (an arrival on an incomplete phase would corrupt its count).
     if (!dp && ls > 0 && lo >= hi) mbar_wait_cluster_guarded(&xbar[2], (uint32_t)((ls - 1) & 1), a.dp_timeout_cycles, a.dp_error);
     // ---- 2. push slice q of G to its owner q; owner sums the 8 received slices (rank order) ----
+    // (nobar: a CTA that trained no image this step passed no barrier since zeroing G: order that first)
+    if (nobar && lo >= hi) __syncthreads();
     const uint32_t parity = (uint32_t)(ls & 1);
     if (threadIdx.x == 0) st_async_f64(dsmem_map(&loss_rx[rank], 0), cta_loss, dsmem_map(&xbar[0], 0));
     for (int i = threadIdx.x; i < kCluster * kSlice4; i += blockDim.x) {
@@ -572,6 +588,8 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     // Early push (below): no CTA barrier follows the exchange any more, so order every thread's reads of G
     // here before any thread can reach the next step's zeroing of G (the threads wait for xbar[0] next anyway).
     if (packed && TLB_PUSH_EARLY) __syncthreads();
+    if (nobar)  // every read of G (the pushes above) is complete: zero it for the next step's backward
+      for (int i = threadIdx.x; i < kPStride; i += blockDim.x) s.G[i] = 0.0f;
     mark(s, 9);
     if (threadIdx.x == 0)
       mbar_arrive_expect_tx(&xbar[0], kCluster * kSlice * sizeof(float) + (rank == 0 ? kCluster * sizeof(double) : 0));
@@ -643,21 +661,24 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
         else packed_prev2 = v;
       }
       mark(s, 11);
+      float pnew = threadIdx.x < kSlice ? s.P[j] : 0.0f;
       if (threadIdx.x < kSlice && j < kNParam) {
         const float gsum = (float)((double)dsum * kPackUnfix);
-        s.P[j] = fsub(s.P[j], fmul(a.rate, __fdiv_rn(gsum, (float)m_global)));
-        if (cid == 0) __stcg(a.params + j, s.P[j]);
+        pnew = fsub(pnew, fmul(a.rate, __fdiv_rn(gsum, (float)m_global)));
+        if (!(nobar && rank == 0)) s.P[j] = pnew;  // rank 0 under nobar: written by its own push below
+        if (cid == 0) __stcg(a.params + j, pnew);
       }
       if (TLB_PUSH_EARLY && threadIdx.x < kSlice) {
         // ---- 5 (early). push this parameter into the 7 peers right away (no CTA barrier between the
-        // per-word polls and the push): slice 0 to the peers' xbar[1], slices 1-7 to their xbar[2]
-        const float v = s.P[j];
+        // per-word polls and the push): slice 0 to the peers' xbar[1], slices 1-7 to their xbar[2];
+        // under nobar rank 0 also pushes slice 0 into itself (its threads wait for it on xbar[1])
         uint64_t* const pbar = rank == 0 ? &xbar[1] : &xbar[2];
 #pragma unroll
         for (int qi = 0; qi < kCluster - 1; ++qi) {
           const int q = qi < (int)rank ? qi : qi + 1;
-          st_async_f32(dsmem_map(s.P + j, q), v, dsmem_map(pbar, q));
+          st_async_f32(dsmem_map(s.P + j, q), pnew, dsmem_map(pbar, q));
         }
+        if (nobar && rank == 0) st_async_f32(dsmem_map(s.P + j, 0), pnew, dsmem_map(pbar, 0));
       }
       if (blockIdx.x == 0 && threadIdx.x == kSlice) {
         const double l = (double)dsum * kPackUnfix;
@@ -729,7 +750,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       st_async_v4(dsmem_map(s.P + o, q), *reinterpret_cast<const float4*>(s.P + o), dsmem_map(pbar, q));
     }
     if (threadIdx.x == 0) {
-      mbar_arrive_expect_tx(&xbar[1], rank == 0 ? 0u : (uint32_t)(kSlice * sizeof(float)));
+      mbar_arrive_expect_tx(&xbar[1], (rank == 0 && !nobar) ? 0u : (uint32_t)(kSlice * sizeof(float)));
       mbar_arrive_expect_tx(&xbar[2], (uint32_t)((rank == 0 ? kCluster - 1 : kCluster - 2) * kSlice * sizeof(float)));
     }
     if (!dp) {
