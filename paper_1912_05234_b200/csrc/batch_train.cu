@@ -770,21 +770,26 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
           cta_loss += (double)(0.5f * l);
         }
       }
-      for (int it = t; it < cnt * 192; it += T) {
-        const int k = it / 192, j = it - k * 192;
+      for (int it = t; it < cnt * 96; it += T) {  // two pooled columns (j, j + 1) per lane
+        const int k = it / 96, j = 2 * (it - k * 96);
         float* reg = regs + k * kImgRegion;
         const float* dz = reg + kOffOd + 16;
-        float ds = 0.0f;
+        float ds0 = 0.0f, ds1 = 0.0f;
 #pragma unroll
-        for (int i = 0; i < 10; ++i) ds = __fmaf_rn(P[kFC + i * 192 + j], dz[i], ds);
-        ds *= 0.25f;  // backavgpool (nn.cpp:148-158)
+        for (int i = 0; i < 10; ++i) {
+          const float2 w = *reinterpret_cast<const float2*>(P + kFC + i * 192 + j);
+          ds0 = __fmaf_rn(w.x, dz[i], ds0);
+          ds1 = __fmaf_rn(w.y, dz[i], ds1);
+        }
+        ds0 *= 0.25f;  // backavgpool (nn.cpp:148-158)
+        ds1 *= 0.25f;
         const int i2 = j >> 4, py = (j >> 2) & 3, px = j & 3;
         float* d2 = reg + kOffD2 + i2 * kD2K + (4 + 2 * py) * 8 + 2 * px;
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
-          float2* q2 = reinterpret_cast<float2*>(d2 + rr * 8);
-          const float2 g = *q2;
-          *q2 = make_float2(ds * g.x, ds * g.y);
+          float4* q4 = reinterpret_cast<float4*>(d2 + rr * 8);
+          const float4 g = *q4;
+          *q4 = make_float4(ds0 * g.x, ds0 * g.y, ds1 * g.z, ds1 * g.w);
         }
       }
       __syncthreads();
