@@ -8,7 +8,8 @@ or mis-indexed ready-flag wait would read the previous case's bytes and change t
 import numpy as np
 
 CASES = ((1, 100), (83, 7), (200, 100), (5000, 100), (300, 100), (1001, 77), (2, 1), (3, 1), (4, 1), (5, 1),
-         (129, 1), (800, 100), (801, 100), (10000, 100))
+         (129, 1), (800, 100), (801, 100), (10000, 100),
+         (6000, 2500), (4099, 1337))  # groups > 2 MiB on the link: fixed ~1 MiB chunks, not group-aligned
 
 
 def bits(a):

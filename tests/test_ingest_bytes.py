@@ -59,10 +59,16 @@ def test_train_bytes_bitwise_equal_to_train_on_images(mode):
         # large groups (batched kernel in fast mode) and a ragged tail
         want_b, _ = c.train(p0, images, lab, epochs=1, batch=640)
         got_b, _ = c.train_u8(p0, px, lab, epochs=1, batch=640)
+        # groups > 2 MiB of bytes on the link: fixed ~1 MiB chunks (not group-aligned), resident reference
+        px5, lab5 = synth_make_digits(6000, 2)
+        im5 = px5.astype(np.float32) / np.float32(255.0)
+        want_c, want_cl = c.train(p0, im5, lab5, epochs=2, batch=2900)
+        got_c, got_cl = c.train_u8(p0, px5, lab5, epochs=2, batch=2900)
     for got in (got_p, idx_p):
         assert np.array_equal(got.view(np.uint32), want_p.view(np.uint32))
     assert list(got_l) == list(want_l) == list(idx_l)
     assert np.array_equal(got_b.view(np.uint32), want_b.view(np.uint32))
+    assert np.array_equal(got_c.view(np.uint32), want_c.view(np.uint32)) and list(got_cl) == list(want_cl)
 
 
 @pytest.mark.gpu
