@@ -119,3 +119,28 @@ def test_wide_engines_agree_on_a_large_group():
         a, la = ctx.wide_train(p0, x, y, epochs=1, batch=300, engine="tc")
         b, lb = ctx.wide_train(p0, x, y, epochs=1, batch=300, engine="fp32")
     assert rel_err(a, b, floor=1e-3) <= 5e-5 and rel_err(la, lb) <= 1e-6
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_wide_train_two_epochs_vs_reference_composition(wref, orc):
+    """Two epochs of three SGD groups each (6 updates, the last group of each epoch ragged) on the tensor-core
+    engine against the reference's own operators composed step by step: the error stays inside the
+    tolerance over the whole run, not just after one update."""
+    from oracle import widened
+    from paper_1912_05234_b200 import Context
+    x, y = widened.make_set(orc, 10, 3)
+    p0 = widened.init_params(7)
+    want, want_l = p0, []
+    for _ in range(2):
+        tot = 0.0
+        for lo in range(0, 10, 4):
+            want, l, _ = wref.train_step(x[lo:lo + 4], y[lo:lo + 4], want, 0.05)
+            tot += l
+        want_l.append(tot / 10)
+    with Context(0) as ctx:
+        got, losses = ctx.wide_train(p0, x, y, rate=0.05, epochs=2, batch=4, engine="tc")
+    assert rel_err(np.asarray(losses), np.asarray(want_l)) <= REL_TOL, (losses, want_l)
+    assert rel_err(got, want, floor=1e-3) <= REL_TOL, rel_err(got, want, floor=1e-3)
+    d_got, d_want = got - p0, want - p0
+    assert np.max(np.abs(d_got - d_want)) <= 1e-3 * np.max(np.abs(d_want))
