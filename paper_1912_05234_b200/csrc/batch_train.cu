@@ -287,8 +287,35 @@ __device__ __forceinline__ void backin_item(const float* W2, float* regs, int bi
     const int i = 3 * ig + ii;
     const float* wrow = WP ? W2 + kK2 + (i * 6 + c) * 25 : W2 + i * kW2Stride + c * 40;
     const float* d2i = reg + kOffD2 + i * kD2K;
-    backin_acc<WP>(d2i, wrow, pA, 0, min(4, pA), accA);
-    backin_acc<WP>(d2i, wrow, pB, max(0, pB - 7), 4, accB);
+    if constexpr (WP) {  // each weight row loaded once for both d_s1 rows (valid u: A <= pA, B >= pB - 7)
+#pragma unroll 1
+      for (int u = 0; u < 5; ++u) {
+        float w[5];
+#pragma unroll
+        for (int v = 0; v < 5; ++v) w[v] = wrow[u * 5 + v];
+        if (u <= pA) {
+          float d[8];
+          load_row<8>(d2i + (4 + pA - u) * 8, d);
+#pragma unroll
+          for (int q = 0; q < 12; ++q)
+#pragma unroll
+            for (int v = 0; v < 5; ++v)
+              if (q - v >= 0 && q - v < 8) accA[q] = __fmaf_rn(w[v], d[q - v], accA[q]);
+        }
+        if (u >= pB - 7) {
+          float d[8];
+          load_row<8>(d2i + (4 + pB - u) * 8, d);
+#pragma unroll
+          for (int q = 0; q < 12; ++q)
+#pragma unroll
+            for (int v = 0; v < 5; ++v)
+              if (q - v >= 0 && q - v < 8) accB[q] = __fmaf_rn(w[v], d[q - v], accB[q]);
+        }
+      }
+    } else {
+      backin_acc<WP>(d2i, wrow, pA, 0, min(4, pA), accA);
+      backin_acc<WP>(d2i, wrow, pB, max(0, pB - 7), 4, accB);
+    }
   }
 #pragma unroll
   for (int q = 0; q < 12; ++q) {
