@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
   if (pf_valid && step_bytes(a, pf.step)) {  // the first round's bytes: converted by every thread
     __syncthreads();
     mbar_wait(&bar[0], 0);
-    convert_pixels(pxring, ring, a.images_wb + ridx[0] * kImg, rb.cnt[0], t, T);
+    convert_pixels(pxring, ring, (a.images_wb ? a.images_wb + ridx[0] * kImg : nullptr), rb.cnt[0], t, T);
     __syncthreads();
   }
   uint32_t consumed = 0;
@@ -779,7 +779,7 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
         const int nb = buf ^ 1;
         if (t >= nfc && rbst[nb]) {
           mbar_wait(&bar[nb], ((consumed + 1) >> 1) & 1);
-          convert_pixels(pxring + nb * NI * kImg, ring + nb * NI * kImg, a.images_wb + ridx[nb] * kImg, rb.cnt[nb],
+          convert_pixels(pxring + nb * NI * kImg, ring + nb * NI * kImg, (a.images_wb ? a.images_wb + ridx[nb] * kImg : nullptr), rb.cnt[nb],
                          t - nfc, T - nfc);
         }
       }

@@ -109,6 +109,7 @@ struct tlb_ctx {
   bool use_cluster = true;
   int64_t shard_stride = 0;  // DP shard layout of the images/labels passed to the shard / fused-DP entry points
   int batched = -1;  // batched fast train kernel: -1 auto (TLB_BATCHED or the group-size rule), 0 off, 1 on
+  bool one_epoch_call = false;  // tlb_train* of a single epoch: byte-ingested images need no fp32 write-back
   DevBuf work, losses, loss_part, barrier;  // persistent-train workspaces
   DevBuf stage[8];                 // host-API staging buffers
   // Overlapped ingestion for tlb_train: the dataset is copied chunk by chunk on `copy_stream` while
@@ -570,7 +571,7 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.dp_timeout_cycles = (long long)(kWaitLimitSeconds * 2.0e9);  // ~2 GHz SM clock
   a.local_stride = (dp || grad_out) ? c->shard_stride : 0;
   a.pixels = ready ? pixels : nullptr;  // bytes only while the ingestion flags are live (the first epoch)
-  a.images_wb = const_cast<float*>(d_images);
+  a.images_wb = c->one_epoch_call ? nullptr : const_cast<float*>(d_images);
   if (clustered) {
     if (dp) {  // fused data parallelism: slice s lives on rank s % world (peer memory)
       a.dp_world = dp->world;
@@ -1079,6 +1080,12 @@ static int train_host(tlb_ctx* c, HostImages src, const int32_t* labels, int64_t
     return pageable && !copies_first ? ingest_pageable(c, src, d_img, plan, c->ready_token)
                                      : ingest_images(c, src, d_img, n, chunk, batch, c->ready_token);
   };
+  // a one-epoch call never reads the fp32 images back: byte-ingested images skip the write-back
+  c->one_epoch_call = epochs == 1;
+  struct ResetFlag {
+    tlb_ctx* c;
+    ~ResetFlag() { c->one_epoch_call = false; }
+  } reset_flag{c};
   if (copies_first) TLB_TRY(ingest_images(c, src, d_img, n, chunk, batch, c->ready_token));
   if (!on_epoch) {
     TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, 0, epochs, batch, d_loss, 0, 0, -1, nullptr, nullptr,

@@ -137,7 +137,7 @@ __device__ __forceinline__ void convert_pixels(const uint8_t* px, float* img, fl
     const float4 v = make_float4(__fdiv_rn((float)(w & 0xffu), 255.0f), __fdiv_rn((float)((w >> 8) & 0xffu), 255.0f),
                                  __fdiv_rn((float)((w >> 16) & 0xffu), 255.0f), __fdiv_rn((float)(w >> 24), 255.0f));
     reinterpret_cast<float4*>(img)[q] = v;
-    __stcg(reinterpret_cast<float4*>(wb) + q, v);
+    if (wb) __stcg(reinterpret_cast<float4*>(wb) + q, v);  // nullptr: a one-epoch call, no later reader
   }
 }
 

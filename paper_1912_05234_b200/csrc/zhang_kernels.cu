@@ -54,7 +54,7 @@ __device__ __forceinline__ void first_bytes(const Smem& s, const TrainArgs& a, b
   if (!valid || !step_bytes(a, j.step)) return;
   __syncthreads();  // the issuer's s.jidx[0]
   mbar_wait(&s.bar[0], 0);
-  convert_pixels(s.px, s.img, a.images_wb + s.jidx[0] * kImg, 1, threadIdx.x, blockDim.x);
+  convert_pixels(s.px, s.img, (a.images_wb ? a.images_wb + s.jidx[0] * kImg : nullptr), 1, threadIdx.x, blockDim.x);
   __syncthreads();
 }
 

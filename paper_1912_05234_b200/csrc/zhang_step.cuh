@@ -1394,13 +1394,13 @@ __device__ __forceinline__ void convert_next_bytes(const Smem& s, const NextByte
   const int t = threadIdx.x - kConv2Lanes, T = blockDim.x - kConv2Lanes;
   const uint32_t* px = reinterpret_cast<const uint32_t*>(s.px + nb->buf * kImg);
   float4* img = reinterpret_cast<float4*>(s.img + nb->buf * kImg);
-  float4* wb = reinterpret_cast<float4*>(nb->wb + s.jidx[nb->buf] * kImg);
+  float4* wb = nb->wb ? reinterpret_cast<float4*>(nb->wb + s.jidx[nb->buf] * kImg) : nullptr;
   for (int q = t; q < kImg / 4; q += T) {
     const uint32_t w = px[q];
     const float4 v = make_float4(__fdiv_rn((float)(w & 0xffu), 255.0f), __fdiv_rn((float)((w >> 8) & 0xffu), 255.0f),
                                  __fdiv_rn((float)((w >> 16) & 0xffu), 255.0f), __fdiv_rn((float)(w >> 24), 255.0f));
     img[q] = v;
-    __stcg(wb + q, v);
+    if (wb) __stcg(wb + q, v);
   }
 }
 
