@@ -210,13 +210,28 @@ __device__ __forceinline__ void conv1_item_p(const float* P, const float* W1P, c
       }
     }
   }
-  const float nbx = neg_log2e_times(P[kB1 + ip]), nby = neg_log2e_times(P[kB1 + ip + 3]);
+  // logistic and pool on the channel pairs too (FFMA2 / FADD2 / FMUL2; the ex2 and rcp MUFU ops stay scalar)
+  const float2 nb = make_float2(neg_log2e_times(P[kB1 + ip]), neg_log2e_times(P[kB1 + ip + 3]));
+  const float2 kl = bc2(-1.4426950408889634f), one = bc2(1.0f);
+  auto logistic2 = [&](float2 acc) {
+    const float2 z = __ffma2_rn(acc, kl, nb);
+    float2 e, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(z.x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(z.y));
+    const float2 d = __fadd2_rn(one, e);
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(d.x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(d.y));
+    return r;
+  };
   float px[3], py2[3];
 #pragma unroll
   for (int j = 0; j < 3; ++j) {  // avgpool (nn.cpp:144): ((p00 + p01) + p10) + p11, then * 0.25f
-    const float2 p00 = a[0][2 * j], p01 = a[0][2 * j + 1], p10 = a[1][2 * j], p11 = a[1][2 * j + 1];
-    px[j] = (((logistic(p00.x, nbx) + logistic(p01.x, nbx)) + logistic(p10.x, nbx)) + logistic(p11.x, nbx)) * 0.25f;
-    py2[j] = (((logistic(p00.y, nby) + logistic(p01.y, nby)) + logistic(p10.y, nby)) + logistic(p11.y, nby)) * 0.25f;
+    const float2 p = __fmul2_rn(__fadd2_rn(__fadd2_rn(__fadd2_rn(logistic2(a[0][2 * j]), logistic2(a[0][2 * j + 1])),
+                                                      logistic2(a[1][2 * j])),
+                                           logistic2(a[1][2 * j + 1])),
+                                bc2(0.25f));
+    px[j] = p.x;
+    py2[j] = p.y;
   }
   float* d0 = s1s + k * 864 + (ip * 12 + py) * 12 + 3 * xs;
   float* d1 = d0 + 3 * 144;
