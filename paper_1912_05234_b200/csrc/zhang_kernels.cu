@@ -419,6 +419,12 @@ constexpr int kCluster = TLB_CLUSTER;
 #ifndef TLB_PUSH_EARLY
 #define TLB_PUSH_EARLY 1  // single GPU: each owner thread pushes its updated parameter as soon as its word completed
 #endif
+#ifndef TLB_DP_PENDING
+#define TLB_DP_PENDING 1
+#endif
+#ifndef TLB_DP_PUSH_EARLY
+#define TLB_DP_PUSH_EARLY 1
+#endif
 #ifndef TLB_STEP_NOBAR
 #define TLB_STEP_NOBAR 1  // with TLB_PUSH_EARLY: no CTA barrier at the step start (G zeroed after the push)
 #endif
@@ -516,6 +522,9 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
   // conv1 as soon as slice 0 has landed -- its own owner threads still finishing their slices do not hold
   // it back (their own-slice writes are ordered before conv2 by conv1's barrier).
   const bool nobar = TLB_PUSH_EARLY && TLB_STEP_NOBAR && TLB_PACKED_ACC && !dp && a.grad_out == nullptr;
+  // fused data parallelism: the same per-thread early push after the slice counter completed
+  const bool dp_early = TLB_PUSH_EARLY && TLB_DP_PUSH_EARLY && dp && a.grad_out == nullptr;
+  const bool dp_pend = dp_early && TLB_DP_PENDING;  // fused DP: wait for slices 1-7 after conv1 as well
   if (nobar) {
     for (int i = threadIdx.x; i < kPStride; i += blockDim.x) s.G[i] = 0.0f;
     __syncthreads();
@@ -564,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
         }
       }
       // (single GPU: parameter slices 1-7 of the previous step's update land during conv1)
-      const bool pending = !dp && ls > 0;
+      const bool pending = (!dp || dp_pend) && ls > 0;
       const NextBytes nb{buf ^ 1, ((consumed + 1) >> 1) & 1, a.images_wb};
       forward_image<false>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf, pending ? &xbar[2] : nullptr,
                            (uint32_t)((ls - 1) & 1), a.dp_timeout_cycles, a.dp_error, a.pixels ? &nb : nullptr, ls > 0);
@@ -574,7 +583,8 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     }
     // A CTA without an image this step still completes the previous step's slice 1-7 phase before it
     // re-arms that barrier below (an arrival on an incomplete phase would corrupt its count).
-    if (!dp && ls > 0 && lo >= hi) mbar_wait_cluster_guarded(&xbar[2], (uint32_t)((ls - 1) & 1), a.dp_timeout_cycles, a.dp_error);
+    if ((!dp || dp_pend) && ls > 0 && lo >= hi)
+      mbar_wait_cluster_guarded(&xbar[2], (uint32_t)((ls - 1) & 1), a.dp_timeout_cycles, a.dp_error);
     // ---- 2. push slice q of G to its owner q; owner sums the 8 received slices (rank order) ----
     // (nobar: a CTA that trained no image this step passed no barrier since zeroing G: order that first)
     if (nobar && lo >= hi) __syncthreads();
@@ -727,6 +737,15 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
             if (cid == 0) __stcg(a.params + j, s.P[j]);
           }
         }
+        if (dp_early) {  // fused DP: push the updated parameter into the 7 peers right away (as single-GPU)
+          const float v = s.P[j];
+          uint64_t* const pb = rank == 0 ? &xbar[1] : &xbar[2];
+#pragma unroll
+          for (int qi = 0; qi < kCluster - 1; ++qi) {
+            const int q = qi < (int)rank ? qi : qi + 1;
+            st_async_f32(dsmem_map(s.P + j, q), v, dsmem_map(pb, q));
+          }
+        }
       }
       if (blockIdx.x == 0 && threadIdx.x == kSlice) {
         const double l = (double)(long long)(dp ? ld_sys_u64(lacc + b) : __ldcg(lacc + b)) * kUnfix;
@@ -738,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
         }
       }
     }
-    const bool pushed = packed && TLB_PUSH_EARLY;
+    const bool pushed = (packed && TLB_PUSH_EARLY) || dp_early;
     if (!pushed) __syncthreads();
     mark(s, 12);
     // ---- 5. push the updated slice into the other CTAs of the cluster (unless pushed early above) ----
@@ -755,6 +774,11 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     }
     if (!dp) {
       mbar_wait_cluster_guarded(&xbar[1], parity, a.dp_timeout_cycles, a.dp_error);  // slice 0 (1-7: after conv1)
+    } else if (dp_pend) {  // fused DP: slice 0 now (all threads agree on a timeout), slices 1-7 after conv1
+      if (__syncthreads_or(!mbar_wait_cluster_for(&xbar[1], parity, a.dp_timeout_cycles))) {
+        if (threadIdx.x == 0) atomicExch(a.dp_error, 1u);
+        return;
+      }
     } else if (__syncthreads_or(!mbar_wait_cluster_for(&xbar[1], parity, a.dp_timeout_cycles) ||
                                 !mbar_wait_cluster_for(&xbar[2], parity, a.dp_timeout_cycles))) {
       if (threadIdx.x == 0) atomicExch(a.dp_error, 1u);
@@ -767,6 +791,10 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
     if (a.step_end > a.step_begin)
       mbar_wait_cluster_guarded(&xbar[2], (uint32_t)((a.step_end - a.step_begin - 1) & 1), a.dp_timeout_cycles, a.dp_error);
     cluster_sync_all();  // no CTA leaves while a peer's DSMEM traffic may still target it
+  } else if (dp_pend && a.step_end > a.step_begin) {
+    // fused DP: the last step's slices 1-7 have landed before this CTA leaves (bounded: a CTA that gave up
+    // on a peer returned earlier, so no unbounded cluster barrier here)
+    mbar_wait_cluster_guarded(&xbar[2], (uint32_t)((a.step_end - a.step_begin - 1) & 1), a.dp_timeout_cycles, a.dp_error);
   }
 }
 
