@@ -88,19 +88,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
-def build_variant(tag: str, defines: list[str]) -> str:
-    """Developer A/B builds: the library with zhang_kernels.cu compiled under extra -D flags, written to
-    lib/variants/libtloom_b200_<tag>.so (select at run time with TLB_LIB=<path>)."""
+def build_variant(tag: str, defines: list[str], sources: tuple[str, ...] = ("zhang_kernels.cu",)) -> str:
+    """Developer A/B builds: the library with `sources` (default zhang_kernels.cu) compiled under extra -D
+    flags, written to lib/variants/libtloom_b200_<tag>.so (select at run time with TLB_LIB=<path>)."""
     lib = build()
     vdir = os.path.join(OBJ, "variant_" + tag)
     os.makedirs(vdir, exist_ok=True)
-    obj = os.path.join(vdir, "zhang_kernels.o")
-    cmd = [NVCC] + CU_FLAGS + ["-D" + d for d in defines] + ["-c", os.path.join(CSRC, "zhang_kernels.cu"), "-o", obj]
-    out = subprocess.run(cmd, capture_output=True, text=True)
-    if out.returncode != 0:
-        raise RuntimeError(f"variant build failed:\n{out.stderr}")
-    objs = [obj] + [os.path.join(OBJ, os.path.splitext(src)[0].replace("/", "_") + ".o")
-                    for src in SOURCES + HOST_SOURCES if src != "zhang_kernels.cu"]
+    objs = []
+    for src in sources:
+        obj = os.path.join(vdir, os.path.splitext(src)[0] + ".o")
+        cmd = [NVCC] + CU_FLAGS + ["-D" + d for d in defines] + ["-c", os.path.join(CSRC, src), "-o", obj]
+        out = subprocess.run(cmd, capture_output=True, text=True)
+        if out.returncode != 0:
+            raise RuntimeError(f"variant build failed:\n{out.stderr}")
+        objs.append(obj)
+    objs += [os.path.join(OBJ, os.path.splitext(src)[0].replace("/", "_") + ".o")
+             for src in SOURCES + HOST_SOURCES if src not in sources]
     os.makedirs(os.path.join(LIBDIR, "variants"), exist_ok=True)
     vlib = os.path.join(LIBDIR, "variants", f"libtloom_b200_{tag}.so")
     out = subprocess.run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", vlib] + objs, capture_output=True,
