@@ -76,6 +76,11 @@ struct Layout {
 
 extern __shared__ __align__(128) float bt_smem[];
 
+#ifndef TLB_PAIR_SHARE_DEFAULT
+#define TLB_PAIR_SHARE_DEFAULT 0.54f
+#endif
+constexpr float kPairShare = TLB_PAIR_SHARE_DEFAULT;
+
 // logistic(acc + b) with nb = -b log2(e): one FFMA, ex2.approx.ftz, add, rcp.approx.ftz (fast mode).
 __device__ __forceinline__ float logistic(float acc, float nb) {
   constexpr float kNegLog2e = -1.4426950408889634f;
@@ -619,11 +624,39 @@ struct Round {
   int64_t step, e, hi;
 };
 
+// Which examples of a group a CTA trains.  Default: static_chunk(m, grid, cta).  With two CTAs per SM the
+// warp schedulers favour the CTA that arrived first (measured: it finishes its rounds 13% sooner on
+// 144-148 of 148 SMs, profiles/r2/trace_batch_*_trb2.json), so the partner idles through the tail of
+// every step.  Paired mapping: SM pair p (SMs ranked by id) owns static_chunk(m, grid / 2, p); its first
+// CTA (slot 0) trains `share` of it rounded to whole rounds, slot 1 the rest.  The partial row and the
+// loss slot are indexed by the work id 2p + slot, so which examples are summed into which row -- and the
+// result -- does not depend on where the hardware placed the CTAs.
+struct WorkMap {
+  int wid;      // work id: partial row, chunk
+  int paired;   // 1: SM-pair mapping
+  float share;  // slot 0's share of the pair's examples
+};
+
 template <int NI>
-__device__ __forceinline__ bool first_round(const TrainArgs& a, int64_t from, Round& r) {
+__device__ __forceinline__ void work_chunk(int64_t m, const WorkMap& w, int64_t& lo, int64_t& hi) {
+  if (!w.paired) {
+    static_chunk(m, gridDim.x, w.wid, lo, hi);
+    return;
+  }
+  int64_t plo, phi;
+  static_chunk(m, gridDim.x / 2, w.wid >> 1, plo, phi);
+  const int64_t len = phi - plo;
+  int64_t s0 = (int64_t)__fmul_rn(w.share, (float)len);
+  s0 = min(len, (s0 + NI / 2) / NI * NI);
+  if (w.wid & 1) lo = plo + s0, hi = phi;
+  else lo = plo, hi = plo + s0;
+}
+
+template <int NI>
+__device__ __forceinline__ bool first_round(const TrainArgs& a, const WorkMap& w, int64_t from, Round& r) {
   for (int64_t st = from; st < a.step_end; ++st) {
     int64_t lo, hi;
-    static_chunk(local_size(a, st), gridDim.x, blockIdx.x, lo, hi);
+    work_chunk<NI>(local_size(a, st), w, lo, hi);
     if (lo < hi) {
       r = Round{st, lo, hi};
       return true;
@@ -632,12 +665,53 @@ __device__ __forceinline__ bool first_round(const TrainArgs& a, int64_t from, Ro
   return false;
 }
 template <int NI>
-__device__ __forceinline__ bool next_round(const TrainArgs& a, Round& r) {
+__device__ __forceinline__ bool next_round(const TrainArgs& a, const WorkMap& w, Round& r) {
   if (r.e + NI < r.hi) {
     r.e += NI;
     return true;
   }
-  return first_round<NI>(a, r.step + 1, r);
+  return first_round<NI>(a, w, r.step + 1, r);
+}
+
+// Paired mapping (MINB == 2): every CTA publishes (SM id, arrival slot on its SM); after a grid barrier each
+// CTA ranks its SM among the SMs present.  Any SM without exactly two CTAs (or an odd grid) keeps the
+// default mapping on every CTA -- all CTAs read the same table, so they agree.  `scratch` holds >= 544 ints.
+__device__ WorkMap pair_map(const TrainArgs& a, int* scratch, unsigned int& target) {
+  constexpr int kMaxSm = 512;
+  static_assert((kMaxSm + kPairMaxGrid) * 4 <= kBatchWorkExtraBytes, "slot counters + table fit");
+  const int t = threadIdx.x, T = blockDim.x, nb = gridDim.x;
+  unsigned int* slots = reinterpret_cast<unsigned int*>(a.work + (int64_t)nb * kPStride);  // zeroed at launch
+  unsigned int* table = slots + kMaxSm;
+  if (t == 0) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const unsigned int slot = smid < kMaxSm ? atomicAdd(slots + smid, 1u) : 2u;
+    __stcg(table + blockIdx.x, smid < kMaxSm && slot < 2 ? (smid << 1 | slot) : 0xffffffffu);
+  }
+  grid_sync(a.barrier, target);
+  int* hist = scratch;           // [kMaxSm] CTAs per SM id
+  int* flags = scratch + kMaxSm;  // [0] bad, [1] my SM's rank x 2
+  for (int q = t; q < kMaxSm; q += T) hist[q] = 0;
+  if (t < 2) flags[t] = 0;
+  __syncthreads();
+  for (int q = t; q < nb; q += T) {
+    const unsigned int v = __ldcg(table + q);
+    if (v == 0xffffffffu) flags[0] = 1;
+    else atomicAdd(hist + (v >> 1), 1);
+  }
+  __syncthreads();
+  const unsigned int mine = __ldcg(table + blockIdx.x);
+  int below = 0;
+  for (int q = t; q < kMaxSm; q += T) {
+    if (hist[q] != 0 && hist[q] != 2) flags[0] = 1;
+    if (mine != 0xffffffffu && q < (int)(mine >> 1)) below += hist[q];
+  }
+  if (below) atomicAdd(flags + 1, below);
+  __syncthreads();
+  WorkMap w{(int)blockIdx.x, 0, 0.5f};
+  if (!flags[0] && (nb & 1) == 0) w = WorkMap{flags[1] + (int)(mine & 1), 1, a.pair_share};
+  __syncthreads();  // scratch is reused by the caller
+  return w;
 }
 
 // Issuer: the round's labels (cp.async, completed at the round's start) and ONE bulk copy of its images.
@@ -693,11 +767,13 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
     mbar_init(&bar[1], 1);
     fence_barrier_init();
   }
+  WorkMap wm{(int)blockIdx.x, 0, 0.5f};
+  if (MINB == 2 && a.pair_share > 0.0f) wm = pair_map(a, reinterpret_cast<int*>(regs), target);
   for (int q = t; q < NI * kImgRegion; q += T) regs[q] = 0.0f;  // dz2 pad rows stay zero
   __syncthreads();
   const bool issuer = t == T - 32;  // lane 0 of the last warp (idle in S2/S6 of a full round)
   Round pf;
-  bool pf_valid = first_round<NI>(a, a.step_begin, pf);
+  bool pf_valid = first_round<NI>(a, wm, a.step_begin, pf);
   if (issuer && pf_valid) issue_round<NI>(a, ring, pxring, rb, lab, bar, 0, pf);
   if (pf_valid && step_bytes(a, pf.step)) {  // the first round's bytes: converted by every thread
     __syncthreads();
@@ -707,13 +783,26 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
   }
   uint32_t consumed = 0;
 
+  // profiling (tlb_ctx_set_trace): per step and CTA, globaltimer stamps [8]: 0 step start (weights
+  // staged), 1 rounds done, 2 after grid barrier 1, 3 reduction done, 4 after grid barrier 2, 5 rounds;
+  // step 0's row also holds 6 the SM id and 7 the kernel entry time
+  unsigned long long* const trace = (a.trace && t == 0) ? a.trace + (int64_t)blockIdx.x * 8 : nullptr;
+  const auto stamp = [&](int64_t st, int k) {
+    if (trace) trace[(st - a.step_begin) * nb * 8 + k] = globaltimer_ns();
+  };
+  if (trace) {  // 6: SM id, 7: kernel entry (step 0's row)
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    trace[6] = smid;
+    trace[7] = globaltimer_ns();
+  }
   int64_t ks = umod(a.step_begin, a.steps_per_epoch), ep = udiv(a.step_begin, a.steps_per_epoch);
   for (int64_t st = a.step_begin; st < a.step_end; ++st, ks = ks + 1 == a.steps_per_epoch ? (++ep, 0) : ks + 1) {
     int64_t l_lo, l_hi;
     local_range_k(a, ks, l_lo, l_hi);
     const int64_t m = l_hi - l_lo;
     int64_t lo, hi;
-    static_chunk(m, nb, blockIdx.x, lo, hi);
+    work_chunk<NI>(m, wm, lo, hi);
 
     // ---- the step's weights -> shared (+ padded conv copies), zero the CTA gradient ----
     {
@@ -740,6 +829,7 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
     __syncthreads();
 
     double cta_loss = 0.0;  // thread 0: this CTA's example losses in example order (fp64)
+    stamp(st, 0);
     for (int64_t e = lo; e < hi; e += NI) {
       const int cnt = (int)min((int64_t)NI, hi - e);
       const int buf = consumed & 1;
@@ -749,7 +839,7 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
         rbst[buf ^ 1] = 0;    // (issue_round sets it for a next round that arrives as bytes)
         if (pf_valid) {
           Round nx = pf;
-          if (next_round<NI>(a, nx)) {
+          if (next_round<NI>(a, wm, nx)) {
             issue_round<NI>(a, ring, pxring, rb, lab, bar, buf ^ 1, nx);  // buf^1 was last read by the previous round's S6
             pf = nx;
           } else {
@@ -863,15 +953,18 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
     }
 
     // ---- CTA partial -> work row; grid barrier; ordered reduction + sgd_step; grid barrier ----
-    if (lo < hi) {
-      float4* dst = reinterpret_cast<float4*>(a.work + (int64_t)blockIdx.x * kPStride);
+    stamp(st, 1);
+    if (trace) trace[(st - a.step_begin) * nb * 8 + 5] = (unsigned long long)((hi - lo + NI - 1) / NI);
+    if (lo < hi || wm.paired) {  // paired mapping: every row is written (zero if its chunk is empty)
+      float4* dst = reinterpret_cast<float4*>(a.work + (int64_t)wm.wid * kPStride);
       const float4* src = reinterpret_cast<const float4*>(G);
       for (int q = t; q < kPStride / 4; q += T) __stcg(dst + q, src[q]);
-      if (t == 0) a.loss_part[blockIdx.x] = cta_loss;
+      if (t == 0) a.loss_part[wm.wid] = cta_loss;
     }
     grid_sync(a.barrier, target);
+    stamp(st, 2);
     const int64_t block = m > 0 ? udiv(m + nb - 1, nb) : 1;
-    const int64_t nrows = m > 0 ? udiv(m + block - 1, block) : 0;  // CTAs that had examples
+    const int64_t nrows = wm.paired ? nb : m > 0 ? udiv(m + block - 1, block) : 0;  // rows with examples
     {
       int64_t j0, j1;
       static_chunk(kNParam, nb, blockIdx.x, j0, j1);
@@ -919,7 +1012,9 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
         else a.epoch_loss[ep] = (ks == a.steps_per_epoch - 1) ? __ddiv_rn(l, (double)a.n) : l;
       }
     }
+    stamp(st, 3);
     grid_sync(a.barrier, target);
+    stamp(st, 4);
   }
 }
 
@@ -929,6 +1024,15 @@ cudaError_t prep(int* occ) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Layout<NI>::kBytes);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, T, Layout<NI>::kBytes);
+}
+
+// Slot 0's share of an SM pair's examples (TLB_PAIR_SHARE overrides; 0 = per-CTA static chunks).
+inline float pair_share() {
+  static const float v = [] {
+    const char* e = std::getenv("TLB_PAIR_SHARE");
+    return e ? std::strtof(e, nullptr) : kPairShare;
+  }();
+  return v;
 }
 
 template <int NI, int T, int MINB, bool PAIR>
@@ -944,7 +1048,13 @@ cudaError_t launch_cfg(const TrainArgs& a, int sm_count, int64_t m_max, cudaStre
   }
   e = cudaMemsetAsync(a.barrier, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return e;
-  void* args[] = {const_cast<TrainArgs*>(&a)};
+  TrainArgs la = a;
+  la.pair_share = (MINB == 2 && grid % 2 == 0 && grid <= kPairMaxGrid) ? pair_share() : 0.0f;
+  if (la.pair_share > 0.0f) {  // the paired mapping's per-SM slot counters (after the grid's partial rows)
+    e = cudaMemsetAsync(a.work + (int64_t)grid * kPStride, 0, 512 * sizeof(unsigned int), st);
+    if (e != cudaSuccess) return e;
+  }
+  void* args[] = {&la};
   return cudaLaunchCooperativeKernel((const void*)train_batch_kernel<NI, T, MINB, PAIR>, dim3(grid), dim3(T), args,
                                      Layout<NI>::kBytes, st);
 }

@@ -532,7 +532,9 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
                              : train_grid(c, std::max<int64_t>(m_local, 1), threads);
   if (grid <= 0) return fail(TLB_ERR_CUDA, "train: batched kernel configuration failed");
   const int64_t rows = exact(c) ? std::max<int64_t>(m_local, 1) : grid;
-  TLB_CUDA(c->work.ensure(clustered ? tlb::cluster_work_bytes() : (size_t)rows * TLB_PSTRIDE * sizeof(float)));
+  TLB_CUDA(c->work.ensure(clustered ? tlb::cluster_work_bytes()
+                                     : (size_t)rows * TLB_PSTRIDE * sizeof(float) +
+                                           (batched ? tlb::kBatchWorkExtraBytes : 0)));
   TLB_CUDA(c->losses.ensure((size_t)std::max<int64_t>(m_local, 1) * sizeof(float)));
   TLB_CUDA(c->barrier.ensure(tlb::cluster_size() * sizeof(unsigned int)));
   TLB_CUDA(c->loss_part.ensure((size_t)(clustered ? 2 * clusters : grid) * sizeof(double)));

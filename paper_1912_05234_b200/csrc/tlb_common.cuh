@@ -170,6 +170,13 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 
 // Sense-free grid barrier for a cooperative (co-resident) launch.  `target` advances by gridDim.x
 // on every call; the counter is zeroed by the host before each launch.
+// Device-wide nanosecond clock (same time base on every SM; profiling stamps).
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+
 __device__ __forceinline__ void grid_sync(unsigned int* counter, unsigned int& target) {
   __syncthreads();
   target += gridDim.x;

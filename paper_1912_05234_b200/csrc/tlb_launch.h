@@ -79,6 +79,9 @@ struct TrainArgs {
   float* md_params[8];
   double* md_epoch_loss[8];
   unsigned int* md_bar;
+  // Batched kernel with two CTAs per SM (batch_train.cu): the CTA that reaches the SM's slot counter first
+  // is scheduled ahead of its partner; it trains this share of the SM's examples (set at launch).
+  float pair_share;
 };
 
 struct CellArgs {
@@ -119,6 +122,9 @@ cudaError_t launch_cells(bool exact, const CellArgs& a, int grid, cudaStream_t s
 cudaError_t launch_eval(bool exact, const EvalArgs& a, int grid, int threads, cudaStream_t st);
 // Fast-mode batched train kernel for large groups (batch_train.cu): NI images per CTA round.
 int batch_train_grid(int sm_count, int64_t m_max);
+// The batched kernel's work buffer: [grid][3904] partial rows + this many bytes (SM-pair mapping scratch).
+constexpr size_t kBatchWorkExtraBytes = 8192;
+constexpr int kPairMaxGrid = 1024;
 cudaError_t launch_train_batch(const TrainArgs& a, int sm_count, int64_t m_max, cudaStream_t st);
 // Fast-mode batched inference (infer_kernels.cu): forward + argmax + correct count over n images.
 cudaError_t launch_infer(const EvalArgs& a, int sm_count, cudaStream_t st);

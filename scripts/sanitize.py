@@ -16,8 +16,8 @@ from paper_1912_05234_b200 import Context  # noqa: E402
 from paper_1912_05234_b200.runtime import (init_params, synth_make_set, wide_init_params,  # noqa: E402
                                            wide_make_set)
 
-CASES = ["train_exact", "train_fast_cluster", "train_fast_flat", "forward", "cells", "eval", "wide_tc", "wide_fp32",
-         "synth"]
+CASES = ["train_exact", "train_fast_cluster", "train_fast_flat", "train_batched", "train_batched_big", "forward",
+         "cells", "eval", "wide_tc", "wide_fp32", "synth"]
 ap = argparse.ArgumentParser()
 ap.add_argument("--only", default=",".join(CASES))
 args = ap.parse_args()
@@ -34,6 +34,15 @@ for case in args.only.split(","):
         with Context(0, mode="fast") as c:
             c.set_cluster(False)
             c.train(p0, x[:12], y[:12], epochs=1, batch=6)
+    elif case == "train_batched":  # batch_train.cu (TLB_BATCH_CFG picks the configuration)
+        with Context(0, mode="fast") as c:
+            c.set_batched(1)
+            c.train(p0, x[:12], y[:12], epochs=1, batch=6)
+    elif case == "train_batched_big":  # a full grid: with 2 CTAs per SM the SM-pair work mapping is live
+        bx, by = synth_make_set(600, 2)
+        with Context(0, mode="fast") as c:
+            c.set_batched(1)
+            c.train(p0, bx, by, epochs=1, batch=600)
     elif case == "forward":
         with Context(0, mode="exact") as c:
             c.forward(x[:4], p0, acts=True)

@@ -78,8 +78,44 @@ def test_batch_16k_vs_oracle(orc):
     want_p, want_l = orc.train(x, y, p0, epochs=1, batch=16384)
     with Context(0, mode="fast") as c:
         got_p, got_l = c.train(p0, x, y, epochs=1, batch=16384)
+        again_p, again_l = c.train(p0, x, y, epochs=1, batch=16384)
     check_weights(got_p, want_p)
     assert rel(got_l, want_l) <= REL_TOL
+    # two CTAs per SM, SM-pair work mapping: rows follow (SM rank, slot), not the hardware's placement
+    assert np.array_equal(bits(got_p), bits(again_p)) and list(got_l) == list(again_l)
+
+
+_SHARE_RUN = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from paper_1912_05234_b200 import Context
+d = np.load({inp!r})
+with Context(0, mode="fast") as c:
+    p, l = c.train(d["p0"], d["x"], d["y"], epochs=1, batch=16384)
+np.savez({out!r}, p=p, l=np.asarray(l))
+"""
+
+
+@pytest.mark.parametrize("share", ["0", "0.62"])
+def test_batch_16k_pair_share_variants(orc, tmp_path, share):
+    """The SM-pair mapping's split (TLB_PAIR_SHARE; 0 = per-CTA static chunks) moves examples between the
+    two partial rows of an SM pair; every split must train the same group to within the tolerance."""
+    import os
+    import subprocess
+    import sys
+    x, y = orc.make_set(32768, 1)
+    p0 = orc.init_params(42)
+    want_p, want_l = orc.train(x, y, p0, epochs=1, batch=16384)
+    inp, out = str(tmp_path / "in.npz"), str(tmp_path / "out.npz")
+    np.savez(inp, x=x, y=y, p0=p0)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TLB_PAIR_SHARE=share)
+    r = subprocess.run([sys.executable, "-c", _SHARE_RUN.format(root=root, inp=inp, out=out)], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = np.load(out)
+    check_weights(got["p"], want_p)
+    assert rel(got["l"], want_l) <= REL_TOL
 
 
 def test_batch_256k_tiled_group_equals_base_step(orc, zhang_sets):
