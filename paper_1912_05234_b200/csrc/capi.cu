@@ -111,6 +111,7 @@ struct tlb_ctx {
   int batched = -1;  // batched fast train kernel: -1 auto (TLB_BATCHED or the group-size rule), 0 off, 1 on
   bool one_epoch_call = false;  // tlb_train* of a single epoch: byte-ingested images need no fp32 write-back
   DevBuf work, losses, loss_part, barrier;  // persistent-train workspaces
+  DevBuf eval_claim;                         // batched inference: round counter
   DevBuf stage[8];                 // host-API staging buffers
   // Overlapped ingestion for tlb_train: the dataset is copied chunk by chunk on `copy_stream` while
   // the train kernel runs; a stream memory operation raises ready[k] to the call's token after
@@ -676,6 +677,7 @@ int tlb_ctx_destroy(tlb_ctx* c) {
   c->losses.release();
   c->loss_part.release();
   c->barrier.release();
+  c->eval_claim.release();
   for (auto& s : c->stage) s.release();
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   if (c->copy_stream2) cudaStreamSynchronize(c->copy_stream2);
@@ -1346,8 +1348,10 @@ int tlb_evaluate_device(tlb_ctx* c, const float* d_images, const int32_t* d_labe
   if (!c || !d_params) return fail(TLB_ERR_ARG, "tlb_evaluate_device: null argument");
   if (n <= 0) return TLB_OK;
   TLB_TRY(set_device(c));
-  tlb::EvalArgs a{d_images, d_labels, n, d_params, d_pred, nullptr, d_correct};
+  tlb::EvalArgs a{d_images, d_labels, n, d_params, d_pred, nullptr, d_correct, nullptr};
   if (!exact(c) && c->grid_override == 0 && c->threads_override == 0) {  // batched forward-only kernel
+    TLB_CUDA(c->eval_claim.ensure(sizeof(unsigned long long)));
+    a.claim = static_cast<unsigned long long*>(c->eval_claim.p);
     TLB_CUDA(tlb::launch_infer(a, c->sm_count, c->stream));
     return TLB_OK;
   }

@@ -335,6 +335,11 @@ __global__ void __launch_bounds__(THREADS, MINB) infer_kernel(EvalArgs a) {
 
   int64_t lo, hi;
   static_chunk(a.n, gridDim.x, blockIdx.x, lo, hi);
+  // Dynamic rounds (a.claim): thread 0 claims round indices two ahead (the atomic's latency hides behind a
+  // round); sfirst[buf] = first image of the round in ring buffer buf, -1 = none (the CTA is done).
+  __shared__ int64_t sfirst[2];
+  const int64_t nrounds = (a.n + NI - 1) / NI;
+  unsigned long long pending = 0;
   if (t == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -372,19 +377,42 @@ __global__ void __launch_bounds__(THREADS, MINB) infer_kernel(EvalArgs a) {
   }
   __syncthreads();
   auto issue = [&](int buf, int64_t first) {  // thread 0: one bulk copy for the round's images
-    const int cnt = (int)min((int64_t)NI, hi - first);
+    const int cnt = (int)min((int64_t)NI, (a.claim ? a.n : hi) - first);
     fence_proxy_async_smem();
     mbar_arrive_expect_tx(&bar[buf], (uint32_t)(cnt * kImg * sizeof(float)));
     tma_load_1d(ring + buf * NI * kImg, a.images + first * kImg, (uint32_t)(cnt * kImg * sizeof(float)), &bar[buf]);
   };
-  if (t == 0 && lo < hi) issue(0, lo);
+  if (a.claim) {
+    if (t == 0) {
+      const unsigned long long r0 = atomicAdd(a.claim, 1ull);
+      pending = atomicAdd(a.claim, 1ull);
+      sfirst[0] = (int64_t)r0 < nrounds ? (int64_t)r0 * NI : -1;
+      if (sfirst[0] >= 0) issue(0, sfirst[0]);
+    }
+    __syncthreads();
+  } else if (t == 0 && lo < hi) {
+    issue(0, lo);
+  }
   unsigned long long correct = 0;
   uint32_t round = 0;
-  for (int64_t first = lo; first < hi; first += NI, ++round) {
+  for (int64_t first = lo;; first += NI, ++round) {
     const int buf = round & 1;
-    const int cnt = (int)min((int64_t)NI, hi - first);
+    if (a.claim) first = sfirst[buf];  // written by thread 0 before the previous round's first barrier
+    if (a.claim ? first < 0 : first >= hi) break;
+    const int cnt = (int)min((int64_t)NI, (a.claim ? a.n : hi) - first);
     mbar_wait(&bar[buf], (round >> 1) & 1);
-    if (t == 0 && first + NI < hi) issue(buf ^ 1, first + NI);  // buffer buf^1 was last read before this round
+    if (t == 0) {  // buffer buf^1 was last read before this round
+      if (a.claim) {
+        const int64_t nx = (int64_t)pending < nrounds ? (int64_t)pending * NI : -1;
+        sfirst[buf ^ 1] = nx;
+        if (nx >= 0) {
+          issue(buf ^ 1, nx);
+          pending = atomicAdd(a.claim, 1ull);  // consumed a round later
+        }
+      } else if (first + NI < hi) {
+        issue(buf ^ 1, first + NI);
+      }
+    }
     const float* imgs = ring + buf * NI * kImg;
     for (int it = t; it < cnt * 144; it += THREADS) {
       if constexpr (PAIR) conv1_item_p(P, W1, imgs, s1s, it);
@@ -426,7 +454,13 @@ cudaError_t launch_cfg(const EvalArgs& a, int sm_count, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int64_t rounds = (a.n + NI - 1) / NI;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(rounds, (int64_t)std::max(occ, 1) * sm_count));
-  kern<<<grid, THREADS, smem, st>>>(a);
+  EvalArgs la = a;
+  if (std::getenv("TLB_INFER_STATIC")) la.claim = nullptr;  // A/B: static per-CTA chunks
+  if (la.claim) {
+    e = cudaMemsetAsync(la.claim, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<grid, THREADS, smem, st>>>(la);
   return cudaGetLastError();
 }
 

@@ -105,6 +105,9 @@ struct EvalArgs {
   int32_t* pred;   // nullable
   float* yhat;     // nullable
   unsigned long long* correct;  // nullable
+  // Batched inference: rounds are claimed from this counter (zeroed at launch) so co-resident CTAs share
+  // the work however the schedulers favour them; nullptr = static per-CTA chunks.
+  unsigned long long* claim;
 };
 
 size_t smem_bytes();
