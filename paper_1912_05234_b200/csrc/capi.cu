@@ -70,6 +70,15 @@ struct DevBuf {
   }
 };
 
+// Per-context result block (device, mirrored in the pinned host block of a host call): the error words,
+// the parameters and up to kOutEpochs epoch losses, so tlb_train's results return in ONE D2H copy (four
+// small copies had cost 16-20 us per call after the kernel).
+constexpr size_t kOutParamOff = 8 * sizeof(unsigned int);
+constexpr size_t kOutLossOff = kOutParamOff + TLB_PSTRIDE * sizeof(float);
+constexpr int32_t kOutEpochs = 1024;
+constexpr size_t kOutBytes = kOutLossOff + kOutEpochs * sizeof(double);
+static_assert(kOutLossOff % 8 == 0, "fp64 losses");
+
 struct HostBuf {  // pinned host memory (async H2D/D2H staging of small per-call blocks)
   void* p = nullptr;
   size_t cap = 0;
@@ -112,6 +121,7 @@ struct tlb_ctx {
   bool one_epoch_call = false;  // tlb_train* of a single epoch: byte-ingested images need no fp32 write-back
   DevBuf work, losses, loss_part, barrier;  // persistent-train workspaces
   DevBuf eval_claim;                         // batched inference: round counter
+  DevBuf outblk;  // [dev_err 4 | ready_err 4 words | params | epoch losses]: one D2H per host call (kOut*)
   DevBuf stage[8];                 // host-API staging buffers
   // Overlapped ingestion for tlb_train: the dataset is copied chunk by chunk on `copy_stream` while
   // the train kernel runs; a stream memory operation raises ready[k] to the call's token after
@@ -569,6 +579,10 @@ int enqueue_train(tlb_ctx* c, const float* d_images, const int32_t* d_labels, in
   a.ready_token = token;
   a.chunk = chunk;
   a.ready_step_end = a.step_begin + spe;  // only the call's first epoch can outrun the copies
+  a.ready_g0 = a.step_begin % spe;        // the ramp's chunk of a group without divisions on the device
+  a.chunk_shift = 0;
+  if (chunk < 0)
+    while ((int64_t)1 << (a.chunk_shift + 1) <= -chunk) ++a.chunk_shift;
   a.dp_error = static_cast<unsigned int*>(c->dev_err.p);        // single GPU: abort word of the bounded waits
   a.fix_err = static_cast<unsigned int*>(c->dev_err.p) + 1;
   a.dp_timeout_cycles = (long long)(kWaitLimitSeconds * 2.0e9);  // ~2 GHz SM clock
@@ -648,10 +662,13 @@ int tlb_ctx_create(int device, tlb_ctx** out) {
     (void)cudaGetLastError();  // no cluster launch on this device: the flat kernel is used
     c->max_clusters = 0;
   }
-  if (e == cudaSuccess) e = c->ready_err.ensure(4 * sizeof(unsigned int));
-  if (e == cudaSuccess) e = c->dev_err.ensure(4 * sizeof(unsigned int));
-  if (e == cudaSuccess) e = cudaMemset(c->dev_err.p, 0, 4 * sizeof(unsigned int));
-  if (e == cudaSuccess) e = cudaMemset(c->ready_err.p, 0, 4 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = c->outblk.ensure(kOutBytes);
+  if (e == cudaSuccess) e = cudaMemset(c->outblk.p, 0, kOutBytes);
+  if (e == cudaSuccess) {  // views into outblk (never freed on their own)
+    c->dev_err.p = c->outblk.p;
+    c->ready_err.p = static_cast<char*>(c->outblk.p) + 4 * sizeof(unsigned int);
+    c->dev_err.cap = c->ready_err.cap = 4 * sizeof(unsigned int);
+  }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream2, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->copy_gate, cudaEventDisableTiming);
@@ -682,8 +699,9 @@ int tlb_ctx_destroy(tlb_ctx* c) {
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   if (c->copy_stream2) cudaStreamSynchronize(c->copy_stream2);
   c->ready.release();
-  c->ready_err.release();
-  c->dev_err.release();
+  c->ready_err.p = c->dev_err.p = nullptr;  // views into outblk
+  c->ready_err.cap = c->dev_err.cap = 0;
+  c->outblk.release();
   c->pin.release();
   c->bounce.release();
   for (cudaEvent_t ev : c->bounce_ev) cudaEventDestroy(ev);
@@ -828,14 +846,29 @@ struct HostTrace {
   bool on;
   std::chrono::steady_clock::time_point t0;
   std::string log;
+  cudaEvent_t ev[4] = {};  // device-side: before the kernel, after it, after the D2H, (spare)
+  int nev = 0;
   HostTrace() : on(std::getenv("TLB_HOST_TRACE") != nullptr), t0(std::chrono::steady_clock::now()) {}
   void mark(const char* what) {
     if (!on) return;
     const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
     log += std::string(" ") + what + "=" + std::to_string((int)us);
   }
+  void event(cudaStream_t st) {  // device timeline stamp on the stream (trace mode only)
+    if (!on || nev >= 4) return;
+    cudaEventCreate(&ev[nev]);
+    cudaEventRecord(ev[nev++], st);
+  }
   ~HostTrace() {
-    if (on) fprintf(stderr, "tlb_train host us:%s\n", log.c_str());
+    if (!on) return;
+    for (int i = 1; i < nev; ++i) {
+      float ms = 0.0f;
+      cudaEventSynchronize(ev[i]);
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      log += " dev" + std::to_string(i) + "=" + std::to_string((int)(ms * 1000.0f));
+    }
+    for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
+    fprintf(stderr, "tlb_train host us:%s\n", log.c_str());
   }
 };
 
@@ -1056,17 +1089,25 @@ static int train_host(tlb_ctx* c, HostImages src, const int32_t* labels, int64_t
   }
   const unsigned int* rdy = overlap ? static_cast<const unsigned int*>(c->ready.p) : nullptr;
   TLB_TRY(stage_in(c, 1, labels, (size_t)n, &d_lab));
-  TLB_TRY(stage_out(c, 2, TLB_PSTRIDE, &d_p));
+  // params / losses / watchdog words: the context's result block (one D2H at the end) mirrored by a pinned
+  // host block (async copies, one sync); calls of more than kOutEpochs epochs stage params / losses apart
+  const bool one_copy = epochs <= kOutEpochs;
+  char* const ob = static_cast<char*>(c->outblk.p);
+  if (one_copy) {
+    d_p = reinterpret_cast<float*>(ob + kOutParamOff);
+    d_loss = reinterpret_cast<double*>(ob + kOutLossOff);
+  } else {
+    TLB_TRY(stage_out(c, 2, TLB_PSTRIDE, &d_p));
+    TLB_TRY(stage_out(c, 3, (size_t)epochs, &d_loss));
+  }
   TLB_CUDA(cudaMemsetAsync(d_p, 0, TLB_PSTRIDE * sizeof(float), c->stream));
-  // params / losses / watchdog words travel through a pinned host block (async copies, one sync)
-  const size_t pin_bytes = TLB_PSTRIDE * sizeof(float) + (size_t)epochs * sizeof(double) + 8 * sizeof(unsigned int);
-  TLB_CUDA(c->pin.ensure(pin_bytes));
-  float* h_p = static_cast<float*>(c->pin.p);
-  double* h_loss = reinterpret_cast<double*>(h_p + TLB_PSTRIDE);
-  unsigned int* h_err = reinterpret_cast<unsigned int*>(h_loss + epochs);
+  TLB_CUDA(c->pin.ensure(kOutLossOff + (size_t)epochs * sizeof(double)));
+  char* const hb = static_cast<char*>(c->pin.p);
+  unsigned int* h_err = reinterpret_cast<unsigned int*>(hb);  // [0..3] dev_err, [4..6] ready_err
+  float* h_p = reinterpret_cast<float*>(hb + kOutParamOff);
+  double* h_loss = reinterpret_cast<double*>(hb + kOutLossOff);
   std::memcpy(h_p, params, TLB_NPARAM * sizeof(float));
   TLB_CUDA(cudaMemcpyAsync(d_p, h_p, TLB_NPARAM * sizeof(float), cudaMemcpyHostToDevice, c->stream));
-  TLB_TRY(stage_out(c, 3, (size_t)epochs, &d_loss));
   // Launch the kernel first, then enqueue the chunk copies (the host's enqueue calls overlap the running
   // kernel, which polls the ready flags): pinned sources DMA straight from the caller's memory, pageable
   // ones through the pinned bounce slots filled by host worker threads (ingest_pageable).
@@ -1092,8 +1133,10 @@ static int train_host(tlb_ctx* c, HostImages src, const int32_t* labels, int64_t
   } reset_flag{c};
   if (copies_first) TLB_TRY(ingest_images(c, src, d_img, n, chunk, batch, c->ready_token));
   if (!on_epoch) {
+    ht.event(c->stream);
     TLB_TRY(enqueue_train(c, d_img, d_lab, n, d_p, rate, 0, epochs, batch, d_loss, 0, 0, -1, nullptr, nullptr,
                           rdy, c->ready_token, chunk, nullptr, src.d_u8));
+    ht.event(c->stream);
     ht.mark("launched");
     if (overlap && !copies_first) TLB_TRY(ingest());
     ht.mark("ingest_enqueued");
@@ -1107,15 +1150,20 @@ static int train_host(tlb_ctx* c, HostImages src, const int32_t* labels, int64_t
       on_epoch(e + 1, mean, user);
     }
   }
-  TLB_CUDA(cudaMemcpyAsync(h_p, d_p, TLB_NPARAM * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-  if (epoch_loss) TLB_CUDA(cudaMemcpyAsync(h_loss, d_loss, epochs * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  if (overlap) TLB_CUDA(cudaMemcpyAsync(h_err, c->ready_err.p, 3 * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
-  TLB_CUDA(cudaMemcpyAsync(h_err + 4, c->dev_err.p, 4 * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+  if (one_copy) {  // error words + params (+ losses) in one copy
+    TLB_CUDA(cudaMemcpyAsync(hb, ob, kOutLossOff + (epoch_loss ? epochs * sizeof(double) : 0), cudaMemcpyDeviceToHost,
+                             c->stream));
+  } else {
+    TLB_CUDA(cudaMemcpyAsync(h_p, d_p, TLB_NPARAM * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    if (epoch_loss) TLB_CUDA(cudaMemcpyAsync(h_loss, d_loss, epochs * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    TLB_CUDA(cudaMemcpyAsync(h_err, ob, 8 * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+  }
+  ht.event(c->stream);
   ht.mark("d2h_enqueued");
   TLB_CUDA(cudaStreamSynchronize(c->stream));
   ht.mark("stream_synced");
   {
-    const unsigned int dev_words[4] = {h_err[4], h_err[5], h_err[6], h_err[7]};
+    const unsigned int dev_words[4] = {h_err[0], h_err[1], h_err[2], h_err[3]};
     TLB_TRY(device_status(c, dev_words));  // params stay untouched on a device failure
   }
   std::memcpy(params, h_p, TLB_NPARAM * sizeof(float));
@@ -1123,7 +1171,7 @@ static int train_host(tlb_ctx* c, HostImages src, const int32_t* labels, int64_t
   if (overlap) {
     TLB_CUDA(cudaStreamSynchronize(c->copy_stream));  // (the kernel consumed every chunk: already done)
     TLB_CUDA(cudaStreamSynchronize(c->copy_stream2));
-    const unsigned int err[3] = {h_err[0], h_err[1], h_err[2]};
+    const unsigned int err[3] = {h_err[4], h_err[5], h_err[6]};
     if (err[0]) {
       TLB_CUDA(cudaMemset(c->ready_err.p, 0, sizeof(err)));
       return fail(TLB_ERR_CUDA, "tlb_train: dataset chunk " + std::to_string(err[1]) + " never became ready (flag " +

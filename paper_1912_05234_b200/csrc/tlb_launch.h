@@ -40,6 +40,8 @@ struct TrainArgs {
   int64_t chunk;  // (chunk < 0: ramp of -chunk = C groups, a power of two: chunks of groups 0 | 1 | 2-3 |
                   //  4-7 | ... up to C, then C groups each -- the first step waits for one group only)
   int64_t ready_step_end;
+  int64_t ready_g0;  // group (within its epoch) of step_begin
+  int chunk_shift;   // ramp: log2 C
   unsigned int* ready_err;  // [3] diagnostic words: set when a ready flag never arrives (then the kernel
                             // proceeds and the host call fails instead of hanging)
   // Fused data parallelism over NVLink peer memory (clustered kernel, dp_world > 0): rank dp_rank of

@@ -88,14 +88,17 @@ __device__ __forceinline__ const float* job_image(const TrainArgs& a, const Job&
 __device__ __forceinline__ void wait_ready_at(const TrainArgs& a, int64_t step, int64_t index) {
   if (!a.ready || step >= a.ready_step_end) return;
   int64_t k;
+  // g = step's group in its epoch: steps < ready_step_end lie within one epoch of step_begin, so no
+  // division (the issuer computes this on every job; the divisions had cost ~0.3 us per batch-100 step)
+  int64_t g = step - a.step_begin + a.ready_g0;
+  if (g >= a.steps_per_epoch) g -= a.steps_per_epoch;
   if (a.chunk > 0) {
     k = udiv(index, a.chunk);
   } else if (a.chunk < 0) {  // ramp (see TrainArgs::chunk): groups 0 | 1 | 2-3 | ... | C/2..C-1, then C each
-    const int64_t C = -a.chunk, g = umod(step, a.steps_per_epoch);
+    const int64_t C = -a.chunk;
     if (g < C) k = g == 0 ? 0 : 64 - __clzll((long long)g);
-    else k = (63 - __clzll((long long)C)) + 1 + udiv(g - C, C);
+    else k = a.chunk_shift + 1 + ((g - C) >> a.chunk_shift);
   } else {  // geometric (see TrainArgs::chunk): groups 0, 1, then [2^e, 2^e + 2^(e-1)), [.., 2^(e+1))
-    const int64_t g = umod(step, a.steps_per_epoch);
     if (g < 2) {
       k = g;
     } else {
