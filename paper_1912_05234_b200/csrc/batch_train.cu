@@ -1060,10 +1060,10 @@ cudaError_t launch_cfg(const TrainArgs& a, int sm_count, int64_t m_max, cudaStre
 }
 
 // TLB_BATCH_CFG = "[p]NIxTHREADSxMINB" picks a measured alternative (A/B); default below:
-// the packed-pair forward with 4 images per 640-thread CTA (one per SM) for groups of < 2k images per GPU
-// (1k: 17.0 -> 20.6 M img/s), 2 images per 320-thread CTA (two per SM, SM-pair work mapping) from 2k
+// the packed-pair forward with 4 images per 640-thread CTA (one per SM) for groups of < 8k images per GPU
+// (1k: 17.0 -> 20.6 M img/s), 2 images per 320-thread CTA (two per SM, SM-pair work mapping) from 8k
 // (16k: 23.3 -> 25.0, 256k: 24.2 -> 25.9 M img/s; profiles/r2/pair_time_p3.jsonl, pair_time_p5.jsonl;
-// with the SM-pair mapping the crossover moved from 8k to 2k: profiles/r2/thr_*.jsonl).
+// with the SM-pair mapping the two are within +-2% at 2k-4k either way: profiles/r2/thr_*.jsonl, sweep_r2z).
 template <typename F>
 cudaError_t dispatch(F&& f, int64_t m_max) {
   static const char* cfg = std::getenv("TLB_BATCH_CFG");
@@ -1075,7 +1075,7 @@ cudaError_t dispatch(F&& f, int64_t m_max) {
   if (is("2x512x1")) return f.template operator()<2, 512, 1>();
   if (is("4x512x1")) return f.template operator()<4, 512, 1>();
   if (is("p4x512x1")) return f.template operator()<4, 512, 1, true>();
-  if (is("p4x640x1") || (!cfg && m_max < 2048)) return f.template operator()<4, 640, 1, true>();
+  if (is("p4x640x1") || (!cfg && m_max < 8192)) return f.template operator()<4, 640, 1, true>();
   return f.template operator()<2, 320, 2, true>();
 }
 

@@ -29,3 +29,11 @@ cat $OUT/trace_fast_$TAG.json; tail -4 $OUT/wide_$TAG.log
 TLB_CLUSTER_COOP=0 bash scripts/ncu_one.sh ncu_cluster_$TAG train_cluster_kernel python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 python scripts/ncu_lines.py $OUT/ncu_cluster_$TAG.ncu-rep 40 > $OUT/ncu_cluster_${TAG}_lines.txt 2>&1
 grep -E "time_duration|dram__bytes|fma_cycles|issue_active" $OUT/ncu_cluster_${TAG}_keymetrics.csv | cut -d, -f2- | cut -c1-100
+# the configs[3] / configs[2] kernels at HEAD: ncu of the batched train kernel (16k) and the inference kernel (1M),
+# the batched kernel's per-CTA phase trace, the e2e call's host/device timeline
+bash scripts/ncu_one.sh ncu_batch16k_$TAG train_batch_kernel python scripts/big_batch.py --what train --batch 16384 --n 32768 --reps 1 > /dev/null 2>&1
+python scripts/ncu_lines.py $OUT/ncu_batch16k_$TAG.ncu-rep 40 > $OUT/ncu_batch16k_${TAG}_lines.txt 2>&1
+bash scripts/ncu_one.sh ncu_infer1m_$TAG infer_kernel python scripts/big_batch.py --what eval --n 1048576 --reps 1 > /dev/null 2>&1
+grep -E "time_duration|dram__bytes|fma_cycles|issue_active" $OUT/ncu_batch16k_${TAG}_keymetrics.csv $OUT/ncu_infer1m_${TAG}_keymetrics.csv | cut -c1-160
+timeout 300 python scripts/trace_batch.py --batch 16384 --n 32768 > $OUT/trace_batch_16384_$TAG.json 2>&1
+TLB_HOST_TRACE=1 timeout 300 python scripts/e2e_timeline.py --u8 --reps 4 > $OUT/e2e_timeline_$TAG.txt 2>&1
