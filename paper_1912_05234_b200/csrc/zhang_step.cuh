@@ -49,6 +49,12 @@ constexpr int kThreads = 512;
 #define TLB_GK2K_SPLIT 96
 #endif
 
+#ifndef TLB_C2_DIRECT
+// 1: the pair conv2 reads its weight pairs straight from P (two scalar loads, 900 floats apart) instead of
+// the K2K float2 copy, so the clustered step needs no K2K rebuild after each exchange (8.65 -> 8.71 M img/s,
+// profiles/r2/b_*_c2d1.json); 0: K2K copy in the Kp slot, rebuilt from P whenever P changes
+#define TLB_C2_DIRECT 1
+#endif
 #ifndef TLB_C2K
 #define TLB_C2K 8  // pair conv2: columns per lane (8: 96 lanes, 4: 192 lanes)
 #endif
@@ -230,7 +236,7 @@ __device__ __forceinline__ void load_params(const Smem& s, const float* params) 
   }
   __syncthreads();
   if constexpr (!EXACT && TLB_PAIR) {
-    build_k2k(s);
+    if (!TLB_C2_DIRECT) build_k2k(s);
   } else {
     for (int idx = threadIdx.x; idx < kKp; idx += blockDim.x) {
       const int row = idx >> 3, k = idx & 7;
@@ -407,6 +413,7 @@ __device__ __forceinline__ void stage_conv2_kpair(const Smem& s) {
   const int h = it & 1, xh = (it >> 1) % XB, r = (it / (2 * XB)) & 1, rest = it / (4 * XB);
   const int ip = rest % 6, py = rest / 6, y = 2 * py + r, x0 = COLS * xh;
   const float2* k2k = reinterpret_cast<const float2*>(s.Kp) + ip * 150;
+  const float* k2a = s.P + kK2 + ip * 150;  // TLB_C2_DIRECT: k2[ip] and k2[ip + 6] (900 floats later)
   float2 acc[COLS];
 #pragma unroll
   for (int o = 0; o < COLS; ++o) acc[o] = make_float2(0.0f, 0.0f);
@@ -423,7 +430,8 @@ __device__ __forceinline__ void stage_conv2_kpair(const Smem& s) {
       }
 #pragma unroll
       for (int kx = 0; kx < 5; ++kx) {
-        const float2 w = k2k[c * 25 + ky * 5 + kx];
+        const float2 w = TLB_C2_DIRECT ? make_float2(k2a[c * 25 + ky * 5 + kx], k2a[900 + c * 25 + ky * 5 + kx])
+                                       : k2k[c * 25 + ky * 5 + kx];
 #pragma unroll
         for (int o = 0; o < COLS; ++o) acc[o] = __ffma2_rn(bcast2(in[o + kx]), w, acc[o]);
       }
@@ -1416,7 +1424,7 @@ __device__ __forceinline__ void forward_image(const Smem& s, const float* img, i
   // clustered kernel: the parameters conv2 and later stages read may still be arriving during conv1
   if (post_conv1) mbar_wait_cluster_guarded(post_conv1, post_conv1_parity, wait_limit, abort);
   if constexpr (!EXACT && TLB_PAIR) {
-    if (rebuild_k2p) {  // clustered kernel: P changed in the last exchange -> the conv2 weight pairs
+    if (rebuild_k2p && !TLB_C2_DIRECT) {  // clustered kernel: P changed in the last exchange -> the conv2 weight pairs
       build_k2k(s);
       __syncthreads();
     }
