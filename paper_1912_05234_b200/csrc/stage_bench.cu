@@ -52,7 +52,6 @@ __device__ void fill(const Smem& s) {
   }
 #if TLB_PAIR
   __syncthreads();
-  build_k2k(s);  // the fast product conv2 reads the k2 kernel pairs from the Kp slot
 #endif
   for (int q = t; q < 12 * 64; q += n) {
     const int i = q >> 6, y = (q >> 3) & 7, x = q & 7;

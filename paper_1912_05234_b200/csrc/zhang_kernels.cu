@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
       const bool pending = (!dp || dp_pend) && ls > 0;
       const NextBytes nb{buf ^ 1, ((consumed + 1) >> 1) & 1, a.images_wb};
       forward_image<false>(s, s.img + buf * kImg, -1, nullptr, true, s.lab + buf, pending ? &xbar[2] : nullptr,
-                           (uint32_t)((ls - 1) & 1), a.dp_timeout_cycles, a.dp_error, a.pixels ? &nb : nullptr, ls > 0);
+                           (uint32_t)((ls - 1) & 1), a.dp_timeout_cycles, a.dp_error, a.pixels ? &nb : nullptr);
       if (threadIdx.x == 0) cta_loss = __dadd_rn(cta_loss, (double)example_loss(s, s.lab[buf], nullptr));
       backward_image<false, true>(s, s.img + buf * kImg, nullptr);
       ++consumed;

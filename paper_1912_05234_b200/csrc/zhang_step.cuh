@@ -49,12 +49,6 @@ constexpr int kThreads = 512;
 #define TLB_GK2K_SPLIT 96
 #endif
 
-#ifndef TLB_C2_DIRECT
-// 1: the pair conv2 reads its weight pairs straight from P (two scalar loads, 900 floats apart) instead of
-// the K2K float2 copy, so the clustered step needs no K2K rebuild after each exchange (8.65 -> 8.71 M img/s,
-// profiles/r2/b_*_c2d1.json); 0: K2K copy in the Kp slot, rebuilt from P whenever P changes
-#define TLB_C2_DIRECT 1
-#endif
 #ifndef TLB_C2K
 #define TLB_C2K 8  // pair conv2: columns per lane (8: 96 lanes, 4: 192 lanes)
 #endif
@@ -133,10 +127,10 @@ constexpr int kTerm = 12 * 864;         // backin per-kernel terms
 
 __device__ __forceinline__ int dzp_at(int i, int R, int col) { return i * kDzpK + R * kDzpRow + col; }
 // Fast mode (TLB_GK2K): a second copy of dz2 as kernel pairs (dz2[ip], dz2[ip+6]) [6][8][8] float2 for the
-// packed-pair g_k2, in the Kp slot after the conv2 weight pairs; rows padded to 20 floats and pair planes to
+// packed-pair g_k2, in the Kp slot (from float 1800); rows padded to 20 floats and pair planes to
 // 164 (both 4 mod 32 banks in 16-byte units: a warp's row loads of different rows / pairs do not collide).
 constexpr int kDzkOff = 1800, kDzkRow = 20, kDzkPlane = 8 * kDzkRow + 4;
-static_assert(kDzkOff + 6 * kDzkPlane <= kKp, "dz2 pairs fit the Kp slot after K2K");
+static_assert(kDzkOff + 6 * kDzkPlane <= kKp, "dz2 pairs fit the Kp slot");
 __device__ __forceinline__ int dzk_at(int ip, int y, int x) { return kDzkOff + ip * kDzkPlane + y * kDzkRow + 2 * x; }
 // c1 / dz1 channel planes padded 576 -> 580 floats: the six channel rows of one y start in six different
 // bank groups (580 mod 32 = 4), so the C1 weight-gradient lanes read them conflict-free.
@@ -217,9 +211,8 @@ __device__ __forceinline__ void issue_image(const Smem& s, int buf, const float*
   tma_load_1d(s.img + buf * kImg, src, kImg * sizeof(float), &s.bar[buf]);
 }
 
-// Parameters (3,898 floats, padded) global -> shared, then the padded k2 copy.  __ldcg: other CTAs
-// rewrote them in the previous step's SGD phase, so bypass L1.  Ends with __syncthreads.
-__device__ __forceinline__ void build_k2k(const Smem& s);
+// Parameters (3,898 floats, padded) global -> shared, then (EXACT / scalar conv2) the padded k2 copy.
+// __ldcg: other CTAs rewrote them in the previous step's SGD phase, so bypass L1.  Ends with __syncthreads.
 template <bool EXACT = true>
 __device__ __forceinline__ void load_params(const Smem& s, const float* params) {
   const float4* src = reinterpret_cast<const float4*>(params);
@@ -235,9 +228,7 @@ __device__ __forceinline__ void load_params(const Smem& s, const float* params) 
       if (base + u * (int)blockDim.x < kPStride / 4) dst[base + u * blockDim.x] = v[u];
   }
   __syncthreads();
-  if constexpr (!EXACT && TLB_PAIR) {
-    if (!TLB_C2_DIRECT) build_k2k(s);
-  } else {
+  if constexpr (EXACT || !TLB_PAIR) {  // (the pair conv2 reads its weight pairs straight from P)
     for (int idx = threadIdx.x; idx < kKp; idx += blockDim.x) {
       const int row = idx >> 3, k = idx & 7;
       s.Kp[idx] = k < 5 ? s.P[kK2 + row * 5 + k] : 0.0f;
@@ -331,8 +322,9 @@ __device__ __forceinline__ void stage_conv1_rows2(const Smem& s, const float* im
 // profiles/r2/ffma2_peak_r2k.json), one operand a broadcast scalar:
 //   conv1 : pixel (broadcast) x (k1[c], k1[c+3])            -> (c1[c], c1[c+3])
 //   conv2 : s1 (broadcast) x (k2[i][c], k2[i+6][c])         -> (out[i], out[i+6])
-// The conv2 weight pairs K2K [6][6][25] float2 live in the Kp slot, rebuilt from P whenever P changes;
-// every activation keeps its canonical layout, so the backward stages are the scalar ones.  (Pair
+// The conv2 weight pair is two scalar loads from P (k2[i] and k2[i+6], 900 floats apart): a float2 copy
+// rebuilt after every exchange cost more than the extra loads (profiles/r2/b_*_c2d1.json); every
+// activation keeps its canonical layout, so the backward stages are the scalar ones.  (Pair
 // layouts for the backward contractions were measured slower at one image per SM: their weight-pair and
 // dz2-pair loads cost more shared-memory wavefronts than the halved FFMA issue saves; profiles/README.md.)
 // Fast-mode arithmetic (FFMA, fixed summation trees; within the north-star 1e-4); EXACT keeps the scalar
@@ -392,14 +384,6 @@ __device__ __forceinline__ void stage_conv1_pair(const Smem& s, const float* img
   *reinterpret_cast<float2*>(s.s1 + ((ip + 3) * 12 + py) * 12 + 2 * xs) = make_float2(pv[0].y, pv[1].y);
 }
 
-// K2K[(ip*6 + c)*25 + t] = (k2[ip][c][t], k2[ip+6][c][t]): conv2 / backin kernel-pair weights (Kp slot).
-__device__ __forceinline__ void build_k2k(const Smem& s) {
-  for (int q = threadIdx.x; q < 900; q += blockDim.x) {
-    const int ip = q / 150, r = q - ip * 150;
-    reinterpret_cast<float2*>(s.Kp)[q] = make_float2(s.P[kK2 + ip * 150 + r], s.P[kK2 + (ip + 6) * 150 + r]);
-  }
-}
-
 // conv2 on kernel pairs (i, i+6): lane = (channel half h, column block xh, pool row r, kernel pair ip,
 // pooled row py), h fastest.  The s1 row value is the broadcast operand, (k2[i][c], k2[i+6][c]) the weight
 // pair; COLS columns of conv row y = 2py + r over the lane's 3 channels (15 x 5 x COLS FFMA2), the two
@@ -412,8 +396,7 @@ __device__ __forceinline__ void stage_conv2_kpair(const Smem& s) {
   if (it >= kLanes) return;
   const int h = it & 1, xh = (it >> 1) % XB, r = (it / (2 * XB)) & 1, rest = it / (4 * XB);
   const int ip = rest % 6, py = rest / 6, y = 2 * py + r, x0 = COLS * xh;
-  const float2* k2k = reinterpret_cast<const float2*>(s.Kp) + ip * 150;
-  const float* k2a = s.P + kK2 + ip * 150;  // TLB_C2_DIRECT: k2[ip] and k2[ip + 6] (900 floats later)
+  const float* k2a = s.P + kK2 + ip * 150;  // k2[ip] (and k2[ip + 6], 900 floats later)
   float2 acc[COLS];
 #pragma unroll
   for (int o = 0; o < COLS; ++o) acc[o] = make_float2(0.0f, 0.0f);
@@ -430,8 +413,7 @@ __device__ __forceinline__ void stage_conv2_kpair(const Smem& s) {
       }
 #pragma unroll
       for (int kx = 0; kx < 5; ++kx) {
-        const float2 w = TLB_C2_DIRECT ? make_float2(k2a[c * 25 + ky * 5 + kx], k2a[900 + c * 25 + ky * 5 + kx])
-                                       : k2k[c * 25 + ky * 5 + kx];
+        const float2 w = make_float2(k2a[c * 25 + ky * 5 + kx], k2a[900 + c * 25 + ky * 5 + kx]);
 #pragma unroll
         for (int o = 0; o < COLS; ++o) acc[o] = __ffma2_rn(bcast2(in[o + kx]), w, acc[o]);
       }
@@ -1416,19 +1398,12 @@ template <bool EXACT>
 __device__ __forceinline__ void forward_image(const Smem& s, const float* img, int label, const float* y,
                                               bool want_dz, const int* lab = nullptr, uint64_t* post_conv1 = nullptr,
                                               uint32_t post_conv1_parity = 0, long long wait_limit = 0,
-                                              unsigned int* abort = nullptr, const NextBytes* next_bytes = nullptr,
-                                              bool rebuild_k2p = false) {
+                                              unsigned int* abort = nullptr, const NextBytes* next_bytes = nullptr) {
   call_conv1<EXACT>(img);
   __syncthreads();
   if (lab) label = *lab;
   // clustered kernel: the parameters conv2 and later stages read may still be arriving during conv1
   if (post_conv1) mbar_wait_cluster_guarded(post_conv1, post_conv1_parity, wait_limit, abort);
-  if constexpr (!EXACT && TLB_PAIR) {
-    if (rebuild_k2p && !TLB_C2_DIRECT) {  // clustered kernel: P changed in the last exchange -> the conv2 weight pairs
-      build_k2k(s);
-      __syncthreads();
-    }
-  }
   mark(s, 3);
   call_conv2<EXACT>();  // includes avgpool
   convert_next_bytes(s, next_bytes);
