@@ -1,7 +1,7 @@
 #!/bin/bash
 TAG=${1:-c2k}
 OUT=gpurun_out; mkdir -p $OUT
-V=paper_1912_05234_b200/lib/variants/libtloom_b200_c2direct.so
+V=paper_1912_05234_b200/lib/variants/libtloom_b200_dprt.so
 for r in 1 2 3; do
 python bench.py --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 > $OUT/b_base_${r}_$TAG.json
 TLB_LIB=$V python bench.py --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 > $OUT/b_direct_${r}_$TAG.json
