@@ -619,23 +619,39 @@ __device__ __forceinline__ void conv2_item_kp(const float* P, const float* W2p, 
   }
 }
 
-// Rounds of one CTA: (step, first local example, end of the CTA's chunk).
+// Rounds of one CTA: (step, first local example, end of the CTA's range -- the group's size when
+// interleaved, the contiguous chunk's end otherwise --, the CTA's position index j in the group).
 struct Round {
-  int64_t step, e, hi;
+  int64_t step, e, hi, j;
 };
 
-// Which examples of a group a CTA trains.  Default: static_chunk(m, grid, cta).  With two CTAs per SM the
-// warp schedulers favour the CTA that arrived first (measured: it finishes its rounds 13% sooner on
-// 144-148 of 148 SMs, profiles/r2/trace_batch_*_trb2.json), so the partner idles through the tail of
-// every step.  Paired mapping: SM pair p (SMs ranked by id) owns static_chunk(m, grid / 2, p); its first
-// CTA (slot 0) trains `share` of it rounded to whole rounds, slot 1 the rest.  The partial row and the
-// loss slot are indexed by the work id 2p + slot, so which examples are summed into which row -- and the
-// result -- does not depend on where the hardware placed the CTAs.
+// Which rounds of a group a CTA trains (round r = local examples [r NI, r NI + NI)).
+// Interleaved (TLB_BT_INTERLEAVE, default): round r belongs to CTA r % grid, so any prefix of the group
+// feeds every CTA's first rounds -- a host call's ingestion chunks (tlb_train on host buffers) are
+// consumed as they land instead of the whole first group having to arrive before the last CTA can start.
+// With two CTAs per SM the warp schedulers favour the CTA that arrived first (measured: it finishes its
+// rounds 13% sooner on 144-148 of 148 SMs, profiles/r2/trace_batch_*_trb2.json), so the partner would idle
+// through the tail of every step.  Paired mapping: round r belongs to SM pair p = r % (grid / 2) at
+// position j = r / (grid / 2); slot 0 (the first-arrived CTA) takes the positions where floor(j share)
+// steps (`share` of them), slot 1 the others.  Partial rows and loss slots are indexed by the work id
+// 2p + slot, so which examples are summed into which row -- and the result -- does not depend on where
+// the hardware placed the CTAs.  TLB_BT_INTERLEAVE=0: contiguous static chunks (the earlier mapping).
+#ifndef TLB_BT_INTERLEAVE
+#define TLB_BT_INTERLEAVE 1
+#endif
 struct WorkMap {
-  int wid;      // work id: partial row, chunk
+  int wid;      // work id: partial row, rounds
   int paired;   // 1: SM-pair mapping
   float share;  // slot 0's share of the pair's examples
+  int share_q;  // share in 1/1024
 };
+
+// Slot of a pair's position j: slot 0 takes the positions where floor(j share) steps (share in 1/1024).
+// (An exact per-pair count -- round(n share) of the pair's n positions, spread by division -- measured
+// slower: profiles/r2/bt_ilv*_ilv4.jsonl.)
+__device__ __forceinline__ int pair_slot(int64_t j, int q) {
+  return (((j + 1) * q) >> 10) != ((j * q) >> 10) ? 0 : 1;
+}
 
 template <int NI>
 __device__ __forceinline__ void work_chunk(int64_t m, const WorkMap& w, int64_t& lo, int64_t& hi) {
@@ -652,25 +668,66 @@ __device__ __forceinline__ void work_chunk(int64_t m, const WorkMap& w, int64_t&
   else lo = plo, hi = plo + s0;
 }
 
-template <int NI>
+// The CTA's first round at position >= j of a group of m examples (r.step is the caller's).  ILV: the
+// interleaved mapping (launches whose groups give every CTA >= 4 rounds); otherwise contiguous chunks
+// (with fewer rounds a contiguous chunk can end in a partial round -- 1k images on 148 CTAs: 4 + 3 images
+// each -- where whole interleaved rounds put 8 images on some CTAs: -5% at 1k, profiles/r2/bt_ilv*_ilv1.jsonl).
+template <int NI, bool ILV>
+__device__ __forceinline__ bool seek_round(const WorkMap& w, int64_t m, int64_t j, Round& r) {
+  if constexpr (!ILV) {
+    int64_t lo, hi;
+    work_chunk<NI>(m, w, lo, hi);
+    if (lo + j * NI >= hi) return false;
+    r.e = lo + j * NI;
+    r.hi = hi;
+    r.j = j;
+    return true;
+  }
+  const int64_t R = (m + NI - 1) / NI;
+  if (!w.paired) {
+    const int64_t rr = w.wid + j * (int64_t)gridDim.x;
+    if (rr >= R) return false;
+    r.e = rr * NI;
+    r.hi = m;
+    r.j = j;
+    return true;
+  }
+  const int P = (int)gridDim.x >> 1, p = w.wid >> 1, sl = w.wid & 1;
+  for (;; ++j) {
+    const int64_t rr = p + j * (int64_t)P;
+    if (rr >= R) return false;
+    if (pair_slot(j, w.share_q) == sl) {
+      r.e = rr * NI;
+      r.hi = m;
+      r.j = j;
+      return true;
+    }
+  }
+}
+// The CTA's next round of the same group (false: none left).
+template <int NI, bool ILV>
+__device__ __forceinline__ bool step_round(const WorkMap& w, Round& r) {
+  if constexpr (ILV) return seek_round<NI, true>(w, r.hi, r.j + 1, r);
+  if (r.e + NI >= r.hi) return false;
+  r.e += NI;
+  ++r.j;
+  return true;
+}
+
+template <int NI, bool ILV>
 __device__ __forceinline__ bool first_round(const TrainArgs& a, const WorkMap& w, int64_t from, Round& r) {
   for (int64_t st = from; st < a.step_end; ++st) {
-    int64_t lo, hi;
-    work_chunk<NI>(local_size(a, st), w, lo, hi);
-    if (lo < hi) {
-      r = Round{st, lo, hi};
+    if (seek_round<NI, ILV>(w, local_size(a, st), 0, r)) {
+      r.step = st;
       return true;
     }
   }
   return false;
 }
-template <int NI>
+template <int NI, bool ILV>
 __device__ __forceinline__ bool next_round(const TrainArgs& a, const WorkMap& w, Round& r) {
-  if (r.e + NI < r.hi) {
-    r.e += NI;
-    return true;
-  }
-  return first_round<NI>(a, w, r.step + 1, r);
+  if (step_round<NI, ILV>(w, r)) return true;
+  return first_round<NI, ILV>(a, w, r.step + 1, r);
 }
 
 // Paired mapping (MINB == 2): every CTA publishes (SM id, arrival slot on its SM); after a grid barrier each
@@ -708,8 +765,9 @@ __device__ WorkMap pair_map(const TrainArgs& a, int* scratch, unsigned int& targ
   }
   if (below) atomicAdd(flags + 1, below);
   __syncthreads();
-  WorkMap w{(int)blockIdx.x, 0, 0.5f};
-  if (!flags[0] && (nb & 1) == 0) w = WorkMap{flags[1] + (int)(mine & 1), 1, a.pair_share};
+  WorkMap w{(int)blockIdx.x, 0, 0.5f, 512};
+  if (!flags[0] && (nb & 1) == 0)
+    w = WorkMap{flags[1] + (int)(mine & 1), 1, a.pair_share, (int)__float2int_rn(a.pair_share * 1024.0f)};
   __syncthreads();  // scratch is reused by the caller
   return w;
 }
@@ -743,7 +801,7 @@ __device__ __forceinline__ void issue_round(const TrainArgs& a, float* ring, uin
   tma_load_1d(ring + buf * NI * kImg, a.images + first * kImg, (uint32_t)(cnt * kImg * sizeof(float)), &bar[buf]);
 }
 
-template <int NI, int T, int MINB, bool PAIR>
+template <int NI, int T, int MINB, bool PAIR, bool ILV>
 __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
   static_assert(T % 32 == 0, "stage loops run whole warps");
   using L = Layout<NI>;
@@ -767,13 +825,13 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
     mbar_init(&bar[1], 1);
     fence_barrier_init();
   }
-  WorkMap wm{(int)blockIdx.x, 0, 0.5f};
+  WorkMap wm{(int)blockIdx.x, 0, 0.5f, 512};
   if (MINB == 2 && a.pair_share > 0.0f) wm = pair_map(a, reinterpret_cast<int*>(regs), target);
   for (int q = t; q < NI * kImgRegion; q += T) regs[q] = 0.0f;  // dz2 pad rows stay zero
   __syncthreads();
   const bool issuer = t == T - 32;  // lane 0 of the last warp (idle in S2/S6 of a full round)
   Round pf;
-  bool pf_valid = first_round<NI>(a, wm, a.step_begin, pf);
+  bool pf_valid = first_round<NI, ILV>(a, wm, a.step_begin, pf);
   if (issuer && pf_valid) issue_round<NI>(a, ring, pxring, rb, lab, bar, 0, pf);
   if (pf_valid && step_bytes(a, pf.step)) {  // the first round's bytes: converted by every thread
     __syncthreads();
@@ -801,9 +859,6 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
     int64_t l_lo, l_hi;
     local_range_k(a, ks, l_lo, l_hi);
     const int64_t m = l_hi - l_lo;
-    int64_t lo, hi;
-    work_chunk<NI>(m, wm, lo, hi);
-
     // ---- the step's weights -> shared (+ padded conv copies), zero the CTA gradient ----
     {
       const float4* src = reinterpret_cast<const float4*>(a.params);
@@ -830,8 +885,10 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
 
     double cta_loss = 0.0;  // thread 0: this CTA's example losses in example order (fp64)
     stamp(st, 0);
-    for (int64_t e = lo; e < hi; e += NI) {
-      const int cnt = (int)min((int64_t)NI, hi - e);
+    Round cur{st, 0, 0, 0};
+    int64_t nrounds = 0;  // this CTA's rounds of the step (trace)
+    for (bool have = seek_round<NI, ILV>(wm, m, 0, cur); have; have = step_round<NI, ILV>(wm, cur), ++nrounds) {
+      const int cnt = (int)min((int64_t)NI, cur.hi - cur.e);
       const int buf = consumed & 1;
       mbar_wait(&bar[buf], (consumed >> 1) & 1);
       if (issuer) {
@@ -839,7 +896,7 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
         rbst[buf ^ 1] = 0;    // (issue_round sets it for a next round that arrives as bytes)
         if (pf_valid) {
           Round nx = pf;
-          if (next_round<NI>(a, wm, nx)) {
+          if (next_round<NI, ILV>(a, wm, nx)) {
             issue_round<NI>(a, ring, pxring, rb, lab, bar, buf ^ 1, nx);  // buf^1 was last read by the previous round's S6
             pf = nx;
           } else {
@@ -954,8 +1011,8 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
 
     // ---- CTA partial -> work row; grid barrier; ordered reduction + sgd_step; grid barrier ----
     stamp(st, 1);
-    if (trace) trace[(st - a.step_begin) * nb * 8 + 5] = (unsigned long long)((hi - lo + NI - 1) / NI);
-    if (lo < hi || wm.paired) {  // paired mapping: every row is written (zero if its chunk is empty)
+    if (trace) trace[(st - a.step_begin) * nb * 8 + 5] = (unsigned long long)nrounds;
+    {  // every row is written (zero if the CTA had no round: small groups)
       float4* dst = reinterpret_cast<float4*>(a.work + (int64_t)wm.wid * kPStride);
       const float4* src = reinterpret_cast<const float4*>(G);
       for (int q = t; q < kPStride / 4; q += T) __stcg(dst + q, src[q]);
@@ -963,8 +1020,7 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
     }
     grid_sync(a.barrier, target);
     stamp(st, 2);
-    const int64_t block = m > 0 ? udiv(m + nb - 1, nb) : 1;
-    const int64_t nrows = wm.paired ? nb : m > 0 ? udiv(m + block - 1, block) : 0;  // rows with examples
+    const int64_t nrows = nb;  // every CTA's row (written above)
     {
       int64_t j0, j1;
       static_chunk(kNParam, nb, blockIdx.x, j0, j1);
@@ -1018,9 +1074,9 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
   }
 }
 
-template <int NI, int T, int MINB, bool PAIR>
+template <int NI, int T, int MINB, bool PAIR, bool ILV = false>
 cudaError_t prep(int* occ) {
-  auto kern = train_batch_kernel<NI, T, MINB, PAIR>;
+  auto kern = train_batch_kernel<NI, T, MINB, PAIR, ILV>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Layout<NI>::kBytes);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, T, Layout<NI>::kBytes);
@@ -1038,7 +1094,10 @@ inline float pair_share() {
 template <int NI, int T, int MINB, bool PAIR>
 cudaError_t launch_cfg(const TrainArgs& a, int sm_count, int64_t m_max, cudaStream_t st, int* grid_out) {
   int occ = 0;
+  int occ_ilv = 0;
   cudaError_t e = prep<NI, T, MINB, PAIR>(&occ);
+  if (e == cudaSuccess) e = prep<NI, T, MINB, PAIR, true>(&occ_ilv);
+  occ = std::min(occ, occ_ilv);
   if (e != cudaSuccess) return e;
   const int64_t cap = (int64_t)std::max(occ, 1) * sm_count;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cap, (m_max + NI - 1) / NI));
@@ -1055,7 +1114,14 @@ cudaError_t launch_cfg(const TrainArgs& a, int sm_count, int64_t m_max, cudaStre
     if (e != cudaSuccess) return e;
   }
   void* args[] = {&la};
-  return cudaLaunchCooperativeKernel((const void*)train_batch_kernel<NI, T, MINB, PAIR>, dim3(grid), dim3(T), args,
+  // Interleaved rounds only while a host call's ingestion chunks are landing (a.ready: tlb_train on host
+  // buffers) and every CTA gets >= 4 rounds of a full group (see seek_round): with the data resident the
+  // contiguous chunks are ~2% faster (profiles/r2/bt_ilv*_ilv5.jsonl), with chunks in flight interleaving
+  // lets every CTA start on the first chunk (16k e2e 17-20 -> 23 M img/s).
+  const bool ilv = TLB_BT_INTERLEAVE && a.ready != nullptr && m_max >= 4LL * NI * grid;
+  const void* kern = ilv ? (const void*)train_batch_kernel<NI, T, MINB, PAIR, true>
+                         : (const void*)train_batch_kernel<NI, T, MINB, PAIR, false>;
+  return cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(T), args,
                                      Layout<NI>::kBytes, st);
 }
 

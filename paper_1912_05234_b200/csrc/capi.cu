@@ -1055,7 +1055,14 @@ static int train_host(tlb_ctx* c, HostImages src, const int32_t* labels, int64_t
   const int64_t group_bytes = batch * 784 * (int64_t)sizeof(float);
   int64_t cap = 1;  // ramp cap C: groups per steady chunk, a power of two
   while (cap * group_bytes < (int64_t)(1 << 20)) cap *= 2;
-  const int64_t chunk = chunk_env >= 0 ? chunk_env : -cap;
+  // Large groups train on the batched kernel, whose CTAs take the group's rounds interleaved while chunks
+  // are in flight (round r on CTA r % grid, batch_train.cu): any prefix of a group feeds every CTA, so
+  // chunks of batch / 8 images (1k..16k) are consumed as they land -- with whole-group chunks the first
+  // group's bytes had to arrive before the last CTA could start (16k: ~0.25 ms of a 1.6 ms call).
+  const bool batched_launch = !exact(c) && c->grid_override == 0 && use_batched(c, std::min(batch, n));
+  const int64_t chunk = chunk_env >= 0       ? chunk_env
+                        : batched_launch ? std::min<int64_t>(16384, std::max<int64_t>(1024, batch / 8))
+                                         : -cap;
   const int64_t nchunks = ingest_chunks(n, chunk, batch);
   // Byte source: the chunks of bytes (1/4 of the fp32 volume) stream in like fp32 chunks and the train
   // kernel converts each image where it is trained (a separate conversion kernel could not run beside a

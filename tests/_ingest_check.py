@@ -1,6 +1,10 @@
 """Overlapped-ingestion check shared by tests/test_gpu_parity.py (in process, default chunk policy) and
 run as ``python tests/_ingest_check.py`` under other TLB_INGEST_CHUNK policies: tlb_train on host
-buffers (pageable and pinned) must equal tlb_train_device on resident data, bit for bit.
+buffers (pageable and pinned) must equal tlb_train_device on resident data, bit for bit -- except, in
+fast mode, for groups the batched kernel trains with >= 4 rounds per CTA (>= INTERLEAVE_MIN images): while
+ingestion chunks are in flight it takes the group's rounds interleaved across CTAs (every CTA can start
+on the first chunk), with the data resident in contiguous chunks (~2% faster), so the per-CTA partial
+sums group different examples; there the two calls agree to within summation-order noise (WEIGHT_TOL).
 
 Every case trains on its own window of the corpus (a per-case offset, and labels rotated by the case
 index), so the staging buffer never already holds the expected images from an earlier call: a missing
@@ -10,6 +14,10 @@ import numpy as np
 CASES = ((1, 100), (83, 7), (200, 100), (5000, 100), (300, 100), (1001, 77), (2, 1), (3, 1), (4, 1), (5, 1),
          (129, 1), (800, 100), (801, 100), (10000, 100),
          (6000, 2500), (4099, 1337))  # groups > 2 MiB on the link: fixed ~1 MiB chunks, not group-aligned
+
+
+INTERLEAVE_MIN = 4 * 4 * 148  # rounds of NI = 4 images on a 148-CTA grid (batch_train.cu launch_cfg)
+WEIGHT_TOL = 1e-5            # relative, |w| floored at 1e-3 (as the parity tests)
 
 
 def bits(a):
@@ -39,8 +47,14 @@ def check(orc, tr_x, tr_y, mode):
             d_l = torch.zeros(2, dtype=torch.float64, device=dev)
             c.train_device(d_x.data_ptr(), d_y.data_ptr(), n, d_p.data_ptr(), 0.05, 0, 2, batch, d_l.data_ptr())
             torch.cuda.synchronize()
-            assert np.array_equal(bits(got_p), bits(d_p.cpu().numpy()[:3898])), (mode, n, batch)
-            assert list(got_l) == d_l.cpu().numpy().tolist(), (mode, n, batch)
+            want_p, want_l = d_p.cpu().numpy()[:3898], d_l.cpu().numpy()
+            if mode == "fast" and min(batch, n) >= INTERLEAVE_MIN:
+                d = np.abs(got_p.astype(np.float64) - want_p) / np.maximum(np.abs(want_p), 1e-3)
+                assert float(d.max()) <= WEIGHT_TOL, (mode, n, batch, float(d.max()))
+                assert np.allclose(got_l, want_l, rtol=1e-6, atol=0), (mode, n, batch)
+                continue
+            assert np.array_equal(bits(got_p), bits(want_p)), (mode, n, batch)
+            assert list(got_l) == want_l.tolist(), (mode, n, batch)
 
 
 def main():
