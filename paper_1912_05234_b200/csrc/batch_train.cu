@@ -9,7 +9,8 @@
 //     CTA's gradient accumulator G (shared memory) is updated once per round per output;
 //   * the NI images of a round are contiguous in HBM and arrive with ONE TMA bulk copy into a
 //     double-buffered ring (the next round -- possibly the next step's first -- is in flight meanwhile).
-// Per step (one SGD group): each CTA trains static_chunk(m, grid, cta) of the group's examples, writes
+// Per step (one SGD group): each CTA trains its rounds of the group (a contiguous chunk, or interleaved
+// rounds while a host call's chunks are in flight; SM-pair shares with two CTAs per SM: seek_round), writes
 // its partial gradient row, grid barrier, CTA b reduces parameters static_chunk(3898, grid, b) over the
 // partial rows in CTA order (fixed tree: deterministic run to run) and applies sgd_step
 // (network.cpp:171-180) or, in DP shard mode, writes the shard's gradient sum; grid barrier.
