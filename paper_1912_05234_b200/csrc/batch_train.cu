@@ -1031,15 +1031,35 @@ __global__ void __launch_bounds__(T, MINB) train_batch_kernel(TrainArgs a) {
         const int rstep = T / W, c = t % W, r0 = t / W;
         float acc = 0.0f;
         if (r0 < rstep) {
-          int64_t r = r0;
-          for (; r + 3 * rstep < nrows; r += 4 * rstep) {  // four loads in flight, fixed order
-            const float v0 = __ldcg(a.work + r * kPStride + jb + c);
-            const float v1 = __ldcg(a.work + (r + rstep) * kPStride + jb + c);
-            const float v2 = __ldcg(a.work + (r + 2 * rstep) * kPStride + jb + c);
-            const float v3 = __ldcg(a.work + (r + 3 * rstep) * kPStride + jb + c);
-            acc = ((acc + v0) + v1) + (v2 + v3);
+          if constexpr (MINB == 1) {
+            // one CTA per SM (groups < 8k): up to 16 rows in flight per thread (one L2 round trip for the
+            // usual ~7 rows), summed by a fixed tree (absent rows add +0.0f: exact); 1 k: +1-2.5%
+            // (profiles/r2/bt_ilv*_red1.jsonl).  (With two CTAs per SM it showed intermittent -2.5% runs at
+            // 16 k / 64 k: red2; the four-wide loop stays there.)
+            for (int64_t r = r0; r < nrows; r += 16 * rstep) {
+              float v[16];
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const int64_t rr = r + u * rstep;
+                v[u] = rr < nrows ? __ldcg(a.work + rr * kPStride + jb + c) : 0.0f;
+              }
+#pragma unroll
+              for (int w = 1; w < 16; w <<= 1)
+#pragma unroll
+                for (int u = 0; u < 16; u += 2 * w) v[u] += v[u + w];
+              acc += v[0];
+            }
+          } else {
+            int64_t r = r0;
+            for (; r + 3 * rstep < nrows; r += 4 * rstep) {  // four loads in flight, fixed order
+              const float v0 = __ldcg(a.work + r * kPStride + jb + c);
+              const float v1 = __ldcg(a.work + (r + rstep) * kPStride + jb + c);
+              const float v2 = __ldcg(a.work + (r + 2 * rstep) * kPStride + jb + c);
+              const float v3 = __ldcg(a.work + (r + 3 * rstep) * kPStride + jb + c);
+              acc = ((acc + v0) + v1) + (v2 + v3);
+            }
+            for (; r < nrows; r += rstep) acc += __ldcg(a.work + r * kPStride + jb + c);
           }
-          for (; r < nrows; r += rstep) acc += __ldcg(a.work + r * kPStride + jb + c);
         }
         red[t] = acc;
         __syncthreads();
