@@ -85,6 +85,32 @@ def test_batch_16k_vs_oracle(orc):
     assert np.array_equal(bits(got_p), bits(again_p)) and list(got_l) == list(again_l)
 
 
+def test_batch_16k_resident_vs_oracle(orc):
+    """The same group trained from device-resident data (tlb_train_device): the batched kernel takes
+    contiguous per-CTA chunks there (the host call above interleaves its rounds while chunks land), with
+    the SM-pair split -- also within the tolerance of the oracle, and deterministic."""
+    import torch
+    from paper_1912_05234_b200 import Context
+    x, y = orc.make_set(32768, 1)
+    p0 = orc.init_params(42)
+    want_p, want_l = orc.train(x, y, p0, epochs=1, batch=16384)
+    dev = torch.device("cuda:0")
+    got = []
+    with Context(0, mode="fast") as c:
+        c.set_stream(torch.cuda.current_stream().cuda_stream)
+        d_x, d_y = torch.from_numpy(x).to(dev), torch.from_numpy(np.asarray(y, np.int32)).to(dev)
+        for _ in range(2):
+            d_p = torch.zeros(3904, device=dev)
+            d_p[:3898] = torch.from_numpy(p0).to(dev)
+            d_l = torch.zeros(1, dtype=torch.float64, device=dev)
+            c.train_device(d_x.data_ptr(), d_y.data_ptr(), len(y), d_p.data_ptr(), 0.05, 0, 1, 16384, d_l.data_ptr())
+            torch.cuda.synchronize()
+            got.append((d_p.cpu().numpy()[:3898].copy(), d_l.cpu().numpy().copy()))
+    check_weights(got[0][0], want_p)
+    assert rel(got[0][1], want_l) <= REL_TOL
+    assert np.array_equal(bits(got[0][0]), bits(got[1][0])) and np.array_equal(got[0][1], got[1][1])
+
+
 _SHARE_RUN = """
 import sys, numpy as np
 sys.path.insert(0, {root!r})
