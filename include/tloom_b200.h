@@ -119,6 +119,14 @@ int tlb_pixels_to_images_device(tlb_ctx* ctx, const uint8_t* d_pixels, int64_t c
 /* mnist::make_set invariants (mnist.cpp:126-154): pixels in [0,1], labels in 0..9 (ValueError). */
 int tlb_validate_set(const float* images, const int32_t* labels, int64_t n);
 
+/* ---- host memory -------------------------------------------------------------------------------- */
+/* Page-lock (and unlock) a caller-owned host range for the direct-DMA ingestion path of tlb_train /
+ * tlb_evaluate (no reference counterpart: the C++ mirror keeps its last training set registered across
+ * net::train calls, tloom/network.hpp).  Returns TLB_ERR_CUDA if the range cannot be registered (e.g. it
+ * overlaps a registered range); the call then simply takes the pageable path. */
+int tlb_host_register(tlb_ctx* ctx, const void* ptr, size_t bytes);
+int tlb_host_unregister(tlb_ctx* ctx, const void* ptr);
+
 /* ---- network, host buffers (replaces tloom::net, network.hpp:59-86) --------------------------- */
 /* net::train (network.cpp:209-251): params updated in place; epoch_loss[epochs] = mean losses.
  * Errors as the reference: n==0, epochs<0, !(rate>0) -> TLB_ERR_ERROR; batch<1 -> TLB_ERR_ERROR. */

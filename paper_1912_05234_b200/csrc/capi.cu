@@ -1189,6 +1189,29 @@ static int train_host(tlb_ctx* c, HostImages src, const int32_t* labels, int64_t
   return TLB_OK;
 }
 
+int tlb_host_register(tlb_ctx* c, const void* ptr, size_t bytes) {
+  if (!c || !ptr || bytes == 0) return fail(TLB_ERR_ARG, "tlb_host_register: null argument");
+  TLB_TRY(set_device(c));
+  const cudaError_t e = cudaHostRegister(const_cast<void*>(ptr), bytes,
+                                         cudaHostRegisterPortable | cudaHostRegisterReadOnly);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(TLB_ERR_CUDA, std::string("tlb_host_register: ") + cudaGetErrorString(e));
+  }
+  return TLB_OK;
+}
+
+int tlb_host_unregister(tlb_ctx* c, const void* ptr) {
+  if (!c || !ptr) return fail(TLB_ERR_ARG, "tlb_host_unregister: null argument");
+  TLB_TRY(set_device(c));
+  const cudaError_t e = cudaHostUnregister(const_cast<void*>(ptr));
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(TLB_ERR_CUDA, std::string("tlb_host_unregister: ") + cudaGetErrorString(e));
+  }
+  return TLB_OK;
+}
+
 int tlb_train(tlb_ctx* c, const float* images, const int32_t* labels, int64_t n, float* params, float rate,
               int32_t epochs, int64_t batch, double* epoch_loss, tlb_epoch_cb on_epoch, void* user) {
   if (c && params && !images && n > 0) return fail(TLB_ERR_ARG, "tlb_train: null dataset");

@@ -134,6 +134,34 @@ void epoch_trampoline(int epoch, double mean, void* user) {
 }
 }  // namespace
 
+namespace {
+// The training set of the last net::train calls: a set trained twice in a row has its image storage
+// page-locked (tlb_host_register) from the second call on, so every later call DMAs straight from it
+// instead of staging through the pinned bounce slots (the pageable path).  The Tensor copy keeps the
+// storage alive -- and its address unique -- for as long as it is registered; a different set replaces
+// it (the old range is unregistered first).  Accessed under the device lock.
+struct PinnedSet {
+  Tensor images;  // shares the caller's storage
+  const float* ptr = nullptr;
+  std::size_t bytes = 0;
+  bool registered = false;
+};
+PinnedSet g_pinned;
+
+void pin_training_set(tlb_ctx* ctx, const Tensor& images) {
+  constexpr std::size_t kMinBytes = 4u << 20;  // smaller sets: the bounce path is as fast
+  const std::span<const float> v = images.data();
+  const std::size_t bytes = v.size_bytes();
+  if (bytes < kMinBytes) return;
+  if (v.data() == g_pinned.ptr && bytes == g_pinned.bytes) {  // seen before (and still alive: we hold it)
+    if (!g_pinned.registered) g_pinned.registered = tlb_host_register(ctx, v.data(), bytes) == TLB_OK;
+    return;
+  }
+  if (g_pinned.registered) (void)tlb_host_unregister(ctx, g_pinned.ptr);
+  g_pinned = PinnedSet{images, v.data(), bytes, false};  // registered if the next call trains it again
+}
+}  // namespace
+
 TrainResult train(const Params& p, const mnist::MnistSet& data, const Hyper& h,
                   const std::function<void(int, double)>& on_epoch) {
   p.validate();
@@ -150,6 +178,7 @@ TrainResult train(const Params& p, const mnist::MnistSet& data, const Hyper& h,
   std::vector<double> losses(static_cast<std::size_t>(h.epochs));
   {
     auto dev = detail::device();
+    pin_training_set(dev.ctx, data.images);
     detail::check(tlb_train(dev.ctx, images.data(), labels, data.size(), w.data(), h.rate, h.epochs, h.batch,
                             losses.data(), on_epoch ? epoch_trampoline : nullptr,
                             const_cast<std::function<void(int, double)>*>(&on_epoch)));

@@ -1,7 +1,8 @@
 // e2e_bench.cpp -- end-to-end timing of the C++ drop-in: tloom::net::train called exactly as the
 // reference's callers call it (proj/tools/tensorloom_cli.cpp:102-112, proj/tests/acceptance.cpp:245):
-// a host MnistSet (std::vector storage, pageable memory) in, TrainResult out, one epoch per call.
-// Every call moves the dataset host -> device and the parameters back inside the timed region.
+// a host MnistSet (std::vector storage) in, TrainResult out, one epoch per call.  Every call moves the
+// dataset host -> device and the parameters back inside the timed region (the mirror page-locks the set's
+// storage from its second call on, so the timed calls DMA straight from it; the H2D itself stays per call).
 //
 //   tloom-e2e-bench [--n 10000] [--batch 100] [--rate 0.05] [--steps 10] [--warmup 3] [--mode fast|exact]
 //
@@ -69,7 +70,8 @@ int main(int argc, char** argv) {
     const double med = sorted.empty() ? 0.0 : sorted[sorted.size() / 2];
     const long long h2d = (long long)n * 784 * 4 + (long long)n * 4 + 3898 * 4;
     const long long d2h = 3898 * 4 + 8;
-    std::printf("{\"api\": \"tloom::net::train (C++ drop-in, MnistSet in pageable host memory)\", \"mode\": \"%s\", "
+    std::printf("{\"api\": \"tloom::net::train (C++ drop-in on a host MnistSet; the mirror page-locks a set it trains twice)\", "
+                "\"mode\": \"%s\", "
                 "\"n\": %lld, \"batch\": %lld, \"steps\": %d, \"warmup\": %d, \"images_per_s\": %.6f, "
                 "\"call_ms\": {\"median\": %.6f, \"min\": %.6f, \"max\": %.6f}, \"h2d_bytes_per_step\": %lld, "
                 "\"d2h_bytes_per_step\": %lld, \"epoch_loss\": [",
