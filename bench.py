@@ -207,8 +207,8 @@ def run_reference(args):
 
 
 NCU_CAPTURES = {  # (mode, batch, n) -> committed `ncu --set full` key metrics of that exact launch
-    ("fast", 100, 10000): "profiles/r2/ncu_cluster_r2g_keymetrics.csv",         # train_cluster_kernel
-    ("fast", 16384, 32768): "profiles/r2/ncu_batch16k_r2g_keymetrics.csv",     # train_batch_kernel<2,320,2,1>
+    ("fast", 100, 10000): "profiles/r2/ncu_cluster_r2i_keymetrics.csv",         # train_cluster_kernel
+    ("fast", 16384, 32768): "profiles/r2/ncu_batch16k_r2i_keymetrics.csv",     # train_batch_kernel<2,320,2,1>
 }
 
 
