@@ -412,6 +412,9 @@ __global__ void __launch_bounds__(kThreads, 1) train_kernel(TrainArgs a) {
 // (every CTA that adds into it in step s+1 has observed that signal); packed words are never zeroed.
 // Not the reference's example-order chain: EXACT mode keeps train_kernel<true>.
 // ------------------------------------------------------------------------------------------------
+#ifndef TLB_POLL_NS
+#define TLB_POLL_NS 32  // back-off between the packed-word polls of the single-GPU exchange (ns)
+#endif
 #ifndef TLB_CLUSTER
 #define TLB_CLUSTER 8  // CTAs per cluster (16 = the non-portable cluster size: A/B)
 #endif
@@ -659,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1) train_cluster_kernel(TrainArgs a)
               atomicExch(a.dp_error, 1u);
               return;
             }
-            __nanosleep(32);
+            if (TLB_POLL_NS > 0) __nanosleep(TLB_POLL_NS);
           }
         };
         if ((threadIdx.x & 31) == 0) poll();
