@@ -64,6 +64,8 @@ _SIGS = {
     "tlb_synth_make_set": (C.c_int, [C.c_int64, C.c_uint64, f32p, i32p]),
     "tlb_validate_set": (C.c_int, [f32p, i32p, C.c_int64]),
     # raw addresses (c_void_p) on the e2e path: ~4 us per ctypes pointer conversion avoided per call
+    "tlb_host_register": (C.c_int, [vp, vp, C.c_size_t]),
+    "tlb_host_unregister": (C.c_int, [vp, vp]),
     "tlb_train": (C.c_int, [vp, vp, vp, C.c_int64, vp, C.c_float, C.c_int32, C.c_int64, vp, EPOCH_CB, vp]),
     "tlb_train_u8": (C.c_int, [vp, vp, vp, C.c_int64, vp, C.c_float, C.c_int32, C.c_int64, vp, EPOCH_CB, vp]),
     "tlb_train_idx": (C.c_int, [vp, vp, C.c_size_t, vp, C.c_size_t, vp, C.c_float, C.c_int32, C.c_int64, vp,

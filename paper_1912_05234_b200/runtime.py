@@ -198,6 +198,14 @@ class Context:
         the whole dataset; > 0 = only this rank's shards, the shard of group g at example g * local_stride."""
         _check(self._L.tlb_ctx_set_shard_layout(self._h, int(local_stride)))
 
+    def host_register(self, array) -> None:
+        """Page-lock a host array (numpy, C-contiguous) so tlb_train / tlb_evaluate DMA straight from it
+        (tlb_host_register); the caller keeps the array alive until host_unregister."""
+        _check(self._L.tlb_host_register(self._h, array.ctypes.data, array.nbytes))
+
+    def host_unregister(self, array) -> None:
+        _check(self._L.tlb_host_unregister(self._h, array.ctypes.data))
+
     def set_trace(self, d_trace_ptr: int) -> None:
         """Per-stage clock64 stamps of CTA 0 into a device buffer of [steps][16] uint64 (0 disables)."""
         _check(self._L.tlb_ctx_set_trace(self._h, C.c_void_p(d_trace_ptr or None)))

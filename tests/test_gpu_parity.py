@@ -395,3 +395,24 @@ def test_overlapped_ingestion_chunk_policies(policy):
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "ingestion ok" in out.stdout
+
+
+def test_host_registered_dataset_trains_identically(orc, zhang_sets):
+    """tlb_host_register on a pageable numpy dataset (what the C++ mirror does for a set it trains twice):
+    the call then takes the direct-DMA path and trains the same weights, bit for bit, as the pageable
+    bounce path; unregistering restores the pageable path."""
+    from paper_1912_05234_b200 import Context
+    (tr_x, tr_y), _ = zhang_sets
+    x = np.ascontiguousarray(tr_x[:3000])
+    y = np.ascontiguousarray(tr_y[:3000], np.int32)
+    p0 = orc.init_params(42)
+    with Context(0, mode="fast") as c:
+        want_p, want_l = c.train(p0, x, y, epochs=2, batch=100)
+        c.host_register(x)
+        try:
+            got_p, got_l = c.train(p0, x, y, epochs=2, batch=100)
+        finally:
+            c.host_unregister(x)
+        again_p, again_l = c.train(p0, x, y, epochs=2, batch=100)
+    assert np.array_equal(bits(got_p), bits(want_p)) and list(got_l) == list(want_l)
+    assert np.array_equal(bits(again_p), bits(want_p)) and list(again_l) == list(want_l)
